@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark of the PLSSVM B200 hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config C1] [--mode implicit|cached|auto]
+    python bench.py --impl reference ...        # the CPU oracle as the reference arm
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config): C1 = 2^14 points x 2^10
+features, RBF (gamma = 1/d), fp64, implicit Q~p, C = 1, eps = 1e-10, synthetic
+make_classification "planes" data (synth/).  A step = one pass of the whole hot path
+(SURVEY §8(a) rows a0-a8): plssvm_train_ex on inputs resident in HBM (transform, q, CG to
+eps, bias/alpha) followed by plssvm_predict_ex on the 2^13 test points.  `value` = CG
+iterations per second of the whole job (max over ranks); ms_per_step = train + predict.
+N > 1 (torchrun): Q~ row-sharded over the ranks (NCCL all-gather of p, all-reduce of the CG
+scalars), test points sharded for predict; the problem size is fixed -> "scaling": "strong".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "CG iterations/s & kernel-matvec FLOP/s (% peak), train time; 1/2/4/8 B200"
+UNIT = "CG it/s"
+KNAMES = {0: "linear", 1: "polynomial", 2: "rbf"}
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs x DFMA/clk/SM x 2 x max SM clock
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: FFMA
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for ln in fh:
+                    parts = [x.strip() for x in ln.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def matvec_flops(m, d):
+    """Algorithmic flops of one Q~p product: 2d per distinct entry of the symmetric Q~."""
+    m1 = m - 1
+    return 2.0 * d * m1 * (m1 + 1) / 2.0
+
+
+def cpu_baseline(cfg, X, y, target_s=15.0, m_cap=None):
+    """The oracle (as it stands) on the host cores: oracle.train on the first m_s points (same d,
+    same kernel), m_s sized for ~target_s of CPU work; both of its phases (Q~ formation and the
+    dense CG GEMVs) are O(m^2), so iterations/s is scaled by (m_s/m)^2 to the full workload."""
+    import oracle
+
+    oracle.build()
+    cores = oracle.num_threads()
+    m = cfg.m
+    t0 = time.perf_counter()
+    ms0 = min(m, 1024)
+    oracle.train(X[:ms0], y[:ms0], cfg.kernel, cfg.gamma, cfg.degree, cfg.coef0, cfg.C, cfg.eps)
+    t1 = time.perf_counter() - t0
+    ms = int(min(m, ms0 * math.sqrt(target_s / max(t1, 1e-3))) // 128 * 128)
+    ms = max(ms0, ms if m_cap is None else min(ms, m_cap))
+    Xs, ys = X[:ms], y[:ms]
+    if ys.min() == ys.max():
+        ys = ys.copy()
+        ys[-1] = -ys[0]
+    t0 = time.perf_counter()
+    alpha, b, it, st, tm = oracle.train(Xs, ys, cfg.kernel, cfg.gamma, cfg.degree, cfg.coef0, cfg.C, cfg.eps,
+                                        timings=True)
+    ts = time.perf_counter() - t0
+    scale = (m / ms) ** 2
+    return {"value": it / (ts * scale), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"oracle.train on the first {ms} of {m} points (d={cfg.d}, {KNAMES[cfg.kernel]}, eps "
+                      f"{cfg.eps:g}): {it} CG iterations in {ts:.2f} s (Q~ formation {tm[0]:.2f} s, CG {tm[1]:.2f} s);"
+                      f" time scaled by (m/m_s)^2 = {scale:.2f} to the full workload",
+            "sample_seconds": ts, "sample_iterations": it, "sample_m": ms}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import oracle
+
+    oracle.build()
+    X, y, Z, yz = synth.config_data(cfg, n_test=0)
+    # size one step for ~ (a few minutes) / (steps + warmup)
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    cal = cpu_baseline(cfg, X, y, target_s=per_step)
+    ms = cal["sample_m"]
+    Xs, ys = X[:ms], y[:ms]
+    for _ in range(args.warmup):
+        oracle.train(Xs, ys, cfg.kernel, cfg.gamma, cfg.degree, cfg.coef0, cfg.C, cfg.eps)
+    its, t0 = 0, time.perf_counter()
+    for _ in range(args.steps):
+        _, _, it, _ = oracle.train(Xs, ys, cfg.kernel, cfg.gamma, cfg.degree, cfg.coef0, cfg.C, cfg.eps)
+        its += it
+    ts = time.perf_counter() - t0
+    scale = (cfg.m / ms) ** 2
+    value = its / (ts * scale)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * ts * scale / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, args, "oracle"),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cal["cores"], "kind": "oracle",
+                             "sample": f"each step: oracle.train on the first {ms} of {cfg.m} points; time scaled "
+                                       f"by (m/m_s)^2 = {scale:.2f}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(cfg, args, mode):
+    return {"workload": f"{cfg.name}: 2^{int(math.log2(cfg.m))} x 2^{int(math.log2(cfg.d))} {KNAMES[cfg.kernel]} "
+                        f"{cfg.dtype} {mode} Q~p, CG to eps={cfg.eps:g}, + predict on {cfg.n_test} test points",
+            "m": cfg.m, "d": cfg.d, "kernel": KNAMES[cfg.kernel], "gamma": cfg.gamma, "degree": cfg.degree,
+            "coef0": cfg.coef0, "C": cfg.C, "eps": cfg.eps, "mode": mode, "n_test": cfg.n_test,
+            "parallelism": f"row-sharded Q~ x{args.gpus}" if args.gpus > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (X 128 MiB + X^T 128 MiB + Z 64 MiB per step > 126 MB L2); no flush"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--mode", default="implicit", choices=["implicit", "cached", "auto"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = synth.configs()[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2202_12674_b200 as pl
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = pl.comm_from_torch_distributed(local) if world > 1 else None
+
+    mode = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED, "auto": pl.MODE_AUTO}[args.mode]
+    dt = np.float32 if cfg.dtype == "f32" else np.float64
+    X, y, Z, yz = synth.config_data(cfg)
+    n = Z.shape[0]
+    z0, z1 = rank * n // world, (rank + 1) * n // world  # test-point shard of this rank
+    tX = torch.from_numpy(X).to(dev)
+    ty = torch.from_numpy(y).to(dev)
+    tZ = torch.from_numpy(np.ascontiguousarray(Z[z0:z1])).to(dev)
+    kw = dict(gamma=cfg.gamma, degree=cfg.degree, coef0=cfg.coef0)
+
+    def opts():
+        return pl.options(mode=mode, comm=comm, device=local)
+
+    def step():
+        alpha, b, st, stats = pl.plssvm_train_ex(tX, ty, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=opts(), **kw)
+        f, lab, (tk, nl) = pl.plssvm_predict_ex(tX, alpha, float(b.item()), tZ, cfg.kernel, opts=opts(), **kw)
+        return stats, nl, alpha, b, lab
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    per = []
+    with sampler:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            per.append(step())
+        ev1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = ev0.elapsed_time(ev1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    clocks = sampler.summary()
+    iters = sum(s.iterations for s, *_ in per)
+    matvecs = sum(s.iterations for s, *_ in per)
+    t_mv = sum(s.t_matvec for s, *_ in per)
+    launches = sum(s.gpu_launches + int(nl) for s, nl, *_ in per)
+    stats0 = per[-1][0]
+    mode_used = {1: "implicit", 2: "cached"}[stats0.mode_used]
+
+    # ---- roofline of the dominant kernel (the Q~p product), timed with CUDA events on its stream
+    avg_mv = t_mv / max(1, matvecs)
+    if mode_used == "implicit":
+        fl = matvec_flops(cfg.m, cfg.d) / world  # this rank's share (symmetric work split)
+        peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else FP32_PEAK_TFLOPS
+        achieved = fl / avg_mv / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "k_matvec_implicit",
+                "per_launch": f"2*d*E flops, E = m'(m'+1)/2 distinct Q~ entries ({fl:.4g} flops per launch per rank)",
+                "peak_source": "derived: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md); fp32: 128 FFMA/clk",
+                "avg_launch_s": avg_mv}
+    else:
+        s = 8 if cfg.dtype == "f64" else 4
+        mpad = int(math.ceil(cfg.m / (128 * world)) * 128 * world)
+        by = (mpad / world) * mpad * s
+        peak = measured_peaks().get("hbm_gbs", 6650.0)
+        achieved = by / avg_mv / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "k_gemv_cached", "per_launch": f"{by:.4g} bytes of cached Q~ band",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)", "avg_launch_s": avg_mv}
+
+    line = {"metric": METRIC, "value": iters / t, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (sklearn make_classification planes, seeded)",
+            "config": config_dict(cfg, args, mode_used), "gpu_launches": launches, "clocks": clocks,
+            "roofline": roof,
+            "train": {"iterations_per_step": iters / args.steps, "t_train_s": stats0.t_total,
+                      "t_cg_s": stats0.t_cg, "t_precompute_s": stats0.t_precompute,
+                      "t_transform_s": stats0.t_transform, "t_q_s": stats0.t_q, "rel_residual": stats0.rel_residual,
+                      "bytes_per_gpu": stats0.bytes_per_gpu, "launches_in_cg": stats0.launches_in_cg,
+                      "matvec_ms_avg": 1e3 * avg_mv, "matvec_ms_min": 1e3 * stats0.t_matvec_min}}
+
+    # ---- e2e: same metric through the public API with HOST buffers (pinned), copies inside
+    if not args.no_e2e:
+        hX = torch.from_numpy(X).pin_memory().numpy()
+        hy = torch.from_numpy(y).pin_memory().numpy()
+        hZ = torch.from_numpy(np.ascontiguousarray(Z[z0:z1])).pin_memory().numpy()
+        for _ in range(1):
+            a_h, b_h, _, _ = pl.plssvm_train_ex(hX, hy, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=opts(), **kw)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        its_e = 0
+        for _ in range(args.steps):
+            a_h, b_h, st, stt = pl.plssvm_train_ex(hX, hy, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=opts(), **kw)
+            f_h, lab_h, _ = pl.plssvm_predict_ex(hX, a_h, b_h, hZ, cfg.kernel, opts=opts(), **kw)
+            its_e += stt.iterations
+        te = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        es = X.itemsize
+        h2d = X.nbytes + y.nbytes + X.nbytes + a_h.nbytes + hZ.nbytes
+        d2h = a_h.nbytes + es + f_h.nbytes + lab_h.nbytes
+        line["e2e"] = {"value": its_e / te, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                       "ms_per_step": 1e3 * te / args.steps,
+                       "api": "plssvm_train_ex + plssvm_predict_ex on pinned host numpy buffers"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, X, y)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        pl.plssvm_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

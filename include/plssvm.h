@@ -1,0 +1,166 @@
+/*
+ * plssvm.h -- C ABI of the B200-native PLSSVM hot path (LS-SVM training by CG on the
+ * reduced kernel system Q~, and prediction).  extern "C", plain pointers and sizes only.
+ *
+ * Citations: P:L = PAPER.md line L (arXiv 2202.12674, Van Craen/Breyer/Pflüger),
+ *            S:L = SPEC.md line L.  DESIGN.md lists every reading of the paper used here.
+ *
+ * What is computed (one call of plssvm_train*):
+ *   full LS-SVM system  [[Q, 1],[1^T, 0]] [alpha; b] = [y; 0],  Q_ij = k(x_i,x_j) + delta_ij/C
+ *                                                                  (Eq. 11)
+ *   reduced system      Q~ a~ = y_bar - y_m 1                       (Eq. 14)
+ *   Q~_ij = k(x_i,x_j) + delta_ij/C - k(x_m,x_j) - k(x_i,x_m) + k(x_m,x_m) + 1/C
+ *                                                                  (Eq. 16)
+ *   x_m = the LAST point (index m-1); CG = Shewchuk's algorithm, x0 = 0,
+ *   stop when ||r|| <= eps ||r0|| on the recurrence residual (R-5)
+ *   b = y_m + Q_mm <1, a~> - <q, a~>  (Eq. 15),  alpha = (a~, -sum a~)
+ * Kernels: 0 linear <x,z>; 1 polynomial (gamma <x,z> + coef0)^degree;
+ *                      2 radial exp(-gamma ||x - z||^2).
+ * Decision function (Eq. 10, labels absorbed into alpha, R-2):
+ *   f(z) = sum_i alpha_i k(x_i, z) + b ; label = +1 if f >= 0 else -1 (sgn(0) -> +1).
+ *
+ * Memory / ownership: unless options.device_pointers != 0, every pointer is a HOST pointer
+ * owned by the caller; the library copies what it needs to the device, never retains a
+ * pointer after return and never returns memory the caller must free.  With
+ * device_pointers != 0, X, y, alpha, b, Z, decision, labels, p, out are DEVICE pointers on
+ * options.device (e.g. torch tensors' data_ptr()), and all work is ordered on
+ * options.stream (cudaStream_t, NULL = a library-owned stream); the call still returns only
+ * after the results are written (it synchronises that stream).
+ * Layout: X is point-major (row i = point i), m x d, C-contiguous (numpy/torch default);
+ * Z is n x d, same layout.  The device transposes to the paper's feature-major layout
+ * itself.
+ * Errors: every entry point returns a plssvm_status_t; on any error the outputs are left
+ * untouched (except PLSSVM_W_NOT_CONVERGED, which fills alpha and b) and
+ * plssvm_last_error() returns a thread-local message valid until the next call on the thread.
+ * There is no CPU fallback: without a usable CUDA device every compute call returns
+ * PLSSVM_E_CUDA.
+ * Thread safety: concurrent calls must use different devices or different streams.
+ */
+#ifndef PLSSVM_B200_H
+#define PLSSVM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PLSSVM_API __attribute__((visibility("default")))
+#else
+#define PLSSVM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { PLSSVM_LINEAR = 0, PLSSVM_POLYNOMIAL = 1, PLSSVM_RBF = 2 } plssvm_kernel_t;
+
+typedef enum {
+    PLSSVM_OK = 0,
+    PLSSVM_E_INVALID_ARG = 1,  /* m < 2, d < 1, C <= 0, gamma <= 0 (poly/rbf), degree < 1,
+                                  eps <= 0, unknown kernel, non-finite X/Z, NULL pointer */
+    PLSSVM_E_LABELS = 2,       /* a y_i not in {-1,+1}, or only one class present */
+    PLSSVM_E_OOM = 3,          /* device allocation failed */
+    PLSSVM_E_CUDA = 4,         /* CUDA runtime error / no device */
+    PLSSVM_E_NCCL = 5,         /* NCCL error in row-sharded mode */
+    PLSSVM_E_NUMERICAL = 6,    /* CG breakdown: p.Q~p <= 0 or non-finite */
+    PLSSVM_W_NOT_CONVERGED = 7 /* max_iter reached before ||r|| <= eps ||r0||; alpha, b filled */
+} plssvm_status_t;
+
+typedef enum { PLSSVM_F64 = 0, PLSSVM_F32 = 1 } plssvm_dtype_t;
+typedef enum { PLSSVM_MODE_AUTO = 0, PLSSVM_MODE_IMPLICIT = 1, PLSSVM_MODE_CACHED = 2 } plssvm_mode_t;
+
+/* Options for the _ex entry points.  plssvm_default_options() fills the defaults given in
+ * brackets.  All-zero is NOT the default (stream/comm NULL are fine, but mode 0 = AUTO). */
+typedef struct {
+    int32_t mode;            /* plssvm_mode_t [AUTO: cached when Q~ fits in free HBM, §8(a3')] */
+    int32_t x0;              /* CG start: 0 = zeros [0], 1 = ones (reproduces paper Fig. 3) */
+    int64_t max_iter;        /* CG iteration cap; <= 0 means m-1 [0] */
+    int64_t replace_every;   /* explicit residual r = rhs - Q~x every R iterations; 0 = off [0] */
+    int64_t fixed_iter;      /* > 0: run exactly this many CG iterations, ignore eps (throughput
+                                benchmarking); the returned model is the state after them [0] */
+    int32_t device;          /* CUDA device ordinal [0] */
+    int32_t device_pointers; /* 1: X,y,alpha,b,Z,... are device pointers on `device` [0] */
+    void *stream;            /* cudaStream_t to order work on; NULL = library stream [NULL] */
+    void *comm;              /* plssvm_comm_t from plssvm_comm_init (row-sharded multi-GPU,
+                                one process per GPU); NULL = single GPU [NULL] */
+    int64_t cache_budget_bytes; /* AUTO/CACHED: max bytes for the cached Q~ band;
+                                   <= 0 means 90 % of free HBM after the other buffers [0] */
+} plssvm_options_t;
+
+/* Statistics of one training call (all times are device-event seconds). */
+typedef struct {
+    int64_t iterations;              /* CG iterations performed */
+    int64_t matvecs;                 /* Q~ products performed (incl. initial / replacement) */
+    double rel_residual;             /* ||r|| / ||r0|| of the recurrence at exit */
+    int32_t mode_used;               /* PLSSVM_MODE_IMPLICIT or PLSSVM_MODE_CACHED */
+    int32_t num_ranks;               /* 1, or the communicator size */
+    double t_h2d, t_transform, t_q, t_precompute, t_cg, t_bias_d2h, t_total;
+    double t_matvec;                 /* summed duration of the Q~p kernels (CUDA events) */
+    double t_matvec_min;             /* shortest single Q~p kernel duration */
+    int64_t bytes_per_gpu;           /* device bytes allocated by this call on this GPU */
+    int64_t gpu_launches;            /* kernels launched by this call (this rank) */
+    int64_t launches_in_cg;          /* of which inside the CG loop */
+} plssvm_stats_t;
+
+PLSSVM_API void plssvm_default_options(plssvm_options_t *opts);
+
+/* ---- training (Eq. 11-16 + CG) ------------------------------------------------------
+ * X [m*d] point-major, y [m] entries +1/-1.  alpha [m] out, b [1] out.
+ * gamma is used by poly/rbf (must be > 0 there); degree (>= 1) and coef0 by poly only. */
+PLSSVM_API int plssvm_train(const double *X, const double *y, int64_t m, int64_t d, int kernel, double gamma,
+                 int degree, double coef0, double C, double eps, double *alpha, double *b);
+PLSSVM_API int plssvm_train_f32(const float *X, const float *y, int64_t m, int64_t d, int kernel, float gamma,
+                     int degree, float coef0, float C, float eps, float *alpha, float *b);
+/* dtype selects double (X, y, alpha, b are double*) or float (float*).  opts/stats nullable. */
+PLSSVM_API int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtype, int kernel,
+                    double gamma, int degree, double coef0, double C, double eps,
+                    const plssvm_options_t *opts, void *alpha, void *b, plssvm_stats_t *stats);
+
+/* ---- prediction (Eq. 10) -------------------------------------------------------------
+ * X [m*d] training points, alpha [m], b: the model.  Z [n*d] points to classify.
+ * decision [n] (nullable) receives f(z); labels [n] (nullable) receives +1/-1. */
+PLSSVM_API int plssvm_predict(const double *X, const double *alpha, double b, int64_t m, int64_t d, int kernel,
+                   double gamma, int degree, double coef0, const double *Z, int64_t n,
+                   double *decision, int32_t *labels);
+PLSSVM_API int plssvm_predict_f32(const float *X, const float *alpha, float b, int64_t m, int64_t d, int kernel,
+                       float gamma, int degree, float coef0, const float *Z, int64_t n,
+                       float *decision, int32_t *labels);
+PLSSVM_API int plssvm_predict_ex(const void *X, const void *alpha, double b, int64_t m, int64_t d, int dtype,
+                      int kernel, double gamma, int degree, double coef0, const void *Z, int64_t n,
+                      const plssvm_options_t *opts, void *decision, int32_t *labels, double *t_kernel);
+/* t_kernel (nullable, 2 doubles): [0] duration (s) of the predict tile kernel, [1] number of
+ * kernels this call launched. */
+
+/* ---- the hot product alone (diagnostics, parity tests, roofline) ----------------------
+ * out[m-1] = Q~ p for p [m-1] (Eq. 16), computed `repeats` times (>= 1) with the mode in
+ * opts (IMPLICIT: recompute tiles; CACHED: precompute Q~ once then stream it).
+ * t_kernel (nullable, 3 doubles) receives: mean, min duration (s) of one Q~p product, and
+ * the one-time precompute duration (cached mode, else 0). */
+PLSSVM_API int plssvm_qtilde_matvec(const void *X, const void *p, int64_t m, int64_t d, int dtype, int kernel,
+                         double gamma, int degree, double coef0, double C, int32_t repeats,
+                         const plssvm_options_t *opts, void *out, double *t_kernel);
+
+/* ---- multi-GPU (one process per GPU, row-sharded Q~; NCCL over NVLink) -----------------
+ * plssvm_comm_unique_id writes an opaque 128-byte NCCL id (rank 0 creates it, the caller
+ * broadcasts it, e.g. with torch.distributed); every rank then calls plssvm_comm_init.
+ * The communicator is bound to `device`.  Destroy with plssvm_comm_destroy. */
+typedef void *plssvm_comm_t;
+PLSSVM_API int plssvm_comm_unique_id(void *id128);
+PLSSVM_API int plssvm_comm_init(const void *id128, int32_t nranks, int32_t rank, int32_t device, plssvm_comm_t *comm);
+PLSSVM_API int plssvm_comm_destroy(plssvm_comm_t comm);
+
+/* Host-side partition rule (no GPU needed): rows [row_begin, row_end) of the padded
+ * (m-1)-system owned by `rank` of `nranks`, and the padded length m_pad (a multiple of
+ * 128 * nranks).  Rows >= m-1 are padding (masked). */
+PLSSVM_API int plssvm_partition(int64_t m, int32_t nranks, int32_t rank, int64_t *row_begin, int64_t *row_end,
+                     int64_t *m_pad);
+
+/* ---- misc ------------------------------------------------------------------------------ */
+PLSSVM_API const char *plssvm_last_error(void); /* thread-local; "" when the last call succeeded */
+PLSSVM_API const char *plssvm_version(void);    /* build string: version, sm arch, CUDA and NCCL versions */
+PLSSVM_API int plssvm_device_count(void);       /* visible CUDA devices (0 when none / no driver) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLSSVM_B200_H */

@@ -1,0 +1,10 @@
+"""B200-native PLSSVM hot path: LS-SVM training by CG on the reduced kernel system Q~
+(arXiv 2202.12674) behind the C ABI include/plssvm.h.  This package holds the CUDA sources
+(csrc/), the in-tree build (_build.py) and the thin ctypes binding (binding.py).
+It never imports ``oracle/``; it has no CPU fallback."""
+from .binding import (  # noqa: F401
+    LINEAR, POLYNOMIAL, RBF, F64, F32, MODE_AUTO, MODE_IMPLICIT, MODE_CACHED, PlssvmError, options, load,
+    plssvm_train, plssvm_train_ex, plssvm_predict, plssvm_predict_ex, plssvm_qtilde_matvec, plssvm_partition,
+    plssvm_version, plssvm_device_count, plssvm_last_error, plssvm_comm_unique_id, plssvm_comm_init,
+    plssvm_comm_destroy, comm_from_torch_distributed,
+)

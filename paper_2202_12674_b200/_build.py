@@ -1,0 +1,56 @@
+"""Build the C-ABI shared library libplssvm_b200.so IN-TREE with nvcc for sm_100a.
+
+    python -m paper_2202_12674_b200._build          (or __graft_entry__.build())
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIBDIR = os.path.join(PKG, "lib")
+LIB = os.path.join(LIBDIR, "libplssvm_b200.so")
+SOURCES = ["capi.cu", "driver.cu", "comm.cu"]
+HEADERS = ["common.cuh", "tile_engine.cuh", "kernels.cuh", "driver.h"]
+
+
+def nccl_dirs():
+    import nvidia.nccl  # torch-bundled NCCL 2.28 (header + libnccl.so.2)
+
+    base = list(nvidia.nccl.__path__)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "plssvm.h"), __file__]
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    inc, libd = nccl_dirs()
+    cmd = [
+        "nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+        "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
+        "-I", os.path.join(ROOT, "include"), "-I", inc,
+        "-o", LIB, *[os.path.join(CSRC, f) for f in SOURCES],
+        "-L", libd, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libd}", "-lcudart",
+    ]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,294 @@
+"""Thin ctypes binding of include/plssvm.h (argument marshalling only).
+
+Every function here has the name of the C entry point it calls.  Host inputs are numpy
+arrays; torch CUDA tensors are passed as device pointers (options.device_pointers = 1) on
+torch's current stream.  No arithmetic of the method happens in Python, and there is no
+fallback: if the shared library is missing or the call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import numpy as np
+
+from . import _build
+
+LINEAR, POLYNOMIAL, RBF = 0, 1, 2
+F64, F32 = 0, 1
+MODE_AUTO, MODE_IMPLICIT, MODE_CACHED = 0, 1, 2
+OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED = range(8)
+STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
+                6: "E_NUMERICAL", 7: "W_NOT_CONVERGED"}
+
+EXPORTS = ["plssvm_default_options", "plssvm_train", "plssvm_train_f32", "plssvm_train_ex", "plssvm_predict",
+           "plssvm_predict_f32", "plssvm_predict_ex", "plssvm_qtilde_matvec", "plssvm_comm_unique_id",
+           "plssvm_comm_init", "plssvm_comm_destroy", "plssvm_partition", "plssvm_last_error", "plssvm_version",
+           "plssvm_device_count"]
+
+
+class plssvm_options_t(ct.Structure):
+    _fields_ = [("mode", ct.c_int32), ("x0", ct.c_int32), ("max_iter", ct.c_int64), ("replace_every", ct.c_int64),
+                ("fixed_iter", ct.c_int64), ("device", ct.c_int32), ("device_pointers", ct.c_int32),
+                ("stream", ct.c_void_p), ("comm", ct.c_void_p), ("cache_budget_bytes", ct.c_int64)]
+
+
+class plssvm_stats_t(ct.Structure):
+    _fields_ = [("iterations", ct.c_int64), ("matvecs", ct.c_int64), ("rel_residual", ct.c_double),
+                ("mode_used", ct.c_int32), ("num_ranks", ct.c_int32), ("t_h2d", ct.c_double),
+                ("t_transform", ct.c_double), ("t_q", ct.c_double), ("t_precompute", ct.c_double),
+                ("t_cg", ct.c_double), ("t_bias_d2h", ct.c_double), ("t_total", ct.c_double),
+                ("t_matvec", ct.c_double), ("t_matvec_min", ct.c_double), ("bytes_per_gpu", ct.c_int64),
+                ("gpu_launches", ct.c_int64), ("launches_in_cg", ct.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class PlssvmError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libplssvm_b200.so (building it in-tree first if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_build.LIB):
+        if not build_if_missing:
+            raise FileNotFoundError(f"{_build.LIB} missing: run __graft_entry__.build()")
+        _build.build()
+    L = ct.CDLL(_build.LIB)
+    vp, i64, i32, d, i = ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_double, ct.c_int
+    L.plssvm_default_options.argtypes = [ct.POINTER(plssvm_options_t)]
+    L.plssvm_default_options.restype = None
+    L.plssvm_train_ex.argtypes = [vp, vp, i64, i64, i, i, d, i, d, d, d, ct.POINTER(plssvm_options_t), vp, vp,
+                                  ct.POINTER(plssvm_stats_t)]
+    L.plssvm_train.argtypes = [vp, vp, i64, i64, i, d, i, d, d, d, vp, vp]
+    L.plssvm_train_f32.argtypes = [vp, vp, i64, i64, i, ct.c_float, i, ct.c_float, ct.c_float, ct.c_float, vp, vp]
+    L.plssvm_predict.argtypes = [vp, vp, d, i64, i64, i, d, i, d, vp, i64, vp, vp]
+    L.plssvm_predict_f32.argtypes = [vp, vp, ct.c_float, i64, i64, i, ct.c_float, i, ct.c_float, vp, i64, vp, vp]
+    L.plssvm_predict_ex.argtypes = [vp, vp, d, i64, i64, i, i, d, i, d, vp, i64, ct.POINTER(plssvm_options_t), vp,
+                                    vp, vp]
+    L.plssvm_qtilde_matvec.argtypes = [vp, vp, i64, i64, i, i, d, i, d, d, i32, ct.POINTER(plssvm_options_t), vp,
+                                       ct.POINTER(ct.c_double)]
+    L.plssvm_comm_unique_id.argtypes = [vp]
+    L.plssvm_comm_init.argtypes = [vp, i32, i32, i32, ct.POINTER(vp)]
+    L.plssvm_comm_destroy.argtypes = [vp]
+    L.plssvm_partition.argtypes = [i64, i32, i32, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
+    L.plssvm_last_error.restype = ct.c_char_p
+    L.plssvm_version.restype = ct.c_char_p
+    L.plssvm_device_count.restype = ct.c_int
+    for name in EXPORTS:
+        if name not in ("plssvm_default_options", "plssvm_last_error", "plssvm_version", "plssvm_device_count"):
+            getattr(L, name).restype = ct.c_int
+    _lib = L
+    return L
+
+
+def _check(status, allow=(OK,)):
+    if status not in allow:
+        raise PlssvmError(status, load().plssvm_last_error().decode())
+    return status
+
+
+def _is_torch_cuda(a) -> bool:
+    return type(a).__module__.startswith("torch") and getattr(a, "is_cuda", False)
+
+
+def _dtype_code(a) -> int:
+    s = str(a.dtype)
+    if s.endswith("float64"):
+        return F64
+    if s.endswith("float32"):
+        return F32
+    raise TypeError(f"unsupported dtype {a.dtype}")
+
+
+def _host(a, dt):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64 if dt == F64 else np.float32))
+
+
+def options(**kw) -> plssvm_options_t:
+    o = plssvm_options_t()
+    load().plssvm_default_options(ct.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def _device_opts(o, tensors):
+    import torch
+
+    o.device_pointers = 1
+    o.device = tensors[0].device.index or 0
+    o.stream = torch.cuda.current_stream(tensors[0].device).cuda_stream
+    return o
+
+
+# ------------------------------------------------------------------------------ entry points
+def plssvm_version() -> str:
+    return load().plssvm_version().decode()
+
+
+def plssvm_device_count() -> int:
+    return load().plssvm_device_count()
+
+
+def plssvm_last_error() -> str:
+    return load().plssvm_last_error().decode()
+
+
+def plssvm_partition(m: int, nranks: int, rank: int):
+    """(row_begin, row_end, m_pad) of `rank` in the padded (m-1)-system (host logic, no GPU)."""
+    b, e, mp = ct.c_int64(), ct.c_int64(), ct.c_int64()
+    _check(load().plssvm_partition(m, nranks, rank, ct.byref(b), ct.byref(e), ct.byref(mp)))
+    return b.value, e.value, mp.value
+
+
+def plssvm_train(X, y, kernel, gamma=1.0, degree=3, coef0=0.0, C=1.0, eps=1e-10):
+    """Host numpy in / out, fp64 (plssvm_train) or fp32 (plssvm_train_f32) by X's dtype."""
+    dt = F32 if str(getattr(X, "dtype", "")) == "float32" else F64
+    X, y = _host(X, dt), _host(y, dt)
+    m, d = X.shape
+    alpha = np.empty(m, dtype=X.dtype)
+    b = np.zeros(1, dtype=X.dtype)
+    L = load()
+    if dt == F64:
+        st = L.plssvm_train(X.ctypes.data, y.ctypes.data, m, d, kernel, gamma, degree, coef0, C, eps,
+                            alpha.ctypes.data, b.ctypes.data)
+    else:
+        st = L.plssvm_train_f32(X.ctypes.data, y.ctypes.data, m, d, kernel, gamma, degree, coef0, C, eps,
+                                alpha.ctypes.data, b.ctypes.data)
+    _check(st, (OK, W_NOT_CONVERGED))
+    return alpha, float(b[0]), st
+
+
+def plssvm_train_ex(X, y, kernel, gamma=1.0, degree=3, coef0=0.0, C=1.0, eps=1e-10, opts=None, alpha=None, b=None):
+    """numpy (host) or torch CUDA tensors (device pointers).  Returns (alpha, b, status, stats)."""
+    o = opts if opts is not None else options()
+    stats = plssvm_stats_t()
+    dt = _dtype_code(X)
+    m, d = X.shape
+    L = load()
+    if _is_torch_cuda(X):
+        import torch
+
+        _device_opts(o, [X])
+        X, y = X.contiguous(), y.contiguous()
+        alpha = torch.empty(m, dtype=X.dtype, device=X.device) if alpha is None else alpha
+        b = torch.empty(1, dtype=X.dtype, device=X.device) if b is None else b
+        st = L.plssvm_train_ex(X.data_ptr(), y.data_ptr(), m, d, dt, kernel, gamma, degree, coef0, C, eps,
+                               ct.byref(o), alpha.data_ptr(), b.data_ptr(), ct.byref(stats))
+        _check(st, (OK, W_NOT_CONVERGED))
+        return alpha, b, st, stats
+    X, y = _host(X, dt), _host(y, dt)
+    alpha = np.empty(m, dtype=X.dtype) if alpha is None else alpha
+    b = np.zeros(1, dtype=X.dtype) if b is None else b
+    st = L.plssvm_train_ex(X.ctypes.data, y.ctypes.data, m, d, dt, kernel, gamma, degree, coef0, C, eps, ct.byref(o),
+                           alpha.ctypes.data, b.ctypes.data, ct.byref(stats))
+    _check(st, (OK, W_NOT_CONVERGED))
+    return alpha, float(b[0]), st, stats
+
+
+def plssvm_predict(X, alpha, b, Z, kernel, gamma=1.0, degree=3, coef0=0.0):
+    """Host numpy; returns (decision[n], labels[n])."""
+    dt = F32 if str(getattr(X, "dtype", "")) == "float32" else F64
+    X, alpha, Z = _host(X, dt), _host(alpha, dt), _host(Z, dt)
+    m, d = X.shape
+    n = Z.shape[0]
+    f = np.empty(n, dtype=X.dtype)
+    lab = np.empty(n, dtype=np.int32)
+    L = load()
+    fn = L.plssvm_predict if dt == F64 else L.plssvm_predict_f32
+    _check(fn(X.ctypes.data, alpha.ctypes.data, b, m, d, kernel, gamma, degree, coef0, Z.ctypes.data, n,
+              f.ctypes.data, lab.ctypes.data))
+    return f, lab
+
+
+def plssvm_predict_ex(X, alpha, b, Z, kernel, gamma=1.0, degree=3, coef0=0.0, opts=None):
+    """numpy or torch CUDA tensors.  Returns (decision, labels, (kernel_seconds, launches))."""
+    o = opts if opts is not None else options()
+    dt = _dtype_code(X)
+    m, d = X.shape
+    n = Z.shape[0]
+    tk = (ct.c_double * 2)()
+    L = load()
+    if _is_torch_cuda(X):
+        import torch
+
+        _device_opts(o, [X])
+        f = torch.empty(n, dtype=X.dtype, device=X.device)
+        lab = torch.empty(n, dtype=torch.int32, device=X.device)
+        _check(L.plssvm_predict_ex(X.contiguous().data_ptr(), alpha.contiguous().data_ptr(), float(b), m, d, dt,
+                                   kernel, gamma, degree, coef0, Z.contiguous().data_ptr(), n, ct.byref(o),
+                                   f.data_ptr(), lab.data_ptr(), tk))
+        return f, lab, tuple(tk)
+    X, alpha, Z = _host(X, dt), _host(alpha, dt), _host(Z, dt)
+    f = np.empty(n, dtype=X.dtype)
+    lab = np.empty(n, dtype=np.int32)
+    _check(L.plssvm_predict_ex(X.ctypes.data, alpha.ctypes.data, float(b), m, d, dt, kernel, gamma, degree, coef0,
+                               Z.ctypes.data, n, ct.byref(o), f.ctypes.data, lab.ctypes.data, tk))
+    return f, lab, tuple(tk)
+
+
+def plssvm_qtilde_matvec(X, p, kernel, gamma=1.0, degree=3, coef0=0.0, C=1.0, repeats=1, opts=None):
+    """out = Q~ p (length m-1).  Returns (out, (mean_s, min_s, precompute_s))."""
+    o = opts if opts is not None else options()
+    dt = _dtype_code(X)
+    m, d = X.shape
+    tk = (ct.c_double * 3)()
+    L = load()
+    if _is_torch_cuda(X):
+        import torch
+
+        _device_opts(o, [X])
+        out = torch.empty(m - 1, dtype=X.dtype, device=X.device)
+        _check(L.plssvm_qtilde_matvec(X.contiguous().data_ptr(), p.contiguous().data_ptr(), m, d, dt, kernel, gamma,
+                                      degree, coef0, C, repeats, ct.byref(o), out.data_ptr(), tk))
+        return out, tuple(tk)
+    X, p = _host(X, dt), _host(p, dt)
+    out = np.empty(m - 1, dtype=X.dtype)
+    _check(L.plssvm_qtilde_matvec(X.ctypes.data, p.ctypes.data, m, d, dt, kernel, gamma, degree, coef0, C, repeats,
+                                  ct.byref(o), out.ctypes.data, tk))
+    return out, tuple(tk)
+
+
+def plssvm_comm_unique_id() -> bytes:
+    buf = ct.create_string_buffer(128)
+    _check(load().plssvm_comm_unique_id(buf))
+    return buf.raw
+
+
+def plssvm_comm_init(uid: bytes, nranks: int, rank: int, device: int):
+    h = ct.c_void_p()
+    buf = ct.create_string_buffer(uid, 128)
+    _check(load().plssvm_comm_init(buf, nranks, rank, device, ct.byref(h)))
+    return h.value
+
+
+def plssvm_comm_destroy(comm) -> None:
+    _check(load().plssvm_comm_destroy(comm))
+
+
+def comm_from_torch_distributed(device: int):
+    """Create the NCCL communicator of this rank; torch.distributed only broadcasts the id."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    uid = plssvm_comm_unique_id() if rank == 0 else bytes(128)
+    t = torch.tensor(list(uid), dtype=torch.uint8)
+    if dist.get_backend() == "nccl":
+        t = t.cuda(device)
+    dist.broadcast(t, 0)
+    return plssvm_comm_init(bytes(t.cpu().tolist()), world, rank, device)

@@ -1,0 +1,260 @@
+// capi.cu -- the extern "C" boundary declared in include/plssvm.h: validation, error
+// conventions (status codes + thread-local message), dispatch to the device driver.
+// Validation rules (plssvm.h): m >= 2, d >= 1; y_i in {-1,+1}
+// with both classes present; C > 0; gamma > 0 for poly/rbf and degree >= 1
+// (P:248-249); eps > 0; kernel in {0,1,2}; finite X / Z.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/plssvm.h"
+#include "common.cuh"
+#include "driver.h"
+
+#ifndef PLSSVM_VERSION
+#define PLSSVM_VERSION "0.1.0"
+#endif
+
+extern "C" int plssvm_comm_unique_id_impl(void *id128);
+extern "C" int plssvm_comm_init_impl(const void *id128, int32_t nranks, int32_t rank, int32_t device, void **out);
+extern "C" int plssvm_comm_destroy_impl(void *c);
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(F f) {
+    g_last_error.clear();
+    try {
+        return f();
+    } catch (const plssvm::Error &e) {
+        return fail(e.code, e.what());
+    } catch (const std::exception &e) {
+        return fail(PLSSVM_E_CUDA, e.what());
+    }
+}
+
+int device_ok(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0)
+        return fail(PLSSVM_E_CUDA, "no CUDA device available (the library has no CPU fallback)");
+    if (device < 0 || device >= n) return fail(PLSSVM_E_INVALID_ARG, "options.device out of range");
+    return PLSSVM_OK;
+}
+
+int check_params(int64_t m, int64_t d, int kernel, double gamma, int degree, double C) {
+    if (m < 2) return fail(PLSSVM_E_INVALID_ARG, "m must be >= 2");
+    if (d < 1) return fail(PLSSVM_E_INVALID_ARG, "d must be >= 1");
+    if (kernel < 0 || kernel > 2) return fail(PLSSVM_E_INVALID_ARG, "kernel must be 0 (linear), 1 (polynomial) or 2 (rbf)");
+    if (!(C > 0) || !std::isfinite(C)) return fail(PLSSVM_E_INVALID_ARG, "C must be > 0");
+    if (kernel != 0 && (!(gamma > 0) || !std::isfinite(gamma))) return fail(PLSSVM_E_INVALID_ARG, "gamma must be > 0");
+    if (kernel == 1 && degree < 1) return fail(PLSSVM_E_INVALID_ARG, "degree must be >= 1");
+    return PLSSVM_OK;
+}
+
+// Host-side checks of host buffers only (device buffers are the caller's responsibility).
+template <typename T>
+int check_finite(const T *a, int64_t n, const char *what) {
+    for (int64_t i = 0; i < n; ++i)
+        if (!std::isfinite(static_cast<double>(a[i]))) return fail(PLSSVM_E_INVALID_ARG, std::string(what) + " is not finite");
+    return PLSSVM_OK;
+}
+
+template <typename T>
+int check_labels(const T *y, int64_t m) {
+    bool pos = false, neg = false;
+    for (int64_t i = 0; i < m; ++i) {
+        if (y[i] == T(1)) pos = true;
+        else if (y[i] == T(-1)) neg = true;
+        else return fail(PLSSVM_E_LABELS, "labels must be +1 or -1");
+    }
+    if (!pos || !neg) return fail(PLSSVM_E_LABELS, "both classes (+1 and -1) must be present");
+    return PLSSVM_OK;
+}
+
+plssvm_options_t defaults() {
+    plssvm_options_t o;
+    plssvm_default_options(&o);
+    return o;
+}
+
+template <typename T>
+int host_checks_train(const void *X, const void *y, int64_t m, int64_t d) {
+    int s = check_finite(static_cast<const T *>(X), m * d, "X");
+    if (s) return s;
+    return check_labels(static_cast<const T *>(y), m);
+}
+
+}  // namespace
+
+extern "C" {
+
+void plssvm_default_options(plssvm_options_t *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->mode = PLSSVM_MODE_AUTO;
+    o->x0 = 0;
+    o->max_iter = 0;
+    o->replace_every = 0;
+    o->fixed_iter = 0;
+    o->device = 0;
+    o->device_pointers = 0;
+    o->stream = nullptr;
+    o->comm = nullptr;
+    o->cache_budget_bytes = 0;
+}
+
+int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtype, int kernel, double gamma, int degree,
+                    double coef0, double C, double eps, const plssvm_options_t *opts, void *alpha, void *b,
+                    plssvm_stats_t *stats) {
+    g_last_error.clear();
+    const plssvm_options_t o = opts ? *opts : defaults();
+    if (!X || !y || !alpha || !b) return fail(PLSSVM_E_INVALID_ARG, "NULL pointer argument");
+    if (dtype != PLSSVM_F64 && dtype != PLSSVM_F32) return fail(PLSSVM_E_INVALID_ARG, "dtype must be 0 (f64) or 1 (f32)");
+    int s = check_params(m, d, kernel, gamma, degree, C);
+    if (s) return s;
+    if (!(eps > 0) || !std::isfinite(eps)) return fail(PLSSVM_E_INVALID_ARG, "eps must be > 0");
+    if (o.mode < 0 || o.mode > 2) return fail(PLSSVM_E_INVALID_ARG, "options.mode must be 0, 1 or 2");
+    if (o.x0 != 0 && o.x0 != 1) return fail(PLSSVM_E_INVALID_ARG, "options.x0 must be 0 or 1");
+    if (!o.device_pointers) {
+        s = dtype == PLSSVM_F64 ? host_checks_train<double>(X, y, m, d) : host_checks_train<float>(X, y, m, d);
+        if (s) return s;
+    }
+    if ((s = device_ok(o.device))) return s;
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    plssvm::Problem pb{X, y, m, d, dtype, kernel, gamma, degree, coef0, C, eps};
+    return guarded([&] { return plssvm::train(pb, o, alpha, b, stats); });
+}
+
+int plssvm_train(const double *X, const double *y, int64_t m, int64_t d, int kernel, double gamma, int degree,
+                 double coef0, double C, double eps, double *alpha, double *b) {
+    return plssvm_train_ex(X, y, m, d, PLSSVM_F64, kernel, gamma, degree, coef0, C, eps, nullptr, alpha, b, nullptr);
+}
+
+int plssvm_train_f32(const float *X, const float *y, int64_t m, int64_t d, int kernel, float gamma, int degree,
+                     float coef0, float C, float eps, float *alpha, float *b) {
+    return plssvm_train_ex(X, y, m, d, PLSSVM_F32, kernel, gamma, degree, coef0, C, eps, nullptr, alpha, b, nullptr);
+}
+
+int plssvm_predict_ex(const void *X, const void *alpha, double b, int64_t m, int64_t d, int dtype, int kernel,
+                      double gamma, int degree, double coef0, const void *Z, int64_t n, const plssvm_options_t *opts,
+                      void *decision, int32_t *labels, double *t_kernel) {
+    g_last_error.clear();
+    const plssvm_options_t o = opts ? *opts : defaults();
+    if (!X || !alpha || !Z) return fail(PLSSVM_E_INVALID_ARG, "NULL pointer argument");
+    if (dtype != PLSSVM_F64 && dtype != PLSSVM_F32) return fail(PLSSVM_E_INVALID_ARG, "dtype must be 0 (f64) or 1 (f32)");
+    if (m < 1) return fail(PLSSVM_E_INVALID_ARG, "m must be >= 1");
+    int s = check_params(m < 2 ? 2 : m, d, kernel, gamma, degree, 1.0);
+    if (s) return s;
+    if (n < 0) return fail(PLSSVM_E_INVALID_ARG, "n must be >= 0");
+    if (n == 0) return PLSSVM_OK;
+    if (!std::isfinite(b)) return fail(PLSSVM_E_INVALID_ARG, "b is not finite");
+    if (!o.device_pointers) {
+        if (dtype == PLSSVM_F64) {
+            if ((s = check_finite(static_cast<const double *>(X), m * d, "X"))) return s;
+            if ((s = check_finite(static_cast<const double *>(Z), n * d, "Z"))) return s;
+            if ((s = check_finite(static_cast<const double *>(alpha), m, "alpha"))) return s;
+        } else {
+            if ((s = check_finite(static_cast<const float *>(X), m * d, "X"))) return s;
+            if ((s = check_finite(static_cast<const float *>(Z), n * d, "Z"))) return s;
+            if ((s = check_finite(static_cast<const float *>(alpha), m, "alpha"))) return s;
+        }
+    }
+    if ((s = device_ok(o.device))) return s;
+    plssvm::Problem pb{X, nullptr, m, d, dtype, kernel, gamma, degree, coef0, 1.0, 1.0};
+    return guarded([&] { return plssvm::predict(pb, alpha, b, Z, n, o, decision, labels, t_kernel); });
+}
+
+int plssvm_predict(const double *X, const double *alpha, double b, int64_t m, int64_t d, int kernel, double gamma,
+                   int degree, double coef0, const double *Z, int64_t n, double *decision, int32_t *labels) {
+    return plssvm_predict_ex(X, alpha, b, m, d, PLSSVM_F64, kernel, gamma, degree, coef0, Z, n, nullptr, decision, labels,
+                             nullptr);
+}
+
+int plssvm_predict_f32(const float *X, const float *alpha, float b, int64_t m, int64_t d, int kernel, float gamma,
+                       int degree, float coef0, const float *Z, int64_t n, float *decision, int32_t *labels) {
+    return plssvm_predict_ex(X, alpha, b, m, d, PLSSVM_F32, kernel, gamma, degree, coef0, Z, n, nullptr, decision, labels,
+                             nullptr);
+}
+
+int plssvm_qtilde_matvec(const void *X, const void *p, int64_t m, int64_t d, int dtype, int kernel, double gamma,
+                         int degree, double coef0, double C, int32_t repeats, const plssvm_options_t *opts, void *out,
+                         double *t_kernel) {
+    g_last_error.clear();
+    const plssvm_options_t o = opts ? *opts : defaults();
+    if (!X || !p || !out) return fail(PLSSVM_E_INVALID_ARG, "NULL pointer argument");
+    if (dtype != PLSSVM_F64 && dtype != PLSSVM_F32) return fail(PLSSVM_E_INVALID_ARG, "dtype must be 0 (f64) or 1 (f32)");
+    int s = check_params(m, d, kernel, gamma, degree, C);
+    if (s) return s;
+    if (!o.device_pointers) {
+        s = dtype == PLSSVM_F64 ? check_finite(static_cast<const double *>(X), m * d, "X")
+                                : check_finite(static_cast<const float *>(X), m * d, "X");
+        if (s) return s;
+    }
+    if ((s = device_ok(o.device))) return s;
+    plssvm::Problem pb{X, nullptr, m, d, dtype, kernel, gamma, degree, coef0, C, 1.0};
+    return guarded([&] { return plssvm::qtilde_matvec(pb, p, repeats, o, out, t_kernel); });
+}
+
+int plssvm_comm_unique_id(void *id128) {
+    g_last_error.clear();
+    if (!id128) return fail(PLSSVM_E_INVALID_ARG, "NULL id buffer");
+    int s = plssvm_comm_unique_id_impl(id128);
+    return s ? fail(s, "ncclGetUniqueId failed") : PLSSVM_OK;
+}
+
+int plssvm_comm_init(const void *id128, int32_t nranks, int32_t rank, int32_t device, plssvm_comm_t *comm) {
+    g_last_error.clear();
+    if (!id128 || !comm) return fail(PLSSVM_E_INVALID_ARG, "NULL pointer argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PLSSVM_E_INVALID_ARG, "bad rank / nranks");
+    int s = device_ok(device);
+    if (s) return s;
+    s = plssvm_comm_init_impl(id128, nranks, rank, device, comm);
+    return s ? fail(s, "ncclCommInitRank failed") : PLSSVM_OK;
+}
+
+int plssvm_comm_destroy(plssvm_comm_t comm) { return plssvm_comm_destroy_impl(comm); }
+
+int plssvm_partition(int64_t m, int32_t nranks, int32_t rank, int64_t *row_begin, int64_t *row_end, int64_t *m_pad) {
+    g_last_error.clear();
+    if (m < 2 || nranks < 1 || rank < 0 || rank >= nranks || !row_begin || !row_end || !m_pad)
+        return fail(PLSSVM_E_INVALID_ARG, "bad partition arguments");
+    const int64_t mpad = plssvm::round_up(m, static_cast<int64_t>(plssvm::kTile) * nranks);
+    const int64_t nb = mpad / nranks;
+    *m_pad = mpad;
+    *row_begin = static_cast<int64_t>(rank) * nb;
+    *row_end = *row_begin + nb;
+    return PLSSVM_OK;
+}
+
+const char *plssvm_last_error(void) { return g_last_error.c_str(); }
+
+const char *plssvm_version(void) {
+    static std::string v;
+    if (v.empty()) {
+        int rt = 0;
+        cudaRuntimeGetVersion(&rt);
+        v = std::string("plssvm-b200 ") + PLSSVM_VERSION + " sm_100a CUDA-runtime " + std::to_string(rt / 1000) + "." +
+            std::to_string((rt % 1000) / 10) + " " + plssvm::nccl_version_string();
+    }
+    return v.c_str();
+}
+
+int plssvm_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// comm.cu -- NCCL plumbing for the row-sharded multi-GPU mode (one process per GPU).
+// Per CG iteration: all-gather of the p shards and sum all-reduces of the CG scalars
+// (north_star; the paper sums per-device vectors through the host).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <string>
+
+#include "common.cuh"
+#include "driver.h"
+
+namespace plssvm {
+
+struct CommHandle {
+    ncclComm_t nccl;
+    int rank, nranks, device;
+};
+
+#define PLS_NCCL(call)                                                                                \
+    do {                                                                                              \
+        ncclResult_t r_ = (call);                                                                     \
+        if (r_ != ncclSuccess) throw ::plssvm::Error(5, std::string(#call) + " -> " + ncclGetErrorString(r_)); \
+    } while (0)
+
+int comm_rank(const CommHandle *c) { return c->rank; }
+int comm_size(const CommHandle *c) { return c->nranks; }
+int comm_device(const CommHandle *c) { return c->device; }
+
+void comm_allreduce_sum_f64(CommHandle *c, double *buf, int64_t count, void *stream) {
+    PLS_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum, c->nccl,
+                           static_cast<cudaStream_t>(stream)));
+}
+
+// In-place all-gather: rank r's shard lives at buf + r * count_per_rank.
+void comm_allgather(CommHandle *c, void *buf, int64_t count_per_rank, int dtype, void *stream) {
+    const size_t es = dtype == PLSSVM_F32 ? 4 : 8;
+    char *b = static_cast<char *>(buf);
+    PLS_NCCL(ncclAllGather(b + static_cast<size_t>(c->rank) * count_per_rank * es, b,
+                           static_cast<size_t>(count_per_rank), dtype == PLSSVM_F32 ? ncclFloat : ncclDouble, c->nccl,
+                           static_cast<cudaStream_t>(stream)));
+}
+
+const char *nccl_version_string() {
+    static std::string v;
+    if (v.empty()) {
+        int code = 0;
+        ncclGetVersion(&code);
+        v = "NCCL " + std::to_string(code / 10000) + "." + std::to_string((code / 100) % 100) + "." +
+            std::to_string(code % 100);
+    }
+    return v.c_str();
+}
+
+}  // namespace plssvm
+
+using plssvm::CommHandle;
+
+extern "C" int plssvm_comm_unique_id_impl(void *id128) {
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return PLSSVM_E_NCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    memcpy(id128, &id, sizeof(id));
+    return PLSSVM_OK;
+}
+
+extern "C" int plssvm_comm_init_impl(const void *id128, int32_t nranks, int32_t rank, int32_t device, void **out) {
+    if (cudaSetDevice(device) != cudaSuccess) return PLSSVM_E_CUDA;
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    auto *h = new CommHandle{nullptr, rank, nranks, device};
+    ncclResult_t r = ncclCommInitRank(&h->nccl, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete h;
+        return PLSSVM_E_NCCL;
+    }
+    *out = h;
+    return PLSSVM_OK;
+}
+
+extern "C" int plssvm_comm_destroy_impl(void *c) {
+    auto *h = static_cast<CommHandle *>(c);
+    if (!h) return PLSSVM_OK;
+    ncclCommDestroy(h->nccl);
+    delete h;
+    return PLSSVM_OK;
+}

@@ -1,0 +1,624 @@
+// driver.cu -- host driver of the hot path: buffers, mode selection, the CG loop, bias.
+//
+// One call of train<T>() performs, on this process' GPU:
+//   a0 stage X to HBM + transform to the padded feature-major layout
+//   a1 q cache / norms / Q_mm                                    (Eq. 12)
+//   a2 rhs + CG init (x0 = 0: r = p = rhs)                        (Eq. 14)
+//   a3 Q~p  implicit tiles (Eq. 16)  or  a3'+a3'' cached precompute + streaming GEMV
+//   a4 fused CG updates, a5 convergence test on delta (Shewchuk)
+//   a6 bias + alpha (Eq. 15)
+//   a8 (row-sharded multi-GPU) NCCL all-gather of p, all-reduce of the CG scalars
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "driver.h"
+#include "kernels.cuh"
+
+namespace plssvm {
+
+namespace {
+
+// ---- stream-ordered device allocations, freed at scope exit -------------------------------
+struct Arena {
+    cudaStream_t s;
+    std::vector<void *> ptrs;
+    int64_t bytes = 0;
+    explicit Arena(cudaStream_t st) : s(st) {}
+    template <typename T>
+    T *alloc(int64_t n) {
+        void *p = nullptr;
+        const size_t sz = std::max<int64_t>(n, 1) * sizeof(T);
+        PLS_CUDA(cudaMallocAsync(&p, sz, s));
+        ptrs.push_back(p);
+        bytes += static_cast<int64_t>(sz);
+        return static_cast<T *>(p);
+    }
+    ~Arena() {
+        for (void *p : ptrs) cudaFreeAsync(p, s);
+    }
+};
+
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    bool owned = false;
+    explicit StreamGuard(void *user) {
+        if (user) {
+            s = static_cast<cudaStream_t>(user);
+        } else {
+            PLS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            owned = true;
+        }
+    }
+    ~StreamGuard() {
+        if (owned) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t make() {
+        cudaEvent_t e;
+        PLS_CUDA(cudaEventCreate(&e));
+        ev.push_back(e);
+        return e;
+    }
+    ~Events() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+double elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    PLS_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return 1e-3 * ms;
+}
+
+void setup_mempool(int dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+}
+
+template <typename T>
+const T *stage_input(Arena &A, const void *src, int64_t n, bool device_ptr, cudaStream_t s) {
+    if (device_ptr) return static_cast<const T *>(src);
+    T *d = A.alloc<T>(n);
+    PLS_CUDA(cudaMemcpyAsync(d, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d;
+}
+
+template <typename T>
+void launch_transform(const T *X, int64_t m, int64_t d, T *Xt, int64_t ld, int64_t dpad, cudaStream_t s,
+                      int64_t &launches) {
+    dim3 grid(static_cast<unsigned>(ceil_div(ld, 32)), static_cast<unsigned>(ceil_div(dpad, 32)));
+    k_transform<T><<<grid, dim3(32, 8), 0, s>>>(X, m, d, Xt, ld, dpad);
+    PLS_CHECK_LAUNCH();
+    ++launches;
+}
+
+// Row-band geometry of this rank: padded length mpad (multiple of 128 * P), tiles per rank.
+struct Geometry {
+    int64_t m1, mpad, dpad, nb, g0;
+    int T, band0, band1, P, rank;
+};
+
+template <typename T>
+Geometry geometry(int64_t m, int64_t d, int P, int rank) {
+    Geometry g;
+    g.m1 = m - 1;
+    g.P = P;
+    g.rank = rank;
+    g.mpad = round_up(m, static_cast<int64_t>(kTile) * P);
+    g.dpad = round_up(d, Tile<T>::BK);
+    g.T = static_cast<int>(g.mpad / kTile);
+    const int per = g.T / P;
+    g.band0 = rank * per;
+    g.band1 = g.band0 + per;
+    g.nb = static_cast<int64_t>(per) * kTile;
+    g.g0 = static_cast<int64_t>(g.band0) * kTile;
+    return g;
+}
+
+// Tiles of this rank: rows I of the band against every column block J; inside the band only
+// the upper triangle J >= I (mirrored), outside it the full row (row sums only).
+std::vector<int2> band_tiles(const Geometry &g) {
+    std::vector<int2> t;
+    for (int I = g.band0; I < g.band1; ++I)
+        for (int J = 0; J < g.T; ++J) {
+            const bool inband = (J >= g.band0 && J < g.band1);
+            if (!inband || J >= I) t.push_back(make_int2(I, J));
+        }
+    return t;
+}
+
+template <typename T>
+struct Ctx {
+    Geometry g;
+    KParams<T> kp;
+    T invC;
+    cudaStream_t s;
+    CommHandle *comm;
+    // device buffers
+    T *Xt, *q, *nrm, *ylab, *x, *r, *p, *y, *Ypart, *partials, *xfull, *Qc;
+    double *scal;
+    unsigned *counter;
+    int2 *tiles;
+    int ntiles;
+    bool cached;
+    int64_t launches = 0, launches_cg = 0;
+};
+
+template <typename T>
+void set_smem_attrs() {
+    const int bytes = static_cast<int>(Tile<T>::SMEM_BYTES);
+    PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<LINEAR, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<POLYNOMIAL, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PLS_CUDA(cudaFuncSetAttribute(k_precompute<LINEAR, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PLS_CUDA(cudaFuncSetAttribute(k_precompute<POLYNOMIAL, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PLS_CUDA(cudaFuncSetAttribute(k_precompute<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<LINEAR, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<POLYNOMIAL, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+// Q~ times the full vector `pfull` -> Ypart (slots) ; returns the number of slots to finalize.
+template <typename T>
+int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
+    const Geometry &g = c.g;
+    if (c.cached) {
+        const int64_t warps = ceil_div(g.nb, 4);
+        const int blocks = static_cast<int>(ceil_div(warps * 32, 256));
+        k_gemv_cached<T><<<blocks, 256, 0, c.s>>>(c.Qc, pfull, g.mpad, g.nb, c.Ypart);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        return 1;
+    }
+    const size_t sm = Tile<T>::SMEM_BYTES;
+    switch (c.kp.kernel) {
+        case LINEAR:
+            k_matvec_implicit<LINEAR, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, pfull,
+                                                                         c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
+                                                                         c.Ypart, g.nb);
+            break;
+        case POLYNOMIAL:
+            k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm,
+                                                                             pfull, c.kp, c.invC, c.scal, g.m1, g.band0,
+                                                                             g.band1, c.Ypart, g.nb);
+            break;
+        default:
+            k_matvec_implicit<RBF, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, pfull,
+                                                                      c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
+                                                                      c.Ypart, g.nb);
+    }
+    PLS_CHECK_LAUNCH();
+    ++c.launches;
+    return g.T;
+}
+
+template <typename T>
+void launch_precompute(Ctx<T> &c) {
+    const Geometry &g = c.g;
+    const size_t sm = Tile<T>::SMEM_BYTES;
+    switch (c.kp.kernel) {
+        case LINEAR:
+            k_precompute<LINEAR, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+                                                                    c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
+            break;
+        case POLYNOMIAL:
+            k_precompute<POLYNOMIAL, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+                                                                        c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
+            break;
+        default:
+            k_precompute<RBF, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+                                                                 c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
+    }
+    PLS_CHECK_LAUNCH();
+    ++c.launches;
+}
+
+template <typename T>
+void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par, int set_delta0) {
+    const Geometry &g = c.g;
+    k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, nslots, g.nb, g.g0, g.m1, pband, c.y, mode, c.ylab,
+                                                       c.r, pout, c.scal, par, set_delta0, c.partials, c.counter, 1);
+    PLS_CHECK_LAUNCH();
+    ++c.launches;
+}
+
+int dtype_of(float) { return PLSSVM_F32; }
+int dtype_of(double) { return PLSSVM_F64; }
+
+template <typename T>
+void allreduce(Ctx<T> &c, int slot, int count) {
+    if (c.comm) comm_allreduce_sum_f64(c.comm, c.scal + slot, count, c.s);
+}
+template <typename T>
+void allgather(Ctx<T> &c, T *full) {
+    if (c.comm) comm_allgather(c.comm, full, c.g.nb, dtype_of(T()), c.s);
+}
+
+// Common setup: geometry, buffers, H2D, transform, q.  Returns the context.
+template <typename T>
+void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bool need_labels, Events &E,
+           cudaEvent_t e_h2d, cudaEvent_t e_tr, cudaEvent_t e_q) {
+    int P = 1, rank = 0;
+    if (c.comm) {
+        P = comm_size(c.comm);
+        rank = comm_rank(c.comm);
+    }
+    c.g = geometry<T>(pb.m, pb.d, P, rank);
+    const Geometry &g = c.g;
+    c.kp = KParams<T>{pb.kernel, static_cast<T>(pb.gamma), pb.degree, static_cast<T>(pb.coef0)};
+    c.invC = static_cast<T>(1.0 / pb.C);
+    const bool dev = o.device_pointers != 0;
+    const T *Xs = stage_input<T>(A, pb.X, pb.m * pb.d, dev, c.s);
+    if (need_labels) {
+        c.ylab = const_cast<T *>(stage_input<T>(A, pb.y, pb.m, dev, c.s));
+    } else {
+        c.ylab = A.alloc<T>(pb.m);
+        PLS_CUDA(cudaMemsetAsync(c.ylab, 0, pb.m * sizeof(T), c.s));
+    }
+    PLS_CUDA(cudaEventRecord(e_h2d, c.s));
+    c.Xt = A.alloc<T>(g.dpad * g.mpad);
+    launch_transform<T>(Xs, pb.m, pb.d, c.Xt, g.mpad, g.dpad, c.s, c.launches);
+    PLS_CUDA(cudaEventRecord(e_tr, c.s));
+    c.q = A.alloc<T>(g.mpad);
+    c.nrm = A.alloc<T>(g.mpad);
+    c.scal = A.alloc<double>(S_COUNT);
+    PLS_CUDA(cudaMemsetAsync(c.scal, 0, S_COUNT * sizeof(double), c.s));
+    k_q_norms<T><<<static_cast<unsigned>(ceil_div(g.mpad, 256)), 256, 0, c.s>>>(c.Xt, g.mpad, pb.m, pb.d, c.kp, c.invC,
+                                                                                 c.ylab, c.q, c.nrm, c.scal);
+    PLS_CHECK_LAUNCH();
+    ++c.launches;
+    PLS_CUDA(cudaEventRecord(e_q, c.s));
+    c.partials = A.alloc<T>(kVecBlocks);
+    c.counter = A.alloc<unsigned>(1);
+    PLS_CUDA(cudaMemsetAsync(c.counter, 0, sizeof(unsigned), c.s));
+    std::vector<int2> tl = band_tiles(g);
+    c.ntiles = static_cast<int>(tl.size());
+    c.tiles = A.alloc<int2>(c.ntiles);
+    PLS_CUDA(cudaMemcpyAsync(c.tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
+    PLS_CUDA(cudaStreamSynchronize(c.s));  // tl goes out of scope
+    set_smem_attrs<T>();
+}
+
+// Mode selection (north_star: "mode picked by measurement"; SURVEY §8 decision 8): cached
+// whenever the Q~ band fits the budget -- the precompute costs about one implicit product and
+// every later product becomes an HBM stream (≈ 50-100x cheaper than a recompute).
+template <typename T>
+bool choose_cached(const Geometry &g, const plssvm_options_t &o) {
+    if (o.mode == PLSSVM_MODE_IMPLICIT) return false;
+    const int64_t need = g.nb * g.mpad * static_cast<int64_t>(sizeof(T));
+    size_t free_b = 0, total_b = 0;
+    PLS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    int64_t budget = o.cache_budget_bytes > 0 ? o.cache_budget_bytes : static_cast<int64_t>(0.9 * free_b);
+    budget = std::min<int64_t>(budget, static_cast<int64_t>(free_b) - (int64_t(1) << 28));
+    if (need <= budget) return true;
+    if (o.mode == PLSSVM_MODE_CACHED)
+        throw Error(PLSSVM_E_OOM, "cached mode: Q~ band of " + std::to_string(need) + " bytes does not fit (" +
+                                      std::to_string(budget) + " available)");
+    return false;
+}
+
+template <typename T>
+int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, void *b_out, plssvm_stats_t *st) {
+    PLS_CUDA(cudaSetDevice(o.device));
+    setup_mempool(o.device);
+    StreamGuard sg(o.stream);
+    Ctx<T> c{};
+    c.s = sg.s;
+    c.comm = static_cast<CommHandle *>(o.comm);
+    Arena A(c.s);
+    Events E;
+    cudaEvent_t e0 = E.make(), e_h2d = E.make(), e_tr = E.make(), e_q = E.make(), e_pre = E.make(), e_cg = E.make(),
+                e_end = E.make();
+    const auto wall0 = std::chrono::steady_clock::now();
+    PLS_CUDA(cudaEventRecord(e0, c.s));
+    setup<T>(c, A, pb, o, true, E, e_h2d, e_tr, e_q);
+    const Geometry &g = c.g;
+
+    c.x = A.alloc<T>(g.nb);
+    c.r = A.alloc<T>(g.nb);
+    c.y = A.alloc<T>(g.nb);
+    c.p = A.alloc<T>(g.mpad);
+    c.xfull = A.alloc<T>(g.mpad);
+    PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
+    T *pband = c.p + g.g0;
+
+    c.cached = choose_cached<T>(g, o);
+    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? 1 : g.T) * g.nb);
+    if (c.cached) {
+        c.Qc = A.alloc<T>(g.nb * g.mpad);
+        launch_precompute<T>(c);
+    }
+    PLS_CUDA(cudaEventRecord(e_pre, c.s));
+
+    // ---- CG init (a2) ----
+    const int64_t imax = o.max_iter > 0 ? o.max_iter : g.m1;
+    if (o.x0 == 0) {
+        k_init<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.ylab, g.nb, g.g0, g.m1, T(0), 1, c.scal,
+                                                       c.partials, c.counter, 1);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        allreduce(c, S_DELTA0, 2);
+    } else {
+        k_init<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.ylab, g.nb, g.g0, g.m1, T(1), 0, c.scal,
+                                                       c.partials, c.counter, 1);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        PLS_CUDA(cudaMemcpyAsync(c.xfull + g.g0, c.x, g.nb * sizeof(T), cudaMemcpyDeviceToDevice, c.s));
+        allgather(c, c.xfull);
+        const int ns = launch_qtilde_product<T>(c, c.xfull);
+        finalize<T>(c, ns, nullptr, 1, pband, 0, 1);  // r = rhs - Q~x0, p = r, delta0
+        allreduce(c, S_DELTA0, 2);
+    }
+    allgather(c, c.p);
+    int64_t matvecs = (o.x0 == 0) ? 0 : 1;
+
+    // host-visible scalars (pinned) for the convergence test (a5)
+    double *hs = nullptr;
+    PLS_CUDA(cudaMallocHost(&hs, S_COUNT * sizeof(double)));
+    struct HostFree {
+        double *p;
+        ~HostFree() { cudaFreeHost(p); }
+    } hf{hs};
+    PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    PLS_CUDA(cudaStreamSynchronize(c.s));
+    const double delta0 = hs[S_DELTA0];
+    double delta = hs[S_DELTA];
+    const double eps2 = pb.eps * pb.eps;
+    const int64_t launches_before_cg = c.launches;
+
+    cudaEvent_t mv0 = E.make(), mv1 = E.make();
+    double t_mv = 0.0, t_mv_min = 1e30;
+    int64_t it = 0;
+    int par = 0;
+    int status = PLSSVM_OK;
+    auto keep_going = [&]() {
+        if (it >= imax) return false;
+        if (o.fixed_iter > 0) return it < o.fixed_iter;
+        return delta > eps2 * delta0;
+    };
+    while (keep_going()) {
+        PLS_CUDA(cudaEventRecord(mv0, c.s));
+        const int ns = launch_qtilde_product<T>(c, c.p);
+        PLS_CUDA(cudaEventRecord(mv1, c.s));
+        ++matvecs;
+        finalize<T>(c, ns, pband, 0, nullptr, par, 0);
+        allreduce(c, S_PAP, 1);
+        k_update_xr<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.y, g.nb, c.scal, par, c.partials,
+                                                            c.counter);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        allreduce(c, S_DELTA + (par ^ 1), 1);
+        if (o.replace_every > 0 && it > 0 && it % o.replace_every == 0) {
+            // explicit residual r = rhs - Q~x (Shewchuk B2 replacement, option R > 0)
+            PLS_CUDA(cudaMemcpyAsync(c.xfull + g.g0, c.x, g.nb * sizeof(T), cudaMemcpyDeviceToDevice, c.s));
+            allgather(c, c.xfull);
+            const int ns2 = launch_qtilde_product<T>(c, c.xfull);
+            ++matvecs;
+            finalize<T>(c, ns2, nullptr, 1, nullptr, par ^ 1, 0);
+            allreduce(c, S_DELTA + (par ^ 1), 1);
+        }
+        k_update_p<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, par);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        allgather(c, c.p);
+        PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        PLS_CUDA(cudaStreamSynchronize(c.s));
+        const double tm = elapsed(mv0, mv1);
+        t_mv += tm;
+        t_mv_min = std::min(t_mv_min, tm);
+        ++it;
+        const double pap = hs[S_PAP];
+        delta = hs[S_DELTA + (par ^ 1)];
+        par ^= 1;
+        if (!(pap > 0.0) || !std::isfinite(pap) || !std::isfinite(delta)) {
+            status = PLSSVM_E_NUMERICAL;
+            break;
+        }
+    }
+    c.launches_cg = c.launches - launches_before_cg;
+    PLS_CUDA(cudaEventRecord(e_cg, c.s));
+    if (status == PLSSVM_OK && o.fixed_iter <= 0 && delta > eps2 * delta0) status = PLSSVM_W_NOT_CONVERGED;
+
+    if (status != PLSSVM_E_NUMERICAL) {
+        // ---- bias + alpha (a6) ----
+        k_bias_sums<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.q, g.nb, g.g0, c.scal, 0, c.partials, c.counter);
+        PLS_CHECK_LAUNCH();
+        k_bias_sums<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.q, g.nb, g.g0, c.scal, 1, c.partials, c.counter);
+        PLS_CHECK_LAUNCH();
+        c.launches += 2;
+        allreduce(c, S_SUMX, 2);
+        PLS_CUDA(cudaMemcpyAsync(c.xfull + g.g0, c.x, g.nb * sizeof(T), cudaMemcpyDeviceToDevice, c.s));
+        allgather(c, c.xfull);
+        const bool dev = o.device_pointers != 0;
+        T *alpha_d = dev ? static_cast<T *>(alpha_out) : A.alloc<T>(pb.m);
+        T *b_d = dev ? static_cast<T *>(b_out) : A.alloc<T>(1);
+        k_assemble<T><<<static_cast<unsigned>(ceil_div(pb.m, 256)), 256, 0, c.s>>>(c.xfull, pb.m, c.scal, alpha_d, b_d);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        if (!dev) {
+            PLS_CUDA(cudaMemcpyAsync(alpha_out, alpha_d, pb.m * sizeof(T), cudaMemcpyDeviceToHost, c.s));
+            PLS_CUDA(cudaMemcpyAsync(b_out, b_d, sizeof(T), cudaMemcpyDeviceToHost, c.s));
+        }
+    }
+    PLS_CUDA(cudaEventRecord(e_end, c.s));
+    PLS_CUDA(cudaStreamSynchronize(c.s));
+    if (st) {
+        st->iterations = it;
+        st->matvecs = matvecs;
+        st->rel_residual = delta0 > 0 ? std::sqrt(delta / delta0) : 0.0;
+        st->mode_used = c.cached ? PLSSVM_MODE_CACHED : PLSSVM_MODE_IMPLICIT;
+        st->num_ranks = g.P;
+        st->t_h2d = elapsed(e0, e_h2d);
+        st->t_transform = elapsed(e_h2d, e_tr);
+        st->t_q = elapsed(e_tr, e_q);
+        st->t_precompute = elapsed(e_q, e_pre);
+        st->t_cg = elapsed(e_pre, e_cg);
+        st->t_bias_d2h = elapsed(e_cg, e_end);
+        st->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+        st->t_matvec = t_mv;
+        st->t_matvec_min = it > 0 ? t_mv_min : 0.0;
+        st->bytes_per_gpu = A.bytes;
+        st->gpu_launches = c.launches;
+        st->launches_in_cg = c.launches_cg;
+    }
+    return status;
+}
+
+template <typename T>
+int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, const plssvm_options_t &o, void *out,
+                       double *t_kernel) {
+    PLS_CUDA(cudaSetDevice(o.device));
+    setup_mempool(o.device);
+    StreamGuard sg(o.stream);
+    Ctx<T> c{};
+    c.s = sg.s;
+    c.comm = static_cast<CommHandle *>(o.comm);
+    Arena A(c.s);
+    Events E;
+    cudaEvent_t e0 = E.make(), e1 = E.make(), e2 = E.make(), e3 = E.make();
+    setup<T>(c, A, pb, o, false, E, e0, e1, e2);
+    const Geometry &g = c.g;
+    c.y = A.alloc<T>(g.nb);
+    c.p = A.alloc<T>(g.mpad);
+    PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
+    const bool dev = o.device_pointers != 0;
+    PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
+    c.cached = (o.mode == PLSSVM_MODE_CACHED) || (o.mode == PLSSVM_MODE_AUTO && choose_cached<T>(g, o));
+    if (c.cached) (void)choose_cached<T>(g, o);  // throws E_OOM if CACHED does not fit
+    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? 1 : g.T) * g.nb);
+    double t_pre = 0.0;
+    if (c.cached) {
+        c.Qc = A.alloc<T>(g.nb * g.mpad);
+        PLS_CUDA(cudaEventRecord(e0, c.s));
+        launch_precompute<T>(c);
+        PLS_CUDA(cudaEventRecord(e1, c.s));
+        PLS_CUDA(cudaStreamSynchronize(c.s));
+        t_pre = elapsed(e0, e1);
+    }
+    double tsum = 0.0, tmin = 1e30;
+    int ns = 1;
+    for (int rep = 0; rep < std::max(1, repeats); ++rep) {
+        PLS_CUDA(cudaEventRecord(e2, c.s));
+        ns = launch_qtilde_product<T>(c, c.p);
+        PLS_CUDA(cudaEventRecord(e3, c.s));
+        PLS_CUDA(cudaEventSynchronize(e3));
+        const double t = elapsed(e2, e3);
+        tsum += t;
+        tmin = std::min(tmin, t);
+    }
+    finalize<T>(c, ns, c.p + g.g0, 0, nullptr, 0, 0);
+    // gather the band results into the full vector (reuse p as the gather buffer)
+    T *yfull = A.alloc<T>(g.mpad);
+    PLS_CUDA(cudaMemcpyAsync(yfull + g.g0, c.y, g.nb * sizeof(T), cudaMemcpyDeviceToDevice, c.s));
+    allgather(c, yfull);
+    PLS_CUDA(cudaMemcpyAsync(out, yfull, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c.s));
+    PLS_CUDA(cudaStreamSynchronize(c.s));
+    if (t_kernel) {
+        t_kernel[0] = tsum / std::max(1, repeats);
+        t_kernel[1] = tmin;
+        t_kernel[2] = t_pre;
+    }
+    return PLSSVM_OK;
+}
+
+template <typename T>
+int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *Zin, int64_t n, const plssvm_options_t &o,
+                 void *decision, int32_t *labels, double *t_kernel) {
+    PLS_CUDA(cudaSetDevice(o.device));
+    setup_mempool(o.device);
+    StreamGuard sg(o.stream);
+    cudaStream_t s = sg.s;
+    Arena A(s);
+    Events E;
+    cudaEvent_t e0 = E.make(), e1 = E.make();
+    int64_t launches = 0;
+    const bool dev = o.device_pointers != 0;
+    const int64_t m = pb.m, d = pb.d;
+    const int64_t mpad = round_up(m, kTile), npad = round_up(n, kTile);
+    const int64_t L = std::max(mpad, npad);
+    const int64_t dpad = round_up(d, Tile<T>::BK);
+    const T *Xs = stage_input<T>(A, pb.X, m * d, dev, s);
+    const T *Zs = stage_input<T>(A, Zin, n * d, dev, s);
+    T *Xt = A.alloc<T>(dpad * L), *Zt = A.alloc<T>(dpad * L);
+    launch_transform<T>(Xs, m, d, Xt, L, dpad, s, launches);
+    launch_transform<T>(Zs, n, d, Zt, L, dpad, s, launches);
+    T *alpha = A.alloc<T>(L);
+    PLS_CUDA(cudaMemsetAsync(alpha, 0, L * sizeof(T), s));
+    PLS_CUDA(cudaMemcpyAsync(alpha, alpha_in, m * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    T *nx = A.alloc<T>(L), *nz = A.alloc<T>(L);
+    KParams<T> kp{pb.kernel, static_cast<T>(pb.gamma), pb.degree, static_cast<T>(pb.coef0)};
+    if (pb.kernel == RBF) {
+        k_norms<T><<<static_cast<unsigned>(ceil_div(L, 256)), 256, 0, s>>>(Xt, L, L, d, nx);
+        k_norms<T><<<static_cast<unsigned>(ceil_div(L, 256)), 256, 0, s>>>(Zt, L, L, d, nz);
+        PLS_CHECK_LAUNCH();
+        launches += 2;
+    }
+    const int tilesI = static_cast<int>(npad / kTile), tilesJ = static_cast<int>(mpad / kTile);
+    T *Fpart = A.alloc<T>(static_cast<int64_t>(tilesJ) * npad);
+    set_smem_attrs<T>();
+    const size_t sm = Tile<T>::SMEM_BYTES;
+    const int grid = tilesI * tilesJ;
+    PLS_CUDA(cudaEventRecord(e0, s));
+    switch (pb.kernel) {
+        case LINEAR:
+            k_predict_tiles<LINEAR, T><<<grid, kThreads, sm, s>>>(Zt, npad, Xt, L, dpad, nz, nx, alpha, kp, tilesI, Fpart);
+            break;
+        case POLYNOMIAL:
+            k_predict_tiles<POLYNOMIAL, T><<<grid, kThreads, sm, s>>>(Zt, npad, Xt, L, dpad, nz, nx, alpha, kp, tilesI,
+                                                                      Fpart);
+            break;
+        default:
+            k_predict_tiles<RBF, T><<<grid, kThreads, sm, s>>>(Zt, npad, Xt, L, dpad, nz, nx, alpha, kp, tilesI, Fpart);
+    }
+    PLS_CHECK_LAUNCH();
+    PLS_CUDA(cudaEventRecord(e1, s));
+    ++launches;
+    T *f_d = (dev && decision) ? static_cast<T *>(decision) : A.alloc<T>(n);
+    int32_t *l_d = (dev && labels) ? labels : A.alloc<int32_t>(n);
+    k_predict_finalize<T><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, s>>>(Fpart, tilesJ, npad, n, static_cast<T>(b),
+                                                                                 f_d, l_d);
+    PLS_CHECK_LAUNCH();
+    ++launches;
+    if (!dev) {
+        if (decision) PLS_CUDA(cudaMemcpyAsync(decision, f_d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+        if (labels) PLS_CUDA(cudaMemcpyAsync(labels, l_d, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    }
+    PLS_CUDA(cudaStreamSynchronize(s));
+    if (t_kernel) {
+        t_kernel[0] = elapsed(e0, e1);
+        t_kernel[1] = static_cast<double>(launches);
+    }
+    return PLSSVM_OK;
+}
+
+}  // namespace
+
+int train(const Problem &pb, const plssvm_options_t &o, void *alpha, void *b, plssvm_stats_t *st) {
+    return pb.dtype == PLSSVM_F32 ? train_impl<float>(pb, o, alpha, b, st) : train_impl<double>(pb, o, alpha, b, st);
+}
+int predict(const Problem &pb, const void *alpha, double b, const void *Z, int64_t n, const plssvm_options_t &o,
+            void *decision, int32_t *labels, double *t_kernel) {
+    return pb.dtype == PLSSVM_F32 ? predict_impl<float>(pb, alpha, b, Z, n, o, decision, labels, t_kernel)
+                                  : predict_impl<double>(pb, alpha, b, Z, n, o, decision, labels, t_kernel);
+}
+int qtilde_matvec(const Problem &pb, const void *p, int32_t repeats, const plssvm_options_t &o, void *out,
+                  double *t_kernel) {
+    return pb.dtype == PLSSVM_F32 ? qtilde_matvec_impl<float>(pb, p, repeats, o, out, t_kernel)
+                                  : qtilde_matvec_impl<double>(pb, p, repeats, o, out, t_kernel);
+}
+
+}  // namespace plssvm

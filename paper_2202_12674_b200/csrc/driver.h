@@ -1,0 +1,38 @@
+// driver.h -- internal (C++) interface between the C ABI (capi.cu) and the device driver.
+#pragma once
+#include <cstdint>
+#include "../../include/plssvm.h"
+
+namespace plssvm {
+
+struct Problem {
+    const void *X;
+    const void *y;
+    int64_t m, d;
+    int dtype;
+    int kernel;
+    double gamma;
+    int degree;
+    double coef0;
+    double C;
+    double eps;
+};
+
+struct CommHandle;  // comm.cu
+
+// Each returns a plssvm_status_t and throws plssvm::Error for CUDA / NCCL failures.
+int train(const Problem &pb, const plssvm_options_t &o, void *alpha, void *b, plssvm_stats_t *st);
+int predict(const Problem &pb, const void *alpha, double b, const void *Z, int64_t n, const plssvm_options_t &o,
+            void *decision, int32_t *labels, double *t_kernel);
+int qtilde_matvec(const Problem &pb, const void *p, int32_t repeats, const plssvm_options_t &o, void *out,
+                  double *t_kernel);
+
+// comm.cu
+int comm_rank(const CommHandle *c);
+int comm_size(const CommHandle *c);
+int comm_device(const CommHandle *c);
+void comm_allreduce_sum_f64(CommHandle *c, double *buf, int64_t count, void *stream);
+void comm_allgather(CommHandle *c, void *buf, int64_t count_per_rank, int dtype, void *stream);
+const char *nccl_version_string();
+
+}  // namespace plssvm

@@ -1,0 +1,488 @@
+// kernels.cuh -- every device kernel of the hot path (sm_100a).
+//
+//   k_transform        row-major X -> padded feature-major X^T            (paper "transform")
+//   k_q_norms          q_i = k(x_i, x_m), n_i = ||x_i||^2, Q_mm          (Eq. 12)
+//   k_matvec_implicit  Ypart[slot][row] = partial Q~p per tile            (Eq. 16)
+//   k_precompute       Q~ band tiles -> HBM (cached mode, north_star N1)
+//   k_gemv_cached      y_band = Q~_band p streamed from HBM
+//   k_finalize         y = sum_slots Ypart ; p.y  (deterministic)
+//   k_update_xr        x += a p ; r -= a y ; r.r  (fused axpy + norm)
+//   k_update_p         p = r + b p
+//   k_init / k_bias    CG start, Eq. 15 bias + alpha assembly
+//   k_predict          f(z) = sum_i alpha_i k(x_i, z) + b                (Eq. 10)
+#pragma once
+#include "tile_engine.cuh"
+
+namespace plssvm {
+
+// Slots of the device scalar block (double precision storage for every dtype's scalars).
+enum Scal : int {
+    S_QMM = 0,      // Q_mm = k(x_m,x_m) + 1/C
+    S_YM = 1,       // y_m
+    S_PAP = 2,      // p . Q~p   (this iteration)
+    S_DELTA0 = 3,   // delta_0 = r0.r0
+    S_DELTA = 4,    // delta_k at S_DELTA + (k & 1)   (double-buffered by iteration parity)
+    S_ALPHA = 6,    // CG alpha of the last update
+    S_SUMX = 7,     // sum of x (bias)
+    S_QX = 8,       // <q, x>  (bias)
+    S_B = 9,        // bias b
+    S_COUNT = 16
+};
+
+// ---------------------------------------------------------------------------------------
+// Deterministic grid reduction: every block writes its partial; the last block to finish
+// sums the partials in block order and calls fin(total).
+template <typename T, typename F>
+__device__ __forceinline__ void grid_reduce(T v, T *partials, unsigned *counter, F fin) {
+    __shared__ T red[kVecThreads / 32];
+    __shared__ bool last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T s = T(0);
+        for (int w = 0; w < kVecThreads / 32; ++w) s += red[w];
+        partials[blockIdx.x] = s;
+        __threadfence();
+        unsigned done = atomicAdd(counter, 1u);
+        last = (done == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x < 32) {
+        __threadfence();
+        T s = T(0);
+        // lane-strided partial sums, then a fixed shuffle tree: deterministic order
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += ((volatile T *)partials)[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) {
+            fin(s);
+            *counter = 0u;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Layout transform: X[m][d] (point-major, host order) -> Xt[dpad][mpad] feature-major with
+// zero padding.  32x32 smem transpose, grid covers the padded extent.
+template <typename T>
+__global__ void k_transform(const T *__restrict__ X, int64_t m, int64_t d, T *__restrict__ Xt, int64_t mpad,
+                            int64_t dpad) {
+    __shared__ T t[32][33];
+    const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32, f0 = static_cast<int64_t>(blockIdx.y) * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        int64_t p = p0 + r, f = f0 + threadIdx.x;
+        t[r][threadIdx.x] = (p < m && f < d) ? X[p * d + f] : T(0);
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        int64_t f = f0 + r, p = p0 + threadIdx.x;
+        if (f < dpad && p < mpad) Xt[f * mpad + p] = t[threadIdx.x][r];
+    }
+}
+
+// q cache and norms: q_i = k(x_i, x_m) for i < m-1 (0 beyond), n_i = ||x_i||^2,
+// S_QMM = k(x_m, x_m) + 1/C, S_YM = y_m.  RBF q uses the direct squared distance.
+template <typename T>
+__global__ void k_q_norms(const T *__restrict__ Xt, int64_t mpad, int64_t m, int64_t d, KParams<T> kp, T invC,
+                          const T *__restrict__ y, T *__restrict__ q, T *__restrict__ nrm, double *scal) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= mpad) return;
+    const int64_t xm = m - 1;
+    T s = T(0), n = T(0), dist = T(0);
+    for (int64_t k = 0; k < d; ++k) {
+        const T a = Xt[k * mpad + i], b = Xt[k * mpad + xm];
+        s = fma(a, b, s);
+        n = fma(a, a, n);
+        const T t = a - b;
+        dist = fma(t, t, dist);
+    }
+    T kv;
+    if (kp.kernel == LINEAR) {
+        kv = s;
+    } else if (kp.kernel == POLYNOMIAL) {
+        const T base = kp.gamma * s + kp.coef0;
+        kv = T(1);
+        for (int t = 0; t < kp.degree; ++t) kv *= base;
+    } else {
+        if constexpr (sizeof(T) == 4) kv = expf(-kp.gamma * dist);
+        else kv = exp(-kp.gamma * dist);
+    }
+    nrm[i] = n;
+    q[i] = (i < xm) ? kv : T(0);
+    if (i == xm) {
+        scal[S_QMM] = static_cast<double>(kv + invC);
+        scal[S_YM] = static_cast<double>(y[xm]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Shared epilogue: Q~ entry from the contracted value (Eq. 16 with cached q):
+//   Q~_ij = k(x_i,x_j) + delta_ij/C - q_j - q_i + Q_mm  ;  0 outside the (m-1)-system.
+template <int KT, typename T>
+__device__ __forceinline__ T qtilde_value(T s, int64_t gi, int64_t gj, T ni, T nj, T qi, T qj, T Qmm, T invC,
+                                          int64_t m1, const KParams<T> &kp) {
+    const bool diag = (gi == gj);
+    T v = kernel_value<KT, T>(s, ni, nj, diag, kp);
+    v = v + (diag ? invC : T(0)) - qj - qi + Qmm;
+    return (gi < m1 && gj < m1) ? v : T(0);
+}
+
+// Implicit Q~p over a list of 128x128 tiles (I, J).  Tiles with I < J inside this rank's row
+// band [band0, band1) are used twice (mirroring): their row sums go to rows of I
+// and their column sums (Q~_IJ^T p_I) to rows of J.  Every (slot, row-block) pair of the
+// partial buffer Ypart[T][band_rows] is written exactly once per call, so the finalize sum
+// is deterministic.
+template <int KT, typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_matvec_implicit(const T *__restrict__ Xt, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
+                      const T *__restrict__ q, const T *__restrict__ nrm, const T *__restrict__ p, KParams<T> kp,
+                      T invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
+                      T *__restrict__ Ypart, int64_t band_rows) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *smem = reinterpret_cast<T *>(smem_raw);
+    const int2 tile = tiles[blockIdx.x];
+    const int I = tile.x, J = tile.y;
+    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
+    T acc[8][8];
+    contract_tile<T>(Xt + row0, Xt + col0, mpad, dpad, smem, acc);
+
+    const int ry = thread_ry(), rx = thread_rx();
+    const T Qmm = static_cast<T>(scal[S_QMM]);
+    T qi[8], ni[8], pi[8], qj[8], nj[8], pj[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int64_t gi = row0 + micro_index<T>(ry, e), gj = col0 + micro_index<T>(rx, e);
+        qi[e] = q[gi]; pi[e] = p[gi]; ni[e] = (KT == RBF) ? nrm[gi] : T(0);
+        qj[e] = q[gj]; pj[e] = p[gj]; nj[e] = (KT == RBF) ? nrm[gj] : T(0);
+    }
+    T rs[8], cs[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) rs[e] = cs[e] = T(0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t gi = row0 + micro_index<T>(ry, i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t gj = col0 + micro_index<T>(rx, j);
+            const T v = qtilde_value<KT, T>(acc[i][j], gi, gj, ni[i], nj[j], qi[i], qj[j], Qmm, invC, m1, kp);
+            rs[i] = fma(v, pj[j], rs[i]);
+            cs[j] = fma(v, pi[i], cs[j]);
+        }
+    }
+    // row sums: reduce over the 8 rx lanes of the warp, then over the 2 warps sharing ry
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 1);
+        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 2);
+        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 4);
+        cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 8);
+        cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 16);
+    }
+    T *redr = smem;               // [2][128]
+    T *redc = smem + 2 * kTile;   // [4][128]
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if ((lane & 7) == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) redr[(w & 1) * kTile + micro_index<T>(ry, e)] = rs[e];
+    }
+    if (lane < 8) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) redc[(w >> 1) * kTile + micro_index<T>(rx, e)] = cs[e];
+    }
+    __syncthreads();
+    const bool mirrored = (I != J) && (J >= band0) && (J < band1);
+    const int64_t lrow0 = row0 - static_cast<int64_t>(band0) * kTile;
+    if (threadIdx.x < kTile) {
+        const int t = threadIdx.x;
+        Ypart[static_cast<int64_t>(J) * band_rows + lrow0 + t] = redr[t] + redr[kTile + t];
+    } else if (mirrored) {
+        const int t = threadIdx.x - kTile;
+        const int64_t lcol0 = col0 - static_cast<int64_t>(band0) * kTile;
+        Ypart[static_cast<int64_t>(I) * band_rows + lcol0 + t] =
+            (redc[t] + redc[kTile + t]) + (redc[2 * kTile + t] + redc[3 * kTile + t]);
+    }
+}
+
+// Cached mode, one-time precompute: full rows [band0*128, band1*128) of Q~ (both triangles)
+// into Qc[local_row][mpad] from the same tiles (upper tiles mirrored as transposed stores).
+template <int KT, typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_precompute(const T *__restrict__ Xt, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
+                 const T *__restrict__ q, const T *__restrict__ nrm, KParams<T> kp, T invC,
+                 const double *__restrict__ scal, int64_t m1, int band0, int band1, T *__restrict__ Qc) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *smem = reinterpret_cast<T *>(smem_raw);
+    const int2 tile = tiles[blockIdx.x];
+    const int I = tile.x, J = tile.y;
+    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
+    T acc[8][8];
+    contract_tile<T>(Xt + row0, Xt + col0, mpad, dpad, smem, acc);
+    const int ry = thread_ry(), rx = thread_rx();
+    const T Qmm = static_cast<T>(scal[S_QMM]);
+    const bool mirrored = (I != J) && (J >= band0) && (J < band1);
+    const int64_t b0 = static_cast<int64_t>(band0) * kTile;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t gi = row0 + micro_index<T>(ry, i);
+        const T qi = q[gi], ni = (KT == RBF) ? nrm[gi] : T(0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t gj = col0 + micro_index<T>(rx, j);
+            const T qj = q[gj], nj = (KT == RBF) ? nrm[gj] : T(0);
+            const T v = qtilde_value<KT, T>(acc[i][j], gi, gj, ni, nj, qi, qj, Qmm, invC, m1, kp);
+            Qc[(gi - b0) * mpad + gj] = v;
+            if (mirrored) Qc[(gj - b0) * mpad + gi] = v;
+        }
+    }
+}
+
+// Cached mode: y[r] = sum_j Qc[r][j] p[j] for the band's rows.  One warp per 4 rows, 16-byte
+// streaming loads (L1 no-allocate), p re-used across the 4 rows from L1/L2.  HBM-bound.
+template <typename T>
+__global__ void __launch_bounds__(256) k_gemv_cached(const T *__restrict__ Qc, const T *__restrict__ p, int64_t mpad,
+                                                     int64_t rows, T *__restrict__ Ypart) {
+    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    constexpr int VEC = 16 / sizeof(T);
+    constexpr int R = 4;
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = warp * R;
+    if (r0 >= rows) return;
+    T acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = T(0);
+    const int64_t nv = mpad / VEC;
+    const V *pv = reinterpret_cast<const V *>(p);
+    for (int64_t c = lane; c < nv; c += 32) {
+        const V pp = pv[c];
+        const T *pe = reinterpret_cast<const T *>(&pp);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            V a;
+            const V *src = reinterpret_cast<const V *>(Qc + (r0 + r) * mpad) + c;
+            if constexpr (sizeof(T) == 8) {
+                asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                             : "=d"(a.x), "=d"(a.y) : "l"(src));
+            } else {
+                asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(src));
+            }
+            const T *ae = reinterpret_cast<const T *>(&a);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[r] = fma(ae[v], pe[v], acc[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) Ypart[r0 + r] = acc[r];
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// CG vector kernels on this rank's band (local length nb, rows with global index >= m1 are
+// padding and stay 0).  Scalars live in `scal` (double) so no host round trip is needed.
+
+// y_i = sum_s Ypart[s][i] (fixed slot order), then pAp = p . y  (mode 0), or for the initial
+// / replaced residual (mode 1): r_i = rhs_i - y_i, r.r -> S_DELTA+par (and S_DELTA0 if init).
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_finalize(const T *__restrict__ Ypart, int nslots, int64_t nb, int64_t g0, int64_t m1,
+               const T *__restrict__ pband, T *__restrict__ y, int mode, const T *__restrict__ yl, T *__restrict__ r,
+               T *__restrict__ pout, double *scal, int par, int set_delta0, T *partials, unsigned *counter,
+               int write_scalar) {
+    T part = T(0);
+    const double ym = scal[S_YM];
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        T s = T(0);
+        for (int k = 0; k < nslots; ++k) s += Ypart[static_cast<int64_t>(k) * nb + i];
+        const bool valid = (g0 + i) < m1;
+        s = valid ? s : T(0);
+        if (mode == 0) {
+            y[i] = s;
+            part = fma(pband[i], s, part);
+        } else {
+            // rhs_i = y_i - y_m (Eq. 14)
+            const T rhs = valid ? static_cast<T>(static_cast<double>(yl[g0 + i]) - ym) : T(0);
+            const T ri = valid ? rhs - s : T(0);
+            r[i] = ri;
+            if (pout) pout[i] = ri;
+            part = fma(ri, ri, part);
+        }
+    }
+    grid_reduce<T>(part, partials, counter, [&](T tot) {
+        if (!write_scalar) return;
+        if (mode == 0) {
+            scal[S_PAP] = static_cast<double>(tot);
+        } else {
+            scal[S_DELTA + par] = static_cast<double>(tot);
+            if (set_delta0) scal[S_DELTA0] = static_cast<double>(tot);
+        }
+    });
+}
+
+// Local partial of a scalar only (multi-rank: the partial is all-reduced by NCCL before use).
+// x += a p ; r -= a y ; delta_new = r.r   with a = delta_k / pAp  (Shewchuk)
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_update_xr(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p, const T *__restrict__ y, int64_t nb,
+                double *scal, int par, T *partials, unsigned *counter) {
+    const T a = static_cast<T>(scal[S_DELTA + par] / scal[S_PAP]);
+    T part = T(0);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        x[i] = fma(a, p[i], x[i]);
+        const T ri = fma(-a, y[i], r[i]);
+        r[i] = ri;
+        part = fma(ri, ri, part);
+    }
+    grid_reduce<T>(part, partials, counter, [&](T tot) {
+        scal[S_DELTA + (par ^ 1)] = static_cast<double>(tot);
+        scal[S_ALPHA] = static_cast<double>(a);
+    });
+}
+
+// p = r + b p  with b = delta_{k+1} / delta_k
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_update_p(T *__restrict__ p, const T *__restrict__ r, int64_t nb, const double *scal, int par) {
+    const T b = static_cast<T>(scal[S_DELTA + (par ^ 1)] / scal[S_DELTA + par]);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = fma(b, p[i], r[i]);
+}
+
+// x = x0 (0 or 1 on valid rows), and, for x0 = 0, r = p = rhs, delta0 = r.r.
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_init(T *__restrict__ x, T *__restrict__ r, T *__restrict__ p, const T *__restrict__ yl, int64_t nb, int64_t g0,
+           int64_t m1, T x0, int zero_start, double *scal, T *partials, unsigned *counter, int write_scalar) {
+    const double ym = scal[S_YM];
+    T part = T(0);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const bool valid = (g0 + i) < m1;
+        x[i] = valid ? x0 : T(0);
+        if (zero_start) {
+            const T rhs = valid ? static_cast<T>(static_cast<double>(yl[g0 + i]) - ym) : T(0);
+            r[i] = rhs;
+            p[i] = rhs;
+            part = fma(rhs, rhs, part);
+        }
+    }
+    if (zero_start)
+        grid_reduce<T>(part, partials, counter, [&](T tot) {
+            if (write_scalar) {
+                scal[S_DELTA + 0] = static_cast<double>(tot);
+                scal[S_DELTA0] = static_cast<double>(tot);
+            }
+        });
+}
+
+// Bias (Eq. 15): partial sums sum(x) and <q, x> over the band (two grid reductions).
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_bias_sums(const T *__restrict__ x, const T *__restrict__ q, int64_t nb, int64_t g0, double *scal, int which,
+                T *partials, unsigned *counter) {
+    T part = T(0);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        part = (which == 0) ? part + x[i] : fma(q[g0 + i], x[i], part);
+    grid_reduce<T>(part, partials, counter, [&](T tot) { scal[which == 0 ? S_SUMX : S_QX] = static_cast<double>(tot); });
+}
+
+// b = y_m + Q_mm sum(x) - <q,x> (Eq. 15); alpha = (x_0..x_{m-2}, -sum x).
+template <typename T>
+__global__ void k_assemble(const T *__restrict__ xfull, int64_t m, double *scal, T *__restrict__ alpha, T *__restrict__ bout) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const T sx = static_cast<T>(scal[S_SUMX]);
+    if (i < m - 1) alpha[i] = xfull[i];
+    if (i == m - 1) {
+        alpha[i] = -sx;
+        const T b = static_cast<T>(scal[S_YM]) + static_cast<T>(scal[S_QMM]) * sx - static_cast<T>(scal[S_QX]);
+        *bout = b;
+        scal[S_B] = static_cast<double>(b);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Predict (Eq. 10): tiles (I over test points Zt, J over training points Xt); the epilogue
+// forms alpha_j k(z_i, x_j) and row-reduces into Fpart[J][i] (deterministic slots).
+template <int KT, typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_predict_tiles(const T *__restrict__ Zt, int64_t npad, const T *__restrict__ Xt, int64_t mpad, int64_t dpad,
+                    const T *__restrict__ nz, const T *__restrict__ nx, const T *__restrict__ alpha, KParams<T> kp,
+                    int tilesI, T *__restrict__ Fpart) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *smem = reinterpret_cast<T *>(smem_raw);
+    const int I = blockIdx.x % tilesI, J = blockIdx.x / tilesI;
+    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
+    T acc[8][8];
+    // The engine reads both operands with one leading dimension: the driver stores Zt and Xt
+    // with ld = max(npad, mpad), passed here as `mpad` (see predict_impl).
+    contract_tile<T>(Zt + row0, Xt + col0, mpad, dpad, smem, acc);
+    const int ry = thread_ry(), rx = thread_rx();
+    T rs[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t gi = row0 + micro_index<T>(ry, i);
+        const T ni = (KT == RBF) ? nz[gi] : T(0);
+        T s = T(0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t gj = col0 + micro_index<T>(rx, j);
+            const T nj = (KT == RBF) ? nx[gj] : T(0);
+            const T kv = kernel_value<KT, T>(acc[i][j], ni, nj, false, kp);
+            s = fma(alpha[gj], kv, s);
+        }
+        rs[i] = s;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 1);
+        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 2);
+        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 4);
+    }
+    T *redr = smem;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if ((lane & 7) == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) redr[(w & 1) * kTile + micro_index<T>(ry, e)] = rs[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < kTile) Fpart[static_cast<int64_t>(J) * npad + row0 + threadIdx.x] = redr[threadIdx.x] + redr[kTile + threadIdx.x];
+}
+
+template <typename T>
+__global__ void k_norms(const T *__restrict__ Xt, int64_t ld, int64_t n, int64_t d, T *__restrict__ nrm) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T s = T(0);
+    for (int64_t k = 0; k < d; ++k) {
+        const T a = Xt[k * ld + i];
+        s = fma(a, a, s);
+    }
+    nrm[i] = s;
+}
+
+// f_i = sum_J Fpart[J][i] + b ; label = f >= 0 ? +1 : -1
+template <typename T>
+__global__ void k_predict_finalize(const T *__restrict__ Fpart, int nslots, int64_t npad, int64_t n, T b,
+                                   T *__restrict__ f, int32_t *__restrict__ labels) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T s = T(0);
+    for (int k = 0; k < nslots; ++k) s += Fpart[static_cast<int64_t>(k) * npad + i];
+    const T v = s + b;
+    if (f) f[i] = v;
+    if (labels) labels[i] = (v >= T(0)) ? 1 : -1;
+}
+
+}  // namespace plssvm

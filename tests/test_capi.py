@@ -1,0 +1,126 @@
+"""CPU-side checks of the C-ABI library: it loads, exports exactly what include/plssvm.h
+declares, validates its arguments, implements the host partition rule, and refuses to
+compute without a GPU (no CPU fallback)."""
+import ctypes as ct
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2202_12674_b200 as pl
+from paper_2202_12674_b200 import binding
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "plssvm.h")).read()
+    return sorted(set(re.findall(r"PLSSVM_API\s+[\w\s\*]*?\b(plssvm_\w+)\s*\(", src)))
+
+
+def exported_symbols():
+    import subprocess
+
+    out = subprocess.check_output(["nm", "-D", "--defined-only", binding.lib_path()], text=True)
+    return sorted({ln.split()[-1] for ln in out.splitlines() if ln.split()[-1].startswith("plssvm_")})
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    L = pl.load()
+    decl = declared_symbols()
+    assert len(decl) == 15
+    for name in decl:
+        assert hasattr(L, name), name
+    assert exported_symbols() == decl  # nothing else is public
+    assert sorted(binding.EXPORTS) == decl
+
+
+def test_version_and_device_count():
+    v = pl.plssvm_version()
+    assert "sm_100a" in v and "NCCL 2." in v
+    assert pl.plssvm_device_count() >= 0
+
+
+def test_default_options():
+    o = pl.options()
+    assert (o.mode, o.x0, o.max_iter, o.replace_every, o.fixed_iter, o.device, o.device_pointers) == (0, 0, 0, 0, 0, 0, 0)
+    assert o.stream is None and o.comm is None
+
+
+@pytest.mark.parametrize("m,P", [(2, 1), (256, 1), (16384, 1), (16384, 8), (1000, 3), (65536, 8), (131072, 8)])
+def test_partition_rule(m, P):
+    bands = [pl.plssvm_partition(m, P, r) for r in range(P)]
+    mpad = bands[0][2]
+    assert mpad % (128 * P) == 0 and mpad >= m and mpad - m < 128 * P
+    assert bands[0][0] == 0 and bands[-1][1] == mpad
+    for (b0, e0, _), (b1, e1, _) in zip(bands, bands[1:]):
+        assert e0 == b1
+    sizes = {e - b for b, e, _ in bands}
+    assert len(sizes) == 1 and sizes.pop() % 128 == 0
+
+
+def test_partition_invalid():
+    with pytest.raises(pl.PlssvmError):
+        pl.plssvm_partition(1, 1, 0)
+    with pytest.raises(pl.PlssvmError):
+        pl.plssvm_partition(100, 2, 2)
+
+
+def _train_status(X, y, **kw):
+    L = pl.load()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    alpha = np.full(X.shape[0], 7.0)
+    b = np.full(1, 7.0)
+    args = dict(kernel=2, gamma=0.5, degree=3, coef0=0.0, C=1.0, eps=1e-10)
+    args.update(kw)
+    st = L.plssvm_train(X.ctypes.data, y.ctypes.data, X.shape[0], X.shape[1], args["kernel"], args["gamma"],
+                        args["degree"], args["coef0"], args["C"], args["eps"], alpha.ctypes.data, b.ctypes.data)
+    return st, pl.plssvm_last_error(), alpha, b
+
+
+def test_validation_errors_leave_outputs_untouched():
+    X = np.random.default_rng(0).standard_normal((10, 3))
+    y = np.array([1, -1] * 5, dtype=float)
+    cases = [
+        (dict(C=0.0), binding.E_INVALID_ARG),
+        (dict(C=-1.0), binding.E_INVALID_ARG),
+        (dict(gamma=0.0), binding.E_INVALID_ARG),
+        (dict(kernel=3), binding.E_INVALID_ARG),  # sigmoid is not a PLSSVM kernel
+        (dict(kernel=1, degree=0), binding.E_INVALID_ARG),
+        (dict(eps=0.0), binding.E_INVALID_ARG),
+    ]
+    for kw, code in cases:
+        st, msg, alpha, b = _train_status(X, y, **kw)
+        assert st == code and msg, (kw, st, msg)
+        assert np.all(alpha == 7.0) and b[0] == 7.0
+    st, msg, _, _ = _train_status(X, np.ones(10))
+    assert st == binding.E_LABELS and "both classes" in msg
+    st, msg, _, _ = _train_status(X, np.array([1, -1, 2, 1, 1, 1, -1, -1, 1, 1.0]))
+    assert st == binding.E_LABELS
+    Xn = X.copy()
+    Xn[3, 1] = np.nan
+    st, msg, _, _ = _train_status(Xn, y)
+    assert st == binding.E_INVALID_ARG and "finite" in msg
+    st, msg, _, _ = _train_status(X[:1], y[:1])
+    assert st == binding.E_INVALID_ARG
+
+
+def test_linear_kernel_ignores_gamma_validation():
+    X = np.random.default_rng(0).standard_normal((10, 3))
+    y = np.array([1, -1] * 5, dtype=float)
+    st, msg, _, _ = _train_status(X, y, kernel=0, gamma=0.0)
+    assert st in (binding.OK, binding.E_CUDA)
+
+
+@pytest.mark.skipif(pl.plssvm_device_count() > 0, reason="GPU present")
+def test_no_cpu_fallback_without_gpu():
+    X = np.random.default_rng(0).standard_normal((10, 3))
+    y = np.array([1, -1] * 5, dtype=float)
+    st, msg, alpha, b = _train_status(X, y)
+    assert st == binding.E_CUDA and "no CUDA device" in msg
+    with pytest.raises(pl.PlssvmError):
+        pl.plssvm_predict(X, np.zeros(10), 0.0, X, pl.RBF, 0.5)
+    with pytest.raises(pl.PlssvmError):
+        pl.plssvm_qtilde_matvec(X, np.zeros(9), pl.RBF, 0.5)

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element
+on the same seeded inputs.  Bars (BASELINE.json north_star):
+  * one Q~p product: ||y - y*|| / ||y*|| <= 1e-12 (fp64) / 1e-5 (fp32), plus the element-wise
+    bound |y_i - y*_i| <= tol * (|Q~| |p|)_i
+  * trained alpha: ||a - a*|| / ||a*|| <= 1e-7 ; b: |b - b*| <= 1e-7 max(|b*|, ||a*||_inf) (fp64, eps 1e-10)
+  * predicted labels bit-identical (the decision margins are reported)
+fp32 inputs: the oracle consumes the fp32-rounded X, p and gamma upcast to fp64.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2202_12674_b200 as pl
+import synth
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = [pl.LINEAR, pl.POLYNOMIAL, pl.RBF]
+KNAME = {0: "linear", 1: "poly", 2: "rbf"}
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def kparams(kernel, d, dtype):
+    gamma = 1.0 / d
+    if dtype == np.float32:
+        gamma = float(np.float32(gamma))
+    return dict(gamma=gamma, degree=3, coef0=0.5 if kernel == pl.POLYNOMIAL else 0.0)
+
+
+def check_matvec(X, p, kernel, kp, C, dtype, mode):
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    Xo = X.astype(np.float64)
+    Qt = oracle.qtilde(Xo, kernel, kp["gamma"], kp["degree"], kp["coef0"], C)
+    ref = oracle.matvec(Qt, p.astype(np.float64))
+    scale = np.abs(Qt) @ np.abs(p.astype(np.float64))
+    out, _ = pl.plssvm_qtilde_matvec(X, p, kernel, kp["gamma"], kp["degree"], kp["coef0"], C,
+                                     opts=pl.options(mode=mode))
+    out = out.astype(np.float64)
+    assert rel(out, ref) <= tol, (rel(out, ref), tol)
+    assert np.all(np.abs(out - ref) <= tol * scale + 1e-300), np.max(np.abs(out - ref) / scale)
+
+
+SHAPES = [(2, 1), (3, 3), (5, 16), (33, 17), (127, 64), (128, 1), (129, 3), (255, 100), (256, 16), (1000, 33),
+          (2177, 70)]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("m,d", SHAPES)
+def test_matvec_implicit_small(m, d, kernel, dtype):
+    rng = np.random.default_rng(1000 * m + d + kernel)
+    X = rng.standard_normal((m, d)).astype(dtype)
+    p = rng.standard_normal(m - 1).astype(dtype)
+    check_matvec(X, p, kernel, kparams(kernel, d, dtype), 1.0, dtype, pl.MODE_IMPLICIT)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("m,d", [(3, 3), (129, 3), (1000, 33), (2177, 70)])
+def test_matvec_cached_small(m, d, kernel, dtype):
+    rng = np.random.default_rng(7000 * m + d + kernel)
+    X = rng.standard_normal((m, d)).astype(dtype)
+    p = rng.standard_normal(m - 1).astype(dtype)
+    check_matvec(X, p, kernel, kparams(kernel, d, dtype), 0.5, dtype, pl.MODE_CACHED)
+
+
+@pytest.mark.parametrize("C", [0.1, 10.0])
+def test_matvec_C_and_planes_data(C):
+    X, y, _, _ = synth.planes(1500, 40, seed=5)
+    p = np.random.default_rng(3).standard_normal(1499)
+    for kernel in KERNELS:
+        check_matvec(X, p, kernel, kparams(kernel, 40, np.float64), C, np.float64, pl.MODE_IMPLICIT)
+
+
+def test_matvec_is_deterministic():
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((3000, 50))
+    p = rng.standard_normal(2999)
+    a, _ = pl.plssvm_qtilde_matvec(X, p, pl.RBF, 0.02, repeats=2)
+    b, _ = pl.plssvm_qtilde_matvec(X, p, pl.RBF, 0.02)
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------------------ training
+def check_train(X, y, kernel, kp, C, eps, opts=None, oracle_kw=None, tol=1e-7):
+    a_ref, b_ref, it_ref, st_ref = oracle.train(X.astype(np.float64), y.astype(np.float64), kernel, kp["gamma"],
+                                                kp["degree"], kp["coef0"], C, eps, **(oracle_kw or {}))
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, kernel, kp["gamma"], kp["degree"], kp["coef0"], C, eps,
+                                             opts=opts)
+    assert st == st_ref == 0
+    assert abs(stats.iterations - it_ref) <= 2, (stats.iterations, it_ref)
+    assert rel(alpha, a_ref) <= tol, rel(alpha, a_ref)
+    assert abs(b - b_ref) <= tol * max(abs(b_ref), np.abs(a_ref).max())
+    assert abs(alpha.sum()) <= 1e-10 * (1 + np.abs(alpha).max())
+    return alpha, b, stats
+
+
+@pytest.mark.parametrize("mode", [pl.MODE_IMPLICIT, pl.MODE_CACHED])
+def test_train_c0(mode):
+    cfg = synth.configs()["C0"]
+    X, y, Z, yz = synth.config_data(cfg)
+    kp = dict(gamma=cfg.gamma, degree=cfg.degree, coef0=cfg.coef0)
+    alpha, b, stats = check_train(X, y, cfg.kernel, kp, cfg.C, cfg.eps, opts=pl.options(mode=mode))
+    assert stats.mode_used == mode
+    # predict: labels bit-identical with the oracle's on the test set
+    f_ref, lab_ref = oracle.predict(X, alpha, b, Z, cfg.kernel, cfg.gamma, cfg.degree, cfg.coef0)
+    f, lab = pl.plssvm_predict(X, alpha, b, Z, cfg.kernel, cfg.gamma, cfg.degree, cfg.coef0)
+    assert np.array_equal(lab, lab_ref), np.min(np.abs(f_ref))
+    assert rel(f, f_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("m,d", [(64, 5), (300, 17), (1000, 64), (2049, 31)])
+def test_train_random(m, d, kernel):
+    X, y, _, _ = synth.planes(m, d, seed=100 + m + kernel)
+    kp = kparams(kernel, d, np.float64)
+    check_train(X, y, kernel, kp, 1.0, 1e-10)
+
+
+def test_train_x0_ones_and_replacement_options():
+    X, y, _, _ = synth.planes(700, 20, seed=9)
+    kp = kparams(pl.RBF, 20, np.float64)
+    check_train(X, y, pl.RBF, kp, 1.0, 1e-10, opts=pl.options(x0=1), oracle_kw=dict(x0=1))
+    check_train(X, y, pl.RBF, kp, 1.0, 1e-10, opts=pl.options(replace_every=5), oracle_kw=dict(replace_every=5))
+
+
+def test_train_not_converged_and_fixed_iterations():
+    X, y, _, _ = synth.planes(500, 20, seed=4)
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, pl.RBF, 0.05, eps=1e-10, opts=pl.options(max_iter=3))
+    assert st == 7 and stats.iterations == 3  # W_NOT_CONVERGED, alpha and b filled
+    a_ref, b_ref, it, st_ref = oracle.train(X, y, pl.RBF, 0.05, eps=1e-10, imax=3)
+    assert st_ref == oracle.W_NOT_CONVERGED and rel(alpha, a_ref) <= 1e-10
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, pl.RBF, 0.05, eps=1e-10, opts=pl.options(fixed_iter=5))
+    assert st == 0 and stats.iterations == 5
+
+
+def test_train_worked_examples(golden):
+    for name in ["spec_3point_linear.txt", "square_4point_linear.txt", "square_4point_poly.txt",
+                 "generic_4point_linear.txt"]:
+        g = golden(name)
+        X = np.array([[float(v) for v in row] for row in g["X"]])
+        y = np.array([float(v) for v in g["labels"]])
+        alpha, b, st = pl.plssvm_train(X, y, int(g["kernel"]), float(g["gamma"]), int(g["degree"]),
+                                       float(g["coef0"]), float(g["C"]), 1e-14)
+        assert np.allclose(alpha, [float(v) for v in g["alpha"]], rtol=0, atol=1e-12), name
+        assert abs(b - float(g["b"])) <= 1e-12, name
+
+
+def test_predict_tie_break_through_capi(golden):
+    g = golden("square_4point_linear.txt")
+    X = np.array([[float(v) for v in row] for row in g["X"]])
+    f, lab = pl.plssvm_predict(X, np.array([0.5, 0.5, -0.5, -0.5]), 0.5, np.array([[0.25, 0.5], [0.0, 1.0]]),
+                               pl.LINEAR)
+    assert f[0] == 0.0 and lab[0] == 1 and lab[1] == -1
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_predict_random(kernel, dtype):
+    rng = np.random.default_rng(50 + kernel)
+    X = rng.standard_normal((777, 45)).astype(dtype)
+    Z = rng.standard_normal((333, 45)).astype(dtype)
+    alpha = rng.standard_normal(777).astype(dtype)
+    kp = kparams(kernel, 45, dtype)
+    f_ref, lab_ref = oracle.predict(X.astype(np.float64), alpha.astype(np.float64), 0.25, Z.astype(np.float64),
+                                    kernel, kp["gamma"], kp["degree"], kp["coef0"])
+    f, lab = pl.plssvm_predict(X, alpha, 0.25, Z, kernel, kp["gamma"], kp["degree"], kp["coef0"])
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    assert rel(f, f_ref) <= tol
+    safe = np.abs(f_ref) > 1e3 * tol * np.abs(f_ref).max()
+    assert np.array_equal(lab[safe], lab_ref[safe])
+
+
+def test_fp32_train_runs_and_is_close():
+    cfg = synth.configs()["C3"]
+    X, y, _, _ = synth.config_data(cfg, m=2048, d=256, n_test=0)
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, cfg.kernel, float(np.float32(1 / 256)), cfg.degree, cfg.coef0,
+                                             cfg.C, 1e-6)
+    a_ref, b_ref, it, _ = oracle.train(X.astype(np.float64), y.astype(np.float64), cfg.kernel,
+                                       float(np.float32(1 / 256)), cfg.degree, cfg.coef0, cfg.C, 1e-6)
+    assert alpha.dtype == np.float32 and st in (0, 7)
+    assert rel(alpha, a_ref) <= 1e-3  # fp32 CG plateaus near 4e-5 relative
+
+
+# ------------------------------------------------------------------------------ full size (C1)
+def test_c1_full_size_sampled_rows_and_residual():
+    """BASELINE config C1 (2^14 x 2^10 RBF fp64) in the launch configuration bench.py times:
+    sampled rows of one Q~p product against the oracle's rows, then the trained model's
+    residual on sampled rows and labels on a test subset."""
+    cfg = synth.configs()["C1"]
+    X, y, Z, yz = synth.config_data(cfg)
+    m = cfg.m
+    rng = np.random.default_rng(77)
+    p = rng.standard_normal(m - 1)
+    out, t = pl.plssvm_qtilde_matvec(X, p, cfg.kernel, cfg.gamma, C=cfg.C, opts=pl.options(mode=pl.MODE_IMPLICIT))
+    rows = np.unique(np.concatenate([[0, 1, 127, 128, m - 2], rng.integers(0, m - 1, 59)]))
+    R = oracle.qtilde_rows(X, rows, cfg.kernel, cfg.gamma, C=cfg.C)
+    ref = R @ p
+    scale = np.abs(R) @ np.abs(p)
+    assert np.all(np.abs(out[rows] - ref) <= 1e-12 * scale)
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, cfg.kernel, cfg.gamma, C=cfg.C, eps=cfg.eps,
+                                             opts=pl.options(mode=pl.MODE_IMPLICIT))
+    assert st == 0 and 20 <= stats.iterations <= 40
+    at = alpha[:-1]
+    rhs = y[:-1] - y[-1]
+    res = np.abs(R @ at - rhs[rows])
+    assert np.max(res) <= 1e-8 * np.linalg.norm(rhs)  # residual contract on sampled rows
+    assert abs(alpha.sum()) <= 1e-10 * np.abs(alpha).max()
+    zi = np.arange(0, Z.shape[0], 16)
+    f_ref, lab_ref = oracle.predict(X, alpha, b, Z[zi], cfg.kernel, cfg.gamma)
+    f, lab = pl.plssvm_predict(X, alpha, b, Z, cfg.kernel, cfg.gamma)
+    assert np.array_equal(lab[zi], lab_ref)
