@@ -97,18 +97,19 @@ const T *stage_input(Arena &A, const void *src, int64_t n, bool device_ptr, cuda
     return d;
 }
 
+// rows = padded point count of the destination array (its column count is dpad).
 template <typename T>
-void launch_transform(const T *X, int64_t m, int64_t d, T *Xt, int64_t ld, int64_t dpad, cudaStream_t s,
+void launch_transform(const T *X, int64_t m, int64_t d, T *Xt, int64_t rows, int64_t dpad, cudaStream_t s,
                       int64_t &launches) {
-    dim3 grid(static_cast<unsigned>(ceil_div(ld, 32)), static_cast<unsigned>(ceil_div(dpad, 32)));
-    k_transform<T><<<grid, dim3(32, 8), 0, s>>>(X, m, d, Xt, ld, dpad);
+    dim3 grid(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(ceil_div(dpad, 32)));
+    k_transform<T><<<grid, dim3(32, 8), 0, s>>>(X, m, d, Xt, rows, dpad, Engine<T>::kPointMajor ? 1 : 0);
     PLS_CHECK_LAUNCH();
     ++launches;
 }
 
 // Row-band geometry of this rank: padded length mpad (multiple of 128 * P), tiles per rank.
 struct Geometry {
-    int64_t m1, mpad, dpad, nb, g0;
+    int64_t m1, mpad, dpad, ld, nb, g0;
     int T, band0, band1, P, rank;
 };
 
@@ -119,7 +120,8 @@ Geometry geometry(int64_t m, int64_t d, int P, int rank) {
     g.P = P;
     g.rank = rank;
     g.mpad = round_up(m, static_cast<int64_t>(kTile) * P);
-    g.dpad = round_up(d, Tile<T>::BK);
+    g.dpad = round_up(d, Engine<T>::BK);
+    g.ld = Engine<T>::kPointMajor ? g.dpad : g.mpad;
     g.T = static_cast<int>(g.mpad / kTile);
     const int per = g.T / P;
     g.band0 = rank * per;
@@ -160,7 +162,7 @@ struct Ctx {
 
 template <typename T>
 void set_smem_attrs() {
-    const int bytes = static_cast<int>(Tile<T>::SMEM_BYTES);
+    const int bytes = static_cast<int>(Engine<T>::SMEM_BYTES);
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<LINEAR, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<POLYNOMIAL, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -184,20 +186,20 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
         ++c.launches;
         return 1;
     }
-    const size_t sm = Tile<T>::SMEM_BYTES;
+    const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
         case LINEAR:
-            k_matvec_implicit<LINEAR, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, pfull,
+            k_matvec_implicit<LINEAR, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm, pfull,
                                                                          c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
                                                                          c.Ypart, g.nb);
             break;
         case POLYNOMIAL:
-            k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm,
+            k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm,
                                                                              pfull, c.kp, c.invC, c.scal, g.m1, g.band0,
                                                                              g.band1, c.Ypart, g.nb);
             break;
         default:
-            k_matvec_implicit<RBF, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, pfull,
+            k_matvec_implicit<RBF, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm, pfull,
                                                                       c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
                                                                       c.Ypart, g.nb);
     }
@@ -209,18 +211,18 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
 template <typename T>
 void launch_precompute(Ctx<T> &c) {
     const Geometry &g = c.g;
-    const size_t sm = Tile<T>::SMEM_BYTES;
+    const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
         case LINEAR:
-            k_precompute<LINEAR, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<LINEAR, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                     c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
             break;
         case POLYNOMIAL:
-            k_precompute<POLYNOMIAL, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<POLYNOMIAL, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                         c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
             break;
         default:
-            k_precompute<RBF, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<RBF, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                  c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
     }
     PLS_CHECK_LAUNCH();
@@ -277,8 +279,9 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.nrm = A.alloc<T>(g.mpad);
     c.scal = A.alloc<double>(S_COUNT);
     PLS_CUDA(cudaMemsetAsync(c.scal, 0, S_COUNT * sizeof(double), c.s));
-    k_q_norms<T><<<static_cast<unsigned>(ceil_div(g.mpad, 256)), 256, 0, c.s>>>(c.Xt, g.mpad, pb.m, pb.d, c.kp, c.invC,
-                                                                                 c.ylab, c.q, c.nrm, c.scal);
+    k_q_norms<T><<<static_cast<unsigned>(ceil_div(g.mpad * 32, 256)), 256, 0, c.s>>>(c.Xt, g.mpad, g.dpad, pb.m, pb.d,
+                                                                                      c.kp, c.invC, c.ylab, c.q, c.nrm,
+                                                                                      c.scal);
     PLS_CHECK_LAUNCH();
     ++c.launches;
     PLS_CUDA(cudaEventRecord(e_q, c.s));
@@ -548,41 +551,47 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     int64_t launches = 0;
     const bool dev = o.device_pointers != 0;
     const int64_t m = pb.m, d = pb.d;
+    using EN = Engine<T>;
     const int64_t mpad = round_up(m, kTile), npad = round_up(n, kTile);
+    const int64_t dpad = round_up(d, EN::BK);
+    // point-major: Xp[mpad][dpad], Zp[npad][dpad]; feature-major: both with ld = max(mpad, npad)
     const int64_t L = std::max(mpad, npad);
-    const int64_t dpad = round_up(d, Tile<T>::BK);
+    const int64_t xrows = EN::kPointMajor ? mpad : L, zrows = EN::kPointMajor ? npad : L;
+    const int64_t ldx = EN::kPointMajor ? dpad : L, ldz = EN::kPointMajor ? dpad : L;
     const T *Xs = stage_input<T>(A, pb.X, m * d, dev, s);
     const T *Zs = stage_input<T>(A, Zin, n * d, dev, s);
-    T *Xt = A.alloc<T>(dpad * L), *Zt = A.alloc<T>(dpad * L);
-    launch_transform<T>(Xs, m, d, Xt, L, dpad, s, launches);
-    launch_transform<T>(Zs, n, d, Zt, L, dpad, s, launches);
-    T *alpha = A.alloc<T>(L);
-    PLS_CUDA(cudaMemsetAsync(alpha, 0, L * sizeof(T), s));
+    T *Xl = A.alloc<T>(dpad * xrows), *Zl = A.alloc<T>(dpad * zrows);
+    launch_transform<T>(Xs, m, d, Xl, xrows, dpad, s, launches);
+    launch_transform<T>(Zs, n, d, Zl, zrows, dpad, s, launches);
+    T *alpha = A.alloc<T>(xrows);
+    PLS_CUDA(cudaMemsetAsync(alpha, 0, xrows * sizeof(T), s));
     PLS_CUDA(cudaMemcpyAsync(alpha, alpha_in, m * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    T *nx = A.alloc<T>(L), *nz = A.alloc<T>(L);
+    T *nx = A.alloc<T>(xrows), *nz = A.alloc<T>(zrows);
     KParams<T> kp{pb.kernel, static_cast<T>(pb.gamma), pb.degree, static_cast<T>(pb.coef0)};
     if (pb.kernel == RBF) {
-        k_norms<T><<<static_cast<unsigned>(ceil_div(L, 256)), 256, 0, s>>>(Xt, L, L, d, nx);
-        k_norms<T><<<static_cast<unsigned>(ceil_div(L, 256)), 256, 0, s>>>(Zt, L, L, d, nz);
+        k_norms<T><<<static_cast<unsigned>(ceil_div(xrows * 32, 256)), 256, 0, s>>>(Xl, xrows, dpad, xrows, d, nx);
+        k_norms<T><<<static_cast<unsigned>(ceil_div(zrows * 32, 256)), 256, 0, s>>>(Zl, zrows, dpad, zrows, d, nz);
         PLS_CHECK_LAUNCH();
         launches += 2;
     }
     const int tilesI = static_cast<int>(npad / kTile), tilesJ = static_cast<int>(mpad / kTile);
     T *Fpart = A.alloc<T>(static_cast<int64_t>(tilesJ) * npad);
     set_smem_attrs<T>();
-    const size_t sm = Tile<T>::SMEM_BYTES;
+    const size_t sm = EN::SMEM_BYTES;
     const int grid = tilesI * tilesJ;
     PLS_CUDA(cudaEventRecord(e0, s));
     switch (pb.kernel) {
         case LINEAR:
-            k_predict_tiles<LINEAR, T><<<grid, kThreads, sm, s>>>(Zt, npad, Xt, L, dpad, nz, nx, alpha, kp, tilesI, Fpart);
+            k_predict_tiles<LINEAR, T><<<grid, kThreads, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
+                                                                  Fpart);
             break;
         case POLYNOMIAL:
-            k_predict_tiles<POLYNOMIAL, T><<<grid, kThreads, sm, s>>>(Zt, npad, Xt, L, dpad, nz, nx, alpha, kp, tilesI,
-                                                                      Fpart);
+            k_predict_tiles<POLYNOMIAL, T><<<grid, kThreads, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp,
+                                                                      tilesI, Fpart);
             break;
         default:
-            k_predict_tiles<RBF, T><<<grid, kThreads, sm, s>>>(Zt, npad, Xt, L, dpad, nz, nx, alpha, kp, tilesI, Fpart);
+            k_predict_tiles<RBF, T><<<grid, kThreads, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
+                                                               Fpart);
     }
     PLS_CHECK_LAUNCH();
     PLS_CUDA(cudaEventRecord(e1, s));

@@ -64,40 +64,66 @@ __device__ __forceinline__ void grid_reduce(T v, T *partials, unsigned *counter,
 }
 
 // ---------------------------------------------------------------------------------------
-// Layout transform: X[m][d] (point-major, host order) -> Xt[dpad][mpad] feature-major with
-// zero padding.  32x32 smem transpose, grid covers the padded extent.
+// Layout transform (paper "transform"): X[m][d] point-major (host order) ->
+//   feature-major X^T[dpad][ld] (fp32 FFMA engine, the paper's column-major layout), or
+//   point-major   Xp[ld][dpad]  (fp64 DMMA engine, features contiguous),
+// zero padding everywhere outside m x d (padded features are kernel-neutral, padded points are
+// masked).  32x32 smem tile, the grid covers the padded extent (no separate memset).
 template <typename T>
-__global__ void k_transform(const T *__restrict__ X, int64_t m, int64_t d, T *__restrict__ Xt, int64_t mpad,
-                            int64_t dpad) {
+__global__ void k_transform(const T *__restrict__ X, int64_t m, int64_t d, T *__restrict__ Xt, int64_t ld,
+                            int64_t dpad, int point_major) {
     __shared__ T t[32][33];
     const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32, f0 = static_cast<int64_t>(blockIdx.y) * 32;
+    if (point_major) {
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int64_t p = p0 + r, f = f0 + threadIdx.x;
+            if (p < ld && f < dpad) Xt[p * dpad + f] = (p < m && f < d) ? X[p * d + f] : T(0);
+        }
+        return;
+    }
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        int64_t p = p0 + r, f = f0 + threadIdx.x;
+        const int64_t p = p0 + r, f = f0 + threadIdx.x;
         t[r][threadIdx.x] = (p < m && f < d) ? X[p * d + f] : T(0);
     }
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        int64_t f = f0 + r, p = p0 + threadIdx.x;
-        if (f < dpad && p < mpad) Xt[f * mpad + p] = t[threadIdx.x][r];
+        const int64_t f = f0 + r, p = p0 + threadIdx.x;
+        if (f < dpad && p < ld) Xt[f * ld + p] = t[threadIdx.x][r];
     }
+}
+
+// Element (point i, feature k) of the engine's layout.
+template <typename T>
+__device__ __forceinline__ T elem(const T *X, int64_t i, int64_t k, int64_t mpad, int64_t dpad) {
+    if constexpr (Engine<T>::kPointMajor) return X[i * dpad + k];
+    else return X[k * mpad + i];
 }
 
 // q cache and norms: q_i = k(x_i, x_m) for i < m-1 (0 beyond), n_i = ||x_i||^2,
 // S_QMM = k(x_m, x_m) + 1/C, S_YM = y_m.  RBF q uses the direct squared distance.
+// One warp per point (lanes stride the features; fixed shuffle tree -> deterministic).
 template <typename T>
-__global__ void k_q_norms(const T *__restrict__ Xt, int64_t mpad, int64_t m, int64_t d, KParams<T> kp, T invC,
-                          const T *__restrict__ y, T *__restrict__ q, T *__restrict__ nrm, double *scal) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void k_q_norms(const T *__restrict__ X, int64_t mpad, int64_t dpad, int64_t m, int64_t d, KParams<T> kp,
+                          T invC, const T *__restrict__ y, T *__restrict__ q, T *__restrict__ nrm, double *scal) {
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= mpad) return;
     const int64_t xm = m - 1;
     T s = T(0), n = T(0), dist = T(0);
-    for (int64_t k = 0; k < d; ++k) {
-        const T a = Xt[k * mpad + i], b = Xt[k * mpad + xm];
+    for (int64_t k = lane; k < d; k += 32) {
+        const T a = elem(X, i, k, mpad, dpad), b = elem(X, xm, k, mpad, dpad);
         s = fma(a, b, s);
         n = fma(a, a, n);
         const T t = a - b;
         dist = fma(t, t, dist);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        n += __shfl_xor_sync(0xffffffffu, n, o);
+        dist += __shfl_xor_sync(0xffffffffu, dist, o);
+    }
+    if (lane != 0) return;
     T kv;
     if (kp.kernel == LINEAR) {
         kv = s;
@@ -133,75 +159,65 @@ __device__ __forceinline__ T qtilde_value(T s, int64_t gi, int64_t gj, T ni, T n
 // band [band0, band1) are used twice (mirroring): their row sums go to rows of I
 // and their column sums (Q~_IJ^T p_I) to rows of J.  Every (slot, row-block) pair of the
 // partial buffer Ypart[T][band_rows] is written exactly once per call, so the finalize sum
-// is deterministic.
+// is deterministic.  ld = the engine layout's leading dimension (dpad point-major, mpad
+// feature-major).
 template <int KT, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_matvec_implicit(const T *__restrict__ Xt, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
+    k_matvec_implicit(const T *__restrict__ X, int64_t ld, int64_t dpad, const int2 *__restrict__ tiles,
                       const T *__restrict__ q, const T *__restrict__ nrm, const T *__restrict__ p, KParams<T> kp,
                       T invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
                       T *__restrict__ Ypart, int64_t band_rows) {
+    using E = Engine<T>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *smem = reinterpret_cast<T *>(smem_raw);
     const int2 tile = tiles[blockIdx.x];
     const int I = tile.x, J = tile.y;
     const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
-    T acc[8][8];
-    contract_tile<T>(Xt + row0, Xt + col0, mpad, dpad, smem, acc);
+    T acc[E::R][E::CC];
+    E::contract(E::block(X, row0, ld), E::block(X, col0, ld), ld, dpad, smem, acc);
 
-    const int ry = thread_ry(), rx = thread_rx();
     const T Qmm = static_cast<T>(scal[S_QMM]);
-    T qi[8], ni[8], pi[8], qj[8], nj[8], pj[8];
+    T qi[E::R], ni[E::R], pi[E::R], qj[E::CC], nj[E::CC], pj[E::CC];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const int64_t gi = row0 + micro_index<T>(ry, e), gj = col0 + micro_index<T>(rx, e);
+    for (int e = 0; e < E::R; ++e) {
+        const int64_t gi = row0 + E::row_of(e);
         qi[e] = q[gi]; pi[e] = p[gi]; ni[e] = (KT == RBF) ? nrm[gi] : T(0);
+    }
+#pragma unroll
+    for (int e = 0; e < E::CC; ++e) {
+        const int64_t gj = col0 + E::col_of(e);
         qj[e] = q[gj]; pj[e] = p[gj]; nj[e] = (KT == RBF) ? nrm[gj] : T(0);
     }
-    T rs[8], cs[8];
+    T rs[E::R], cs[E::CC];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) rs[e] = cs[e] = T(0);
+    for (int e = 0; e < E::R; ++e) rs[e] = T(0);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t gi = row0 + micro_index<T>(ry, i);
+    for (int e = 0; e < E::CC; ++e) cs[e] = T(0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int64_t gj = col0 + micro_index<T>(rx, j);
+    for (int i = 0; i < E::R; ++i) {
+        const int64_t gi = row0 + E::row_of(i);
+#pragma unroll
+        for (int j = 0; j < E::CC; ++j) {
+            const int64_t gj = col0 + E::col_of(j);
             const T v = qtilde_value<KT, T>(acc[i][j], gi, gj, ni[i], nj[j], qi[i], qj[j], Qmm, invC, m1, kp);
             rs[i] = fma(v, pj[j], rs[i]);
             cs[j] = fma(v, pi[i], cs[j]);
         }
     }
-    // row sums: reduce over the 8 rx lanes of the warp, then over the 2 warps sharing ry
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 1);
-        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 2);
-        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 4);
-        cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 8);
-        cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 16);
-    }
-    T *redr = smem;               // [2][128]
-    T *redc = smem + 2 * kTile;   // [4][128]
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if ((lane & 7) == 0) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) redr[(w & 1) * kTile + micro_index<T>(ry, e)] = rs[e];
-    }
-    if (lane < 8) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) redc[(w >> 1) * kTile + micro_index<T>(rx, e)] = cs[e];
-    }
+    T *redr = smem;              // [2][128]
+    T *redc = smem + 2 * kTile;  // [4][128]
+    E::reduce_rows(rs, redr);
+    E::reduce_cols(cs, redc);
     __syncthreads();
     const bool mirrored = (I != J) && (J >= band0) && (J < band1);
     const int64_t lrow0 = row0 - static_cast<int64_t>(band0) * kTile;
     if (threadIdx.x < kTile) {
         const int t = threadIdx.x;
-        Ypart[static_cast<int64_t>(J) * band_rows + lrow0 + t] = redr[t] + redr[kTile + t];
+        Ypart[static_cast<int64_t>(J) * band_rows + lrow0 + t] = E::row_total(redr, t);
     } else if (mirrored) {
         const int t = threadIdx.x - kTile;
         const int64_t lcol0 = col0 - static_cast<int64_t>(band0) * kTile;
-        Ypart[static_cast<int64_t>(I) * band_rows + lcol0 + t] =
-            (redc[t] + redc[kTile + t]) + (redc[2 * kTile + t] + redc[3 * kTile + t]);
+        Ypart[static_cast<int64_t>(I) * band_rows + lcol0 + t] = E::col_total(redc, t);
     }
 }
 
@@ -209,27 +225,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 // into Qc[local_row][mpad] from the same tiles (upper tiles mirrored as transposed stores).
 template <int KT, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_precompute(const T *__restrict__ Xt, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
+    k_precompute(const T *__restrict__ X, int64_t ld, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
                  const T *__restrict__ q, const T *__restrict__ nrm, KParams<T> kp, T invC,
                  const double *__restrict__ scal, int64_t m1, int band0, int band1, T *__restrict__ Qc) {
+    using E = Engine<T>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *smem = reinterpret_cast<T *>(smem_raw);
     const int2 tile = tiles[blockIdx.x];
     const int I = tile.x, J = tile.y;
     const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
-    T acc[8][8];
-    contract_tile<T>(Xt + row0, Xt + col0, mpad, dpad, smem, acc);
-    const int ry = thread_ry(), rx = thread_rx();
+    T acc[E::R][E::CC];
+    E::contract(E::block(X, row0, ld), E::block(X, col0, ld), ld, dpad, smem, acc);
     const T Qmm = static_cast<T>(scal[S_QMM]);
     const bool mirrored = (I != J) && (J >= band0) && (J < band1);
     const int64_t b0 = static_cast<int64_t>(band0) * kTile;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t gi = row0 + micro_index<T>(ry, i);
+    for (int i = 0; i < E::R; ++i) {
+        const int64_t gi = row0 + E::row_of(i);
         const T qi = q[gi], ni = (KT == RBF) ? nrm[gi] : T(0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int64_t gj = col0 + micro_index<T>(rx, j);
+        for (int j = 0; j < E::CC; ++j) {
+            const int64_t gj = col0 + E::col_of(j);
             const T qj = q[gj], nj = (KT == RBF) ? nrm[gj] : T(0);
             const T v = qtilde_value<KT, T>(acc[i][j], gi, gj, ni, nj, qi, qj, Qmm, invC, m1, kp);
             Qc[(gi - b0) * mpad + gj] = v;
@@ -413,63 +429,61 @@ __global__ void k_assemble(const T *__restrict__ xfull, int64_t m, double *scal,
 }
 
 // ---------------------------------------------------------------------------------------
-// Predict (Eq. 10): tiles (I over test points Zt, J over training points Xt); the epilogue
+// Predict (Eq. 10): tiles (I over test points Z, J over training points X); the epilogue
 // forms alpha_j k(z_i, x_j) and row-reduces into Fpart[J][i] (deterministic slots).
+// ldz / ldx: leading dimensions of the two arrays in the engine layout.
 template <int KT, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_predict_tiles(const T *__restrict__ Zt, int64_t npad, const T *__restrict__ Xt, int64_t mpad, int64_t dpad,
-                    const T *__restrict__ nz, const T *__restrict__ nx, const T *__restrict__ alpha, KParams<T> kp,
-                    int tilesI, T *__restrict__ Fpart) {
+    k_predict_tiles(const T *__restrict__ Zl, int64_t ldz, int64_t npad, const T *__restrict__ Xl, int64_t ldx,
+                    int64_t dpad, const T *__restrict__ nz, const T *__restrict__ nx, const T *__restrict__ alpha,
+                    KParams<T> kp, int tilesI, T *__restrict__ Fpart) {
+    using E = Engine<T>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *smem = reinterpret_cast<T *>(smem_raw);
     const int I = blockIdx.x % tilesI, J = blockIdx.x / tilesI;
     const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
-    T acc[8][8];
-    // The engine reads both operands with one leading dimension: the driver stores Zt and Xt
-    // with ld = max(npad, mpad), passed here as `mpad` (see predict_impl).
-    contract_tile<T>(Zt + row0, Xt + col0, mpad, dpad, smem, acc);
-    const int ry = thread_ry(), rx = thread_rx();
-    T rs[8];
+    T acc[E::R][E::CC];
+    if constexpr (E::kPointMajor) {
+        E::contract(E::block(Zl, row0, ldz), E::block(Xl, col0, ldx), dpad, dpad, smem, acc);
+    } else {
+        // feature-major: the engine reads both operands with one leading dimension; the driver
+        // stores Z^T and X^T with the same ld.
+        E::contract(E::block(Zl, row0, ldz), E::block(Xl, col0, ldx), ldx, dpad, smem, acc);
+    }
+    T rs[E::R];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t gi = row0 + micro_index<T>(ry, i);
+    for (int i = 0; i < E::R; ++i) {
+        const int64_t gi = row0 + E::row_of(i);
         const T ni = (KT == RBF) ? nz[gi] : T(0);
         T s = T(0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int64_t gj = col0 + micro_index<T>(rx, j);
+        for (int j = 0; j < E::CC; ++j) {
+            const int64_t gj = col0 + E::col_of(j);
             const T nj = (KT == RBF) ? nx[gj] : T(0);
             const T kv = kernel_value<KT, T>(acc[i][j], ni, nj, false, kp);
             s = fma(alpha[gj], kv, s);
         }
         rs[i] = s;
     }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 1);
-        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 2);
-        rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 4);
-    }
     T *redr = smem;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if ((lane & 7) == 0) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) redr[(w & 1) * kTile + micro_index<T>(ry, e)] = rs[e];
-    }
+    E::reduce_rows(rs, redr);
     __syncthreads();
-    if (threadIdx.x < kTile) Fpart[static_cast<int64_t>(J) * npad + row0 + threadIdx.x] = redr[threadIdx.x] + redr[kTile + threadIdx.x];
+    if (threadIdx.x < kTile) Fpart[static_cast<int64_t>(J) * npad + row0 + threadIdx.x] = E::row_total(redr, threadIdx.x);
 }
 
 template <typename T>
-__global__ void k_norms(const T *__restrict__ Xt, int64_t ld, int64_t n, int64_t d, T *__restrict__ nrm) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void k_norms(const T *__restrict__ X, int64_t mpad, int64_t dpad, int64_t n, int64_t d, T *__restrict__ nrm) {
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= n) return;
     T s = T(0);
-    for (int64_t k = 0; k < d; ++k) {
-        const T a = Xt[k * ld + i];
+    for (int64_t k = lane; k < d; k += 32) {
+        const T a = elem(X, i, k, mpad, dpad);
         s = fma(a, a, s);
     }
-    nrm[i] = s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) nrm[i] = s;
 }
 
 // f_i = sum_J Fpart[J][i] + b ; label = f >= 0 ? +1 : -1

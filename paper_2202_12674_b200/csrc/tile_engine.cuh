@@ -1,34 +1,31 @@
-// tile_engine.cuh -- the blocked pairwise-contraction engine shared by the three tile kernels
+// tile_engine.cuh -- the blocked pairwise-contraction engines shared by the three tile kernels
 // (implicit Q~p, Q~ precompute, predict).
 //
 // Paper design it re-derives (§III-C): blocking with padding "at least
 // the size of a full block", block-level caching of 2*blocksize points' feature
-// slabs in shared memory and thread-level register blocking, over
-// the feature-major ("column-major") data layout.
+// slabs in shared memory and thread-level register blocking.
 //
-// sm_100a realisation: a CTA of 256 threads owns a 128 x 128 tile S = X_I X_J^T (row block I,
-// column block J); the contraction over features runs in BK-wide slabs (BK*sizeof(T) = 128 B)
-// staged by a 4-deep cp.async ring into shared memory; each thread keeps an 8 x 8 register
-// micro-tile (DFMA for fp64, FFMA for fp32).  Thread (ry, rx) owns rows
-// ry*VEC + u*16*VEC + v and the same pattern of columns (VEC = 16 B / sizeof(T)), so every
-// shared-memory read is a 16-byte LDS.128 and a warp (4 ry x 8 rx) reads 64 B (A) / 128 B (B)
-// contiguous bytes per instruction: one wavefront, no bank conflicts.
+// A CTA of 256 threads owns a 128 x 128 tile S = X_I X_J^T (row block I, column block J); the
+// contraction over features runs in 128-byte feature slabs staged by a 4-deep cp.async ring.
+//
+//  * fp64 (Engine<double>): DMMA.8x8x4 tensor-core MMAs (mma.sync m8n8k4 f64; tcgen05 has no
+//    f64 kind).  Measured on this B200: DMMA 37.1 TFLOP/s vs DFMA 33.4 (profiles/r01_fp64_peak.txt).
+//    The device layout is POINT-major, X[mpad][dpad] (features contiguous), so one 16-byte
+//    LDS.128 feeds a thread's A (or B) value for two MMAs: MMA "a" uses feature 2q, MMA "b"
+//    feature 2q+1 of each 8-feature group (q = lane % 4; the contraction over k is order-free,
+//    A and B use the same permutation).  Smem rows are 128 B with the chunk swizzle
+//    c ^ (row & 7), and fragment row rho maps to tile row pi(rho) = (rho >> 1) | ((rho & 1) << 2)
+//    so the 8 lanes of each LDS.128 phase hit 8 distinct 16-byte bank groups (no conflicts).
+//    Warp grid 4 (M) x 2 (N); warp tile 32 x 64 = 4 x 8 MMA tiles; 64 fp64 accumulators/thread.
+//  * fp32 (Engine<float>): FFMA register micro-tiles 8 x 8 on the FEATURE-major layout
+//    X^T[dpad][mpad] (the paper's column-major layout); thread (ry, rx) owns rows
+//    ry*4 + 64u + v, every smem read is one conflict-free LDS.128.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace plssvm {
-
-template <typename T>
-struct Tile {
-    static constexpr int BK = 128 / sizeof(T);             // features per slab (16 fp64 / 32 fp32)
-    static constexpr int VEC = 16 / sizeof(T);             // elements per 16-byte vector
-    static constexpr int STAGES = 4;                       // cp.async ring depth
-    static constexpr int SLAB = BK * kTile;                // elements of one operand slab
-    static constexpr int SMEM_ELEMS = STAGES * 2 * SLAB;   // A and B rings
-    static constexpr size_t SMEM_BYTES = SMEM_ELEMS * sizeof(T);  // 128 KiB
-    static constexpr int CPR = kTile * sizeof(T) / 16;     // 16-byte chunks per slab row
-    static constexpr int CHUNKS = BK * CPR / kThreads;     // chunks per thread per operand
-};
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -38,87 +35,254 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Local row (or column) index of the thread's micro-tile element e (0..7): ry*VEC + u*16*VEC + v.
 template <typename T>
-__device__ __forceinline__ int micro_index(int r, int e) {
-    constexpr int VEC = Tile<T>::VEC;
-    return r * VEC + (e / VEC) * (16 * VEC) + (e % VEC);
-}
+struct Engine;
 
-__device__ __forceinline__ int thread_ry() { return ((threadIdx.x >> 5) >> 1) * 4 + ((threadIdx.x & 31) >> 3); }
-__device__ __forceinline__ int thread_rx() { return ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7); }
+// =====================================================================================
+// fp64: DMMA engine on the point-major layout X[mpad][ld], ld = dpad.
+template <>
+struct Engine<double> {
+    using T = double;
+    static constexpr bool kPointMajor = true;
+    static constexpr int BK = 16;                  // features per slab (128 B per row)
+    static constexpr int STAGES = 4;
+    static constexpr int SLAB = kTile * BK;        // doubles per operand slab (16 KiB)
+    static constexpr size_t SMEM_BYTES = size_t(STAGES) * 2 * SLAB * sizeof(T);  // 128 KiB
+    static constexpr int R = 4;                    // accumulator rows per thread (m-tiles)
+    static constexpr int CC = 16;                  // accumulator columns per thread (8 n-tiles x 2)
 
-template <typename T>
-__device__ __forceinline__ void load_slab(T *sA, T *sB, const T *__restrict__ A, const T *__restrict__ B,
-                                          int64_t ld, int64_t k0) {
-    using C = Tile<T>;
-#pragma unroll
-    for (int u = 0; u < C::CHUNKS; ++u) {
-        int ch = threadIdx.x + u * kThreads;
-        int kr = ch / C::CPR, cc = ch % C::CPR;
-        int off = kr * kTile + cc * C::VEC;
-        const int64_t g = (k0 + kr) * ld + cc * C::VEC;
-        cp_async16(sA + off, A + g);
-        cp_async16(sB + off, B + g);
+    __device__ static __forceinline__ int pi(int r) { return (r >> 1) | ((r & 1) << 2); }
+    __device__ static __forceinline__ int wm() { return (threadIdx.x >> 5) & 3; }
+    __device__ static __forceinline__ int wn() { return threadIdx.x >> 7; }
+    __device__ static __forceinline__ int lane() { return threadIdx.x & 31; }
+    // local tile row of accumulator row index i (0..R-1), local tile col of column index j (0..CC-1)
+    __device__ static __forceinline__ int row_of(int i) { return wm() * 32 + i * 8 + pi(lane() >> 2); }
+    __device__ static __forceinline__ int col_of(int j) {
+        return wn() * 64 + (j >> 1) * 8 + pi(2 * (lane() & 3) + (j & 1));
     }
-}
+    // element (point i, feature k) address and the block base pointer
+    __device__ static __forceinline__ const T *block(const T *X, int64_t row0, int64_t ld) { return X + row0 * ld; }
 
-// acc[i][j] = sum_k A[k*ld + row_i] * B[k*ld + col_j] over k < dpad, where A/B point at the
-// first element of the row / column block in the feature-major array (ld = padded points).
-template <typename T>
-__device__ __forceinline__ void contract_tile(const T *__restrict__ A, const T *__restrict__ B, int64_t ld,
-                                              int64_t dpad, T *smem, T (&acc)[8][8]) {
-    using C = Tile<T>;
-    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-    const int ry = thread_ry(), rx = thread_rx();
+    __device__ static __forceinline__ void load_slab(T *sA, T *sB, const T *__restrict__ A, const T *__restrict__ B,
+                                                     int64_t ld, int64_t k0) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = T(0);
-
-    const int nk = static_cast<int>(dpad / C::BK);
-#pragma unroll
-    for (int s = 0; s < C::STAGES - 1; ++s) {
-        if (s < nk) load_slab<T>(smem + s * 2 * C::SLAB, smem + s * 2 * C::SLAB + C::SLAB, A, B, ld,
-                                 static_cast<int64_t>(s) * C::BK);
-        cp_async_commit();
-    }
-    for (int kb = 0; kb < nk; ++kb) {
-        cp_async_wait<C::STAGES - 2>();
-        __syncthreads();
-        const int pf = kb + C::STAGES - 1;
-        if (pf < nk) {
-            const int st = pf % C::STAGES;
-            load_slab<T>(smem + st * 2 * C::SLAB, smem + st * 2 * C::SLAB + C::SLAB, A, B, ld,
-                         static_cast<int64_t>(pf) * C::BK);
+        for (int u = 0; u < 4; ++u) {
+            const int ch = threadIdx.x + u * kThreads;  // 0..1023: row = ch / 8, chunk = ch % 8
+            const int row = ch >> 3, c = ch & 7;
+            const int off = row * BK + ((c ^ (row & 7)) << 1);
+            const int64_t g = row * ld + k0 + c * 2;
+            cp_async16(sA + off, A + g);
+            cp_async16(sB + off, B + g);
         }
-        cp_async_commit();
-        const T *sA = smem + (kb % C::STAGES) * 2 * C::SLAB;
-        const T *sB = sA + C::SLAB;
+    }
+
+    __device__ static __forceinline__ void mma(double (&c)[2], double a, double b) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[0]), "+d"(c[1])
+                     : "d"(a), "d"(b));
+    }
+
+    // acc[i][j] = S[row_of(i)][col_of(j)] = sum_k A[row][k] B[col][k]
+    __device__ static __forceinline__ void contract(const T *__restrict__ A, const T *__restrict__ B, int64_t ld,
+                                                    int64_t dpad, T *smem, T (&acc)[R][CC]) {
 #pragma unroll
-        for (int kk = 0; kk < C::BK; ++kk) {
-            T a[8], b[8];
+        for (int i = 0; i < R; ++i)
 #pragma unroll
-            for (int u = 0; u < 8 / C::VEC; ++u) {
-                V va = *reinterpret_cast<const V *>(sA + kk * kTile + ry * C::VEC + u * 16 * C::VEC);
-                V vb = *reinterpret_cast<const V *>(sB + kk * kTile + rx * C::VEC + u * 16 * C::VEC);
-                const T *pa = reinterpret_cast<const T *>(&va);
-                const T *pb = reinterpret_cast<const T *>(&vb);
+            for (int j = 0; j < CC; ++j) acc[i][j] = 0.0;
+        const int nk = static_cast<int>(dpad / BK);
+        const int ln = lane(), q = ln & 3, prow = pi(ln >> 2);
+        const int arow = wm() * 32 + prow, brow = wn() * 64 + prow;
 #pragma unroll
-                for (int v = 0; v < C::VEC; ++v) {
-                    a[u * C::VEC + v] = pa[v];
-                    b[u * C::VEC + v] = pb[v];
-                }
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < nk) load_slab(smem + s * 2 * SLAB, smem + s * 2 * SLAB + SLAB, A, B, ld, int64_t(s) * BK);
+            cp_async_commit();
+        }
+        for (int kb = 0; kb < nk; ++kb) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            const int pf = kb + STAGES - 1;
+            if (pf < nk) {
+                const int st = pf % STAGES;
+                load_slab(smem + st * 2 * SLAB, smem + st * 2 * SLAB + SLAB, A, B, ld, int64_t(pf) * BK);
             }
+            cp_async_commit();
+            const T *sA = smem + (kb % STAGES) * 2 * SLAB;
+            const T *sB = sA + SLAB;
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int g = 0; g < BK / 8; ++g) {
+                const int c = 4 * g + q;
+                double2 a[4], b[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int r = arow + mt * 8;  // r & 7 == prow
+                    a[mt] = *reinterpret_cast<const double2 *>(sA + r * BK + ((c ^ prow) << 1));
+                }
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) {
+                    const int r = brow + nt * 8;
+                    b[nt] = *reinterpret_cast<const double2 *>(sB + r * BK + ((c ^ prow) << 1));
+                }
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 8; ++nt) {
+                        double(&cc)[2] = *reinterpret_cast<double(*)[2]>(&acc[mt][2 * nt]);
+                        mma(cc, a[mt].x, b[nt].x);
+                    }
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 8; ++nt) {
+                        double(&cc)[2] = *reinterpret_cast<double(*)[2]>(&acc[mt][2 * nt]);
+                        mma(cc, a[mt].y, b[nt].y);
+                    }
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();  // ring is free for reuse by the epilogue
+    }
+
+    // Row sums: rs[i] over this thread's columns -> full-tile row sums in red[128] (deterministic).
+    // red must hold 2*128 elements of scratch.
+    __device__ static __forceinline__ void reduce_rows(T (&rs)[R], T *red) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            rs[i] += __shfl_xor_sync(0xffffffffu, rs[i], 1);
+            rs[i] += __shfl_xor_sync(0xffffffffu, rs[i], 2);
+        }
+        if ((lane() & 3) == 0) {
+#pragma unroll
+            for (int i = 0; i < R; ++i) red[wn() * kTile + row_of(i)] = rs[i];
         }
     }
-    cp_async_wait<0>();
-    __syncthreads();  // ring is free for reuse by the epilogue
-}
+    __device__ static __forceinline__ T row_total(const T *red, int t) { return red[t] + red[kTile + t]; }
+    // Column sums: cs[j] over this thread's rows; scratch 4*128.
+    __device__ static __forceinline__ void reduce_cols(T (&cs)[CC], T *red) {
+#pragma unroll
+        for (int j = 0; j < CC; ++j) {
+            cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 4);
+            cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 8);
+            cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 16);
+        }
+        if ((lane() >> 2) == 0) {
+#pragma unroll
+            for (int j = 0; j < CC; ++j) red[wm() * kTile + col_of(j)] = cs[j];
+        }
+    }
+    __device__ static __forceinline__ T col_total(const T *red, int t) {
+        return (red[t] + red[kTile + t]) + (red[2 * kTile + t] + red[3 * kTile + t]);
+    }
+};
+
+// =====================================================================================
+// fp32: FFMA engine on the feature-major layout X^T[dpad][ld], ld = mpad.
+template <>
+struct Engine<float> {
+    using T = float;
+    static constexpr bool kPointMajor = false;
+    static constexpr int BK = 32;
+    static constexpr int VEC = 4;
+    static constexpr int STAGES = 4;
+    static constexpr int SLAB = BK * kTile;
+    static constexpr size_t SMEM_BYTES = size_t(STAGES) * 2 * SLAB * sizeof(T);  // 128 KiB
+    static constexpr int CPR = kTile * sizeof(T) / 16;  // 16-byte chunks per slab row (32)
+    static constexpr int CHUNKS = BK * CPR / kThreads;  // 4
+    static constexpr int R = 8, CC = 8;
+
+    __device__ static __forceinline__ int ry() { return ((threadIdx.x >> 5) >> 1) * 4 + ((threadIdx.x & 31) >> 3); }
+    __device__ static __forceinline__ int rx() { return ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7); }
+    __device__ static __forceinline__ int micro(int r, int e) { return r * VEC + (e / VEC) * (16 * VEC) + (e % VEC); }
+    __device__ static __forceinline__ int row_of(int i) { return micro(ry(), i); }
+    __device__ static __forceinline__ int col_of(int j) { return micro(rx(), j); }
+    __device__ static __forceinline__ const T *block(const T *X, int64_t row0, int64_t) { return X + row0; }
+
+    __device__ static __forceinline__ void load_slab(T *sA, T *sB, const T *__restrict__ A, const T *__restrict__ B,
+                                                     int64_t ld, int64_t k0) {
+#pragma unroll
+        for (int u = 0; u < CHUNKS; ++u) {
+            const int ch = threadIdx.x + u * kThreads;
+            const int kr = ch / CPR, cc = ch % CPR;
+            const int off = kr * kTile + cc * VEC;
+            const int64_t g = (k0 + kr) * ld + cc * VEC;
+            cp_async16(sA + off, A + g);
+            cp_async16(sB + off, B + g);
+        }
+    }
+
+    __device__ static __forceinline__ void contract(const T *__restrict__ A, const T *__restrict__ B, int64_t ld,
+                                                    int64_t dpad, T *smem, T (&acc)[R][CC]) {
+        const int y = ry(), x = rx();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        const int nk = static_cast<int>(dpad / BK);
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < nk) load_slab(smem + s * 2 * SLAB, smem + s * 2 * SLAB + SLAB, A, B, ld, int64_t(s) * BK);
+            cp_async_commit();
+        }
+        for (int kb = 0; kb < nk; ++kb) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            const int pf = kb + STAGES - 1;
+            if (pf < nk) {
+                const int st = pf % STAGES;
+                load_slab(smem + st * 2 * SLAB, smem + st * 2 * SLAB + SLAB, A, B, ld, int64_t(pf) * BK);
+            }
+            cp_async_commit();
+            const T *sA = smem + (kb % STAGES) * 2 * SLAB;
+            const T *sB = sA + SLAB;
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+                T a[8], b[8];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const float4 va = *reinterpret_cast<const float4 *>(sA + kk * kTile + y * VEC + u * 16 * VEC);
+                    const float4 vb = *reinterpret_cast<const float4 *>(sB + kk * kTile + x * VEC + u * 16 * VEC);
+                    a[u * 4 + 0] = va.x; a[u * 4 + 1] = va.y; a[u * 4 + 2] = va.z; a[u * 4 + 3] = va.w;
+                    b[u * 4 + 0] = vb.x; b[u * 4 + 1] = vb.y; b[u * 4 + 2] = vb.z; b[u * 4 + 3] = vb.w;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+
+    __device__ static __forceinline__ void reduce_rows(T (&rs)[R], T *red) {
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+            rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 1);
+            rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 2);
+            rs[e] += __shfl_xor_sync(0xffffffffu, rs[e], 4);
+        }
+        const int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 7) == 0) {
+#pragma unroll
+            for (int e = 0; e < R; ++e) red[(w & 1) * kTile + row_of(e)] = rs[e];
+        }
+    }
+    __device__ static __forceinline__ T row_total(const T *red, int t) { return red[t] + red[kTile + t]; }
+    __device__ static __forceinline__ void reduce_cols(T (&cs)[CC], T *red) {
+#pragma unroll
+        for (int e = 0; e < CC; ++e) {
+            cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 8);
+            cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 16);
+        }
+        const int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) < 8) {
+#pragma unroll
+            for (int e = 0; e < CC; ++e) red[(w >> 1) * kTile + col_of(e)] = cs[e];
+        }
+    }
+    __device__ static __forceinline__ T col_total(const T *red, int t) {
+        return (red[t] + red[kTile + t]) + (red[2 * kTile + t] + red[3 * kTile + t]);
+    }
+};
 
 // ---- kernel functions on a contracted value s = <x_i, x_j> -------------------
 // RBF uses ||x_i - x_j||^2 = n_i + n_j - 2 s, clamped at 0, with the exact 0 on the diagonal

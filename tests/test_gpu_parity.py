@@ -92,7 +92,8 @@ def check_train(X, y, kernel, kp, C, eps, opts=None, oracle_kw=None, tol=1e-7):
     alpha, b, st, stats = pl.plssvm_train_ex(X, y, kernel, kp["gamma"], kp["degree"], kp["coef0"], C, eps,
                                              opts=opts)
     assert st == st_ref == 0
-    assert abs(stats.iterations - it_ref) <= 2, (stats.iterations, it_ref)
+    # CG iteration counts may legitimately differ by a few between summation orders (R-13)
+    assert abs(stats.iterations - it_ref) <= max(2, 0.05 * it_ref), (stats.iterations, it_ref)
     assert rel(alpha, a_ref) <= tol, rel(alpha, a_ref)
     assert abs(b - b_ref) <= tol * max(abs(b_ref), np.abs(a_ref).max())
     assert abs(alpha.sum()) <= 1e-10 * (1 + np.abs(alpha).max())

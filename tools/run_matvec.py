@@ -1,0 +1,35 @@
+"""Run the Q~p product alone on a BASELINE config (for ncu captures and quick timing).
+
+    python tools/run_matvec.py --config C1 --mode implicit --repeats 3
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2202_12674_b200 as pl  # noqa: E402
+import synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C1")
+ap.add_argument("--mode", default="implicit")
+ap.add_argument("--repeats", type=int, default=3)
+ap.add_argument("--m", type=int, default=0)
+ap.add_argument("--d", type=int, default=0)
+a = ap.parse_args()
+cfg = synth.configs()[a.config]
+m, d = a.m or cfg.m, a.d or cfg.d
+dt = np.float32 if cfg.dtype == "f32" else np.float64
+rng = np.random.default_rng(0)
+X = rng.standard_normal((m, d)).astype(dt)
+p = rng.standard_normal(m - 1).astype(dt)
+mode = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED}[a.mode]
+out, t = pl.plssvm_qtilde_matvec(X, p, cfg.kernel, 1.0 / d, cfg.degree, cfg.coef0, cfg.C, repeats=a.repeats,
+                                 opts=pl.options(mode=mode))
+m1 = m - 1
+fl = 2.0 * d * m1 * (m1 + 1) / 2
+s = np.dtype(dt).itemsize
+print(f"{a.config} m={m} d={d} mode={a.mode}: mean {t[0]*1e3:.3f} ms min {t[1]*1e3:.3f} ms precompute {t[2]*1e3:.3f} ms"
+      f" -> {fl/t[1]/1e12:.2f} TFLOP/s (implicit-equivalent), cached stream {m1*m1*s/t[1]/1e9:.1f} GB/s")
