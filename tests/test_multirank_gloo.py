@@ -1,0 +1,103 @@
+"""World-size-2 (gloo, CPU) check of the row-sharded multi-GPU host logic.
+
+Each rank takes its band from the library's host rule `plssvm_partition`, computes its rows
+of Q~p from the oracle's rows (a stand-in for the device product), and runs the same
+per-iteration exchange sequence as the driver: all-gather of p, all-reduce of p.Ap and of
+delta.  The assembled solution must equal the single-process oracle CG, and the gathered
+product the full product."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, result_path):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    import paper_2202_12674_b200 as pl
+    import synth
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, y, _, _ = synth.planes(300, 7, seed=3)
+    m = X.shape[0]
+    m1 = m - 1
+    b0, b1, mpad = pl.plssvm_partition(m, world, rank)
+    nb = b1 - b0
+    rows = np.arange(b0, b1)
+    valid = rows < m1
+    R = np.zeros((nb, m1))
+    R[valid] = oracle.qtilde_rows(X, rows[valid], oracle.RBF, 0.2, C=1.0)
+
+    def band_product(pfull):  # this rank's rows of Q~ p (padding rows are 0)
+        return R @ pfull[:m1]
+
+    def allgather(band):
+        out = [torch.zeros(nb, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(out, torch.from_numpy(band.copy()))
+        return torch.cat(out).numpy()
+
+    def allreduce(v):
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    # product check
+    p = np.random.default_rng(1).standard_normal(mpad)
+    p[m1:] = 0.0
+    yfull = allgather(band_product(p))
+    # sharded CG (driver sequence), x0 = 0
+    rhs = np.where(valid, y[np.minimum(rows, m - 1)] - y[m - 1], 0.0)
+    x = np.zeros(nb)
+    r = rhs.copy()
+    pb = r.copy()
+    delta = allreduce(r @ r)
+    delta0 = delta
+    it = 0
+    while it < m1 and delta > 1e-20 * delta0:
+        pf = allgather(pb)
+        yb = band_product(pf)
+        pap = allreduce(pb @ yb)
+        a = delta / pap
+        x += a * pb
+        r -= a * yb
+        dnew = allreduce(r @ r)
+        pb = r + (dnew / delta) * pb
+        delta = dnew
+        it += 1
+    xfull = allgather(x)[:m1]
+    if rank == 0:
+        Qt = oracle.qtilde(X, oracle.RBF, 0.2, C=1.0)
+        ref_y = Qt @ p[:m1]
+        xo, ito, st = oracle.cg(Qt, y[:-1] - y[-1], eps=1e-10)
+        np.savez(result_path, y=yfull[:m1], ref_y=ref_y, x=xfull, ref_x=xo, it=it, ito=ito, mpad=mpad)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_row_sharded_cg_gloo(tmp_path, world):
+    path = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    res = np.load(path)
+    assert res["mpad"] % (128 * world) == 0
+    assert np.linalg.norm(res["y"] - res["ref_y"]) <= 1e-13 * np.linalg.norm(res["ref_y"])
+    assert np.linalg.norm(res["x"] - res["ref_x"]) <= 1e-8 * np.linalg.norm(res["ref_x"])
+    assert abs(int(res["it"]) - int(res["ito"])) <= 2
