@@ -149,6 +149,22 @@ PLSSVM_API int plssvm_comm_unique_id(void *id128);
 PLSSVM_API int plssvm_comm_init(const void *id128, int32_t nranks, int32_t rank, int32_t device, plssvm_comm_t *comm);
 PLSSVM_API int plssvm_comm_destroy(plssvm_comm_t comm);
 
+/* Caller-supplied transport (e.g. MPI, or a host-staged gloo exchange in tests): the same
+ * row-sharded driver, with the two collectives it needs delegated to these callbacks.  Both
+ * operate IN PLACE on DEVICE memory of `device`, must be complete (or ordered on `stream`)
+ * when they return, and return 0 on success (anything else aborts the call with
+ * PLSSVM_E_NCCL).  The struct is copied; ctx is passed through untouched. */
+typedef struct {
+    void *ctx;
+    /* buf[0..count) <- sum over ranks of buf[0..count)   (doubles) */
+    int (*allreduce_sum_f64)(void *ctx, double *buf, int64_t count, void *stream);
+    /* rank r's count_per_rank elements live at buf + r * count_per_rank; afterwards every rank
+     * holds all nranks * count_per_rank elements.  dtype: PLSSVM_F64 / PLSSVM_F32. */
+    int (*allgather)(void *ctx, void *buf, int64_t count_per_rank, int32_t dtype, void *stream);
+} plssvm_comm_callbacks_t;
+PLSSVM_API int plssvm_comm_init_callbacks(const plssvm_comm_callbacks_t *cb, int32_t nranks, int32_t rank,
+                                          int32_t device, plssvm_comm_t *comm);
+
 /* Host-side partition rule (no GPU needed): rows [row_begin, row_end) of the padded
  * (m-1)-system owned by `rank` of `nranks`, and the padded length m_pad (a multiple of
  * 128 * nranks).  Rows >= m-1 are padding (masked). */

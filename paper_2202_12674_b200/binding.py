@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CU
 
 EXPORTS = ["plssvm_default_options", "plssvm_train", "plssvm_train_f32", "plssvm_train_ex", "plssvm_predict",
            "plssvm_predict_f32", "plssvm_predict_ex", "plssvm_qtilde_matvec", "plssvm_comm_unique_id",
-           "plssvm_comm_init", "plssvm_comm_destroy", "plssvm_partition", "plssvm_last_error", "plssvm_version",
+           "plssvm_comm_init", "plssvm_comm_init_callbacks", "plssvm_comm_destroy", "plssvm_partition", "plssvm_last_error", "plssvm_version",
            "plssvm_device_count"]
 
 
@@ -43,6 +43,14 @@ class plssvm_stats_t(ct.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+ALLREDUCE_CB = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_void_p)
+ALLGATHER_CB = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_void_p)
+
+
+class plssvm_comm_callbacks_t(ct.Structure):
+    _fields_ = [("ctx", ct.c_void_p), ("allreduce_sum_f64", ALLREDUCE_CB), ("allgather", ALLGATHER_CB)]
 
 
 class PlssvmError(RuntimeError):
@@ -84,6 +92,7 @@ def load(build_if_missing: bool = True):
     L.plssvm_comm_unique_id.argtypes = [vp]
     L.plssvm_comm_init.argtypes = [vp, i32, i32, i32, ct.POINTER(vp)]
     L.plssvm_comm_destroy.argtypes = [vp]
+    L.plssvm_comm_init_callbacks.argtypes = [ct.POINTER(plssvm_comm_callbacks_t), i32, i32, i32, ct.POINTER(vp)]
     L.plssvm_partition.argtypes = [i64, i32, i32, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
     L.plssvm_last_error.restype = ct.c_char_p
     L.plssvm_version.restype = ct.c_char_p
@@ -276,8 +285,90 @@ def plssvm_comm_init(uid: bytes, nranks: int, rank: int, device: int):
     return h.value
 
 
+_CALLBACK_KEEPALIVE = {}
+
+
+def plssvm_comm_init_callbacks(allreduce_sum_f64, allgather, nranks: int, rank: int, device: int):
+    """Communicator whose two collectives are Python callables (see plssvm.h)."""
+    cb = plssvm_comm_callbacks_t(None, ALLREDUCE_CB(allreduce_sum_f64), ALLGATHER_CB(allgather))
+    h = ct.c_void_p()
+    _check(load().plssvm_comm_init_callbacks(ct.byref(cb), nranks, rank, device, ct.byref(h)))
+    _CALLBACK_KEEPALIVE[h.value] = cb
+    return h.value
+
+
 def plssvm_comm_destroy(comm) -> None:
     _check(load().plssvm_comm_destroy(comm))
+    _CALLBACK_KEEPALIVE.pop(comm, None)
+
+
+def comm_host_staged(device: int):
+    """Communicator over torch.distributed (any backend, e.g. gloo) with host staging: each
+    collective synchronises the driver's stream, copies the device buffer to host, runs the
+    torch.distributed collective and copies back.  For testing the row-sharded driver with
+    several processes on ONE GPU (NCCL refuses duplicate devices); not a fast path."""
+    import torch
+    import torch.distributed as dist
+
+    cudart = _cudart()
+    rank, world = dist.get_rank(), dist.get_world_size()
+
+    def d2h(ptr, nbytes, stream):
+        if cudart.cudaStreamSynchronize(ct.c_void_p(stream)) != 0:
+            return None
+        host = torch.empty(nbytes, dtype=torch.uint8)
+        if cudart.cudaMemcpy(ct.c_void_p(host.data_ptr()), ct.c_void_p(ptr), ct.c_size_t(nbytes), 2) != 0:
+            return None
+        return host
+
+    def h2d(ptr, host):
+        # a pageable H2D cudaMemcpy may return before the DMA lands: synchronise the device so
+        # the driver's (non-blocking) stream sees the data
+        st = cudart.cudaMemcpy(ct.c_void_p(ptr), ct.c_void_p(host.data_ptr()), ct.c_size_t(host.numel()), 1)
+        return st or cudart.cudaDeviceSynchronize()
+
+    def allreduce(ctx, buf, count, stream):
+        host = d2h(buf, 8 * count, stream)
+        if host is None:
+            return 1
+        t = host.view(torch.float64)
+        dist.all_reduce(t)
+        return h2d(buf, t.view(torch.uint8))
+
+    def allgather(ctx, buf, count, dtype, stream):
+        es = 8 if dtype == F64 else 4
+        nb = count * es
+        host = d2h(buf + rank * nb, nb, stream)
+        if host is None:
+            return 1
+        parts = [torch.empty(nb, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(parts, host)
+        return h2d(buf, torch.cat(parts))
+
+    return plssvm_comm_init_callbacks(allreduce, allgather, world, rank, device)
+
+
+_cudart_lib = None
+
+
+def _cudart():
+    global _cudart_lib
+    if _cudart_lib is None:
+        import glob
+
+        import torch
+
+        cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime", "lib",
+                                       "libcudart.so*")) + ["libcudart.so.12", "libcudart.so"]
+        for c in cands:
+            try:
+                _cudart_lib = ct.CDLL(c)
+                break
+            except OSError:
+                continue
+        _cudart_lib.cudaMemcpy.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_size_t, ct.c_int]
+        _cudart_lib.cudaStreamSynchronize.argtypes = [ct.c_void_p]
+    return _cudart_lib
 
 
 def comm_from_torch_distributed(device: int):

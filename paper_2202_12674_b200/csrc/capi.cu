@@ -20,6 +20,8 @@
 extern "C" int plssvm_comm_unique_id_impl(void *id128);
 extern "C" int plssvm_comm_init_impl(const void *id128, int32_t nranks, int32_t rank, int32_t device, void **out);
 extern "C" int plssvm_comm_destroy_impl(void *c);
+extern "C" int plssvm_comm_init_callbacks_impl(const plssvm_comm_callbacks_t *cb, int32_t nranks, int32_t rank,
+                                               int32_t device, void **out);
 
 namespace {
 
@@ -219,6 +221,15 @@ int plssvm_comm_init(const void *id128, int32_t nranks, int32_t rank, int32_t de
     if (s) return s;
     s = plssvm_comm_init_impl(id128, nranks, rank, device, comm);
     return s ? fail(s, "ncclCommInitRank failed") : PLSSVM_OK;
+}
+
+int plssvm_comm_init_callbacks(const plssvm_comm_callbacks_t *cb, int32_t nranks, int32_t rank, int32_t device,
+                               plssvm_comm_t *comm) {
+    g_last_error.clear();
+    if (!cb || !comm || !cb->allreduce_sum_f64 || !cb->allgather) return fail(PLSSVM_E_INVALID_ARG, "NULL callback");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PLSSVM_E_INVALID_ARG, "bad rank / nranks");
+    if (device < 0) return fail(PLSSVM_E_INVALID_ARG, "bad device");
+    return plssvm_comm_init_callbacks_impl(cb, nranks, rank, device, comm);
 }
 
 int plssvm_comm_destroy(plssvm_comm_t comm) { return plssvm_comm_destroy_impl(comm); }

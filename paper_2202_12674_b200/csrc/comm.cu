@@ -14,6 +14,8 @@ namespace plssvm {
 struct CommHandle {
     ncclComm_t nccl;
     int rank, nranks, device;
+    bool callbacks;
+    plssvm_comm_callbacks_t cb;
 };
 
 #define PLS_NCCL(call)                                                                                \
@@ -27,12 +29,22 @@ int comm_size(const CommHandle *c) { return c->nranks; }
 int comm_device(const CommHandle *c) { return c->device; }
 
 void comm_allreduce_sum_f64(CommHandle *c, double *buf, int64_t count, void *stream) {
+    if (c->callbacks) {
+        if (c->cb.allreduce_sum_f64(c->cb.ctx, buf, count, stream) != 0)
+            throw Error(PLSSVM_E_NCCL, "user allreduce callback failed");
+        return;
+    }
     PLS_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum, c->nccl,
                            static_cast<cudaStream_t>(stream)));
 }
 
 // In-place all-gather: rank r's shard lives at buf + r * count_per_rank.
 void comm_allgather(CommHandle *c, void *buf, int64_t count_per_rank, int dtype, void *stream) {
+    if (c->callbacks) {
+        if (c->cb.allgather(c->cb.ctx, buf, count_per_rank, dtype, stream) != 0)
+            throw Error(PLSSVM_E_NCCL, "user allgather callback failed");
+        return;
+    }
     const size_t es = dtype == PLSSVM_F32 ? 4 : 8;
     char *b = static_cast<char *>(buf);
     PLS_NCCL(ncclAllGather(b + static_cast<size_t>(c->rank) * count_per_rank * es, b,
@@ -68,7 +80,7 @@ extern "C" int plssvm_comm_init_impl(const void *id128, int32_t nranks, int32_t 
     if (cudaSetDevice(device) != cudaSuccess) return PLSSVM_E_CUDA;
     ncclUniqueId id;
     memcpy(&id, id128, sizeof(id));
-    auto *h = new CommHandle{nullptr, rank, nranks, device};
+    auto *h = new CommHandle{nullptr, rank, nranks, device, false, {}};
     ncclResult_t r = ncclCommInitRank(&h->nccl, nranks, id, rank);
     if (r != ncclSuccess) {
         delete h;
@@ -78,10 +90,16 @@ extern "C" int plssvm_comm_init_impl(const void *id128, int32_t nranks, int32_t 
     return PLSSVM_OK;
 }
 
+extern "C" int plssvm_comm_init_callbacks_impl(const plssvm_comm_callbacks_t *cb, int32_t nranks, int32_t rank,
+                                               int32_t device, void **out) {
+    *out = new CommHandle{nullptr, rank, nranks, device, true, *cb};
+    return PLSSVM_OK;
+}
+
 extern "C" int plssvm_comm_destroy_impl(void *c) {
     auto *h = static_cast<CommHandle *>(c);
     if (!h) return PLSSVM_OK;
-    ncclCommDestroy(h->nccl);
+    if (!h->callbacks) ncclCommDestroy(h->nccl);
     delete h;
     return PLSSVM_OK;
 }
