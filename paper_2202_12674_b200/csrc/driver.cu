@@ -133,12 +133,14 @@ Geometry geometry(int64_t m, int64_t d, int P, int rank) {
 
 // Tiles of this rank: rows I of the band against every column block J; inside the band only
 // the upper triangle J >= I (mirrored), outside it the full row (row sums only).
-std::vector<int2> band_tiles(const Geometry &g) {
+// Each entry is (I, J * NSUB + h): column sub-block h of width 128 / NSUB.
+std::vector<int2> band_tiles(const Geometry &g, int nsub) {
     std::vector<int2> t;
     for (int I = g.band0; I < g.band1; ++I)
         for (int J = 0; J < g.T; ++J) {
             const bool inband = (J >= g.band0 && J < g.band1);
-            if (!inband || J >= I) t.push_back(make_int2(I, J));
+            if (!inband || J >= I)
+                for (int h = 0; h < nsub; ++h) t.push_back(make_int2(I, J * nsub + h));
         }
     return t;
 }
@@ -163,6 +165,15 @@ struct Ctx {
 template <typename T>
 void set_smem_attrs() {
     const int bytes = static_cast<int>(Engine<T>::SMEM_BYTES);
+    PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<LINEAR, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<POLYNOMIAL, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<RBF, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PLS_CUDA(cudaFuncSetAttribute(k_precompute<LINEAR, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PLS_CUDA(cudaFuncSetAttribute(k_precompute<POLYNOMIAL, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PLS_CUDA(cudaFuncSetAttribute(k_precompute<RBF, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<LINEAR, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<POLYNOMIAL, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<RBF, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<LINEAR, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<POLYNOMIAL, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -189,23 +200,23 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
     const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
         case LINEAR:
-            k_matvec_implicit<LINEAR, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm, pfull,
+            k_matvec_implicit<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm, pfull,
                                                                          c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
                                                                          c.Ypart, g.nb);
             break;
         case POLYNOMIAL:
-            k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm,
+            k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm,
                                                                              pfull, c.kp, c.invC, c.scal, g.m1, g.band0,
                                                                              g.band1, c.Ypart, g.nb);
             break;
         default:
-            k_matvec_implicit<RBF, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm, pfull,
+            k_matvec_implicit<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm, pfull,
                                                                       c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
                                                                       c.Ypart, g.nb);
     }
     PLS_CHECK_LAUNCH();
     ++c.launches;
-    return g.T;
+    return g.T * Engine<T>::NSUB;
 }
 
 template <typename T>
@@ -214,15 +225,15 @@ void launch_precompute(Ctx<T> &c) {
     const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
         case LINEAR:
-            k_precompute<LINEAR, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                     c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
             break;
         case POLYNOMIAL:
-            k_precompute<POLYNOMIAL, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                         c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
             break;
         default:
-            k_precompute<RBF, T><<<c.ntiles, kThreads, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                  c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
     }
     PLS_CHECK_LAUNCH();
@@ -232,7 +243,8 @@ void launch_precompute(Ctx<T> &c) {
 template <typename T>
 void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par, int set_delta0) {
     const Geometry &g = c.g;
-    k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, nslots, g.nb, g.g0, g.m1, pband, c.y, mode, c.ylab,
+    k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, nslots, c.cached ? 1 : Engine<T>::NSUB, g.band0,
+                                                       g.nb, g.g0, g.m1, pband, c.y, mode, c.ylab,
                                                        c.r, pout, c.scal, par, set_delta0, c.partials, c.counter, 1);
     PLS_CHECK_LAUNCH();
     ++c.launches;
@@ -288,7 +300,7 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.partials = A.alloc<T>(kVecBlocks);
     c.counter = A.alloc<unsigned>(1);
     PLS_CUDA(cudaMemsetAsync(c.counter, 0, sizeof(unsigned), c.s));
-    std::vector<int2> tl = band_tiles(g);
+    std::vector<int2> tl = band_tiles(g, Engine<T>::NSUB);
     c.ntiles = static_cast<int>(tl.size());
     c.tiles = A.alloc<int2>(c.ntiles);
     PLS_CUDA(cudaMemcpyAsync(c.tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
@@ -340,7 +352,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     T *pband = c.p + g.g0;
 
     c.cached = choose_cached<T>(g, o);
-    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? 1 : g.T) * g.nb);
+    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? 1 : g.T * Engine<T>::NSUB) * g.nb);
     if (c.cached) {
         c.Qc = A.alloc<T>(g.nb * g.mpad);
         launch_precompute<T>(c);
@@ -502,7 +514,7 @@ int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, cons
     PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
     c.cached = (o.mode == PLSSVM_MODE_CACHED) || (o.mode == PLSSVM_MODE_AUTO && choose_cached<T>(g, o));
     if (c.cached) (void)choose_cached<T>(g, o);  // throws E_OOM if CACHED does not fit
-    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? 1 : g.T) * g.nb);
+    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? 1 : g.T * Engine<T>::NSUB) * g.nb);
     double t_pre = 0.0;
     if (c.cached) {
         c.Qc = A.alloc<T>(g.nb * g.mpad);
@@ -574,7 +586,7 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
         PLS_CHECK_LAUNCH();
         launches += 2;
     }
-    const int tilesI = static_cast<int>(npad / kTile), tilesJ = static_cast<int>(mpad / kTile);
+    const int tilesI = static_cast<int>(npad / kTile), tilesJ = static_cast<int>(mpad / EN::TN);
     T *Fpart = A.alloc<T>(static_cast<int64_t>(tilesJ) * npad);
     set_smem_attrs<T>();
     const size_t sm = EN::SMEM_BYTES;
@@ -582,15 +594,15 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     PLS_CUDA(cudaEventRecord(e0, s));
     switch (pb.kernel) {
         case LINEAR:
-            k_predict_tiles<LINEAR, T><<<grid, kThreads, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
+            k_predict_tiles<LINEAR, T><<<grid, Engine<T>::THREADS, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
                                                                   Fpart);
             break;
         case POLYNOMIAL:
-            k_predict_tiles<POLYNOMIAL, T><<<grid, kThreads, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp,
+            k_predict_tiles<POLYNOMIAL, T><<<grid, Engine<T>::THREADS, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp,
                                                                       tilesI, Fpart);
             break;
         default:
-            k_predict_tiles<RBF, T><<<grid, kThreads, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
+            k_predict_tiles<RBF, T><<<grid, Engine<T>::THREADS, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
                                                                Fpart);
     }
     PLS_CHECK_LAUNCH();

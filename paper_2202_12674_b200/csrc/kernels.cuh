@@ -162,7 +162,7 @@ __device__ __forceinline__ T qtilde_value(T s, int64_t gi, int64_t gj, T ni, T n
 // is deterministic.  ld = the engine layout's leading dimension (dpad point-major, mpad
 // feature-major).
 template <int KT, typename T>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
     k_matvec_implicit(const T *__restrict__ X, int64_t ld, int64_t dpad, const int2 *__restrict__ tiles,
                       const T *__restrict__ q, const T *__restrict__ nrm, const T *__restrict__ p, KParams<T> kp,
                       T invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
@@ -171,8 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *smem = reinterpret_cast<T *>(smem_raw);
     const int2 tile = tiles[blockIdx.x];
-    const int I = tile.x, J = tile.y;
-    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
+    const int I = tile.x, Jc = tile.y, J = Jc / E::NSUB;  // Jc: column sub-block of width TN
+    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(Jc) * E::TN;
     T acc[E::R][E::CC];
     E::contract(E::block(X, row0, ld), E::block(X, col0, ld), ld, dpad, smem, acc);
 
@@ -204,27 +204,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             cs[j] = fma(v, pi[i], cs[j]);
         }
     }
-    T *redr = smem;              // [2][128]
-    T *redc = smem + 2 * kTile;  // [4][128]
+    T *redr = smem;              // rows: up to 2 x 128
+    T *redc = smem + 2 * kTile;  // cols: 4 x TN
     E::reduce_rows(rs, redr);
     E::reduce_cols(cs, redc);
     __syncthreads();
+    // slots: row sums of tile (I, Jc) -> slot Jc (rows of I); column sums of a mirrored tile
+    // -> slot I*NSUB (rows of column sub-block Jc).  See k_finalize for the slot validity rule.
     const bool mirrored = (I != J) && (J >= band0) && (J < band1);
     const int64_t lrow0 = row0 - static_cast<int64_t>(band0) * kTile;
-    if (threadIdx.x < kTile) {
-        const int t = threadIdx.x;
-        Ypart[static_cast<int64_t>(J) * band_rows + lrow0 + t] = E::row_total(redr, t);
-    } else if (mirrored) {
-        const int t = threadIdx.x - kTile;
+    for (int t = threadIdx.x; t < kTile; t += E::THREADS)
+        Ypart[static_cast<int64_t>(Jc) * band_rows + lrow0 + t] = E::row_total(redr, t);
+    if (mirrored) {
         const int64_t lcol0 = col0 - static_cast<int64_t>(band0) * kTile;
-        Ypart[static_cast<int64_t>(I) * band_rows + lcol0 + t] = E::col_total(redc, t);
+        for (int t = threadIdx.x; t < E::TN; t += E::THREADS)
+            Ypart[static_cast<int64_t>(I) * E::NSUB * band_rows + lcol0 + t] = E::col_total(redc, t);
     }
 }
 
 // Cached mode, one-time precompute: full rows [band0*128, band1*128) of Q~ (both triangles)
 // into Qc[local_row][mpad] from the same tiles (upper tiles mirrored as transposed stores).
 template <int KT, typename T>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
     k_precompute(const T *__restrict__ X, int64_t ld, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
                  const T *__restrict__ q, const T *__restrict__ nrm, KParams<T> kp, T invC,
                  const double *__restrict__ scal, int64_t m1, int band0, int band1, T *__restrict__ Qc) {
@@ -232,8 +233,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *smem = reinterpret_cast<T *>(smem_raw);
     const int2 tile = tiles[blockIdx.x];
-    const int I = tile.x, J = tile.y;
-    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
+    const int I = tile.x, Jc = tile.y, J = Jc / E::NSUB;
+    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(Jc) * E::TN;
     T acc[E::R][E::CC];
     E::contract(E::block(X, row0, ld), E::block(X, col0, ld), ld, dpad, smem, acc);
     const T Qmm = static_cast<T>(scal[S_QMM]);
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(256) k_gemv_cached(const T *__restrict__ Qc, c
 // / replaced residual (mode 1): r_i = rhs_i - y_i, r.r -> S_DELTA+par (and S_DELTA0 if init).
 template <typename T>
 __global__ void __launch_bounds__(kVecThreads)
-    k_finalize(const T *__restrict__ Ypart, int nslots, int64_t nb, int64_t g0, int64_t m1,
+    k_finalize(const T *__restrict__ Ypart, int nslots, int nsub, int band0, int64_t nb, int64_t g0, int64_t m1,
                const T *__restrict__ pband, T *__restrict__ y, int mode, const T *__restrict__ yl, T *__restrict__ r,
                T *__restrict__ pout, double *scal, int par, int set_delta0, T *partials, unsigned *counter,
                int write_scalar) {
@@ -317,8 +318,18 @@ __global__ void __launch_bounds__(kVecThreads)
     const double ym = scal[S_YM];
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        // Slot validity (k_matvec_implicit): with NSUB = 2 column sub-blocks, the odd slot of an
+        // in-band column block J below this row block R carries nothing (mirrored column sums
+        // go to the even slot).  Fixed slot order -> deterministic.
+        const int R = static_cast<int>((g0 + i) / kTile);
         T s = T(0);
-        for (int k = 0; k < nslots; ++k) s += Ypart[static_cast<int64_t>(k) * nb + i];
+        for (int k = 0; k < nslots; ++k) {
+            if (nsub == 2 && (k & 1)) {
+                const int J = k >> 1;
+                if (J >= band0 && J < R) continue;
+            }
+            s += Ypart[static_cast<int64_t>(k) * nb + i];
+        }
         const bool valid = (g0 + i) < m1;
         s = valid ? s : T(0);
         if (mode == 0) {
@@ -433,15 +444,15 @@ __global__ void k_assemble(const T *__restrict__ xfull, int64_t m, double *scal,
 // forms alpha_j k(z_i, x_j) and row-reduces into Fpart[J][i] (deterministic slots).
 // ldz / ldx: leading dimensions of the two arrays in the engine layout.
 template <int KT, typename T>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
     k_predict_tiles(const T *__restrict__ Zl, int64_t ldz, int64_t npad, const T *__restrict__ Xl, int64_t ldx,
                     int64_t dpad, const T *__restrict__ nz, const T *__restrict__ nx, const T *__restrict__ alpha,
                     KParams<T> kp, int tilesI, T *__restrict__ Fpart) {
     using E = Engine<T>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *smem = reinterpret_cast<T *>(smem_raw);
-    const int I = blockIdx.x % tilesI, J = blockIdx.x / tilesI;
-    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(J) * kTile;
+    const int I = blockIdx.x % tilesI, Jc = blockIdx.x / tilesI;
+    const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(Jc) * E::TN;
     T acc[E::R][E::CC];
     if constexpr (E::kPointMajor) {
         E::contract(E::block(Zl, row0, ldz), E::block(Xl, col0, ldx), dpad, dpad, smem, acc);
@@ -468,7 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     T *redr = smem;
     E::reduce_rows(rs, redr);
     __syncthreads();
-    if (threadIdx.x < kTile) Fpart[static_cast<int64_t>(J) * npad + row0 + threadIdx.x] = E::row_total(redr, threadIdx.x);
+    for (int t = threadIdx.x; t < kTile; t += E::THREADS)
+        Fpart[static_cast<int64_t>(Jc) * npad + row0 + t] = E::row_total(redr, t);
 }
 
 template <typename T>

@@ -5,8 +5,8 @@
 // the size of a full block", block-level caching of 2*blocksize points' feature
 // slabs in shared memory and thread-level register blocking.
 //
-// A CTA of 256 threads owns a 128 x 128 tile S = X_I X_J^T (row block I, column block J); the
-// contraction over features runs in 128-byte feature slabs staged by a 4-deep cp.async ring.
+// A CTA owns a 128 x TN tile S = X_I X_J^T (row block I, column block J); the contraction over
+// features runs in 128-byte feature slabs staged by a 4-deep cp.async ring.
 //
 //  * fp64 (Engine<double>): DMMA.8x8x4 tensor-core MMAs (mma.sync m8n8k4 f64; tcgen05 has no
 //    f64 kind).  Measured on this B200: DMMA 37.1 TFLOP/s vs DFMA 33.4 (profiles/r01_fp64_peak.txt).
@@ -16,8 +16,9 @@
 //    A and B use the same permutation).  Smem rows are 128 B with the chunk swizzle
 //    c ^ (row & 7), and fragment row rho maps to tile row pi(rho) = (rho >> 1) | ((rho & 1) << 2)
 //    so the 8 lanes of each LDS.128 phase hit 8 distinct 16-byte bank groups (no conflicts).
-//    Warp grid 4 (M) x 2 (N); warp tile 32 x 64 = 4 x 8 MMA tiles; 64 fp64 accumulators/thread.
-//  * fp32 (Engine<float>): FFMA register micro-tiles 8 x 8 on the FEATURE-major layout
+//    4 warps (M) per CTA, warp tile 32 x 64 = 4 x 8 MMA tiles, 64 fp64 accumulators/thread,
+//    CTA tile 128 x 64, two CTAs per SM (epilogue of one overlaps the MMAs of the other).
+//  * fp32 (Engine<float>): 256 threads, 128 x 128 tile, FFMA register micro-tiles 8 x 8 on the FEATURE-major layout
 //    X^T[dpad][mpad] (the paper's column-major layout); thread (ry, rx) owns rows
 //    ry*4 + 64u + v, every smem read is one conflict-free LDS.128.
 #pragma once
@@ -39,40 +40,46 @@ template <typename T>
 struct Engine;
 
 // =====================================================================================
-// fp64: DMMA engine on the point-major layout X[mpad][ld], ld = dpad.
+// fp64: DMMA engine on the point-major layout X[mpad][ld], ld = dpad.  CTA = 4 warps (128
+// threads) owning a 128 x 64 tile (warp tile 32 x 64), two CTAs per SM: while one CTA runs its
+// epilogue (kernel function, exp, reductions) the other keeps the tensor pipe busy.
 template <>
 struct Engine<double> {
     using T = double;
     static constexpr bool kPointMajor = true;
+    static constexpr int THREADS = 128;
+    static constexpr int MIN_BLOCKS = 2;           // CTAs per SM
+    static constexpr int TN = 64;                  // tile columns (rows = kTile = 128)
+    static constexpr int NSUB = kTile / TN;        // column sub-blocks per 128-block
     static constexpr int BK = 16;                  // features per slab (128 B per row)
     static constexpr int STAGES = 4;
-    static constexpr int SLAB = kTile * BK;        // doubles per operand slab (16 KiB)
-    static constexpr size_t SMEM_BYTES = size_t(STAGES) * 2 * SLAB * sizeof(T);  // 128 KiB
+    static constexpr int SLAB_A = kTile * BK, SLAB_B = TN * BK;
+    static constexpr int STAGE = SLAB_A + SLAB_B;
+    static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE * sizeof(T);  // 96 KiB
     static constexpr int R = 4;                    // accumulator rows per thread (m-tiles)
     static constexpr int CC = 16;                  // accumulator columns per thread (8 n-tiles x 2)
 
     __device__ static __forceinline__ int pi(int r) { return (r >> 1) | ((r & 1) << 2); }
-    __device__ static __forceinline__ int wm() { return (threadIdx.x >> 5) & 3; }
-    __device__ static __forceinline__ int wn() { return threadIdx.x >> 7; }
+    __device__ static __forceinline__ int wm() { return threadIdx.x >> 5; }
     __device__ static __forceinline__ int lane() { return threadIdx.x & 31; }
     // local tile row of accumulator row index i (0..R-1), local tile col of column index j (0..CC-1)
     __device__ static __forceinline__ int row_of(int i) { return wm() * 32 + i * 8 + pi(lane() >> 2); }
-    __device__ static __forceinline__ int col_of(int j) {
-        return wn() * 64 + (j >> 1) * 8 + pi(2 * (lane() & 3) + (j & 1));
-    }
-    // element (point i, feature k) address and the block base pointer
+    __device__ static __forceinline__ int col_of(int j) { return (j >> 1) * 8 + pi(2 * (lane() & 3) + (j & 1)); }
     __device__ static __forceinline__ const T *block(const T *X, int64_t row0, int64_t ld) { return X + row0 * ld; }
 
     __device__ static __forceinline__ void load_slab(T *sA, T *sB, const T *__restrict__ A, const T *__restrict__ B,
                                                      int64_t ld, int64_t k0) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int ch = threadIdx.x + u * kThreads;  // 0..1023: row = ch / 8, chunk = ch % 8
+        for (int u = 0; u < (kTile * 8) / THREADS; ++u) {  // A: 128 rows x 8 chunks of 16 B
+            const int ch = threadIdx.x + u * THREADS;
             const int row = ch >> 3, c = ch & 7;
-            const int off = row * BK + ((c ^ (row & 7)) << 1);
-            const int64_t g = row * ld + k0 + c * 2;
-            cp_async16(sA + off, A + g);
-            cp_async16(sB + off, B + g);
+            cp_async16(sA + row * BK + ((c ^ (row & 7)) << 1), A + row * ld + k0 + c * 2);
+        }
+#pragma unroll
+        for (int u = 0; u < (TN * 8) / THREADS; ++u) {     // B: 64 rows x 8 chunks
+            const int ch = threadIdx.x + u * THREADS;
+            const int row = ch >> 3, c = ch & 7;
+            cp_async16(sB + row * BK + ((c ^ (row & 7)) << 1), B + row * ld + k0 + c * 2);
         }
     }
 
@@ -91,10 +98,10 @@ struct Engine<double> {
             for (int j = 0; j < CC; ++j) acc[i][j] = 0.0;
         const int nk = static_cast<int>(dpad / BK);
         const int ln = lane(), q = ln & 3, prow = pi(ln >> 2);
-        const int arow = wm() * 32 + prow, brow = wn() * 64 + prow;
+        const int arow = wm() * 32 + prow, brow = prow;
 #pragma unroll
         for (int s = 0; s < STAGES - 1; ++s) {
-            if (s < nk) load_slab(smem + s * 2 * SLAB, smem + s * 2 * SLAB + SLAB, A, B, ld, int64_t(s) * BK);
+            if (s < nk) load_slab(smem + s * STAGE, smem + s * STAGE + SLAB_A, A, B, ld, int64_t(s) * BK);
             cp_async_commit();
         }
         for (int kb = 0; kb < nk; ++kb) {
@@ -103,11 +110,11 @@ struct Engine<double> {
             const int pf = kb + STAGES - 1;
             if (pf < nk) {
                 const int st = pf % STAGES;
-                load_slab(smem + st * 2 * SLAB, smem + st * 2 * SLAB + SLAB, A, B, ld, int64_t(pf) * BK);
+                load_slab(smem + st * STAGE, smem + st * STAGE + SLAB_A, A, B, ld, int64_t(pf) * BK);
             }
             cp_async_commit();
-            const T *sA = smem + (kb % STAGES) * 2 * SLAB;
-            const T *sB = sA + SLAB;
+            const T *sA = smem + (kb % STAGES) * STAGE;
+            const T *sB = sA + SLAB_A;
 #pragma unroll
             for (int g = 0; g < BK / 8; ++g) {
                 const int c = 4 * g + q;
@@ -142,8 +149,8 @@ struct Engine<double> {
         __syncthreads();  // ring is free for reuse by the epilogue
     }
 
-    // Row sums: rs[i] over this thread's columns -> full-tile row sums in red[128] (deterministic).
-    // red must hold 2*128 elements of scratch.
+    // Row sums rs[i] (over this thread's columns) -> red[128] : each tile row is owned by one
+    // warp and 4 lanes (deterministic shuffle tree).  Scratch: 128 elements.
     __device__ static __forceinline__ void reduce_rows(T (&rs)[R], T *red) {
 #pragma unroll
         for (int i = 0; i < R; ++i) {
@@ -152,11 +159,11 @@ struct Engine<double> {
         }
         if ((lane() & 3) == 0) {
 #pragma unroll
-            for (int i = 0; i < R; ++i) red[wn() * kTile + row_of(i)] = rs[i];
+            for (int i = 0; i < R; ++i) red[row_of(i)] = rs[i];
         }
     }
-    __device__ static __forceinline__ T row_total(const T *red, int t) { return red[t] + red[kTile + t]; }
-    // Column sums: cs[j] over this thread's rows; scratch 4*128.
+    __device__ static __forceinline__ T row_total(const T *red, int t) { return red[t]; }
+    // Column sums cs[j] (over this thread's rows) -> 4 warps x TN partials.  Scratch: 4*TN.
     __device__ static __forceinline__ void reduce_cols(T (&cs)[CC], T *red) {
 #pragma unroll
         for (int j = 0; j < CC; ++j) {
@@ -166,11 +173,11 @@ struct Engine<double> {
         }
         if ((lane() >> 2) == 0) {
 #pragma unroll
-            for (int j = 0; j < CC; ++j) red[wm() * kTile + col_of(j)] = cs[j];
+            for (int j = 0; j < CC; ++j) red[wm() * TN + col_of(j)] = cs[j];
         }
     }
     __device__ static __forceinline__ T col_total(const T *red, int t) {
-        return (red[t] + red[kTile + t]) + (red[2 * kTile + t] + red[3 * kTile + t]);
+        return (red[t] + red[TN + t]) + (red[2 * TN + t] + red[3 * TN + t]);
     }
 };
 
@@ -180,6 +187,10 @@ template <>
 struct Engine<float> {
     using T = float;
     static constexpr bool kPointMajor = false;
+    static constexpr int THREADS = kThreads;
+    static constexpr int MIN_BLOCKS = 1;
+    static constexpr int TN = kTile;
+    static constexpr int NSUB = 1;
     static constexpr int BK = 32;
     static constexpr int VEC = 4;
     static constexpr int STAGES = 4;
