@@ -47,6 +47,16 @@ def measured_peaks():
         return {}
 
 
+def traffic_for(key):
+    """ncu-measured DRAM bytes per launch of the dominant kernel (profiles/roofline_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as fh:
+            e = json.load(fh).get(key)
+        return None if e is None else e["dram_read_bytes"] + e["dram_write_bytes"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -273,10 +283,13 @@ def main():
         fl = matvec_flops(cfg.m, cfg.d) / world  # this rank's share (symmetric work split)
         peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else FP32_PEAK_TFLOPS
         achieved = fl / avg_mv / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "k_matvec_implicit",
+        roof = {"bound": "tensor" if cfg.dtype == "f64" else "alu", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic_for(f"{cfg.name}/implicit/k_matvec_implicit") if world == 1 else None,
+                "traffic_unit": "bytes per launch (ncu dram read+write)", "kernel": "k_matvec_implicit",
                 "per_launch": f"2*d*E flops, E = m'(m'+1)/2 distinct Q~ entries ({fl:.4g} flops per launch per rank)",
-                "peak_source": "derived: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md); fp32: 128 FFMA/clk",
+                "peak_source": "fp64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2 (DMMA measured 37.1, "
+                               "profiles/r01_fp64_peak.txt); fp32: 128 FFMA/clk (DESIGN.md)",
                 "avg_launch_s": avg_mv}
     else:
         s = 8 if cfg.dtype == "f64" else 4
@@ -285,7 +298,7 @@ def main():
         peak = measured_peaks().get("hbm_gbs", 6650.0)
         achieved = by / avg_mv / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "k_gemv_cached", "per_launch": f"{by:.4g} bytes of cached Q~ band",
+                "traffic": traffic_for(f"{cfg.name}/cached/k_gemv_cached") if world == 1 else None, "kernel": "k_gemv_cached", "per_launch": f"{by:.4g} bytes of cached Q~ band",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)", "avg_launch_s": avg_mv}
 
     line = {"metric": METRIC, "value": iters / t, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -133,15 +133,22 @@ Geometry geometry(int64_t m, int64_t d, int P, int rank) {
 
 // Tiles of this rank: rows I of the band against every column block J; inside the band only
 // the upper triangle J >= I (mirrored), outside it the full row (row sums only).
-// Each entry is (I, J * NSUB + h): column sub-block h of width 128 / NSUB.
+// Each entry is (I, J * NSUB + h): column sub-block h of width 128 / NSUB.  Raster order for
+// L2 reuse: row blocks in groups of kGroup; inside a group the column sub-blocks advance
+// slowest and the group's rows fastest, so the ~2 x 148 co-resident CTAs touch kGroup row
+// blocks and a few column blocks of X instead of a whole row of tiles (all of X).
 std::vector<int2> band_tiles(const Geometry &g, int nsub) {
+    constexpr int kGroup = 8;
     std::vector<int2> t;
-    for (int I = g.band0; I < g.band1; ++I)
-        for (int J = 0; J < g.T; ++J) {
-            const bool inband = (J >= g.band0 && J < g.band1);
-            if (!inband || J >= I)
-                for (int h = 0; h < nsub; ++h) t.push_back(make_int2(I, J * nsub + h));
-        }
+    for (int I0 = g.band0; I0 < g.band1; I0 += kGroup) {
+        const int I1 = std::min(I0 + kGroup, g.band1);
+        for (int J = 0; J < g.T; ++J)
+            for (int h = 0; h < nsub; ++h)
+                for (int I = I0; I < I1; ++I) {
+                    const bool inband = (J >= g.band0 && J < g.band1);
+                    if (!inband || J >= I) t.push_back(make_int2(I, J * nsub + h));
+                }
+    }
     return t;
 }
 

@@ -18,6 +18,7 @@ ap.add_argument("--mode", default="implicit")
 ap.add_argument("--repeats", type=int, default=3)
 ap.add_argument("--m", type=int, default=0)
 ap.add_argument("--d", type=int, default=0)
+ap.add_argument("--kernel", type=int, default=-1)
 a = ap.parse_args()
 cfg = synth.configs()[a.config]
 m, d = a.m or cfg.m, a.d or cfg.d
@@ -26,10 +27,11 @@ rng = np.random.default_rng(0)
 X = rng.standard_normal((m, d)).astype(dt)
 p = rng.standard_normal(m - 1).astype(dt)
 mode = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED}[a.mode]
-out, t = pl.plssvm_qtilde_matvec(X, p, cfg.kernel, 1.0 / d, cfg.degree, cfg.coef0, cfg.C, repeats=a.repeats,
+kern = cfg.kernel if a.kernel < 0 else a.kernel
+out, t = pl.plssvm_qtilde_matvec(X, p, kern, 1.0 / d, cfg.degree, cfg.coef0, cfg.C, repeats=a.repeats,
                                  opts=pl.options(mode=mode))
 m1 = m - 1
 fl = 2.0 * d * m1 * (m1 + 1) / 2
 s = np.dtype(dt).itemsize
-print(f"{a.config} m={m} d={d} mode={a.mode}: mean {t[0]*1e3:.3f} ms min {t[1]*1e3:.3f} ms precompute {t[2]*1e3:.3f} ms"
+print(f"{a.config} m={m} d={d} kernel={kern} mode={a.mode}: mean {t[0]*1e3:.3f} ms min {t[1]*1e3:.3f} ms precompute {t[2]*1e3:.3f} ms"
       f" -> {fl/t[1]/1e12:.2f} TFLOP/s (implicit-equivalent), cached stream {m1*m1*s/t[1]/1e9:.1f} GB/s")
