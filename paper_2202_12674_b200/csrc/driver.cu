@@ -322,6 +322,14 @@ template <typename T>
 bool choose_cached(const Geometry &g, const plssvm_options_t &o) {
     if (o.mode == PLSSVM_MODE_IMPLICIT) return false;
     const int64_t need = g.nb * g.mpad * static_cast<int64_t>(sizeof(T));
+    // memory this process' stream-ordered pool holds but does not use counts as free
+    int dev = 0;
+    PLS_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        PLS_CUDA(cudaDeviceSynchronize());
+        cudaMemPoolTrimTo(pool, 0);
+    }
     size_t free_b = 0, total_b = 0;
     PLS_CUDA(cudaMemGetInfo(&free_b, &total_b));
     int64_t budget = o.cache_budget_bytes > 0 ? o.cache_budget_bytes : static_cast<int64_t>(0.9 * free_b);

@@ -1,0 +1,99 @@
+"""Per-config measurement table (BASELINE metric: 'every config reports CG iterations/s and
+FLOP/s or GB/s fraction of peak'): one full training per config on one GPU, on the config's
+synthetic data, with the mode the config names.  Writes one JSON object per line.
+
+    python tools/sweep.py [--configs C0,C1,C2,C3,C4] [--out profiles/rNN_sweep.jsonl]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2202_12674_b200 as pl  # noqa: E402
+import synth  # noqa: E402
+
+FP64_PEAK = 148 * 64 * 2 * 1.965e9 / 1e12
+FP32_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def hbm_peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except (OSError, KeyError, ValueError):
+        return 6650.0
+
+
+MODES = {"C0": ["implicit"], "C1": ["implicit", "cached"], "C2": ["cached", "implicit"], "C3": ["cached", "implicit"],
+         "C4": ["cached"]}
+
+
+def run(cfg, mode, repeat=2):
+    X, y, Z, yz = synth.config_data(cfg)
+    dev = torch.device("cuda", 0)
+    tX, ty, tZ = (torch.from_numpy(a).to(dev) for a in (X, y, Z))
+    kw = dict(gamma=cfg.gamma, degree=cfg.degree, coef0=cfg.coef0)
+    md = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED}[mode]
+    best = None
+    for _ in range(repeat):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        alpha, b, st, s = pl.plssvm_train_ex(tX, ty, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=pl.options(mode=md), **kw)
+        torch.cuda.synchronize()
+        tt = time.perf_counter() - t0
+        if best is None or tt < best[0]:
+            best = (tt, s, alpha, b, st)
+    tt, s, alpha, b, st = best
+    f, lab, (tk, _) = pl.plssvm_predict_ex(tX, alpha, float(b.item()), tZ, cfg.kernel, **kw)
+    acc = float((lab.cpu().numpy() == yz.astype(np.int32)).mean()) if len(yz) else None
+    m1 = cfg.m - 1
+    fl = 2.0 * cfg.d * m1 * (m1 + 1) / 2
+    peak_f = FP64_PEAK if cfg.dtype == "f64" else FP32_PEAK
+    mv = s.t_matvec / max(1, s.iterations)
+    row = {"config": cfg.name, "m": cfg.m, "d": cfg.d, "kernel": cfg.kernel, "dtype": cfg.dtype, "mode": mode,
+           "status": st, "iterations": s.iterations, "rel_residual": s.rel_residual, "train_s": tt,
+           "cg_s": s.t_cg, "precompute_s": s.t_precompute, "cg_iterations_per_s": s.iterations / s.t_cg,
+           "matvec_ms": 1e3 * mv, "bytes_per_gpu": s.bytes_per_gpu,
+           "predict_s": tk, "n_test": cfg.n_test, "test_accuracy": acc}
+    if mode == "implicit":
+        row["matvec_tflops"] = fl / mv / 1e12
+        row["frac_of_peak"] = row["matvec_tflops"] / peak_f
+        row["peak_tflops"] = peak_f
+    else:
+        sz = 8 if cfg.dtype == "f64" else 4
+        mpad = math.ceil(cfg.m / 128) * 128
+        row["matvec_gbs"] = mpad * mpad * sz / mv / 1e9
+        row["frac_of_peak"] = row["matvec_gbs"] / hbm_peak()
+        row["peak_gbs"] = hbm_peak()
+        row["precompute_tflops_equiv"] = fl / s.t_precompute / 1e12 if s.t_precompute > 0 else None
+    if cfg.n_test:
+        row["predict_tflops"] = 2.0 * cfg.n_test * cfg.m * cfg.d / tk / 1e12
+    return row
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="C0,C1,C2,C3,C4")
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    cfgs = synth.configs()
+    out = open(a.out, "w") if a.out else None
+    for name in a.configs.split(","):
+        for mode in MODES[name]:
+            row = run(cfgs[name], mode)
+            line = json.dumps(row)
+            print(line, flush=True)
+            if out:
+                out.write(line + "\n")
+                out.flush()
+
+
+if __name__ == "__main__":
+    main()
