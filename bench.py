@@ -298,7 +298,7 @@ def main():
         peak = measured_peaks().get("hbm_gbs", 6650.0)
         achieved = by / avg_mv / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic_for(f"{cfg.name}/cached/k_gemv_cached") if world == 1 else None, "kernel": "k_gemv_cached", "per_launch": f"{by:.4g} bytes of cached Q~ band",
+                "traffic": traffic_for(f"{cfg.name}/cached/k_gemv_tiled") if world == 1 else None, "kernel": "k_gemv_tiled", "per_launch": f"{by:.4g} bytes of cached Q~ band",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)", "avg_launch_s": avg_mv}
 
     line = {"metric": METRIC, "value": iters / t, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -94,7 +94,9 @@ typedef struct {
     double rel_residual;             /* ||r|| / ||r0|| of the recurrence at exit */
     int32_t mode_used;               /* PLSSVM_MODE_IMPLICIT or PLSSVM_MODE_CACHED */
     int32_t num_ranks;               /* 1, or the communicator size */
-    double t_h2d, t_transform, t_q, t_precompute, t_cg, t_bias_d2h, t_total;
+    double t_h2d, t_transform, t_q;
+    double t_alloc;                  /* device work-buffer allocation (stream-ordered pool) */
+    double t_precompute, t_cg, t_bias_d2h, t_total;
     double t_matvec;                 /* summed duration of the Q~p kernels (CUDA events) */
     double t_matvec_min;             /* shortest single Q~p kernel duration */
     int64_t bytes_per_gpu;           /* device bytes allocated by this call on this GPU */

@@ -36,7 +36,8 @@ class plssvm_options_t(ct.Structure):
 class plssvm_stats_t(ct.Structure):
     _fields_ = [("iterations", ct.c_int64), ("matvecs", ct.c_int64), ("rel_residual", ct.c_double),
                 ("mode_used", ct.c_int32), ("num_ranks", ct.c_int32), ("t_h2d", ct.c_double),
-                ("t_transform", ct.c_double), ("t_q", ct.c_double), ("t_precompute", ct.c_double),
+                ("t_transform", ct.c_double), ("t_q", ct.c_double), ("t_alloc", ct.c_double),
+                ("t_precompute", ct.c_double),
                 ("t_cg", ct.c_double), ("t_bias_d2h", ct.c_double), ("t_total", ct.c_double),
                 ("t_matvec", ct.c_double), ("t_matvec_min", ct.c_double), ("bytes_per_gpu", ct.c_int64),
                 ("gpu_launches", ct.c_int64), ("launches_in_cg", ct.c_int64)]

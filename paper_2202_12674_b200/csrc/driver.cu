@@ -166,6 +166,7 @@ struct Ctx {
     int2 *tiles;
     int ntiles;
     bool cached;
+    int nsplit = 1;  // cached GEMV: column splits per row block
     int64_t launches = 0, launches_cg = 0;
 };
 
@@ -192,17 +193,23 @@ void set_smem_attrs() {
     PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
+// Cached GEMV split-K factor: >= 16 CTAs per SM in total (several waves of the ~3 resident
+// CTAs per SM), so the last partial wave costs little even when the band has few row blocks.
+int gemv_splits(const Geometry &g) {
+    const int rowblocks = static_cast<int>(g.nb / kTile);
+    return std::max(1, std::min(g.T, static_cast<int>(ceil_div(16 * 148, rowblocks))));
+}
+
 // Q~ times the full vector `pfull` -> Ypart (slots) ; returns the number of slots to finalize.
 template <typename T>
 int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
     const Geometry &g = c.g;
     if (c.cached) {
-        const int64_t warps = ceil_div(g.nb, 4);
-        const int blocks = static_cast<int>(ceil_div(warps * 32, 256));
-        k_gemv_cached<T><<<blocks, 256, 0, c.s>>>(c.Qc, pfull, g.mpad, g.nb, c.Ypart);
+        const int rowblocks = static_cast<int>(g.nb / kTile);
+        k_gemv_tiled<T><<<rowblocks * c.nsplit, 256, 0, c.s>>>(c.Qc, pfull, g.T, c.nsplit, g.nb, c.Ypart);
         PLS_CHECK_LAUNCH();
         ++c.launches;
-        return 1;
+        return c.nsplit;
     }
     const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
@@ -322,16 +329,21 @@ template <typename T>
 bool choose_cached(const Geometry &g, const plssvm_options_t &o) {
     if (o.mode == PLSSVM_MODE_IMPLICIT) return false;
     const int64_t need = g.nb * g.mpad * static_cast<int64_t>(sizeof(T));
-    // memory this process' stream-ordered pool holds but does not use counts as free
+    // memory this process' stream-ordered pool holds but does not use counts as free (it is
+    // reused by the allocation below without re-mapping; trimming it would cost ~1 s per 100 GB)
     int dev = 0;
     PLS_CUDA(cudaGetDevice(&dev));
     cudaMemPool_t pool;
+    uint64_t pool_idle = 0;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        PLS_CUDA(cudaDeviceSynchronize());
-        cudaMemPoolTrimTo(pool, 0);
+        uint64_t reserved = 0, used = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        pool_idle = reserved > used ? reserved - used : 0;
     }
     size_t free_b = 0, total_b = 0;
     PLS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    free_b += pool_idle;
     int64_t budget = o.cache_budget_bytes > 0 ? o.cache_budget_bytes : static_cast<int64_t>(0.9 * free_b);
     budget = std::min<int64_t>(budget, static_cast<int64_t>(free_b) - (int64_t(1) << 28));
     if (need <= budget) return true;
@@ -351,8 +363,8 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     c.comm = static_cast<CommHandle *>(o.comm);
     Arena A(c.s);
     Events E;
-    cudaEvent_t e0 = E.make(), e_h2d = E.make(), e_tr = E.make(), e_q = E.make(), e_pre = E.make(), e_cg = E.make(),
-                e_end = E.make();
+    cudaEvent_t e0 = E.make(), e_h2d = E.make(), e_tr = E.make(), e_q = E.make(), e_alloc = E.make(), e_pre = E.make(),
+                e_cg = E.make(), e_end = E.make();
     const auto wall0 = std::chrono::steady_clock::now();
     PLS_CUDA(cudaEventRecord(e0, c.s));
     setup<T>(c, A, pb, o, true, E, e_h2d, e_tr, e_q);
@@ -367,11 +379,11 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     T *pband = c.p + g.g0;
 
     c.cached = choose_cached<T>(g, o);
-    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? 1 : g.T * Engine<T>::NSUB) * g.nb);
-    if (c.cached) {
-        c.Qc = A.alloc<T>(g.nb * g.mpad);
-        launch_precompute<T>(c);
-    }
+    c.nsplit = gemv_splits(g);
+    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? c.nsplit : g.T * Engine<T>::NSUB) * g.nb);
+    if (c.cached) c.Qc = A.alloc<T>(g.nb * g.mpad);
+    PLS_CUDA(cudaEventRecord(e_alloc, c.s));
+    if (c.cached) launch_precompute<T>(c);
     PLS_CUDA(cudaEventRecord(e_pre, c.s));
 
     // ---- CG init (a2) ----
@@ -495,7 +507,8 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         st->t_h2d = elapsed(e0, e_h2d);
         st->t_transform = elapsed(e_h2d, e_tr);
         st->t_q = elapsed(e_tr, e_q);
-        st->t_precompute = elapsed(e_q, e_pre);
+        st->t_alloc = elapsed(e_q, e_alloc);
+        st->t_precompute = elapsed(e_alloc, e_pre);
         st->t_cg = elapsed(e_pre, e_cg);
         st->t_bias_d2h = elapsed(e_cg, e_end);
         st->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
@@ -529,7 +542,8 @@ int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, cons
     PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
     c.cached = (o.mode == PLSSVM_MODE_CACHED) || (o.mode == PLSSVM_MODE_AUTO && choose_cached<T>(g, o));
     if (c.cached) (void)choose_cached<T>(g, o);  // throws E_OOM if CACHED does not fit
-    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? 1 : g.T * Engine<T>::NSUB) * g.nb);
+    c.nsplit = gemv_splits(g);
+    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? c.nsplit : g.T * Engine<T>::NSUB) * g.nb);
     double t_pre = 0.0;
     if (c.cached) {
         c.Qc = A.alloc<T>(g.nb * g.mpad);

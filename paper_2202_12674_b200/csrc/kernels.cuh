@@ -4,7 +4,7 @@
 //   k_q_norms          q_i = k(x_i, x_m), n_i = ||x_i||^2, Q_mm          (Eq. 12)
 //   k_matvec_implicit  Ypart[slot][row] = partial Q~p per tile            (Eq. 16)
 //   k_precompute       Q~ band tiles -> HBM (cached mode, north_star N1)
-//   k_gemv_cached      y_band = Q~_band p streamed from HBM
+//   k_gemv_tiled       y_band = Q~_band p streamed from HBM (tiled layout)
 //   k_finalize         y = sum_slots Ypart ; p.y  (deterministic)
 //   k_update_xr        x += a p ; r -= a y ; r.r  (fused axpy + norm)
 //   k_update_p         p = r + b p
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
 }
 
 // Cached mode, one-time precompute: full rows [band0*128, band1*128) of Q~ (both triangles)
-// into Qc[local_row][mpad] from the same tiles (upper tiles mirrored as transposed stores).
+// into the band's tiled array Qc from the same tiles (upper tiles mirrored as transposed stores).
 template <int KT, typename T>
 __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
     k_precompute(const T *__restrict__ X, int64_t ld, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
@@ -239,66 +239,92 @@ __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
     E::contract(E::block(X, row0, ld), E::block(X, col0, ld), ld, dpad, smem, acc);
     const T Qmm = static_cast<T>(scal[S_QMM]);
     const bool mirrored = (I != J) && (J >= band0) && (J < band1);
-    const int64_t b0 = static_cast<int64_t>(band0) * kTile;
+    // Stage the finished 128 x TN tile in shared memory (the ring is free), then write it with
+    // coalesced row stores -- and, for a mirrored tile, the transpose with coalesced stores too.
+    constexpr int SLD = E::TN + 1;  // padded row: conflict-light column reads
+    T *S = smem;
 #pragma unroll
     for (int i = 0; i < E::R; ++i) {
-        const int64_t gi = row0 + E::row_of(i);
+        const int lr = E::row_of(i);
+        const int64_t gi = row0 + lr;
         const T qi = q[gi], ni = (KT == RBF) ? nrm[gi] : T(0);
 #pragma unroll
         for (int j = 0; j < E::CC; ++j) {
-            const int64_t gj = col0 + E::col_of(j);
+            const int lc = E::col_of(j);
+            const int64_t gj = col0 + lc;
             const T qj = q[gj], nj = (KT == RBF) ? nrm[gj] : T(0);
-            const T v = qtilde_value<KT, T>(acc[i][j], gi, gj, ni, nj, qi, qj, Qmm, invC, m1, kp);
-            Qc[(gi - b0) * mpad + gj] = v;
-            if (mirrored) Qc[(gj - b0) * mpad + gi] = v;
+            S[lr * SLD + lc] = qtilde_value<KT, T>(acc[i][j], gi, gj, ni, nj, qi, qj, Qmm, invC, m1, kp);
+        }
+    }
+    __syncthreads();
+    // Tiled layout (see k_gemv_tiled): tile (Ib, J) of this band at ((Ib - band0) * T + J) * 128^2,
+    // row-major 128 x 128 inside.  Every store below is a contiguous run (TLB- and DRAM-friendly).
+    const int T_tiles = static_cast<int>(mpad / kTile);
+    const int h = Jc % E::NSUB;
+    T *dst = Qc + (static_cast<int64_t>(I - band0) * T_tiles + J) * (kTile * kTile) + h * E::TN;
+    for (int idx = threadIdx.x; idx < kTile * E::TN; idx += E::THREADS) {
+        const int r = idx / E::TN, c = idx % E::TN;
+        dst[r * kTile + c] = S[r * SLD + c];
+    }
+    if (mirrored) {
+        T *mdst = Qc + (static_cast<int64_t>(J - band0) * T_tiles + I) * (kTile * kTile) + h * E::TN * kTile;
+        for (int idx = threadIdx.x; idx < kTile * E::TN; idx += E::THREADS) {
+            const int c = idx / kTile, r = idx % kTile;
+            mdst[c * kTile + r] = S[r * SLD + c];
         }
     }
 }
 
-// Cached mode: y[r] = sum_j Qc[r][j] p[j] for the band's rows.  One warp per 4 rows, 16-byte
-// streaming loads (L1 no-allocate), p re-used across the 4 rows from L1/L2.  HBM-bound.
+// Cached mode: y = Q~_band p from the tiled array (tile (Ib, J) = 128 x 128 row-major block at
+// (Ib * T + J) * 128^2).  CTA = one row block x one split of the tile columns (split-K keeps
+// >= ~4 CTAs per SM when there are few row blocks); warp w owns rows 16w..16w+15 and keeps
+// 16 per-lane partial sums across all its tiles; 16-byte streaming loads
+// (ld.global.nc.L1::no_allocate), every load independent.  Partial sums go to Ypart[split].
 template <typename T>
-__global__ void __launch_bounds__(256) k_gemv_cached(const T *__restrict__ Qc, const T *__restrict__ p, int64_t mpad,
-                                                     int64_t rows, T *__restrict__ Ypart) {
+__global__ void __launch_bounds__(256) k_gemv_tiled(const T *__restrict__ Qc, const T *__restrict__ p, int T_tiles,
+                                                    int nsplit, int64_t nb, T *__restrict__ Ypart) {
     using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
     constexpr int VEC = 16 / sizeof(T);
-    constexpr int R = 4;
-    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t r0 = warp * R;
-    if (r0 >= rows) return;
-    T acc[R];
+    constexpr int LPR = kTile / (32 * VEC);  // 16-byte loads per lane per row (2 fp64, 1 fp32)
+    const int Ib = blockIdx.x / nsplit, sp = blockIdx.x % nsplit;
+    const int j0 = static_cast<int>(static_cast<int64_t>(sp) * T_tiles / nsplit);
+    const int j1 = static_cast<int>(static_cast<int64_t>(sp + 1) * T_tiles / nsplit);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T acc[16];
 #pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = T(0);
-    const int64_t nv = mpad / VEC;
-    const V *pv = reinterpret_cast<const V *>(p);
-    for (int64_t c = lane; c < nv; c += 32) {
-        const V pp = pv[c];
-        const T *pe = reinterpret_cast<const T *>(&pp);
+    for (int r = 0; r < 16; ++r) acc[r] = T(0);
+    for (int J = j0; J < j1; ++J) {
+        const T *tile = Qc + (static_cast<int64_t>(Ib) * T_tiles + J) * (kTile * kTile) + (w * 16) * kTile;
+        V pv[LPR];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            V a;
-            const V *src = reinterpret_cast<const V *>(Qc + (r0 + r) * mpad) + c;
-            if constexpr (sizeof(T) == 8) {
-                asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-                             : "=d"(a.x), "=d"(a.y) : "l"(src));
-            } else {
-                asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                             : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(src));
+        for (int u = 0; u < LPR; ++u) pv[u] = reinterpret_cast<const V *>(p + static_cast<int64_t>(J) * kTile)[u * 32 + lane];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+#pragma unroll
+            for (int u = 0; u < LPR; ++u) {
+                const V *src = reinterpret_cast<const V *>(tile + r * kTile) + u * 32 + lane;
+                V a;
+                if constexpr (sizeof(T) == 8) {
+                    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(a.x), "=d"(a.y) : "l"(src));
+                } else {
+                    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(src));
+                }
+                const T *ae = reinterpret_cast<const T *>(&a);
+                const T *pe = reinterpret_cast<const T *>(&pv[u]);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[r] = fma(ae[v], pe[v], acc[r]);
             }
-            const T *ae = reinterpret_cast<const T *>(&a);
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[r] = fma(ae[v], pe[v], acc[r]);
         }
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < 16; ++r) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
     }
     if (lane == 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) Ypart[r0 + r] = acc[r];
+        for (int r = 0; r < 16; ++r) Ypart[static_cast<int64_t>(sp) * nb + static_cast<int64_t>(Ib) * kTile + w * 16 + r] = acc[r];
     }
 }
 
