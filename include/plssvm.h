@@ -85,6 +85,8 @@ typedef struct {
                                 one process per GPU); NULL = single GPU [NULL] */
     int64_t cache_budget_bytes; /* AUTO/CACHED: max bytes for the cached Q~ band;
                                    <= 0 means 90 % of free HBM after the other buffers [0] */
+    int32_t fp32_engine;     /* fp32 implicit Q~p contraction: 0 = tensor cores (tcgen05 kind::tf32,
+                                3xTF32 split) [0]; 1 = CUDA-core FFMA tiles */
 } plssvm_options_t;
 
 /* Statistics of one training call (all times are device-event seconds). */

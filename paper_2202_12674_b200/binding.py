@@ -30,7 +30,8 @@ EXPORTS = ["plssvm_default_options", "plssvm_train", "plssvm_train_f32", "plssvm
 class plssvm_options_t(ct.Structure):
     _fields_ = [("mode", ct.c_int32), ("x0", ct.c_int32), ("max_iter", ct.c_int64), ("replace_every", ct.c_int64),
                 ("fixed_iter", ct.c_int64), ("device", ct.c_int32), ("device_pointers", ct.c_int32),
-                ("stream", ct.c_void_p), ("comm", ct.c_void_p), ("cache_budget_bytes", ct.c_int64)]
+                ("stream", ct.c_void_p), ("comm", ct.c_void_p), ("cache_budget_bytes", ct.c_int64),
+                ("fp32_engine", ct.c_int32)]
 
 
 class plssvm_stats_t(ct.Structure):

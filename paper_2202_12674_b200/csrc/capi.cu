@@ -112,6 +112,7 @@ void plssvm_default_options(plssvm_options_t *o) {
     o->stream = nullptr;
     o->comm = nullptr;
     o->cache_budget_bytes = 0;
+    o->fp32_engine = 0;
 }
 
 int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtype, int kernel, double gamma, int degree,

@@ -16,8 +16,11 @@
 #include <cstring>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "driver.h"
 #include "kernels.cuh"
+#include "tc_engine.cuh"
 
 namespace plssvm {
 
@@ -166,6 +169,10 @@ struct Ctx {
     int2 *tiles;
     int ntiles;
     bool cached;
+    bool tc = false;             // fp32: tcgen05 3xTF32 contraction
+    float *Xhi = nullptr, *Xlo = nullptr;
+    CUtensorMap tm_hi, tm_lo;
+    int64_t dpad_tc = 0;
     int nsplit = 1;  // cached GEMV: column splits per row block
     int64_t launches = 0, launches_cg = 0;
 };
@@ -193,6 +200,77 @@ void set_smem_attrs() {
     PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
+CUtensorMap make_tmap_2d_f32(float *base, int64_t inner, int64_t outer, uint32_t box_inner, uint32_t box_outer) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        PLS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * sizeof(float))};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+// fp32 tensor-core engine setup: hi/lo split arrays (point-major) + TMA descriptors.
+template <typename T>
+void setup_tc(Ctx<T> &c, Arena &A, const T *Xs, int64_t m, int64_t d) {
+    if constexpr (std::is_same<T, float>::value) {
+        const Geometry &g = c.g;
+        c.dpad_tc = round_up(d, Tc::BK);
+        c.Xhi = A.alloc<float>(g.mpad * c.dpad_tc);
+        c.Xlo = A.alloc<float>(g.mpad * c.dpad_tc);
+        const int64_t n = g.mpad * c.dpad_tc;
+        k_split_tf32<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c.s>>>(Xs, m, d, c.Xhi, c.Xlo, g.mpad, c.dpad_tc);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        c.tm_hi = make_tmap_2d_f32(c.Xhi, c.dpad_tc, g.mpad, Tc::BK, kTile);
+        c.tm_lo = make_tmap_2d_f32(c.Xlo, c.dpad_tc, g.mpad, Tc::BK, kTile);
+        const int bytes = static_cast<int>(Tc::SMEM_BYTES);
+        PLS_CUDA(cudaFuncSetAttribute(k_matvec_tc<LINEAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        PLS_CUDA(cudaFuncSetAttribute(k_matvec_tc<POLYNOMIAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        PLS_CUDA(cudaFuncSetAttribute(k_matvec_tc<RBF>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    }
+}
+
+template <typename T>
+bool launch_tc(Ctx<T> &c, const T *pfull) {
+    if constexpr (std::is_same<T, float>::value) {
+        const Geometry &g = c.g;
+        const size_t sm = Tc::SMEM_BYTES;
+        switch (c.kp.kernel) {
+            case LINEAR:
+                k_matvec_tc<LINEAR><<<c.ntiles, Tc::THREADS, sm, c.s>>>(c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, c.q, c.nrm,
+                                                                       pfull, c.kp, c.invC, c.scal, g.m1, g.band0,
+                                                                       g.band1, c.Ypart, g.nb);
+                break;
+            case POLYNOMIAL:
+                k_matvec_tc<POLYNOMIAL><<<c.ntiles, Tc::THREADS, sm, c.s>>>(c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, c.q,
+                                                                           c.nrm, pfull, c.kp, c.invC, c.scal, g.m1,
+                                                                           g.band0, g.band1, c.Ypart, g.nb);
+                break;
+            default:
+                k_matvec_tc<RBF><<<c.ntiles, Tc::THREADS, sm, c.s>>>(c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, c.q, c.nrm,
+                                                                    pfull, c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
+                                                                    c.Ypart, g.nb);
+        }
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        return true;
+    }
+    return false;
+}
+
 // Cached GEMV split-K factor: >= 16 CTAs per SM in total (several waves of the ~3 resident
 // CTAs per SM), so the last partial wave costs little even when the band has few row blocks.
 int gemv_splits(const Geometry &g) {
@@ -211,6 +289,7 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
         ++c.launches;
         return c.nsplit;
     }
+    if (c.tc && launch_tc<T>(c, pfull)) return g.T;
     const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
         case LINEAR:
@@ -300,6 +379,8 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     PLS_CUDA(cudaEventRecord(e_h2d, c.s));
     c.Xt = A.alloc<T>(g.dpad * g.mpad);
     launch_transform<T>(Xs, pb.m, pb.d, c.Xt, g.mpad, g.dpad, c.s, c.launches);
+    c.tc = std::is_same<T, float>::value && o.fp32_engine == 0;
+    if (c.tc) setup_tc<T>(c, A, Xs, pb.m, pb.d);
     PLS_CUDA(cudaEventRecord(e_tr, c.s));
     c.q = A.alloc<T>(g.mpad);
     c.nrm = A.alloc<T>(g.mpad);

@@ -58,6 +58,22 @@ def test_matvec_implicit_small(m, d, kernel, dtype):
     check_matvec(X, p, kernel, kparams(kernel, d, dtype), 1.0, dtype, pl.MODE_IMPLICIT)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("m,d", [(129, 3), (1000, 33), (2177, 70), (4097, 300)])
+def test_matvec_fp32_ffma_engine(m, d, kernel):
+    """fp32 on the CUDA-core FFMA engine (options.fp32_engine = 1); default is tcgen05 3xTF32."""
+    rng = np.random.default_rng(3000 * m + d + kernel)
+    X = rng.standard_normal((m, d)).astype(np.float32)
+    p = rng.standard_normal(m - 1).astype(np.float32)
+    kp = kparams(kernel, d, np.float32)
+    Qt = oracle.qtilde(X.astype(np.float64), kernel, kp["gamma"], kp["degree"], kp["coef0"], 1.0)
+    ref = Qt @ p.astype(np.float64)
+    for eng in (0, 1):
+        out, _ = pl.plssvm_qtilde_matvec(X, p, kernel, kp["gamma"], kp["degree"], kp["coef0"], 1.0,
+                                         opts=pl.options(mode=pl.MODE_IMPLICIT, fp32_engine=eng))
+        assert rel(out, ref) <= 1e-5, (eng, rel(out, ref))
+
+
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("m,d", [(3, 3), (129, 3), (1000, 33), (2177, 70)])

@@ -19,6 +19,7 @@ ap.add_argument("--repeats", type=int, default=3)
 ap.add_argument("--m", type=int, default=0)
 ap.add_argument("--d", type=int, default=0)
 ap.add_argument("--kernel", type=int, default=-1)
+ap.add_argument("--fp32-engine", type=int, default=0)
 a = ap.parse_args()
 cfg = synth.configs()[a.config]
 m, d = a.m or cfg.m, a.d or cfg.d
@@ -29,7 +30,7 @@ p = rng.standard_normal(m - 1).astype(dt)
 mode = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED}[a.mode]
 kern = cfg.kernel if a.kernel < 0 else a.kernel
 out, t = pl.plssvm_qtilde_matvec(X, p, kern, 1.0 / d, cfg.degree, cfg.coef0, cfg.C, repeats=a.repeats,
-                                 opts=pl.options(mode=mode))
+                                 opts=pl.options(mode=mode, fp32_engine=a.fp32_engine))
 m1 = m - 1
 fl = 2.0 * d * m1 * (m1 + 1) / 2
 s = np.dtype(dt).itemsize
