@@ -36,7 +36,13 @@ METRIC = "CG iterations/s & kernel-matvec FLOP/s (% peak), train time; 1/2/4/8 B
 UNIT = "CG it/s"
 KNAMES = {0: "linear", 1: "polynomial", 2: "rbf"}
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs x DFMA/clk/SM x 2 x max SM clock
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: FFMA
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: FFMA (options.fp32_engine = 1)
+
+
+def tf32x3_peak_tflops():
+    """Useful-flop peak of the 3xTF32 tcgen05 path: the measured bf16 dense peak x the guide's
+    nominal tf32/bf16 ratio (1.1 / 2.25 PFLOP/s), / 3 MMAs per useful product."""
+    return measured_peaks().get("bf16_tflops", 1590.0) * (1.1 / 2.25) / 3.0
 
 
 def measured_peaks():
@@ -281,15 +287,15 @@ def main():
     avg_mv = t_mv / max(1, matvecs)
     if mode_used == "implicit":
         fl = matvec_flops(cfg.m, cfg.d) / world  # this rank's share (symmetric work split)
-        peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else FP32_PEAK_TFLOPS
+        peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else tf32x3_peak_tflops()
         achieved = fl / avg_mv / 1e12
-        roof = {"bound": "tensor" if cfg.dtype == "f64" else "alu", "achieved": achieved, "peak": peak,
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic_for(f"{cfg.name}/implicit/k_matvec_implicit") if world == 1 else None,
                 "traffic_unit": "bytes per launch (ncu dram read+write)", "kernel": "k_matvec_implicit",
                 "per_launch": f"2*d*E flops, E = m'(m'+1)/2 distinct Q~ entries ({fl:.4g} flops per launch per rank)",
                 "peak_source": "fp64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2 (DMMA measured 37.1, "
-                               "profiles/r01_fp64_peak.txt); fp32: 128 FFMA/clk (DESIGN.md)",
+                               "profiles/r01_fp64_peak.txt); fp32: measured bf16 x 1.1/2.25 / 3 (3xTF32 tcgen05)",
                 "avg_launch_s": avg_mv}
     else:
         s = 8 if cfg.dtype == "f64" else 4

@@ -200,6 +200,8 @@ void set_smem_attrs() {
     PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
+void tc_set_attrs();
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
 CUtensorMap make_tmap_2d_f32(float *base, int64_t inner, int64_t outer, uint32_t box_inner, uint32_t box_outer) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -236,35 +238,59 @@ void setup_tc(Ctx<T> &c, Arena &A, const T *Xs, int64_t m, int64_t d) {
         ++c.launches;
         c.tm_hi = make_tmap_2d_f32(c.Xhi, c.dpad_tc, g.mpad, Tc::BK, kTile);
         c.tm_lo = make_tmap_2d_f32(c.Xlo, c.dpad_tc, g.mpad, Tc::BK, kTile);
-        const int bytes = static_cast<int>(Tc::SMEM_BYTES);
-        PLS_CUDA(cudaFuncSetAttribute(k_matvec_tc<LINEAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        PLS_CUDA(cudaFuncSetAttribute(k_matvec_tc<POLYNOMIAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        PLS_CUDA(cudaFuncSetAttribute(k_matvec_tc<RBF>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        tc_set_attrs();
     }
+}
+
+template <int KT, int MODE>
+void tc_launch(int grid, cudaStream_t s, const CUtensorMap &ah, const CUtensorMap &al, const CUtensorMap &bh,
+               const CUtensorMap &bl, int64_t dpad, const int2 *tiles, int tilesI, const float *qa, const float *na,
+               const float *qb, const float *nb_, const float *p, KParams<float> kp, float invC, const double *scal,
+               int64_t m1, int band0, int band1, float *Ypart, int64_t band_rows, float *Qc, int T_tiles) {
+    k_tile_tc<KT, MODE><<<grid, Tc::THREADS, Tc::SMEM_BYTES, s>>>(ah, al, bh, bl, dpad, tiles, tilesI, qa, na, qb, nb_, p,
+                                                                 kp, invC, scal, m1, band0, band1, Ypart, band_rows,
+                                                                 Qc, T_tiles);
+    PLS_CHECK_LAUNCH();
+}
+
+template <int MODE, typename... Args>
+void tc_dispatch(int kernel, Args &&...args) {
+    switch (kernel) {
+        case LINEAR: tc_launch<LINEAR, MODE>(args...); break;
+        case POLYNOMIAL: tc_launch<POLYNOMIAL, MODE>(args...); break;
+        default: tc_launch<RBF, MODE>(args...);
+    }
+}
+
+void tc_set_attrs() {
+    const int bytes = static_cast<int>(Tc::SMEM_BYTES);
+#define PLS_TC_ATTR(K, M) PLS_CUDA(cudaFuncSetAttribute(k_tile_tc<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
+    PLS_TC_ATTR(LINEAR, TC_MATVEC); PLS_TC_ATTR(POLYNOMIAL, TC_MATVEC); PLS_TC_ATTR(RBF, TC_MATVEC);
+    PLS_TC_ATTR(LINEAR, TC_PRECOMPUTE); PLS_TC_ATTR(POLYNOMIAL, TC_PRECOMPUTE); PLS_TC_ATTR(RBF, TC_PRECOMPUTE);
+    PLS_TC_ATTR(LINEAR, TC_PREDICT); PLS_TC_ATTR(POLYNOMIAL, TC_PREDICT); PLS_TC_ATTR(RBF, TC_PREDICT);
+#undef PLS_TC_ATTR
 }
 
 template <typename T>
 bool launch_tc(Ctx<T> &c, const T *pfull) {
     if constexpr (std::is_same<T, float>::value) {
         const Geometry &g = c.g;
-        const size_t sm = Tc::SMEM_BYTES;
-        switch (c.kp.kernel) {
-            case LINEAR:
-                k_matvec_tc<LINEAR><<<c.ntiles, Tc::THREADS, sm, c.s>>>(c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, c.q, c.nrm,
-                                                                       pfull, c.kp, c.invC, c.scal, g.m1, g.band0,
-                                                                       g.band1, c.Ypart, g.nb);
-                break;
-            case POLYNOMIAL:
-                k_matvec_tc<POLYNOMIAL><<<c.ntiles, Tc::THREADS, sm, c.s>>>(c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, c.q,
-                                                                           c.nrm, pfull, c.kp, c.invC, c.scal, g.m1,
-                                                                           g.band0, g.band1, c.Ypart, g.nb);
-                break;
-            default:
-                k_matvec_tc<RBF><<<c.ntiles, Tc::THREADS, sm, c.s>>>(c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, c.q, c.nrm,
-                                                                    pfull, c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
-                                                                    c.Ypart, g.nb);
-        }
-        PLS_CHECK_LAUNCH();
+        tc_dispatch<TC_MATVEC>(c.kp.kernel, c.ntiles, c.s, c.tm_hi, c.tm_lo, c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, 0, c.q,
+                               c.nrm, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1, g.band0, g.band1, c.Ypart, g.nb,
+                               static_cast<float *>(nullptr), g.T);
+        ++c.launches;
+        return true;
+    }
+    return false;
+}
+
+template <typename T>
+bool launch_tc_precompute(Ctx<T> &c) {
+    if constexpr (std::is_same<T, float>::value) {
+        const Geometry &g = c.g;
+        tc_dispatch<TC_PRECOMPUTE>(c.kp.kernel, c.ntiles, c.s, c.tm_hi, c.tm_lo, c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, 0,
+                                   c.q, c.nrm, c.q, c.nrm, static_cast<const float *>(nullptr), c.kp, c.invC, c.scal,
+                                   g.m1, g.band0, g.band1, static_cast<float *>(nullptr), g.nb, c.Qc, g.T);
         ++c.launches;
         return true;
     }
@@ -314,6 +340,7 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
 
 template <typename T>
 void launch_precompute(Ctx<T> &c) {
+    if (c.tc && launch_tc_precompute<T>(c)) return;
     const Geometry &g = c.g;
     const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
@@ -696,13 +723,36 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
         PLS_CHECK_LAUNCH();
         launches += 2;
     }
-    const int tilesI = static_cast<int>(npad / kTile), tilesJ = static_cast<int>(mpad / EN::TN);
+    const bool tc = std::is_same<T, float>::value && o.fp32_engine == 0;
+    const int tilesI = static_cast<int>(npad / kTile), tilesJ = static_cast<int>(mpad / (tc ? kTile : EN::TN));
     T *Fpart = A.alloc<T>(static_cast<int64_t>(tilesJ) * npad);
     set_smem_attrs<T>();
     const size_t sm = EN::SMEM_BYTES;
     const int grid = tilesI * tilesJ;
-    PLS_CUDA(cudaEventRecord(e0, s));
-    switch (pb.kernel) {
+    if constexpr (std::is_same<T, float>::value) {
+        if (tc) {
+            // fp32 on tcgen05 (3xTF32): hi/lo split of both operands, TMA descriptors
+            const int64_t dtc = round_up(d, Tc::BK);
+            float *Zh = A.alloc<float>(npad * dtc), *Zlo = A.alloc<float>(npad * dtc);
+            float *Xh = A.alloc<float>(mpad * dtc), *Xlo = A.alloc<float>(mpad * dtc);
+            k_split_tf32<<<static_cast<unsigned>(ceil_div(npad * dtc, 256)), 256, 0, s>>>(Zs, n, d, Zh, Zlo, npad, dtc);
+            k_split_tf32<<<static_cast<unsigned>(ceil_div(mpad * dtc, 256)), 256, 0, s>>>(Xs, m, d, Xh, Xlo, mpad, dtc);
+            PLS_CHECK_LAUNCH();
+            launches += 2;
+            const CUtensorMap zh = make_tmap_2d_f32(Zh, dtc, npad, Tc::BK, kTile);
+            const CUtensorMap zl = make_tmap_2d_f32(Zlo, dtc, npad, Tc::BK, kTile);
+            const CUtensorMap xh = make_tmap_2d_f32(Xh, dtc, mpad, Tc::BK, kTile);
+            const CUtensorMap xl = make_tmap_2d_f32(Xlo, dtc, mpad, Tc::BK, kTile);
+            tc_set_attrs();
+            PLS_CUDA(cudaEventRecord(e0, s));
+            tc_dispatch<TC_PREDICT>(pb.kernel, grid, s, zh, zl, xh, xl, dtc, static_cast<const int2 *>(nullptr), tilesI,
+                                    static_cast<const float *>(nullptr), nz, static_cast<const float *>(nullptr), nx,
+                                    alpha, kp, 0.f, static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,
+                                    static_cast<float *>(nullptr), 0);
+        }
+    }
+    if (!tc) PLS_CUDA(cudaEventRecord(e0, s));
+    if (!tc) switch (pb.kernel) {
         case LINEAR:
             k_predict_tiles<LINEAR, T><<<grid, Engine<T>::THREADS, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
                                                                   Fpart);

@@ -8,6 +8,7 @@
 // precomputed by k_split_tf32) and S = hi.hi^T + hi.lo^T + lo.hi^T (the lo.lo^T term, ~2^-22
 // relative, is dropped): fp32-level accuracy (tools/tc_probe.cu: 1.9e-6 relative vs fp64).
 //
+// The same tile kernel also serves the fp32 cached-mode precompute and predict (TcMode).
 // CTA = 6 warps, one CTA per tile, warp-specialised:
 //   warp 4 (one lane): TMA producer -- 4 boxes of 128 rows x 128 B (A_hi, A_lo, B_hi, B_lo) per
 //                      32-feature slab, SWIZZLE_128B, completion on full[stage] (expect_tx)
@@ -128,12 +129,22 @@ __global__ void k_split_tf32(const float *__restrict__ X, int64_t m, int64_t d, 
     Xlo[idx] = __uint_as_float(l);
 }
 
-template <int KT>
+// Epilogue variants of the tcgen05 tile kernel.
+enum TcMode : int { TC_MATVEC = 0, TC_PRECOMPUTE = 1, TC_PREDICT = 2 };
+
+// One CTA per 128 x 128 tile (I, J): A = rows I of the A arrays, B = rows J of the B arrays.
+//  TC_MATVEC     : Q~ entries -> row sums into Ypart[J] (rows of I) and, for mirrored tiles,
+//                  column sums into Ypart[I] (rows of J)                      (same as k_matvec_implicit)
+//  TC_PRECOMPUTE : Q~ entries -> the band's tiled cached array Qc (tile and mirrored tile)
+//  TC_PREDICT    : alpha_j k(z_i, x_j) -> row sums into Ypart[J] (= Fpart, rows of test block I)
+template <int KT, int MODE>
 __global__ void __launch_bounds__(Tc::THREADS, 1)
-    k_matvec_tc(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo, int64_t dpad,
-                const int2 *__restrict__ tiles, const float *__restrict__ q, const float *__restrict__ nrm,
-                const float *__restrict__ p, KParams<float> kp, float invC, const double *__restrict__ scal, int64_t m1,
-                int band0, int band1, float *__restrict__ Ypart, int64_t band_rows) {
+    k_tile_tc(const __grid_constant__ CUtensorMap tma_hi, const __grid_constant__ CUtensorMap tma_lo,
+              const __grid_constant__ CUtensorMap tmb_hi, const __grid_constant__ CUtensorMap tmb_lo, int64_t dpad,
+              const int2 *__restrict__ tiles, int tilesI, const float *__restrict__ qa, const float *__restrict__ na,
+              const float *__restrict__ qb, const float *__restrict__ nb_, const float *__restrict__ p,
+              KParams<float> kp, float invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
+              float *__restrict__ Ypart, int64_t band_rows, float *__restrict__ Qc, int T_tiles) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     float *ring = reinterpret_cast<float *>(base);
@@ -143,19 +154,28 @@ __global__ void __launch_bounds__(Tc::THREADS, 1)
     uint64_t *accf = empty + Tc::STAGES;                            // [1]
     uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(accf + 1);
     float *colq = reinterpret_cast<float *>(misc + 128);            // [128]
-    float *colp = colq + kTile;                                     // [128]
+    float *colp = colq + kTile;                                     // [128]  (alpha for predict)
     float *coln = colp + kTile;                                     // [128]
     float *redc = coln + kTile;                                     // [4][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int2 tile = tiles[blockIdx.x];
-    const int I = tile.x, J = tile.y;
+    int I, J;
+    if constexpr (MODE == TC_PREDICT) {
+        I = blockIdx.x % tilesI;
+        J = blockIdx.x / tilesI;
+    } else {
+        const int2 tile = tiles[blockIdx.x];
+        I = tile.x;
+        J = tile.y;
+    }
     const int row0 = I * kTile, col0 = J * kTile;
     const int nk = static_cast<int>(dpad / Tc::BK);
 
     if (warp == 4 && lane == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_hi)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_lo)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_hi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_lo)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmb_hi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmb_lo)) : "memory");
         for (int s = 0; s < Tc::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -169,9 +189,9 @@ __global__ void __launch_bounds__(Tc::THREADS, 1)
     }
     if (threadIdx.x < kTile) {
         const int64_t gj = col0 + threadIdx.x;
-        colq[threadIdx.x] = q[gj];
-        colp[threadIdx.x] = p[gj];
-        coln[threadIdx.x] = (KT == RBF) ? nrm[gj] : 0.f;
+        colq[threadIdx.x] = (MODE == TC_PREDICT) ? 0.f : qb[gj];
+        colp[threadIdx.x] = (MODE == TC_PRECOMPUTE) ? 0.f : p[gj];
+        coln[threadIdx.x] = (KT == RBF) ? nb_[gj] : 0.f;
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -186,10 +206,10 @@ __global__ void __launch_bounds__(Tc::THREADS, 1)
                 float *st = ring + size_t(s) * 4 * Tc::OPND;
                 mbar_expect_tx(&full[s], Tc::STAGE_BYTES);
                 const int x = kb * Tc::BK;
-                tma_load_2d(st, &tm_hi, &full[s], x, row0);
-                tma_load_2d(st + Tc::OPND, &tm_lo, &full[s], x, row0);
-                tma_load_2d(st + 2 * Tc::OPND, &tm_hi, &full[s], x, col0);
-                tma_load_2d(st + 3 * Tc::OPND, &tm_lo, &full[s], x, col0);
+                tma_load_2d(st, &tma_hi, &full[s], x, row0);
+                tma_load_2d(st + Tc::OPND, &tma_lo, &full[s], x, row0);
+                tma_load_2d(st + 2 * Tc::OPND, &tmb_hi, &full[s], x, col0);
+                tma_load_2d(st + 3 * Tc::OPND, &tmb_lo, &full[s], x, col0);
             }
         }
     } else if (warp == 5) {
@@ -215,38 +235,71 @@ __global__ void __launch_bounds__(Tc::THREADS, 1)
     } else {  // ---- epilogue warps 0-3: thread = tile row 32w + lane
         const int lr = warp * 32 + lane;
         const int64_t gi = row0 + lr;
-        const float qi = q[gi], pi = p[gi], ni = (KT == RBF) ? nrm[gi] : 0.f;
-        const float Qmm = static_cast<float>(scal[S_QMM]);
-        const bool mirrored = (I != J) && (J >= band0) && (J < band1);
+        const float qi = (MODE == TC_PREDICT) ? 0.f : qa[gi];
+        const float pi = (MODE == TC_MATVEC) ? p[gi] : 0.f;
+        const float ni = (KT == RBF) ? na[gi] : 0.f;
+        const float Qmm = (MODE == TC_PREDICT) ? 0.f : static_cast<float>(scal[S_QMM]);
+        const bool mirrored = (MODE != TC_PREDICT) && (I != J) && (J >= band0) && (J < band1);
         mbar_wait(accf, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
         float rs = 0.f;
+        float *qrow = nullptr, *qmir = nullptr;
+        if constexpr (MODE == TC_PRECOMPUTE) {
+            qrow = Qc + (int64_t(I - band0) * T_tiles + J) * (kTile * kTile) + lr * kTile;
+            if (mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < kTile; c0 += 16) {
             float v[16];
             tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
-            float cs[16];
+            if constexpr (MODE == TC_PREDICT) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int lc = c0 + j;
-                const float qt = qtilde_value<KT, float>(v[j], gi, int64_t(col0 + lc), ni, coln[lc], qi, colq[lc], Qmm,
-                                                         invC, m1, kp);
-                rs = fmaf(qt, colp[lc], rs);
-                cs[j] = qt * pi;
-            }
-            if (mirrored) {
-                const float t = transpose_reduce16(cs, lane);
-                if ((lane & 1) == 0) redc[warp * kTile + c0 + (lane >> 1)] = t;
+                for (int j = 0; j < 16; ++j) {
+                    const int lc = c0 + j;
+                    rs = fmaf(colp[lc], kernel_value<KT, float>(v[j], ni, coln[lc], false, kp), rs);
+                }
+            } else {
+                float cs[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int lc = c0 + j;
+                    const float qt = qtilde_value<KT, float>(v[j], gi, int64_t(col0 + lc), ni, coln[lc], qi, colq[lc],
+                                                             Qmm, invC, m1, kp);
+                    if constexpr (MODE == TC_MATVEC) {
+                        rs = fmaf(qt, colp[lc], rs);
+                        cs[j] = qt * pi;
+                    } else {
+                        cs[j] = qt;
+                    }
+                }
+                if constexpr (MODE == TC_MATVEC) {
+                    if (mirrored) {
+                        const float t = transpose_reduce16(cs, lane);
+                        if ((lane & 1) == 0) redc[warp * kTile + c0 + (lane >> 1)] = t;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4 *>(qrow + c0 + j) = make_float4(cs[j], cs[j + 1], cs[j + 2], cs[j + 3]);
+                    if (mirrored) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) qmir[(c0 + j) * kTile] = cs[j];  // coalesced over lanes
+                    }
+                }
             }
         }
-        const int64_t lrow0 = int64_t(row0) - int64_t(band0) * kTile;
-        Ypart[int64_t(J) * band_rows + lrow0 + lr] = rs;
-        if (mirrored) {
-            asm volatile("bar.sync 1, 128;");
-            const int t = threadIdx.x;
-            const int64_t lcol0 = int64_t(col0) - int64_t(band0) * kTile;
-            Ypart[int64_t(I) * band_rows + lcol0 + t] =
-                (redc[t] + redc[kTile + t]) + (redc[2 * kTile + t] + redc[3 * kTile + t]);
+        if constexpr (MODE == TC_MATVEC || MODE == TC_PREDICT) {
+            const int64_t lrow0 = int64_t(row0) - int64_t(band0) * kTile;
+            Ypart[int64_t(J) * band_rows + lrow0 + lr] = rs;
+        }
+        if constexpr (MODE == TC_MATVEC) {
+            if (mirrored) {
+                asm volatile("bar.sync 1, 128;");
+                const int t = threadIdx.x;
+                const int64_t lcol0 = int64_t(col0) - int64_t(band0) * kTile;
+                Ypart[int64_t(I) * band_rows + lcol0 + t] =
+                    (redc[t] + redc[kTile + t]) + (redc[2 * kTile + t] + redc[3 * kTile + t]);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");

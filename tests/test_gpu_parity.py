@@ -69,9 +69,19 @@ def test_matvec_fp32_ffma_engine(m, d, kernel):
     Qt = oracle.qtilde(X.astype(np.float64), kernel, kp["gamma"], kp["degree"], kp["coef0"], 1.0)
     ref = Qt @ p.astype(np.float64)
     for eng in (0, 1):
-        out, _ = pl.plssvm_qtilde_matvec(X, p, kernel, kp["gamma"], kp["degree"], kp["coef0"], 1.0,
-                                         opts=pl.options(mode=pl.MODE_IMPLICIT, fp32_engine=eng))
-        assert rel(out, ref) <= 1e-5, (eng, rel(out, ref))
+        for mode in (pl.MODE_IMPLICIT, pl.MODE_CACHED):
+            out, _ = pl.plssvm_qtilde_matvec(X, p, kernel, kp["gamma"], kp["degree"], kp["coef0"], 1.0,
+                                             opts=pl.options(mode=mode, fp32_engine=eng))
+            assert rel(out, ref) <= 1e-5, (eng, mode, rel(out, ref))
+    # predict through both engines
+    Z = rng.standard_normal((300, d)).astype(np.float32)
+    alpha = rng.standard_normal(m).astype(np.float32)
+    f_ref, _ = oracle.predict(X.astype(np.float64), alpha.astype(np.float64), 0.1, Z.astype(np.float64), kernel,
+                              kp["gamma"], kp["degree"], kp["coef0"])
+    for eng in (0, 1):
+        f, lab, _ = pl.plssvm_predict_ex(X, alpha, 0.1, Z, kernel, kp["gamma"], kp["degree"], kp["coef0"],
+                                         opts=pl.options(fp32_engine=eng))
+        assert rel(f, f_ref) <= 1e-5, (eng, rel(f, f_ref))
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])

@@ -21,7 +21,15 @@ import paper_2202_12674_b200 as pl  # noqa: E402
 import synth  # noqa: E402
 
 FP64_PEAK = 148 * 64 * 2 * 1.965e9 / 1e12
-FP32_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12
+def tf32x3_peak():
+    try:
+        bf16 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+    except (OSError, KeyError, ValueError):
+        bf16 = 1590.0
+    return bf16 * (1.1 / 2.25) / 3.0
+
+
+FP32_PEAK = tf32x3_peak()
 
 
 def hbm_peak():
