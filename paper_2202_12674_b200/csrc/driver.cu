@@ -110,6 +110,44 @@ void launch_transform(const T *X, int64_t m, int64_t d, T *Xt, int64_t rows, int
     ++launches;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
+// 2-D row-major array [outer][inner] of 4- or 8-byte elements, box {box_inner, box_outer},
+// 128-byte swizzle (box_inner * elem = 128 B).
+CUtensorMap make_tmap_2d(void *base, int elem_bytes, int64_t inner, int64_t outer, uint32_t box_inner,
+                         uint32_t box_outer) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        PLS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * elem_bytes)};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&m, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base,
+                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+CUtensorMap make_tmap_2d_f32(float *base, int64_t inner, int64_t outer, uint32_t box_inner, uint32_t box_outer) {
+    return make_tmap_2d(base, 4, inner, outer, box_inner, box_outer);
+}
+
+// Tile-kernel operands: A = row operand array (rows_a points), B = column operand array.
+Ops<double> make_ops(double *A, int64_t rows_a, double *B, int64_t rows_b, int64_t dpad) {
+    using E = Engine<double>;
+    Ops<double> o;
+    o.a = make_tmap_2d(A, 8, dpad, rows_a, E::BK, kTile);
+    o.b = make_tmap_2d(B, 8, dpad, rows_b, E::BK, E::TN);
+    return o;
+}
+Ops<float> make_ops(float *A, int64_t, float *B, int64_t, int64_t ld) { return Ops<float>{A, B, ld}; }
+
 // Row-band geometry of this rank: padded length mpad (multiple of 128 * P), tiles per rank.
 struct Geometry {
     int64_t m1, mpad, dpad, ld, nb, g0;
@@ -175,6 +213,7 @@ struct Ctx {
     int64_t dpad_tc = 0;
     int nsplit = 1;  // cached GEMV: column splits per row block
     int64_t launches = 0, launches_cg = 0;
+    Ops<T> ops;
 };
 
 template <typename T>
@@ -201,28 +240,6 @@ void set_smem_attrs() {
 }
 
 void tc_set_attrs();
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
-CUtensorMap make_tmap_2d_f32(float *base, int64_t inner, int64_t outer, uint32_t box_inner, uint32_t box_outer) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q;
-        void *fn = nullptr;
-        PLS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    CUtensorMap m;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * sizeof(float))};
-    const cuuint32_t box[2] = {box_inner, box_outer};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
-    return m;
-}
 
 // fp32 tensor-core engine setup: hi/lo split arrays (point-major) + TMA descriptors.
 template <typename T>
@@ -319,17 +336,17 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
     const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
         case LINEAR:
-            k_matvec_implicit<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm, pfull,
+            k_matvec_implicit<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull,
                                                                          c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
                                                                          c.Ypart, g.nb);
             break;
         case POLYNOMIAL:
-            k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm,
+            k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm,
                                                                              pfull, c.kp, c.invC, c.scal, g.m1, g.band0,
                                                                              g.band1, c.Ypart, g.nb);
             break;
         default:
-            k_matvec_implicit<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.dpad, c.tiles, c.q, c.nrm, pfull,
+            k_matvec_implicit<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull,
                                                                       c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
                                                                       c.Ypart, g.nb);
     }
@@ -345,15 +362,15 @@ void launch_precompute(Ctx<T> &c) {
     const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
         case LINEAR:
-            k_precompute<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                     c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
             break;
         case POLYNOMIAL:
-            k_precompute<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                         c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
             break;
         default:
-            k_precompute<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.Xt, g.ld, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
+            k_precompute<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
                                                                  c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
     }
     PLS_CHECK_LAUNCH();
@@ -406,6 +423,7 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     PLS_CUDA(cudaEventRecord(e_h2d, c.s));
     c.Xt = A.alloc<T>(g.dpad * g.mpad);
     launch_transform<T>(Xs, pb.m, pb.d, c.Xt, g.mpad, g.dpad, c.s, c.launches);
+    c.ops = make_ops(c.Xt, g.mpad, c.Xt, g.mpad, g.ld);
     c.tc = std::is_same<T, float>::value && o.fp32_engine == 0;
     if (c.tc) setup_tc<T>(c, A, Xs, pb.m, pb.d);
     PLS_CUDA(cudaEventRecord(e_tr, c.s));
@@ -706,7 +724,6 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     // point-major: Xp[mpad][dpad], Zp[npad][dpad]; feature-major: both with ld = max(mpad, npad)
     const int64_t L = std::max(mpad, npad);
     const int64_t xrows = EN::kPointMajor ? mpad : L, zrows = EN::kPointMajor ? npad : L;
-    const int64_t ldx = EN::kPointMajor ? dpad : L, ldz = EN::kPointMajor ? dpad : L;
     const T *Xs = stage_input<T>(A, pb.X, m * d, dev, s);
     const T *Zs = stage_input<T>(A, Zin, n * d, dev, s);
     T *Xl = A.alloc<T>(dpad * xrows), *Zl = A.alloc<T>(dpad * zrows);
@@ -751,18 +768,19 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
                                     static_cast<float *>(nullptr), 0);
         }
     }
+    const Ops<T> pops = make_ops(Zl, zrows, Xl, xrows, EN::kPointMajor ? dpad : L);
     if (!tc) PLS_CUDA(cudaEventRecord(e0, s));
     if (!tc) switch (pb.kernel) {
         case LINEAR:
-            k_predict_tiles<LINEAR, T><<<grid, Engine<T>::THREADS, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
+            k_predict_tiles<LINEAR, T><<<grid, Engine<T>::THREADS, sm, s>>>(pops, npad, dpad, nz, nx, alpha, kp, tilesI,
                                                                   Fpart);
             break;
         case POLYNOMIAL:
-            k_predict_tiles<POLYNOMIAL, T><<<grid, Engine<T>::THREADS, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp,
-                                                                      tilesI, Fpart);
+            k_predict_tiles<POLYNOMIAL, T><<<grid, Engine<T>::THREADS, sm, s>>>(pops, npad, dpad, nz, nx, alpha, kp,
+                                                                                tilesI, Fpart);
             break;
         default:
-            k_predict_tiles<RBF, T><<<grid, Engine<T>::THREADS, sm, s>>>(Zl, ldz, npad, Xl, ldx, dpad, nz, nx, alpha, kp, tilesI,
+            k_predict_tiles<RBF, T><<<grid, Engine<T>::THREADS, sm, s>>>(pops, npad, dpad, nz, nx, alpha, kp, tilesI,
                                                                Fpart);
     }
     PLS_CHECK_LAUNCH();

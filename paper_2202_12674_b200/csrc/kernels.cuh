@@ -163,18 +163,18 @@ __device__ __forceinline__ T qtilde_value(T s, int64_t gi, int64_t gj, T ni, T n
 // feature-major).
 template <int KT, typename T>
 __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
-    k_matvec_implicit(const T *__restrict__ X, int64_t ld, int64_t dpad, const int2 *__restrict__ tiles,
+    k_matvec_implicit(const __grid_constant__ Ops<T> ops, int64_t dpad, const int2 *__restrict__ tiles,
                       const T *__restrict__ q, const T *__restrict__ nrm, const T *__restrict__ p, KParams<T> kp,
                       T invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
                       T *__restrict__ Ypart, int64_t band_rows) {
     using E = Engine<T>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T *smem = reinterpret_cast<T *>(smem_raw);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    T *smem = align_smem<T>(smem_raw);
     const int2 tile = tiles[blockIdx.x];
     const int I = tile.x, Jc = tile.y, J = Jc / E::NSUB;  // Jc: column sub-block of width TN
     const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(Jc) * E::TN;
     T acc[E::R][E::CC];
-    E::contract(E::block(X, row0, ld), E::block(X, col0, ld), ld, dpad, smem, acc);
+    E::contract(ops, static_cast<int>(row0), static_cast<int>(col0), dpad, smem, acc);
 
     const T Qmm = static_cast<T>(scal[S_QMM]);
     T qi[E::R], ni[E::R], pi[E::R], qj[E::CC], nj[E::CC], pj[E::CC];
@@ -226,17 +226,17 @@ __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
 // into the band's tiled array Qc from the same tiles (upper tiles mirrored as transposed stores).
 template <int KT, typename T>
 __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
-    k_precompute(const T *__restrict__ X, int64_t ld, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
+    k_precompute(const __grid_constant__ Ops<T> ops, int64_t mpad, int64_t dpad, const int2 *__restrict__ tiles,
                  const T *__restrict__ q, const T *__restrict__ nrm, KParams<T> kp, T invC,
                  const double *__restrict__ scal, int64_t m1, int band0, int band1, T *__restrict__ Qc) {
     using E = Engine<T>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T *smem = reinterpret_cast<T *>(smem_raw);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    T *smem = align_smem<T>(smem_raw);
     const int2 tile = tiles[blockIdx.x];
     const int I = tile.x, Jc = tile.y, J = Jc / E::NSUB;
     const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(Jc) * E::TN;
     T acc[E::R][E::CC];
-    E::contract(E::block(X, row0, ld), E::block(X, col0, ld), ld, dpad, smem, acc);
+    E::contract(ops, static_cast<int>(row0), static_cast<int>(col0), dpad, smem, acc);
     const T Qmm = static_cast<T>(scal[S_QMM]);
     const bool mirrored = (I != J) && (J >= band0) && (J < band1);
     // Stage the finished 128 x TN tile in shared memory (the ring is free), then write it with
@@ -471,22 +471,16 @@ __global__ void k_assemble(const T *__restrict__ xfull, int64_t m, double *scal,
 // ldz / ldx: leading dimensions of the two arrays in the engine layout.
 template <int KT, typename T>
 __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
-    k_predict_tiles(const T *__restrict__ Zl, int64_t ldz, int64_t npad, const T *__restrict__ Xl, int64_t ldx,
-                    int64_t dpad, const T *__restrict__ nz, const T *__restrict__ nx, const T *__restrict__ alpha,
-                    KParams<T> kp, int tilesI, T *__restrict__ Fpart) {
+    k_predict_tiles(const __grid_constant__ Ops<T> ops, int64_t npad, int64_t dpad, const T *__restrict__ nz,
+                    const T *__restrict__ nx, const T *__restrict__ alpha, KParams<T> kp, int tilesI,
+                    T *__restrict__ Fpart) {
     using E = Engine<T>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T *smem = reinterpret_cast<T *>(smem_raw);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    T *smem = align_smem<T>(smem_raw);
     const int I = blockIdx.x % tilesI, Jc = blockIdx.x / tilesI;
     const int64_t row0 = static_cast<int64_t>(I) * kTile, col0 = static_cast<int64_t>(Jc) * E::TN;
     T acc[E::R][E::CC];
-    if constexpr (E::kPointMajor) {
-        E::contract(E::block(Zl, row0, ldz), E::block(Xl, col0, ldx), dpad, dpad, smem, acc);
-    } else {
-        // feature-major: the engine reads both operands with one leading dimension; the driver
-        // stores Z^T and X^T with the same ld.
-        E::contract(E::block(Zl, row0, ldz), E::block(Xl, col0, ldx), ldx, dpad, smem, acc);
-    }
+    E::contract(ops, static_cast<int>(row0), static_cast<int>(col0), dpad, smem, acc);
     T rs[E::R];
 #pragma unroll
     for (int i = 0; i < E::R; ++i) {

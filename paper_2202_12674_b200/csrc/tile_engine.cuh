@@ -22,11 +22,58 @@
 //    X^T[dpad][mpad] (the paper's column-major layout); thread (ry, rx) owns rows
 //    ry*4 + 64u + v, every smem read is one conflict-free LDS.128.
 #pragma once
+#include <cuda.h>
+
 #include <type_traits>
 
 #include "common.cuh"
 
 namespace plssvm {
+
+// Operands of a tile kernel.  fp64: two TMA descriptors over the point-major array(s) (box
+// 16 features x 128 rows for the row operand, 16 x 64 for the column operand, SWIZZLE_128B);
+// fp32 (FFMA engine): plain pointers into the feature-major arrays with their leading dimension.
+template <typename T>
+struct Ops;
+template <>
+struct Ops<double> {
+    CUtensorMap a, b;
+};
+template <>
+struct Ops<float> {
+    const float *a, *b;
+    int64_t ld;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbarrier_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbarrier_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity));
+}
+__device__ __forceinline__ void mbarrier_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbarrier_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes));
+}
+__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T *align_smem(unsigned char *raw) {
+    return reinterpret_cast<T *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+}
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -55,7 +102,7 @@ struct Engine<double> {
     static constexpr int STAGES = 4;
     static constexpr int SLAB_A = kTile * BK, SLAB_B = TN * BK;
     static constexpr int STAGE = SLAB_A + SLAB_B;
-    static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE * sizeof(T);  // 96 KiB
+    static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE * sizeof(T) + 1024;  // 96 KiB + alignment
     static constexpr int R = 4;                    // accumulator rows per thread (m-tiles)
     static constexpr int CC = 16;                  // accumulator columns per thread (8 n-tiles x 2)
 
@@ -65,23 +112,7 @@ struct Engine<double> {
     // local tile row of accumulator row index i (0..R-1), local tile col of column index j (0..CC-1)
     __device__ static __forceinline__ int row_of(int i) { return wm() * 32 + i * 8 + pi(lane() >> 2); }
     __device__ static __forceinline__ int col_of(int j) { return (j >> 1) * 8 + pi(2 * (lane() & 3) + (j & 1)); }
-    __device__ static __forceinline__ const T *block(const T *X, int64_t row0, int64_t ld) { return X + row0 * ld; }
-
-    __device__ static __forceinline__ void load_slab(T *sA, T *sB, const T *__restrict__ A, const T *__restrict__ B,
-                                                     int64_t ld, int64_t k0) {
-#pragma unroll
-        for (int u = 0; u < (kTile * 8) / THREADS; ++u) {  // A: 128 rows x 8 chunks of 16 B
-            const int ch = threadIdx.x + u * THREADS;
-            const int row = ch >> 3, c = ch & 7;
-            cp_async16(sA + row * BK + ((c ^ (row & 7)) << 1), A + row * ld + k0 + c * 2);
-        }
-#pragma unroll
-        for (int u = 0; u < (TN * 8) / THREADS; ++u) {     // B: 64 rows x 8 chunks
-            const int ch = threadIdx.x + u * THREADS;
-            const int row = ch >> 3, c = ch & 7;
-            cp_async16(sB + row * BK + ((c ^ (row & 7)) << 1), B + row * ld + k0 + c * 2);
-        }
-    }
+    static constexpr uint32_t STAGE_BYTES = uint32_t(STAGE) * sizeof(T);
 
     __device__ static __forceinline__ void mma(double (&c)[2], double a, double b) {
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -89,31 +120,43 @@ struct Engine<double> {
                      : "d"(a), "d"(b));
     }
 
-    // acc[i][j] = S[row_of(i)][col_of(j)] = sum_k A[row][k] B[col][k]
-    __device__ static __forceinline__ void contract(const T *__restrict__ A, const T *__restrict__ B, int64_t ld,
-                                                    int64_t dpad, T *smem, T (&acc)[R][CC]) {
+    // acc[i][j] = S[row_of(i)][col_of(j)] = sum_k A[row0 + row][k] B[col0 + col][k].
+    // TMA ring: thread 0 issues the two boxes of a slab (SWIZZLE_128B places 16-byte chunk c of
+    // row r at c ^ (r & 7), the layout the fragment loads below expect) and completes them on
+    // full[stage]; each warp releases a stage with one arrive on empty[stage] (count 4); thread 0
+    // refills a stage once all four warps released it.  No block-wide barrier in the loop.
+    __device__ static __forceinline__ void contract(const Ops<double> &ops, int row0, int col0, int64_t dpad, T *smem,
+                                                    T (&acc)[R][CC]) {
+        __shared__ uint64_t full[STAGES], empty[STAGES];
 #pragma unroll
         for (int i = 0; i < R; ++i)
 #pragma unroll
             for (int j = 0; j < CC; ++j) acc[i][j] = 0.0;
         const int nk = static_cast<int>(dpad / BK);
+        if (threadIdx.x == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ops.a)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ops.b)) : "memory");
+            for (int s = 0; s < STAGES; ++s) {
+                mbarrier_init(&full[s], 1);
+                mbarrier_init(&empty[s], THREADS / 32);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < STAGES && s < nk; ++s) {
+                mbarrier_expect_tx(&full[s], STAGE_BYTES);
+                tma_2d(smem + s * STAGE, &ops.a, &full[s], s * BK, row0);
+                tma_2d(smem + s * STAGE + SLAB_A, &ops.b, &full[s], s * BK, col0);
+            }
+        }
         const int ln = lane(), q = ln & 3, prow = pi(ln >> 2);
         const int arow = wm() * 32 + prow, brow = prow;
-#pragma unroll
-        for (int s = 0; s < STAGES - 1; ++s) {
-            if (s < nk) load_slab(smem + s * STAGE, smem + s * STAGE + SLAB_A, A, B, ld, int64_t(s) * BK);
-            cp_async_commit();
-        }
         for (int kb = 0; kb < nk; ++kb) {
-            cp_async_wait<STAGES - 2>();
-            __syncthreads();
-            const int pf = kb + STAGES - 1;
-            if (pf < nk) {
-                const int st = pf % STAGES;
-                load_slab(smem + st * STAGE, smem + st * STAGE + SLAB_A, A, B, ld, int64_t(pf) * BK);
-            }
-            cp_async_commit();
-            const T *sA = smem + (kb % STAGES) * STAGE;
+            const int st = kb % STAGES;
+            const uint32_t par = (kb / STAGES) & 1;
+            mbarrier_wait(&full[st], par);
+            const T *sA = smem + st * STAGE;
             const T *sB = sA + SLAB_A;
 #pragma unroll
             for (int g = 0; g < BK / 8; ++g) {
@@ -144,9 +187,16 @@ struct Engine<double> {
                         mma(cc, a[mt].y, b[nt].y);
                     }
             }
+            __syncwarp();
+            if (ln == 0) mbarrier_arrive(&empty[st]);
+            if (threadIdx.x == 0 && kb + STAGES < nk) {
+                mbarrier_wait(&empty[st], par);
+                mbarrier_expect_tx(&full[st], STAGE_BYTES);
+                tma_2d(smem + st * STAGE, &ops.a, &full[st], (kb + STAGES) * BK, row0);
+                tma_2d(smem + st * STAGE + SLAB_A, &ops.b, &full[st], (kb + STAGES) * BK, col0);
+            }
         }
-        cp_async_wait<0>();
-        __syncthreads();  // ring is free for reuse by the epilogue
+        __syncthreads();  // every stage consumed and no TMA in flight: the ring is free for the epilogue
     }
 
     // Row sums rs[i] (over this thread's columns) -> red[128] : each tile row is owned by one
@@ -195,7 +245,7 @@ struct Engine<float> {
     static constexpr int VEC = 4;
     static constexpr int STAGES = 4;
     static constexpr int SLAB = BK * kTile;
-    static constexpr size_t SMEM_BYTES = size_t(STAGES) * 2 * SLAB * sizeof(T);  // 128 KiB
+    static constexpr size_t SMEM_BYTES = size_t(STAGES) * 2 * SLAB * sizeof(T) + 1024;  // 128 KiB + alignment
     static constexpr int CPR = kTile * sizeof(T) / 16;  // 16-byte chunks per slab row (32)
     static constexpr int CHUNKS = BK * CPR / kThreads;  // 4
     static constexpr int R = 8, CC = 8;
@@ -220,8 +270,11 @@ struct Engine<float> {
         }
     }
 
-    __device__ static __forceinline__ void contract(const T *__restrict__ A, const T *__restrict__ B, int64_t ld,
-                                                    int64_t dpad, T *smem, T (&acc)[R][CC]) {
+    __device__ static __forceinline__ void contract(const Ops<float> &ops, int row0, int col0, int64_t dpad, T *smem,
+                                                    T (&acc)[R][CC]) {
+        const T *__restrict__ A = ops.a + row0;
+        const T *__restrict__ B = ops.b + col0;
+        const int64_t ld = ops.ld;
         const int y = ry(), x = rx();
 #pragma unroll
         for (int i = 0; i < 8; ++i)
