@@ -28,13 +28,16 @@ int comm_rank(const CommHandle *c) { return c->rank; }
 int comm_size(const CommHandle *c) { return c->nranks; }
 int comm_device(const CommHandle *c) { return c->device; }
 
-void comm_allreduce_sum_f64(CommHandle *c, double *buf, int64_t count, void *stream) {
-    if (c->callbacks) {
-        if (c->cb.allreduce_sum_f64(c->cb.ctx, buf, count, stream) != 0)
+// Out-of-place sum all-reduce (send: this rank's partials, recv: the global values).
+void comm_allreduce_sum_f64(CommHandle *c, const double *send, double *recv, int64_t count, void *stream) {
+    if (c->callbacks) {  // the user callback is in place: stage the partials in recv first
+        PLS_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 static_cast<cudaStream_t>(stream)));
+        if (c->cb.allreduce_sum_f64(c->cb.ctx, recv, count, stream) != 0)
             throw Error(PLSSVM_E_NCCL, "user allreduce callback failed");
         return;
     }
-    PLS_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum, c->nccl,
+    PLS_NCCL(ncclAllReduce(send, recv, static_cast<size_t>(count), ncclDouble, ncclSum, c->nccl,
                            static_cast<cudaStream_t>(stream)));
 }
 

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -214,6 +216,8 @@ struct Ctx {
     int nsplit = 1;  // cached GEMV: column splits per row block
     int64_t launches = 0, launches_cg = 0;
     Ops<T> ops;
+    int *ctrl = nullptr;             // device CG control block (kernels.cuh Ctl)
+    const int *cur_ctrl = nullptr;   // ctrl inside the CG loop (loop kernels early-exit when done)
 };
 
 template <typename T>
@@ -263,10 +267,11 @@ template <int KT, int MODE>
 void tc_launch(int grid, cudaStream_t s, const CUtensorMap &ah, const CUtensorMap &al, const CUtensorMap &bh,
                const CUtensorMap &bl, int64_t dpad, const int2 *tiles, int tilesI, const float *qa, const float *na,
                const float *qb, const float *nb_, const float *p, KParams<float> kp, float invC, const double *scal,
-               int64_t m1, int band0, int band1, float *Ypart, int64_t band_rows, float *Qc, int T_tiles) {
+               int64_t m1, int band0, int band1, float *Ypart, int64_t band_rows, float *Qc, int T_tiles,
+               const int *ctrl) {
     k_tile_tc<KT, MODE><<<grid, Tc::THREADS, Tc::SMEM_BYTES, s>>>(ah, al, bh, bl, dpad, tiles, tilesI, qa, na, qb, nb_, p,
                                                                  kp, invC, scal, m1, band0, band1, Ypart, band_rows,
-                                                                 Qc, T_tiles);
+                                                                 Qc, T_tiles, ctrl);
     PLS_CHECK_LAUNCH();
 }
 
@@ -294,7 +299,7 @@ bool launch_tc(Ctx<T> &c, const T *pfull) {
         const Geometry &g = c.g;
         tc_dispatch<TC_MATVEC>(c.kp.kernel, c.ntiles, c.s, c.tm_hi, c.tm_lo, c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, 0, c.q,
                                c.nrm, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1, g.band0, g.band1, c.Ypart, g.nb,
-                               static_cast<float *>(nullptr), g.T);
+                               static_cast<float *>(nullptr), g.T, c.cur_ctrl);
         ++c.launches;
         return true;
     }
@@ -307,7 +312,8 @@ bool launch_tc_precompute(Ctx<T> &c) {
         const Geometry &g = c.g;
         tc_dispatch<TC_PRECOMPUTE>(c.kp.kernel, c.ntiles, c.s, c.tm_hi, c.tm_lo, c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, 0,
                                    c.q, c.nrm, c.q, c.nrm, static_cast<const float *>(nullptr), c.kp, c.invC, c.scal,
-                                   g.m1, g.band0, g.band1, static_cast<float *>(nullptr), g.nb, c.Qc, g.T);
+                                   g.m1, g.band0, g.band1, static_cast<float *>(nullptr), g.nb, c.Qc, g.T,
+                                   static_cast<const int *>(nullptr));
         ++c.launches;
         return true;
     }
@@ -327,7 +333,8 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
     const Geometry &g = c.g;
     if (c.cached) {
         const int rowblocks = static_cast<int>(g.nb / kTile);
-        k_gemv_tiled<T><<<rowblocks * c.nsplit, 256, 0, c.s>>>(c.Qc, pfull, g.T, c.nsplit, g.nb, c.Ypart);
+        k_gemv_tiled<T><<<rowblocks * c.nsplit, 256, 0, c.s>>>(c.Qc, pfull, g.T, c.nsplit, g.nb, c.Ypart,
+                                                                c.cur_ctrl);
         PLS_CHECK_LAUNCH();
         ++c.launches;
         return c.nsplit;
@@ -338,17 +345,17 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
         case LINEAR:
             k_matvec_implicit<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull,
                                                                          c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
-                                                                         c.Ypart, g.nb);
+                                                                         c.Ypart, g.nb, c.cur_ctrl);
             break;
         case POLYNOMIAL:
             k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm,
                                                                              pfull, c.kp, c.invC, c.scal, g.m1, g.band0,
-                                                                             g.band1, c.Ypart, g.nb);
+                                                                             g.band1, c.Ypart, g.nb, c.cur_ctrl);
             break;
         default:
             k_matvec_implicit<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull,
                                                                       c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
-                                                                      c.Ypart, g.nb);
+                                                                      c.Ypart, g.nb, c.cur_ctrl);
     }
     PLS_CHECK_LAUNCH();
     ++c.launches;
@@ -382,7 +389,8 @@ void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par,
     const Geometry &g = c.g;
     k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, nslots, c.cached ? 1 : Engine<T>::NSUB, g.band0,
                                                        g.nb, g.g0, g.m1, pband, c.y, mode, c.ylab,
-                                                       c.r, pout, c.scal, par, set_delta0, c.partials, c.counter, 1);
+                                                       c.r, pout, c.scal, par, set_delta0, c.partials, c.counter, 1,
+                                                       c.cur_ctrl);
     PLS_CHECK_LAUNCH();
     ++c.launches;
 }
@@ -392,7 +400,7 @@ int dtype_of(double) { return PLSSVM_F64; }
 
 template <typename T>
 void allreduce(Ctx<T> &c, int slot, int count) {
-    if (c.comm) comm_allreduce_sum_f64(c.comm, c.scal + slot, count, c.s);
+    if (c.comm) comm_allreduce_sum_f64(c.comm, c.scal + slot + S_L, c.scal + slot, count, c.s);
 }
 template <typename T>
 void allgather(Ctx<T> &c, T *full) {
@@ -532,71 +540,83 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         allreduce(c, S_DELTA0, 2);
     }
     allgather(c, c.p);
-    int64_t matvecs = (o.x0 == 0) ? 0 : 1;
 
-    // host-visible scalars (pinned) for the convergence test (a5)
+    // ---- CG loop (a3-a5, a8): the convergence test runs on the device (k_update_p), the host
+    // enqueues iterations in batches of kBatch and reads the control block once per batch --
+    // no host round trip per iteration; iterations enqueued after convergence are no-ops.
+    c.ctrl = A.alloc<int>(C_COUNT);
+    const int imax_i = static_cast<int>(std::min<int64_t>(imax, INT32_MAX));
+    const int fixed_i = static_cast<int>(std::min<int64_t>(std::max<int64_t>(o.fixed_iter, 0), INT32_MAX));
+    k_cg_start<<<1, 1, 0, c.s>>>(c.scal, c.ctrl, pb.eps * pb.eps, imax_i, fixed_i);
+    PLS_CHECK_LAUNCH();
+    ++c.launches;
     double *hs = nullptr;
-    PLS_CUDA(cudaMallocHost(&hs, S_COUNT * sizeof(double)));
+    PLS_CUDA(cudaMallocHost(&hs, S_COUNT * sizeof(double) + C_COUNT * sizeof(int)));
     struct HostFree {
         double *p;
         ~HostFree() { cudaFreeHost(p); }
     } hf{hs};
-    PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
-    PLS_CUDA(cudaStreamSynchronize(c.s));
-    const double delta0 = hs[S_DELTA0];
-    double delta = hs[S_DELTA];
-    const double eps2 = pb.eps * pb.eps;
+    int *hctrl = reinterpret_cast<int *>(hs + S_COUNT);
     const int64_t launches_before_cg = c.launches;
-
-    cudaEvent_t mv0 = E.make(), mv1 = E.make();
+    constexpr int kBatch = 8;
+    cudaEvent_t mv0[kBatch], mv1[kBatch];
+    for (int b = 0; b < kBatch; ++b) {
+        mv0[b] = E.make();
+        mv1[b] = E.make();
+    }
     double t_mv = 0.0, t_mv_min = 1e30;
     int64_t it = 0;
-    int par = 0;
-    int status = PLSSVM_OK;
-    auto keep_going = [&]() {
-        if (it >= imax) return false;
-        if (o.fixed_iter > 0) return it < o.fixed_iter;
-        return delta > eps2 * delta0;
-    };
-    while (keep_going()) {
-        PLS_CUDA(cudaEventRecord(mv0, c.s));
-        const int ns = launch_qtilde_product<T>(c, c.p);
-        PLS_CUDA(cudaEventRecord(mv1, c.s));
-        ++matvecs;
-        finalize<T>(c, ns, pband, 0, nullptr, par, 0);
-        allreduce(c, S_PAP, 1);
-        k_update_xr<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.y, g.nb, c.scal, par, c.partials,
-                                                            c.counter);
-        PLS_CHECK_LAUNCH();
-        ++c.launches;
-        allreduce(c, S_DELTA + (par ^ 1), 1);
-        if (o.replace_every > 0 && it > 0 && it % o.replace_every == 0) {
-            // explicit residual r = rhs - Q~x (Shewchuk B2 replacement, option R > 0)
-            PLS_CUDA(cudaMemcpyAsync(c.xfull + g.g0, c.x, g.nb * sizeof(T), cudaMemcpyDeviceToDevice, c.s));
-            allgather(c, c.xfull);
-            const int ns2 = launch_qtilde_product<T>(c, c.xfull);
-            ++matvecs;
-            finalize<T>(c, ns2, nullptr, 1, nullptr, par ^ 1, 0);
+    c.cur_ctrl = c.ctrl;
+    while (true) {
+        for (int b = 0; b < kBatch; ++b) {
+            const int64_t k = it + b;  // iteration index if the loop is still running
+            const int par = static_cast<int>(k & 1);
+            PLS_CUDA(cudaEventRecord(mv0[b], c.s));
+            const int ns = launch_qtilde_product<T>(c, c.p);
+            PLS_CUDA(cudaEventRecord(mv1[b], c.s));
+            finalize<T>(c, ns, pband, 0, nullptr, 0, 0);
+            allreduce(c, S_PAP, 1);
+            k_update_xr<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.y, g.nb, c.scal, c.ctrl, c.partials,
+                                                                c.counter);
+            PLS_CHECK_LAUNCH();
+            ++c.launches;
             allreduce(c, S_DELTA + (par ^ 1), 1);
+            if (o.replace_every > 0 && k > 0 && k % o.replace_every == 0) {
+                // explicit residual r = rhs - Q~x (Shewchuk B2 replacement, option R > 0)
+                PLS_CUDA(cudaMemcpyAsync(c.xfull + g.g0, c.x, g.nb * sizeof(T), cudaMemcpyDeviceToDevice, c.s));
+                allgather(c, c.xfull);
+                const int ns2 = launch_qtilde_product<T>(c, c.xfull);
+                finalize<T>(c, ns2, nullptr, 1, nullptr, -1, 0);
+                allreduce(c, S_DELTA + (par ^ 1), 1);
+            }
+            k_update_p<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter);
+            PLS_CHECK_LAUNCH();
+            ++c.launches;
+            allgather(c, c.p);
         }
-        k_update_p<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, par);
-        PLS_CHECK_LAUNCH();
-        ++c.launches;
-        allgather(c, c.p);
         PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        PLS_CUDA(cudaMemcpyAsync(hctrl, c.ctrl, C_COUNT * sizeof(int), cudaMemcpyDeviceToHost, c.s));
         PLS_CUDA(cudaStreamSynchronize(c.s));
-        const double tm = elapsed(mv0, mv1);
-        t_mv += tm;
-        t_mv_min = std::min(t_mv_min, tm);
-        ++it;
-        const double pap = hs[S_PAP];
-        delta = hs[S_DELTA + (par ^ 1)];
-        par ^= 1;
-        if (!(pap > 0.0) || !std::isfinite(pap) || !std::isfinite(delta)) {
-            status = PLSSVM_E_NUMERICAL;
-            break;
+        const int64_t ran = hctrl[C_IT] - it;  // iterations of this batch that did work
+        for (int b = 0; b < ran && b < kBatch; ++b) {
+            const double tm = elapsed(mv0[b], mv1[b]);
+            t_mv += tm;
+            t_mv_min = std::min(t_mv_min, tm);
         }
+        it = hctrl[C_IT];
+        if (std::getenv("PLSSVM_DEBUG"))
+            std::fprintf(stderr, "[plssvm] batch: it=%d done=%d d0=%.6e d[0]=%.6e d[1]=%.6e thr=%.6e pap=%.6e\n",
+                         hctrl[C_IT], hctrl[C_DONE], hs[S_DELTA0], hs[S_DELTA], hs[S_DELTA + 1], hs[S_THR], hs[S_PAP]);
+        if (hctrl[C_DONE] != 0 || ran < kBatch) break;
     }
+    c.cur_ctrl = nullptr;
+    int64_t matvecs = it + ((o.x0 == 0) ? 0 : 1);
+    if (o.replace_every > 0 && it > 1) matvecs += (it - 1) / o.replace_every;
+    const double delta0 = hs[S_DELTA0];
+    const double delta = hs[S_DELTA + (it & 1)];
+    const double eps2 = pb.eps * pb.eps;
+    int status = PLSSVM_OK;
+    if (hctrl[C_DONE] == 2) status = PLSSVM_E_NUMERICAL;
     c.launches_cg = c.launches - launches_before_cg;
     PLS_CUDA(cudaEventRecord(e_cg, c.s));
     if (status == PLSSVM_OK && o.fixed_iter <= 0 && delta > eps2 * delta0) status = PLSSVM_W_NOT_CONVERGED;
@@ -765,7 +785,7 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
             tc_dispatch<TC_PREDICT>(pb.kernel, grid, s, zh, zl, xh, xl, dtc, static_cast<const int2 *>(nullptr), tilesI,
                                     static_cast<const float *>(nullptr), nz, static_cast<const float *>(nullptr), nx,
                                     alpha, kp, 0.f, static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,
-                                    static_cast<float *>(nullptr), 0);
+                                    static_cast<float *>(nullptr), 0, static_cast<const int *>(nullptr));
         }
     }
     const Ops<T> pops = make_ops(Zl, zrows, Xl, xrows, EN::kPointMajor ? dpad : L);

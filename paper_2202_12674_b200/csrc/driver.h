@@ -31,7 +31,7 @@ int qtilde_matvec(const Problem &pb, const void *p, int32_t repeats, const plssv
 int comm_rank(const CommHandle *c);
 int comm_size(const CommHandle *c);
 int comm_device(const CommHandle *c);
-void comm_allreduce_sum_f64(CommHandle *c, double *buf, int64_t count, void *stream);
+void comm_allreduce_sum_f64(CommHandle *c, const double *send, double *recv, int64_t count, void *stream);
 void comm_allgather(CommHandle *c, void *buf, int64_t count_per_rank, int dtype, void *stream);
 const char *nccl_version_string();
 

@@ -26,8 +26,18 @@ enum Scal : int {
     S_SUMX = 7,     // sum of x (bias)
     S_QX = 8,       // <q, x>  (bias)
     S_B = 9,        // bias b
-    S_COUNT = 16
+    S_THR = 10,     // eps^2 delta_0 (the CG stopping threshold on delta)
+    S_L = 16,       // slot s + S_L holds this rank's local partial of slot s; the multi-GPU
+                    // all-reduce is out of place (local -> global), hence idempotent: iterations
+                    // enqueued after convergence cannot corrupt the global scalars
+    S_COUNT = 32
 };
+
+// Device-side CG control block (int32[4]): the loop runs without a host round trip per
+// iteration; every loop kernel returns immediately once `done` is set, so the host can enqueue
+// iterations in batches and read the state once per batch.
+enum Ctl : int { C_IT = 0, C_DONE = 1, C_IMAX = 2, C_FIXED = 3, C_COUNT = 4 };
+__device__ __forceinline__ bool cg_done(const int *ctrl) { return ctrl != nullptr && *(volatile const int *)(ctrl + C_DONE) != 0; }
 
 // ---------------------------------------------------------------------------------------
 // Deterministic grid reduction: every block writes its partial; the last block to finish
@@ -166,8 +176,9 @@ __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
     k_matvec_implicit(const __grid_constant__ Ops<T> ops, int64_t dpad, const int2 *__restrict__ tiles,
                       const T *__restrict__ q, const T *__restrict__ nrm, const T *__restrict__ p, KParams<T> kp,
                       T invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
-                      T *__restrict__ Ypart, int64_t band_rows) {
+                      T *__restrict__ Ypart, int64_t band_rows, const int *ctrl) {
     using E = Engine<T>;
+    if (cg_done(ctrl)) return;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     T *smem = align_smem<T>(smem_raw);
     const int2 tile = tiles[blockIdx.x];
@@ -282,7 +293,8 @@ __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
 // (ld.global.nc.L1::no_allocate), every load independent.  Partial sums go to Ypart[split].
 template <typename T>
 __global__ void __launch_bounds__(256) k_gemv_tiled(const T *__restrict__ Qc, const T *__restrict__ p, int T_tiles,
-                                                    int nsplit, int64_t nb, T *__restrict__ Ypart) {
+                                                    int nsplit, int64_t nb, T *__restrict__ Ypart, const int *ctrl) {
+    if (cg_done(ctrl)) return;
     using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
     constexpr int VEC = 16 / sizeof(T);
     constexpr int LPR = kTile / (32 * VEC);  // 16-byte loads per lane per row (2 fp64, 1 fp32)
@@ -333,13 +345,16 @@ __global__ void __launch_bounds__(256) k_gemv_tiled(const T *__restrict__ Qc, co
 // padding and stay 0).  Scalars live in `scal` (double) so no host round trip is needed.
 
 // y_i = sum_s Ypart[s][i] (fixed slot order), then pAp = p . y  (mode 0), or for the initial
-// / replaced residual (mode 1): r_i = rhs_i - y_i, r.r -> S_DELTA+par (and S_DELTA0 if init).
+// / replaced residual (mode 1): r_i = rhs_i - y_i, r.r -> S_DELTA+par (and S_DELTA0 if init);
+// par < 0: take the slot from the device iteration counter.
 template <typename T>
 __global__ void __launch_bounds__(kVecThreads)
     k_finalize(const T *__restrict__ Ypart, int nslots, int nsub, int band0, int64_t nb, int64_t g0, int64_t m1,
                const T *__restrict__ pband, T *__restrict__ y, int mode, const T *__restrict__ yl, T *__restrict__ r,
                T *__restrict__ pout, double *scal, int par, int set_delta0, T *partials, unsigned *counter,
-               int write_scalar) {
+               int write_scalar, const int *ctrl) {
+    if (cg_done(ctrl)) return;
+    if (par < 0) par = (ctrl[C_IT] & 1) ^ 1;  // residual replacement: the slot of delta_{k+1}
     T part = T(0);
     const double ym = scal[S_YM];
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
@@ -373,10 +388,10 @@ __global__ void __launch_bounds__(kVecThreads)
     grid_reduce<T>(part, partials, counter, [&](T tot) {
         if (!write_scalar) return;
         if (mode == 0) {
-            scal[S_PAP] = static_cast<double>(tot);
+            scal[S_PAP] = scal[S_PAP + S_L] = static_cast<double>(tot);
         } else {
-            scal[S_DELTA + par] = static_cast<double>(tot);
-            if (set_delta0) scal[S_DELTA0] = static_cast<double>(tot);
+            scal[S_DELTA + par] = scal[S_DELTA + par + S_L] = static_cast<double>(tot);
+            if (set_delta0) scal[S_DELTA0] = scal[S_DELTA0 + S_L] = static_cast<double>(tot);
         }
     });
 }
@@ -386,7 +401,9 @@ __global__ void __launch_bounds__(kVecThreads)
 template <typename T>
 __global__ void __launch_bounds__(kVecThreads)
     k_update_xr(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p, const T *__restrict__ y, int64_t nb,
-                double *scal, int par, T *partials, unsigned *counter) {
+                double *scal, const int *ctrl, T *partials, unsigned *counter) {
+    if (cg_done(ctrl)) return;
+    const int par = ctrl[C_IT] & 1;
     const T a = static_cast<T>(scal[S_DELTA + par] / scal[S_PAP]);
     T part = T(0);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
@@ -397,19 +414,54 @@ __global__ void __launch_bounds__(kVecThreads)
         part = fma(ri, ri, part);
     }
     grid_reduce<T>(part, partials, counter, [&](T tot) {
-        scal[S_DELTA + (par ^ 1)] = static_cast<double>(tot);
+        scal[S_DELTA + (par ^ 1)] = scal[S_DELTA + (par ^ 1) + S_L] = static_cast<double>(tot);
         scal[S_ALPHA] = static_cast<double>(a);
     });
 }
 
-// p = r + b p  with b = delta_{k+1} / delta_k
+// p = r + b p  with b = delta_{k+1} / delta_k; the last block then advances the iteration counter
+// and evaluates Shewchuk's loop condition (i < imax and delta > eps^2 delta_0) and the
+// breakdown test (p.Q~p <= 0 or non-finite).  With fixed > 0 the loop runs exactly
+// `fixed` iterations.
 template <typename T>
 __global__ void __launch_bounds__(kVecThreads)
-    k_update_p(T *__restrict__ p, const T *__restrict__ r, int64_t nb, const double *scal, int par) {
+    k_update_p(T *__restrict__ p, const T *__restrict__ r, int64_t nb, const double *scal, int *ctrl,
+               unsigned *counter) {
+    if (cg_done(ctrl)) return;
+    const int par = ctrl[C_IT] & 1;
     const T b = static_cast<T>(scal[S_DELTA + (par ^ 1)] / scal[S_DELTA + par]);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         p[i] = fma(b, p[i], r[i]);
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        const int it = ctrl[C_IT] + 1;
+        const double pap = scal[S_PAP], dnew = scal[S_DELTA + (par ^ 1)];
+        int done = 0;
+        if (!(pap > 0.0) || !isfinite(pap) || !isfinite(dnew)) done = 2;
+        else if (ctrl[C_FIXED] > 0 ? (it >= ctrl[C_FIXED] || dnew == 0.0) : (dnew <= scal[S_THR])) done = 1;
+        else if (it >= ctrl[C_IMAX]) done = 1;
+        ctrl[C_IT] = it;
+        ctrl[C_DONE] = done;
+        *counter = 0u;
+    }
+}
+
+// Loop entry (after delta_0 is final on every rank): threshold and control block.
+__global__ void k_cg_start(double *scal, int *ctrl, double eps2, int imax, int fixed) {
+    const double d0 = scal[S_DELTA0];
+    scal[S_THR] = eps2 * d0;
+    ctrl[C_IT] = 0;
+    ctrl[C_IMAX] = imax;
+    ctrl[C_FIXED] = fixed;
+    ctrl[C_DONE] = (imax <= 0 || (fixed > 0 ? d0 == 0.0 : d0 <= eps2 * d0)) ? 1 : 0;
 }
 
 // x = x0 (0 or 1 on valid rows), and, for x0 = 0, r = p = rhs, delta0 = r.r.
@@ -433,8 +485,8 @@ __global__ void __launch_bounds__(kVecThreads)
     if (zero_start)
         grid_reduce<T>(part, partials, counter, [&](T tot) {
             if (write_scalar) {
-                scal[S_DELTA + 0] = static_cast<double>(tot);
-                scal[S_DELTA0] = static_cast<double>(tot);
+                scal[S_DELTA + 0] = scal[S_DELTA + S_L] = static_cast<double>(tot);
+                scal[S_DELTA0] = scal[S_DELTA0 + S_L] = static_cast<double>(tot);
             }
         });
 }
@@ -448,7 +500,10 @@ __global__ void __launch_bounds__(kVecThreads)
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         part = (which == 0) ? part + x[i] : fma(q[g0 + i], x[i], part);
-    grid_reduce<T>(part, partials, counter, [&](T tot) { scal[which == 0 ? S_SUMX : S_QX] = static_cast<double>(tot); });
+    grid_reduce<T>(part, partials, counter, [&](T tot) {
+        const int sl = which == 0 ? S_SUMX : S_QX;
+        scal[sl] = scal[sl + S_L] = static_cast<double>(tot);
+    });
 }
 
 // b = y_m + Q_mm sum(x) - <q,x> (Eq. 15); alpha = (x_0..x_{m-2}, -sum x).

@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(Tc::THREADS, 1)
               const int2 *__restrict__ tiles, int tilesI, const float *__restrict__ qa, const float *__restrict__ na,
               const float *__restrict__ qb, const float *__restrict__ nb_, const float *__restrict__ p,
               KParams<float> kp, float invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
-              float *__restrict__ Ypart, int64_t band_rows, float *__restrict__ Qc, int T_tiles) {
+              float *__restrict__ Ypart, int64_t band_rows, float *__restrict__ Qc, int T_tiles, const int *ctrl) {
+    if (cg_done(ctrl)) return;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     float *ring = reinterpret_cast<float *>(base);
