@@ -241,3 +241,50 @@ def test_c1_full_size_sampled_rows_and_residual():
     f_ref, lab_ref = oracle.predict(X, alpha, b, Z[zi], cfg.kernel, cfg.gamma)
     f, lab = pl.plssvm_predict(X, alpha, b, Z, cfg.kernel, cfg.gamma)
     assert np.array_equal(lab[zi], lab_ref)
+
+
+def _sampled_rows(m, rng, k=48):
+    return np.unique(np.concatenate([[0, 1, 127, 128, m - 2], rng.integers(0, m - 1, k)]))
+
+
+def test_c3_full_size_fp32_tensor_core_sampled_rows():
+    """C3 (2^15 x 2^11 poly-3 fp32) at full size on the default tcgen05 3xTF32 engine, implicit and
+    cached: sampled rows of Q~p against the oracle's rows (fp32-rounded inputs in fp64)."""
+    cfg = synth.configs()["C3"]
+    X, y, Z, yz = synth.config_data(cfg, n_test=0)
+    rng = np.random.default_rng(33)
+    p = rng.standard_normal(cfg.m - 1).astype(np.float32)
+    rows = _sampled_rows(cfg.m, rng)
+    R = oracle.qtilde_rows(X.astype(np.float64), rows, cfg.kernel, float(np.float32(cfg.gamma)), cfg.degree,
+                           cfg.coef0, cfg.C)
+    ref = R @ p.astype(np.float64)
+    scale = np.abs(R) @ np.abs(p.astype(np.float64))
+    for mode in (pl.MODE_IMPLICIT, pl.MODE_CACHED):
+        out, _ = pl.plssvm_qtilde_matvec(X, p, cfg.kernel, float(np.float32(cfg.gamma)), cfg.degree, cfg.coef0, cfg.C,
+                                         opts=pl.options(mode=mode))
+        err = np.abs(out[rows].astype(np.float64) - ref) / scale
+        assert err.max() <= 1e-5, (mode, err.max())
+
+
+def test_c2_full_size_cached_and_implicit_sampled_rows():
+    """C2 (2^16 x 2^12 linear fp64) at full size: the cached product (34 GB Q~ in HBM) and the
+    implicit product on sampled rows against the oracle; the trained model's residual on the
+    same rows (cached mode, the mode AUTO picks)."""
+    cfg = synth.configs()["C2"]
+    X, y, Z, yz = synth.config_data(cfg, n_test=0)
+    rng = np.random.default_rng(22)
+    p = rng.standard_normal(cfg.m - 1)
+    rows = _sampled_rows(cfg.m, rng, 24)
+    R = oracle.qtilde_rows(X, rows, cfg.kernel, cfg.gamma, C=cfg.C)
+    ref = R @ p
+    scale = np.abs(R) @ np.abs(p)
+    for mode in (pl.MODE_CACHED, pl.MODE_IMPLICIT):
+        out, _ = pl.plssvm_qtilde_matvec(X, p, cfg.kernel, cfg.gamma, C=cfg.C, opts=pl.options(mode=mode))
+        assert np.all(np.abs(out[rows] - ref) <= 1e-12 * scale), mode
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, cfg.kernel, cfg.gamma, C=cfg.C, eps=cfg.eps,
+                                             opts=pl.options(mode=pl.MODE_AUTO))
+    assert st == 0 and stats.mode_used == pl.MODE_CACHED
+    rhs = y[:-1] - y[-1]
+    res = np.abs(R @ alpha[:-1] - rhs[rows])
+    assert np.max(res) <= 1e-7 * np.linalg.norm(rhs)
+    assert abs(alpha.sum()) <= 1e-10 * np.abs(alpha).max()
