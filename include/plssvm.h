@@ -144,7 +144,11 @@ PLSSVM_API int plssvm_qtilde_matvec(const void *X, const void *p, int64_t m, int
                          double gamma, int degree, double coef0, double C, int32_t repeats,
                          const plssvm_options_t *opts, void *out, double *t_kernel);
 
-/* ---- multi-GPU (one process per GPU, row-sharded Q~; NCCL over NVLink) -----------------
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) -----------------------------------
+ * Vectors are row-sharded (rank r owns rows [r*m_pad/P, (r+1)*m_pad/P)).  Cached mode: each
+ * rank stores and streams its rows of Q~.  Implicit mode: the symmetric tile pairs are dealt
+ * out circulantly (tile row I computes pairs (I, I+j mod T), j = 0..T/2), so every rank does
+ * ~1/P of the symmetric work; the partial products are combined by a reduce-scatter.
  * plssvm_comm_unique_id writes an opaque 128-byte NCCL id (rank 0 creates it, the caller
  * broadcasts it, e.g. with torch.distributed); every rank then calls plssvm_comm_init.
  * The communicator is bound to `device`.  Destroy with plssvm_comm_destroy. */
@@ -165,6 +169,10 @@ typedef struct {
     /* rank r's count_per_rank elements live at buf + r * count_per_rank; afterwards every rank
      * holds all nranks * count_per_rank elements.  dtype: PLSSVM_F64 / PLSSVM_F32. */
     int (*allgather)(void *ctx, void *buf, int64_t count_per_rank, int32_t dtype, void *stream);
+    /* optional (NULL: implicit mode falls back to row bands): recv[0..count_per_rank) <- this
+     * rank's block of the element-wise sum over ranks of send[0..nranks*count_per_rank). */
+    int (*reduce_scatter_sum)(void *ctx, const void *send, void *recv, int64_t count_per_rank, int32_t dtype,
+                              void *stream);
 } plssvm_comm_callbacks_t;
 PLSSVM_API int plssvm_comm_init_callbacks(const plssvm_comm_callbacks_t *cb, int32_t nranks, int32_t rank,
                                           int32_t device, plssvm_comm_t *comm);

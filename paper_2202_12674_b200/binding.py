@@ -49,10 +49,12 @@ class plssvm_stats_t(ct.Structure):
 
 ALLREDUCE_CB = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_void_p)
 ALLGATHER_CB = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_void_p)
+REDUCE_SCATTER_CB = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_void_p)
 
 
 class plssvm_comm_callbacks_t(ct.Structure):
-    _fields_ = [("ctx", ct.c_void_p), ("allreduce_sum_f64", ALLREDUCE_CB), ("allgather", ALLGATHER_CB)]
+    _fields_ = [("ctx", ct.c_void_p), ("allreduce_sum_f64", ALLREDUCE_CB), ("allgather", ALLGATHER_CB),
+                ("reduce_scatter_sum", REDUCE_SCATTER_CB)]
 
 
 class PlssvmError(RuntimeError):
@@ -290,9 +292,11 @@ def plssvm_comm_init(uid: bytes, nranks: int, rank: int, device: int):
 _CALLBACK_KEEPALIVE = {}
 
 
-def plssvm_comm_init_callbacks(allreduce_sum_f64, allgather, nranks: int, rank: int, device: int):
-    """Communicator whose two collectives are Python callables (see plssvm.h)."""
-    cb = plssvm_comm_callbacks_t(None, ALLREDUCE_CB(allreduce_sum_f64), ALLGATHER_CB(allgather))
+def plssvm_comm_init_callbacks(allreduce_sum_f64, allgather, nranks: int, rank: int, device: int,
+                               reduce_scatter_sum=None):
+    """Communicator whose collectives are Python callables (see plssvm.h)."""
+    cb = plssvm_comm_callbacks_t(None, ALLREDUCE_CB(allreduce_sum_f64), ALLGATHER_CB(allgather),
+                                 REDUCE_SCATTER_CB(reduce_scatter_sum) if reduce_scatter_sum else REDUCE_SCATTER_CB())
     h = ct.c_void_p()
     _check(load().plssvm_comm_init_callbacks(ct.byref(cb), nranks, rank, device, ct.byref(h)))
     _CALLBACK_KEEPALIVE[h.value] = cb
@@ -304,11 +308,12 @@ def plssvm_comm_destroy(comm) -> None:
     _CALLBACK_KEEPALIVE.pop(comm, None)
 
 
-def comm_host_staged(device: int):
+def comm_host_staged(device: int, circulant: bool = True):
     """Communicator over torch.distributed (any backend, e.g. gloo) with host staging: each
     collective synchronises the driver's stream, copies the device buffer to host, runs the
     torch.distributed collective and copies back.  For testing the row-sharded driver with
-    several processes on ONE GPU (NCCL refuses duplicate devices); not a fast path."""
+    several processes on ONE GPU (NCCL refuses duplicate devices); not a fast path.
+    circulant=False omits the reduce-scatter, so implicit mode uses plain row bands."""
     import torch
     import torch.distributed as dist
 
@@ -347,7 +352,17 @@ def comm_host_staged(device: int):
         dist.all_gather(parts, host)
         return h2d(buf, torch.cat(parts))
 
-    return plssvm_comm_init_callbacks(allreduce, allgather, world, rank, device)
+    def reduce_scatter(ctx, send, recv, count, dtype, stream):
+        es = 8 if dtype == F64 else 4
+        host = d2h(send, world * count * es, stream)
+        if host is None:
+            return 1
+        t = host.view(torch.float64 if dtype == F64 else torch.float32)
+        dist.all_reduce(t)  # sum over ranks, then keep this rank's block
+        return h2d(recv, t[rank * count:(rank + 1) * count].contiguous().view(torch.uint8))
+
+    return plssvm_comm_init_callbacks(allreduce, allgather, world, rank, device,
+                                      reduce_scatter if circulant else None)
 
 
 _cudart_lib = None

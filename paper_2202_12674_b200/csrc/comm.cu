@@ -55,6 +55,19 @@ void comm_allgather(CommHandle *c, void *buf, int64_t count_per_rank, int dtype,
                            static_cast<cudaStream_t>(stream)));
 }
 
+bool comm_has_reduce_scatter(const CommHandle *c) { return !c->callbacks || c->cb.reduce_scatter_sum != nullptr; }
+
+// recv[count_per_rank] <- this rank's block of sum over ranks of send[nranks * count_per_rank].
+void comm_reduce_scatter(CommHandle *c, const void *send, void *recv, int64_t count_per_rank, int dtype, void *stream) {
+    if (c->callbacks) {
+        if (!c->cb.reduce_scatter_sum || c->cb.reduce_scatter_sum(c->cb.ctx, send, recv, count_per_rank, dtype, stream) != 0)
+            throw Error(PLSSVM_E_NCCL, "user reduce_scatter callback failed");
+        return;
+    }
+    PLS_NCCL(ncclReduceScatter(send, recv, static_cast<size_t>(count_per_rank), dtype == PLSSVM_F32 ? ncclFloat : ncclDouble,
+                               ncclSum, c->nccl, static_cast<cudaStream_t>(stream)));
+}
+
 const char *nccl_version_string() {
     static std::string v;
     if (v.empty()) {

@@ -195,6 +195,26 @@ std::vector<int2> band_tiles(const Geometry &g, int nsub) {
     return t;
 }
 
+int dtype_of(float) { return PLSSVM_F32; }
+int dtype_of(double) { return PLSSVM_F64; }
+
+// Circulant assignment of the symmetric tile pairs (SURVEY §8(e) option ii): tile row I owns
+// the pairs (I, (I + j) mod T), j = 0..T/2, except that for even T the pair j = T/2 belongs to
+// the smaller row only -- every unordered pair exactly once, ~T/2 tiles per row.  This rank
+// takes the tile rows of its band.
+std::vector<int2> circulant_tiles(const Geometry &g, int nsub) {
+    std::vector<int2> t;
+    const int half = g.T / 2;
+    for (int I = g.band0; I < g.band1; ++I)
+        for (int j = 0; j <= half; ++j) {
+            if (g.T % 2 == 0 && j == half && I >= half) continue;
+            const int J = (I + j) % g.T;
+            if (j > 0 && J == I) continue;  // T == 1
+            for (int h = 0; h < nsub; ++h) t.push_back(make_int2(I, J * nsub + h));
+        }
+    return t;
+}
+
 template <typename T>
 struct Ctx {
     Geometry g;
@@ -216,6 +236,9 @@ struct Ctx {
     int nsplit = 1;  // cached GEMV: column splits per row block
     int64_t launches = 0, launches_cg = 0;
     Ops<T> ops;
+    bool circ = false;               // implicit multi-GPU: circulant pairs + reduce-scatter
+    T *yfull = nullptr, *ysc = nullptr, *Yfin = nullptr;
+    int nsub_eff = 1;
     int *ctrl = nullptr;             // device CG control block (kernels.cuh Ctl)
     const int *cur_ctrl = nullptr;   // ctrl inside the CG loop (loop kernels early-exit when done)
 };
@@ -294,11 +317,11 @@ void tc_set_attrs() {
 }
 
 template <typename T>
-bool launch_tc(Ctx<T> &c, const T *pfull) {
+bool launch_tc(Ctx<T> &c, const T *pfull, int b0, int b1, int64_t brows) {
     if constexpr (std::is_same<T, float>::value) {
         const Geometry &g = c.g;
         tc_dispatch<TC_MATVEC>(c.kp.kernel, c.ntiles, c.s, c.tm_hi, c.tm_lo, c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, 0, c.q,
-                               c.nrm, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1, g.band0, g.band1, c.Ypart, g.nb,
+                               c.nrm, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows,
                                static_cast<float *>(nullptr), g.T, c.cur_ctrl);
         ++c.launches;
         return true;
@@ -339,27 +362,44 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
         ++c.launches;
         return c.nsplit;
     }
-    if (c.tc && launch_tc<T>(c, pfull)) return g.T;
-    const size_t sm = Engine<T>::SMEM_BYTES;
-    switch (c.kp.kernel) {
-        case LINEAR:
-            k_matvec_implicit<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull,
-                                                                         c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
-                                                                         c.Ypart, g.nb, c.cur_ctrl);
-            break;
-        case POLYNOMIAL:
-            k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm,
-                                                                             pfull, c.kp, c.invC, c.scal, g.m1, g.band0,
-                                                                             g.band1, c.Ypart, g.nb, c.cur_ctrl);
-            break;
-        default:
-            k_matvec_implicit<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull,
-                                                                      c.kp, c.invC, c.scal, g.m1, g.band0, g.band1,
-                                                                      c.Ypart, g.nb, c.cur_ctrl);
+    // circulant multi-GPU: partial products for ALL rows (band = everything), zero-initialised
+    const int b0 = c.circ ? 0 : g.band0, b1 = c.circ ? g.T : g.band1;
+    const int64_t brows = c.circ ? g.mpad : g.nb;
+    const int nslots = g.T * c.nsub_eff;
+    if (c.circ) PLS_CUDA(cudaMemsetAsync(c.Ypart, 0, static_cast<size_t>(nslots) * g.mpad * sizeof(T), c.s));
+    if (c.tc) {
+        launch_tc<T>(c, pfull, b0, b1, brows);
+    } else {
+        const size_t sm = Engine<T>::SMEM_BYTES;
+        switch (c.kp.kernel) {
+            case LINEAR:
+                k_matvec_implicit<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(
+                    c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows,
+                    c.cur_ctrl);
+                break;
+            case POLYNOMIAL:
+                k_matvec_implicit<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(
+                    c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows,
+                    c.cur_ctrl);
+                break;
+            default:
+                k_matvec_implicit<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(
+                    c.ops, g.dpad, c.tiles, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows,
+                    c.cur_ctrl);
+        }
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
     }
+    if (!c.circ) {
+        c.Yfin = c.Ypart;
+        return nslots;
+    }
+    k_slot_sum<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, nslots, g.mpad, g.m1, c.yfull, c.cur_ctrl);
     PLS_CHECK_LAUNCH();
     ++c.launches;
-    return g.T * Engine<T>::NSUB;
+    comm_reduce_scatter(c.comm, c.yfull, c.ysc, g.nb, dtype_of(T()), c.s);
+    c.Yfin = c.ysc;
+    return 1;
 }
 
 template <typename T>
@@ -387,16 +427,13 @@ void launch_precompute(Ctx<T> &c) {
 template <typename T>
 void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par, int set_delta0) {
     const Geometry &g = c.g;
-    k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, nslots, c.cached ? 1 : Engine<T>::NSUB, g.band0,
+    k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Yfin, nslots, (c.cached || c.circ) ? 1 : c.nsub_eff, g.band0,
                                                        g.nb, g.g0, g.m1, pband, c.y, mode, c.ylab,
                                                        c.r, pout, c.scal, par, set_delta0, c.partials, c.counter, 1,
                                                        c.cur_ctrl);
     PLS_CHECK_LAUNCH();
     ++c.launches;
 }
-
-int dtype_of(float) { return PLSSVM_F32; }
-int dtype_of(double) { return PLSSVM_F64; }
 
 template <typename T>
 void allreduce(Ctx<T> &c, int slot, int count) {
@@ -456,6 +493,29 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     set_smem_attrs<T>();
 }
 
+// Product configuration once the mode is known: slot buffers, and for implicit multi-GPU the
+// circulant tile list (+ full-length partial product and reduce-scatter target).
+template <typename T>
+void configure_product(Ctx<T> &c, Arena &A) {
+    const Geometry &g = c.g;
+    c.nsub_eff = c.tc ? 1 : Engine<T>::NSUB;
+    c.nsplit = gemv_splits(g);
+    c.circ = g.P > 1 && !c.cached && comm_has_reduce_scatter(c.comm);
+    if (c.circ) {
+        std::vector<int2> tl = circulant_tiles(g, c.nsub_eff);
+        c.ntiles = static_cast<int>(tl.size());
+        c.tiles = A.alloc<int2>(c.ntiles);
+        PLS_CUDA(cudaMemcpyAsync(c.tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
+        PLS_CUDA(cudaStreamSynchronize(c.s));
+        c.Ypart = A.alloc<T>(static_cast<int64_t>(g.T) * c.nsub_eff * g.mpad);
+        c.yfull = A.alloc<T>(g.mpad);
+        c.ysc = A.alloc<T>(g.nb);
+    } else {
+        c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? c.nsplit : g.T * c.nsub_eff) * g.nb);
+    }
+    c.Yfin = c.Ypart;
+}
+
 // Mode selection (north_star: "mode picked by measurement"; SURVEY §8 decision 8): cached
 // whenever the Q~ band fits the budget -- the precompute costs about one implicit product and
 // every later product becomes an HBM stream (≈ 50-100x cheaper than a recompute).
@@ -513,8 +573,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     T *pband = c.p + g.g0;
 
     c.cached = choose_cached<T>(g, o);
-    c.nsplit = gemv_splits(g);
-    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? c.nsplit : g.T * Engine<T>::NSUB) * g.nb);
+    configure_product<T>(c, A);
     if (c.cached) c.Qc = A.alloc<T>(g.nb * g.mpad);
     PLS_CUDA(cudaEventRecord(e_alloc, c.s));
     if (c.cached) launch_precompute<T>(c);
@@ -688,8 +747,7 @@ int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, cons
     PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
     c.cached = (o.mode == PLSSVM_MODE_CACHED) || (o.mode == PLSSVM_MODE_AUTO && choose_cached<T>(g, o));
     if (c.cached) (void)choose_cached<T>(g, o);  // throws E_OOM if CACHED does not fit
-    c.nsplit = gemv_splits(g);
-    c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? c.nsplit : g.T * Engine<T>::NSUB) * g.nb);
+    configure_product<T>(c, A);
     double t_pre = 0.0;
     if (c.cached) {
         c.Qc = A.alloc<T>(g.nb * g.mpad);

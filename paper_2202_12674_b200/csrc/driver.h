@@ -33,6 +33,8 @@ int comm_size(const CommHandle *c);
 int comm_device(const CommHandle *c);
 void comm_allreduce_sum_f64(CommHandle *c, const double *send, double *recv, int64_t count, void *stream);
 void comm_allgather(CommHandle *c, void *buf, int64_t count_per_rank, int dtype, void *stream);
+bool comm_has_reduce_scatter(const CommHandle *c);
+void comm_reduce_scatter(CommHandle *c, const void *send, void *recv, int64_t count_per_rank, int dtype, void *stream);
 const char *nccl_version_string();
 
 }  // namespace plssvm

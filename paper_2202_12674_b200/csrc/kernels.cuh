@@ -340,6 +340,20 @@ __global__ void __launch_bounds__(256) k_gemv_tiled(const T *__restrict__ Qc, co
     }
 }
 
+// Circulant multi-GPU mode: this rank's partial product over ALL rows, y_i = sum_s Ypart[s][i]
+// in fixed slot order (slots this rank did not write were zeroed); reduce-scattered afterwards.
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_slot_sum(const T *__restrict__ Ypart, int nslots, int64_t rows, int64_t m1, T *__restrict__ y, const int *ctrl) {
+    if (cg_done(ctrl)) return;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        T s = T(0);
+        for (int k = 0; k < nslots; ++k) s += Ypart[static_cast<int64_t>(k) * rows + i];
+        y[i] = i < m1 ? s : T(0);
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // CG vector kernels on this rank's band (local length nb, rows with global index >= m1 are
 // padding and stay 0).  Scalars live in `scal` (double) so no host round trip is needed.

@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, path, kernel, mode, m, d):
+def _worker(rank, world, port, path, kernel, mode, m, d, circ):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -33,7 +33,7 @@ def _worker(rank, world, port, path, kernel, mode, m, d):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    comm = pl.comm_host_staged(0)
+    comm = pl.comm_host_staged(0, circulant=circ)
     X, y, Z, _ = synth.planes(m, d, 64, seed=21 + kernel)
     p = np.random.default_rng(5).standard_normal(m - 1)
     opts = pl.options(mode=mode, comm=comm)
@@ -48,18 +48,23 @@ def _worker(rank, world, port, path, kernel, mode, m, d):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("circ", [True, False])
 @pytest.mark.parametrize("world,kernel,mode,m,d", [
     (2, 2, 1, 1000, 33),    # RBF implicit, m_pad = 1024 -> 4 tiles per band
     (2, 0, 2, 700, 17),     # linear cached
-    (3, 1, 1, 900, 20),     # poly implicit, 3 ranks, ragged tail
+    (3, 1, 1, 900, 20),     # poly implicit, 3 ranks, ragged tail, odd T (9 tiles)
     (4, 2, 2, 1500, 9),     # RBF cached, 4 ranks
+    (4, 2, 1, 2000, 40),    # RBF implicit, 4 ranks, T = 16 (circulant j = T/2 pairs)
 ])
-def test_row_sharded_train_matches_oracle(tmp_path, world, kernel, mode, m, d):
+def test_row_sharded_train_matches_oracle(tmp_path, world, kernel, mode, m, d, circ):
+    """circ=True: implicit products use circulant tile pairs + reduce-scatter; False: row bands."""
+    if mode == 2 and not circ:
+        pytest.skip("cached mode does not use the reduce-scatter")
     import oracle
     import synth
 
     path = str(tmp_path / "r.npz")
-    mp.spawn(_worker, args=(world, _free_port(), path, kernel, mode, m, d), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), path, kernel, mode, m, d, circ), nprocs=world, join=True)
     r = np.load(path)
     X, y, _, _ = synth.planes(m, d, 64, seed=21 + kernel)
     p = np.random.default_rng(5).standard_normal(m - 1)

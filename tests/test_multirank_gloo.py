@@ -101,3 +101,35 @@ def test_row_sharded_cg_gloo(tmp_path, world):
     assert np.linalg.norm(res["y"] - res["ref_y"]) <= 1e-13 * np.linalg.norm(res["ref_y"])
     assert np.linalg.norm(res["x"] - res["ref_x"]) <= 1e-8 * np.linalg.norm(res["ref_x"])
     assert abs(int(res["it"]) - int(res["ito"])) <= 2
+
+
+def circulant_pairs(T, P):
+    """The circulant rule of driver.cu circulant_tiles(): tile row I owns (I, (I+j) % T),
+    j = 0..T/2, the pair j = T/2 (even T) only for I < T/2; rank r takes rows [r T/P, (r+1) T/P)."""
+    per = T // P
+    out = []
+    for r in range(P):
+        tiles = []
+        for I in range(r * per, (r + 1) * per):
+            for j in range(T // 2 + 1):
+                if T % 2 == 0 and j == T // 2 and I >= T // 2:
+                    continue
+                J = (I + j) % T
+                if j > 0 and J == I:
+                    continue
+                tiles.append((I, J))
+        out.append(tiles)
+    return out
+
+
+@pytest.mark.parametrize("T,P", [(8, 2), (9, 3), (16, 4), (64, 8), (1024, 8), (128, 1)])
+def test_circulant_pairs_cover_each_unordered_pair_once_and_balance(T, P):
+    ranks = circulant_pairs(T, P)
+    seen = {}
+    for tiles in ranks:
+        for I, J in tiles:
+            key = (min(I, J), max(I, J))
+            seen[key] = seen.get(key, 0) + 1
+    assert len(seen) == T * (T + 1) // 2 and set(seen.values()) == {1}
+    loads = [len(t) for t in ranks]
+    assert max(loads) / min(loads) <= 1 + 2.0 / T + 1e-12 or T < 16
