@@ -520,7 +520,7 @@ void configure_product(Ctx<T> &c, Arena &A) {
 // whenever the Q~ band fits the budget -- the precompute costs about one implicit product and
 // every later product becomes an HBM stream (≈ 50-100x cheaper than a recompute).
 template <typename T>
-bool choose_cached(const Geometry &g, const plssvm_options_t &o) {
+bool choose_cached(const Geometry &g, const plssvm_options_t &o, CommHandle *comm, cudaStream_t s) {
     if (o.mode == PLSSVM_MODE_IMPLICIT) return false;
     const int64_t need = g.nb * g.mpad * static_cast<int64_t>(sizeof(T));
     // memory this process' stream-ordered pool holds but does not use counts as free (it is
@@ -540,10 +540,23 @@ bool choose_cached(const Geometry &g, const plssvm_options_t &o) {
     free_b += pool_idle;
     int64_t budget = o.cache_budget_bytes > 0 ? o.cache_budget_bytes : static_cast<int64_t>(0.9 * free_b);
     budget = std::min<int64_t>(budget, static_cast<int64_t>(free_b) - (int64_t(1) << 28));
-    if (need <= budget) return true;
+    bool fits = need <= budget;
+    if (comm) {  // every rank must take the same decision (the collectives differ between modes)
+        double *buf = nullptr;
+        PLS_CUDA(cudaMallocAsync(&buf, 2 * sizeof(double), s));
+        const double one = fits ? 1.0 : 0.0;
+        double all = 0.0;
+        PLS_CUDA(cudaMemcpyAsync(buf, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+        comm_allreduce_sum_f64(comm, buf, buf + 1, 1, s);
+        PLS_CUDA(cudaMemcpyAsync(&all, buf + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+        PLS_CUDA(cudaStreamSynchronize(s));
+        PLS_CUDA(cudaFreeAsync(buf, s));
+        fits = all >= comm_size(comm) - 0.5;
+    }
+    if (fits) return true;
     if (o.mode == PLSSVM_MODE_CACHED)
         throw Error(PLSSVM_E_OOM, "cached mode: Q~ band of " + std::to_string(need) + " bytes does not fit (" +
-                                      std::to_string(budget) + " available)");
+                                      std::to_string(budget) + " available on this rank)");
     return false;
 }
 
@@ -572,7 +585,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     T *pband = c.p + g.g0;
 
-    c.cached = choose_cached<T>(g, o);
+    c.cached = choose_cached<T>(g, o, c.comm, c.s);
     configure_product<T>(c, A);
     if (c.cached) c.Qc = A.alloc<T>(g.nb * g.mpad);
     PLS_CUDA(cudaEventRecord(e_alloc, c.s));
@@ -745,8 +758,7 @@ int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, cons
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     const bool dev = o.device_pointers != 0;
     PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
-    c.cached = (o.mode == PLSSVM_MODE_CACHED) || (o.mode == PLSSVM_MODE_AUTO && choose_cached<T>(g, o));
-    if (c.cached) (void)choose_cached<T>(g, o);  // throws E_OOM if CACHED does not fit
+    c.cached = choose_cached<T>(g, o, c.comm, c.s);  // throws E_OOM if CACHED does not fit
     configure_product<T>(c, A);
     double t_pre = 0.0;
     if (c.cached) {
