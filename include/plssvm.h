@@ -67,7 +67,10 @@ typedef enum {
 } plssvm_status_t;
 
 typedef enum { PLSSVM_F64 = 0, PLSSVM_F32 = 1 } plssvm_dtype_t;
-typedef enum { PLSSVM_MODE_AUTO = 0, PLSSVM_MODE_IMPLICIT = 1, PLSSVM_MODE_CACHED = 2 } plssvm_mode_t;
+/* LOWRANK (linear kernel only): Q~p = B^T (X (X^T (B p))) + (p + 1 sum p)/C with B = [I; -1^T]
+ * (Q~ = B^T Q B, Eq. 13), two O(m d) streams over X per product instead of O(m^2 d) -- a
+ * different cost model from the paper's implicit entries; never picked by AUTO. */
+typedef enum { PLSSVM_MODE_AUTO = 0, PLSSVM_MODE_IMPLICIT = 1, PLSSVM_MODE_CACHED = 2, PLSSVM_MODE_LOWRANK = 3 } plssvm_mode_t;
 
 /* Options for the _ex entry points.  plssvm_default_options() fills the defaults given in
  * brackets.  All-zero is NOT the default (stream/comm NULL are fine, but mode 0 = AUTO). */
@@ -87,6 +90,8 @@ typedef struct {
                                    <= 0 means 90 % of free HBM after the other buffers [0] */
     int32_t fp32_engine;     /* fp32 implicit Q~p contraction: 0 = tensor cores (tcgen05 kind::tf32,
                                 3xTF32 split) [0]; 1 = CUDA-core FFMA tiles */
+    int32_t linear_w;        /* predict with the linear kernel through w = sum_i alpha_i x_i (Eq. 15,
+                                O((m+n)d)) [1]; 0 = evaluate the kernel matrix like the other kernels */
 } plssvm_options_t;
 
 /* Statistics of one training call (all times are device-event seconds). */
@@ -94,7 +99,7 @@ typedef struct {
     int64_t iterations;              /* CG iterations performed */
     int64_t matvecs;                 /* Q~ products performed (incl. initial / replacement) */
     double rel_residual;             /* ||r|| / ||r0|| of the recurrence at exit */
-    int32_t mode_used;               /* PLSSVM_MODE_IMPLICIT or PLSSVM_MODE_CACHED */
+    int32_t mode_used;               /* PLSSVM_MODE_IMPLICIT, _CACHED or _LOWRANK */
     int32_t num_ranks;               /* 1, or the communicator size */
     double t_h2d, t_transform, t_q;
     double t_alloc;                  /* device work-buffer allocation (stream-ordered pool) */

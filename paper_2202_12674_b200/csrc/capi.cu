@@ -113,6 +113,7 @@ void plssvm_default_options(plssvm_options_t *o) {
     o->comm = nullptr;
     o->cache_budget_bytes = 0;
     o->fp32_engine = 0;
+    o->linear_w = 1;
 }
 
 int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtype, int kernel, double gamma, int degree,
@@ -125,7 +126,9 @@ int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtyp
     int s = check_params(m, d, kernel, gamma, degree, C);
     if (s) return s;
     if (!(eps > 0) || !std::isfinite(eps)) return fail(PLSSVM_E_INVALID_ARG, "eps must be > 0");
-    if (o.mode < 0 || o.mode > 2) return fail(PLSSVM_E_INVALID_ARG, "options.mode must be 0, 1 or 2");
+    if (o.mode < 0 || o.mode > 3) return fail(PLSSVM_E_INVALID_ARG, "options.mode must be 0, 1, 2 or 3");
+    if (o.mode == PLSSVM_MODE_LOWRANK && kernel != PLSSVM_LINEAR)
+        return fail(PLSSVM_E_INVALID_ARG, "options.mode LOWRANK needs the linear kernel");
     if (o.x0 != 0 && o.x0 != 1) return fail(PLSSVM_E_INVALID_ARG, "options.x0 must be 0 or 1");
     if (!o.device_pointers) {
         s = dtype == PLSSVM_F64 ? host_checks_train<double>(X, y, m, d) : host_checks_train<float>(X, y, m, d);
@@ -203,6 +206,9 @@ int plssvm_qtilde_matvec(const void *X, const void *p, int64_t m, int64_t d, int
         if (s) return s;
     }
     if ((s = device_ok(o.device))) return s;
+    if (o.mode < 0 || o.mode > 3) return fail(PLSSVM_E_INVALID_ARG, "options.mode must be 0, 1, 2 or 3");
+    if (o.mode == PLSSVM_MODE_LOWRANK && kernel != PLSSVM_LINEAR)
+        return fail(PLSSVM_E_INVALID_ARG, "options.mode LOWRANK needs the linear kernel");
     plssvm::Problem pb{X, nullptr, m, d, dtype, kernel, gamma, degree, coef0, C, 1.0};
     return guarded([&] { return plssvm::qtilde_matvec(pb, p, repeats, o, out, t_kernel); });
 }

@@ -237,6 +237,13 @@ struct Ctx {
     int64_t launches = 0, launches_cg = 0;
     Ops<T> ops;
     bool circ = false;               // implicit multi-GPU: circulant pairs + reduce-scatter
+    bool lowrank = false;            // linear kernel, O(md) product (mode LOWRANK)
+    const T *Xraw = nullptr;         // the caller's row-major X on the device (staged or given)
+    int64_t m = 0, d = 0;
+    T *tpart = nullptr, *tvec = nullptr;
+    double *tloc = nullptr;          // [2d]: local partial, global sum (multi-GPU)
+    int lr_parts = 1;
+    int64_t lr_rpb = 1;
     T *yfull = nullptr, *ysc = nullptr, *Yfin = nullptr;
     int nsub_eff = 1;
     int *ctrl = nullptr;             // device CG control block (kernels.cuh Ctl)
@@ -362,6 +369,28 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
         ++c.launches;
         return c.nsplit;
     }
+    if (c.lowrank) {  // Q~p = B^T (X (X^T (B p))) + (p + 1 sum p)/C, O(md)
+        const int64_t r0 = g.g0, r1 = std::max<int64_t>(std::min<int64_t>(g.g0 + g.nb, c.m), g.g0);
+        k_sum_p<T><<<1, 256, 0, c.s>>>(pfull, g.m1, c.scal, c.cur_ctrl);
+        k_colsum_partial<T><<<c.lr_parts, 256, 0, c.s>>>(c.Xraw, c.d, r0, r1, c.lr_rpb, nullptr, pfull, c.m, c.scal,
+                                                         c.tpart, c.cur_ctrl);
+        k_colsum_reduce<T><<<static_cast<unsigned>(ceil_div(c.d, 256)), 256, 0, c.s>>>(c.tpart, c.lr_parts, c.d, c.tvec,
+                                                                                       c.tloc, c.cur_ctrl);
+        PLS_CHECK_LAUNCH();
+        c.launches += 3;
+        if (c.comm) {  // t = sum over ranks (out of place: idempotent after convergence)
+            comm_allreduce_sum_f64(c.comm, c.tloc, c.tloc + c.d, c.d, c.s);
+            k_cast<T><<<static_cast<unsigned>(ceil_div(c.d, 256)), 256, 0, c.s>>>(c.tloc + c.d, c.d, c.tvec);
+            PLS_CHECK_LAUNCH();
+            ++c.launches;
+        }
+        k_rowdot<T><<<static_cast<unsigned>(ceil_div(g.nb * 32, 256)), 256, 0, c.s>>>(
+            c.Xraw, c.d, g.g0, g.nb, c.tvec, 1, T(0), pfull, c.m, c.invC, c.scal, c.Ypart, nullptr, c.cur_ctrl);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        c.Yfin = c.Ypart;
+        return 1;
+    }
     // circulant multi-GPU: partial products for ALL rows (band = everything), zero-initialised
     const int b0 = c.circ ? 0 : g.band0, b1 = c.circ ? g.T : g.band1;
     const int64_t brows = c.circ ? g.mpad : g.nb;
@@ -459,6 +488,9 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.invC = static_cast<T>(1.0 / pb.C);
     const bool dev = o.device_pointers != 0;
     const T *Xs = stage_input<T>(A, pb.X, pb.m * pb.d, dev, c.s);
+    c.Xraw = Xs;
+    c.m = pb.m;
+    c.d = pb.d;
     if (need_labels) {
         c.ylab = const_cast<T *>(stage_input<T>(A, pb.y, pb.m, dev, c.s));
     } else {
@@ -500,7 +532,19 @@ void configure_product(Ctx<T> &c, Arena &A) {
     const Geometry &g = c.g;
     c.nsub_eff = c.tc ? 1 : Engine<T>::NSUB;
     c.nsplit = gemv_splits(g);
-    c.circ = g.P > 1 && !c.cached && comm_has_reduce_scatter(c.comm);
+    c.circ = g.P > 1 && !c.cached && !c.lowrank && comm_has_reduce_scatter(c.comm);
+    if (c.lowrank) {
+        const int64_t r0 = g.g0, r1 = std::min<int64_t>(g.g0 + g.nb, c.m);
+        const int64_t rows = std::max<int64_t>(r1 - r0, 1);
+        c.lr_rpb = std::max<int64_t>(1, ceil_div(rows, 4 * 148));
+        c.lr_parts = static_cast<int>(ceil_div(rows, c.lr_rpb));
+        c.tpart = A.alloc<T>(static_cast<int64_t>(c.lr_parts) * c.d);
+        c.tvec = A.alloc<T>(c.d);
+        c.tloc = A.alloc<double>(2 * c.d);
+        c.Ypart = A.alloc<T>(g.nb);
+        c.Yfin = c.Ypart;
+        return;
+    }
     if (c.circ) {
         std::vector<int2> tl = circulant_tiles(g, c.nsub_eff);
         c.ntiles = static_cast<int>(tl.size());
@@ -585,7 +629,8 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     T *pband = c.p + g.g0;
 
-    c.cached = choose_cached<T>(g, o, c.comm, c.s);
+    c.lowrank = o.mode == PLSSVM_MODE_LOWRANK;
+    c.cached = !c.lowrank && choose_cached<T>(g, o, c.comm, c.s);
     configure_product<T>(c, A);
     if (c.cached) c.Qc = A.alloc<T>(g.nb * g.mpad);
     PLS_CUDA(cudaEventRecord(e_alloc, c.s));
@@ -720,7 +765,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         st->iterations = it;
         st->matvecs = matvecs;
         st->rel_residual = delta0 > 0 ? std::sqrt(delta / delta0) : 0.0;
-        st->mode_used = c.cached ? PLSSVM_MODE_CACHED : PLSSVM_MODE_IMPLICIT;
+        st->mode_used = c.lowrank ? PLSSVM_MODE_LOWRANK : (c.cached ? PLSSVM_MODE_CACHED : PLSSVM_MODE_IMPLICIT);
         st->num_ranks = g.P;
         st->t_h2d = elapsed(e0, e_h2d);
         st->t_transform = elapsed(e_h2d, e_tr);
@@ -758,7 +803,8 @@ int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, cons
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     const bool dev = o.device_pointers != 0;
     PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
-    c.cached = choose_cached<T>(g, o, c.comm, c.s);  // throws E_OOM if CACHED does not fit
+    c.lowrank = o.mode == PLSSVM_MODE_LOWRANK;
+    c.cached = !c.lowrank && choose_cached<T>(g, o, c.comm, c.s);  // throws E_OOM if CACHED does not fit
     configure_product<T>(c, A);
     double t_pre = 0.0;
     if (c.cached) {
@@ -816,6 +862,34 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     const int64_t xrows = EN::kPointMajor ? mpad : L, zrows = EN::kPointMajor ? npad : L;
     const T *Xs = stage_input<T>(A, pb.X, m * d, dev, s);
     const T *Zs = stage_input<T>(A, Zin, n * d, dev, s);
+    if (pb.kernel == LINEAR && o.linear_w) {
+        // f(z) = <w, z> + b with w = sum_i alpha_i x_i (Eq. 15): O((m + n) d)
+        const T *al = stage_input<T>(A, alpha_in, m, dev, s);
+        const int64_t rpb = std::max<int64_t>(1, ceil_div(m, 4 * 148));
+        const int parts = static_cast<int>(ceil_div(m, rpb));
+        T *wpart = A.alloc<T>(static_cast<int64_t>(parts) * d), *w = A.alloc<T>(d);
+        T *f_d = (dev && decision) ? static_cast<T *>(decision) : A.alloc<T>(n);
+        int32_t *l_d = (dev && labels) ? labels : A.alloc<int32_t>(n);
+        PLS_CUDA(cudaEventRecord(e0, s));
+        k_colsum_partial<T><<<parts, 256, 0, s>>>(Xs, d, 0, m, rpb, al, nullptr, m, nullptr, wpart, nullptr);
+        k_colsum_reduce<T><<<static_cast<unsigned>(ceil_div(d, 256)), 256, 0, s>>>(wpart, parts, d, w, nullptr, nullptr);
+        k_rowdot<T><<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(Zs, d, 0, n, w, 0, static_cast<T>(b),
+                                                                                 nullptr, n, T(0), nullptr, f_d, l_d,
+                                                                                 nullptr);
+        PLS_CHECK_LAUNCH();
+        PLS_CUDA(cudaEventRecord(e1, s));
+        launches += 3;
+        if (!dev) {
+            if (decision) PLS_CUDA(cudaMemcpyAsync(decision, f_d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+            if (labels) PLS_CUDA(cudaMemcpyAsync(labels, l_d, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        }
+        PLS_CUDA(cudaStreamSynchronize(s));
+        if (t_kernel) {
+            t_kernel[0] = elapsed(e0, e1);
+            t_kernel[1] = static_cast<double>(launches);
+        }
+        return PLSSVM_OK;
+    }
     T *Xl = A.alloc<T>(dpad * xrows), *Zl = A.alloc<T>(dpad * zrows);
     launch_transform<T>(Xs, m, d, Xl, xrows, dpad, s, launches);
     launch_transform<T>(Zs, n, d, Zl, zrows, dpad, s, launches);

@@ -27,6 +27,7 @@ enum Scal : int {
     S_QX = 8,       // <q, x>  (bias)
     S_B = 9,        // bias b
     S_THR = 10,     // eps^2 delta_0 (the CG stopping threshold on delta)
+    S_SP = 11,      // sum of p (linear low-rank product)
     S_L = 16,       // slot s + S_L holds this rank's local partial of slot s; the multi-GPU
                     // all-reduce is out of place (local -> global), hence idempotent: iterations
                     // enqueued after convergence cannot corrupt the global scalars
@@ -337,6 +338,105 @@ __global__ void __launch_bounds__(256) k_gemv_tiled(const T *__restrict__ Qc, co
     if (lane == 0) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) Ypart[static_cast<int64_t>(sp) * nb + static_cast<int64_t>(Ib) * kTile + w * 16 + r] = acc[r];
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Linear-kernel shortcuts (they change the cost model and are reported
+// separately from the implicit FLOP/s).  X here is the caller's row-major m x d array.
+//
+// Weighted column sums: part[b][k] = sum_{i in rows of block b} c_i X[i][k], with
+//   c_i = coef[i]                                  (coef != nullptr; predict: w = X^T alpha, Eq. 15)
+//   c_i = p[i] (i < m-1), -sum(p) (i = m-1)         (coef == nullptr; low-rank Q~p: X^T B p)
+// restricted to rows [r0, r1).  Deterministic: fixed row order per block, then k_colsum_reduce.
+template <typename T>
+__global__ void __launch_bounds__(256) k_colsum_partial(const T *__restrict__ X, int64_t d, int64_t r0, int64_t r1,
+                                                        int64_t rows_per_block, const T *__restrict__ coef,
+                                                        const T *__restrict__ p, int64_t m, const double *scal,
+                                                        T *__restrict__ part, const int *ctrl) {
+    if (cg_done(ctrl)) return;
+    const int64_t b0 = r0 + static_cast<int64_t>(blockIdx.x) * rows_per_block;
+    const int64_t b1 = b0 + rows_per_block < r1 ? b0 + rows_per_block : r1;
+    const T negs = coef ? T(0) : static_cast<T>(-scal[S_SP]);
+    for (int64_t k = threadIdx.x; k < d; k += blockDim.x) {
+        T s = T(0);
+        for (int64_t i = b0; i < b1; ++i) {
+            const T ci = coef ? coef[i] : (i < m - 1 ? p[i] : negs);
+            s = fma(ci, X[i * d + k], s);
+        }
+        part[static_cast<int64_t>(blockIdx.x) * d + k] = s;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_colsum_reduce(const T *__restrict__ part, int nparts, int64_t d,
+                                                       T *__restrict__ out, double *out_local, const int *ctrl) {
+    if (cg_done(ctrl)) return;
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= d) return;
+    T s = T(0);
+    for (int b = 0; b < nparts; ++b) s += part[static_cast<int64_t>(b) * d + k];
+    out[k] = s;
+    if (out_local) out_local[k] = static_cast<double>(s);
+}
+
+template <typename T>
+__global__ void k_cast(const double *__restrict__ a, int64_t n, T *__restrict__ b) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = static_cast<T>(a[i]);
+}
+
+// sum_{i < m-1} p_i -> scal[S_SP] (single block, fixed order)
+template <typename T>
+__global__ void __launch_bounds__(256) k_sum_p(const T *__restrict__ p, int64_t m1, double *scal, const int *ctrl) {
+    if (cg_done(ctrl)) return;
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < m1; i += blockDim.x) s += static_cast<double>(p[i]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) scal[S_SP] = red[0];
+}
+
+// Row dot products with a d-vector: out[i] = <X[r0 + i], w> + add (one warp per row).
+//  mode 0 (predict):  f_i = <z_i, w> + b, label
+//  mode 1 (low-rank): v_i = <x_i, t> + u_i / C,  y_i = v_i - v_{m-1} for i < m-1 (0 beyond);
+//                     v_{m-1} is recomputed by every warp (it needs only x_{m-1} and t)
+template <typename T>
+__global__ void __launch_bounds__(256) k_rowdot(const T *__restrict__ X, int64_t d, int64_t r0, int64_t nrows,
+                                                const T *__restrict__ w, int mode, T add, const T *__restrict__ p,
+                                                int64_t m, T invC, const double *scal, T *__restrict__ out,
+                                                int32_t *__restrict__ labels, const int *ctrl) {
+    if (cg_done(ctrl)) return;
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= nrows) return;
+    const int64_t i = r0 + row;
+    T s = T(0), sl = T(0);
+    const bool real = i < m;
+    for (int64_t k = lane; k < d; k += 32) {
+        if (real) s = fma(X[i * d + k], w[k], s);
+        if (mode == 1) sl = fma(X[(m - 1) * d + k], w[k], sl);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        sl += __shfl_xor_sync(0xffffffffu, sl, o);
+    }
+    if (lane != 0) return;
+    if (mode == 0) {
+        const T f = s + add;
+        if (out) out[row] = f;
+        if (labels) labels[row] = f >= T(0) ? 1 : -1;
+    } else {
+        const T sp = static_cast<T>(scal[S_SP]);
+        const T vl = sl - sp * invC;                       // u_{m-1} = -sum p
+        const T v = s + (i < m - 1 ? p[i] : T(0)) * invC;  // u_i = p_i
+        out[row] = (i < m - 1) ? v - vl : T(0);
     }
 }
 

@@ -55,11 +55,12 @@ def _worker(rank, world, port, path, kernel, mode, m, d, circ):
     (3, 1, 1, 900, 20),     # poly implicit, 3 ranks, ragged tail, odd T (9 tiles)
     (4, 2, 2, 1500, 9),     # RBF cached, 4 ranks
     (4, 2, 1, 2000, 40),    # RBF implicit, 4 ranks, T = 16 (circulant j = T/2 pairs)
+    (3, 0, 3, 1100, 30),    # linear LOWRANK, 3 ranks (all-reduce of X^T B p)
 ])
 def test_row_sharded_train_matches_oracle(tmp_path, world, kernel, mode, m, d, circ):
     """circ=True: implicit products use circulant tile pairs + reduce-scatter; False: row bands."""
-    if mode == 2 and not circ:
-        pytest.skip("cached mode does not use the reduce-scatter")
+    if mode in (2, 3) and not circ:
+        pytest.skip("cached / low-rank modes do not use the reduce-scatter")
     import oracle
     import synth
 

@@ -288,3 +288,40 @@ def test_c2_full_size_cached_and_implicit_sampled_rows():
     res = np.abs(R @ alpha[:-1] - rhs[rows])
     assert np.max(res) <= 1e-7 * np.linalg.norm(rhs)
     assert abs(alpha.sum()) <= 1e-10 * np.abs(alpha).max()
+
+
+# ------------------------------------------------------------------------------ linear shortcuts
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("m,d", [(2, 1), (3, 3), (129, 3), (1000, 33), (2177, 70)])
+def test_lowrank_linear_product(m, d, dtype):
+    """mode LOWRANK: Q~p = B^T X X^T B p + (p + 1 sum p)/C, against the oracle's explicit Q~."""
+    rng = np.random.default_rng(500 + m + d)
+    X = rng.standard_normal((m, d)).astype(dtype)
+    p = rng.standard_normal(m - 1).astype(dtype)
+    check_matvec(X, p, pl.LINEAR, kparams(pl.LINEAR, d, dtype), 0.7, dtype, pl.MODE_LOWRANK)
+
+
+def test_lowrank_linear_training_and_mode_validation():
+    X, y, _, _ = synth.planes(1500, 24, seed=15)
+    alpha, b, stats = check_train(X, y, pl.LINEAR, kparams(pl.LINEAR, 24, np.float64), 1.0, 1e-10,
+                                  opts=pl.options(mode=pl.MODE_LOWRANK))
+    assert stats.mode_used == pl.MODE_LOWRANK
+    with pytest.raises(pl.PlssvmError):
+        pl.plssvm_train_ex(X, y, pl.RBF, 0.1, opts=pl.options(mode=pl.MODE_LOWRANK))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_linear_predict_w_shortcut(dtype):
+    """Linear predict through w = X^T alpha (default) equals the kernel-matrix path and the oracle."""
+    rng = np.random.default_rng(61)
+    X = rng.standard_normal((1234, 57)).astype(dtype)
+    Z = rng.standard_normal((777, 57)).astype(dtype)
+    alpha = rng.standard_normal(1234).astype(dtype)
+    f_ref, lab_ref = oracle.predict(X.astype(np.float64), alpha.astype(np.float64), -0.2, Z.astype(np.float64),
+                                    pl.LINEAR)
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    for lw in (1, 0):
+        f, lab, _ = pl.plssvm_predict_ex(X, alpha, -0.2, Z, pl.LINEAR, opts=pl.options(linear_w=lw))
+        assert rel(f, f_ref) <= tol, (lw, rel(f, f_ref))
+        safe = np.abs(f_ref) > 1e3 * tol * np.abs(f_ref).max()
+        assert np.array_equal(lab[safe], lab_ref[safe])

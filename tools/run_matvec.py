@@ -27,7 +27,7 @@ dt = np.float32 if cfg.dtype == "f32" else np.float64
 rng = np.random.default_rng(0)
 X = rng.standard_normal((m, d)).astype(dt)
 p = rng.standard_normal(m - 1).astype(dt)
-mode = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED}[a.mode]
+mode = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED, "lowrank": pl.MODE_LOWRANK}[a.mode]
 kern = cfg.kernel if a.kernel < 0 else a.kernel
 out, t = pl.plssvm_qtilde_matvec(X, p, kern, 1.0 / d, cfg.degree, cfg.coef0, cfg.C, repeats=a.repeats,
                                  opts=pl.options(mode=mode, fp32_engine=a.fp32_engine))

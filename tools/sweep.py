@@ -39,7 +39,8 @@ def hbm_peak():
         return 6650.0
 
 
-MODES = {"C0": ["implicit"], "C1": ["implicit", "cached"], "C2": ["cached", "implicit"], "C3": ["cached", "implicit"],
+MODES = {"C0": ["implicit"], "C1": ["implicit", "cached"], "C2": ["cached", "implicit", "lowrank"],
+         "C3": ["cached", "implicit"],
          "C4": ["cached"]}
 
 
@@ -48,7 +49,7 @@ def run(cfg, mode, repeat=2):
     dev = torch.device("cuda", 0)
     tX, ty, tZ = (torch.from_numpy(a).to(dev) for a in (X, y, Z))
     kw = dict(gamma=cfg.gamma, degree=cfg.degree, coef0=cfg.coef0)
-    md = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED}[mode]
+    md = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED, "lowrank": pl.MODE_LOWRANK}[mode]
     best = None
     for _ in range(repeat):
         torch.cuda.synchronize()
@@ -70,7 +71,12 @@ def run(cfg, mode, repeat=2):
            "cg_s": s.t_cg, "precompute_s": s.t_precompute, "cg_iterations_per_s": s.iterations / s.t_cg,
            "matvec_ms": 1e3 * mv, "bytes_per_gpu": s.bytes_per_gpu,
            "predict_s": tk, "n_test": cfg.n_test, "test_accuracy": acc}
-    if mode == "implicit":
+    if mode == "lowrank":  # two streams over X per product (a different cost model, NEXT-2)
+        sz = 8 if cfg.dtype == "f64" else 4
+        row["matvec_gbs"] = 2.0 * cfg.m * cfg.d * sz / mv / 1e9
+        row["frac_of_peak"] = row["matvec_gbs"] / hbm_peak()
+        row["peak_gbs"] = hbm_peak()
+    elif mode == "implicit":
         row["matvec_tflops"] = fl / mv / 1e12
         row["frac_of_peak"] = row["matvec_tflops"] / peak_f
         row["peak_tflops"] = peak_f
