@@ -186,11 +186,11 @@ std::vector<int2> band_tiles(const Geometry &g, int nsub) {
     for (int I0 = g.band0; I0 < g.band1; I0 += kGroup) {
         const int I1 = std::min(I0 + kGroup, g.band1);
         for (int J = 0; J < g.T; ++J)
-            for (int h = 0; h < nsub; ++h)
-                for (int I = I0; I < I1; ++I) {
-                    const bool inband = (J >= g.band0 && J < g.band1);
-                    if (!inband || J >= I) t.push_back(make_int2(I, J * nsub + h));
-                }
+            for (int I = I0; I < I1; ++I) {
+                const bool inband = (J >= g.band0 && J < g.band1);
+                if (!inband || J >= I)
+                    for (int h = 0; h < nsub; ++h) t.push_back(make_int2(I, J * nsub + h));  // halves adjacent:
+            }                                                                             // packed ordinal = idx/nsub
     }
     return t;
 }
@@ -238,6 +238,8 @@ struct Ctx {
     Ops<T> ops;
     bool circ = false;               // implicit multi-GPU: circulant pairs + reduce-scatter
     bool lowrank = false;            // linear kernel, O(md) product (mode LOWRANK)
+    bool packed = false;             // cached mode, symmetric-packed tiles (k_gemv_sym)
+    int64_t nstored = 0;             // stored tiles of the packed layout
     const T *Xraw = nullptr;         // the caller's row-major X on the device (staged or given)
     int64_t m = 0, d = 0;
     T *tpart = nullptr, *tvec = nullptr;
@@ -342,8 +344,8 @@ bool launch_tc_precompute(Ctx<T> &c) {
         const Geometry &g = c.g;
         tc_dispatch<TC_PRECOMPUTE>(c.kp.kernel, c.ntiles, c.s, c.tm_hi, c.tm_lo, c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, 0,
                                    c.q, c.nrm, c.q, c.nrm, static_cast<const float *>(nullptr), c.kp, c.invC, c.scal,
-                                   g.m1, g.band0, g.band1, static_cast<float *>(nullptr), g.nb, c.Qc, g.T,
-                                   static_cast<const int *>(nullptr));
+                                   g.m1, g.band0, g.band1, static_cast<float *>(nullptr), g.nb, c.Qc,
+                                   c.packed ? -1 : g.T, static_cast<const int *>(nullptr));
         ++c.launches;
         return true;
     }
@@ -361,6 +363,25 @@ int gemv_splits(const Geometry &g) {
 template <typename T>
 int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
     const Geometry &g = c.g;
+    if (c.cached && c.packed) {
+        const int b0p = c.circ ? 0 : g.band0;
+        const int64_t brows = c.circ ? g.mpad : g.nb;
+        if (c.circ) PLS_CUDA(cudaMemsetAsync(c.Ypart, 0, static_cast<size_t>(g.T) * g.mpad * sizeof(T), c.s));
+        k_gemv_sym<T><<<static_cast<unsigned>(c.nstored), 256, 0, c.s>>>(c.Qc, c.tiles, c.nsub_eff, pfull, b0p, brows,
+                                                                        c.Ypart, c.cur_ctrl);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        if (!c.circ) {
+            c.Yfin = c.Ypart;
+            return g.T;
+        }
+        k_slot_sum<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, g.T, g.mpad, g.m1, c.yfull, c.cur_ctrl);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        comm_reduce_scatter(c.comm, c.yfull, c.ysc, g.nb, dtype_of(T()), c.s);
+        c.Yfin = c.ysc;
+        return 1;
+    }
     if (c.cached) {
         const int rowblocks = static_cast<int>(g.nb / kTile);
         k_gemv_tiled<T><<<rowblocks * c.nsplit, 256, 0, c.s>>>(c.Qc, pfull, g.T, c.nsplit, g.nb, c.Ypart,
@@ -439,15 +460,15 @@ void launch_precompute(Ctx<T> &c) {
     switch (c.kp.kernel) {
         case LINEAR:
             k_precompute<LINEAR, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
-                                                                    c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
+                                                                    c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc, c.packed ? 1 : 0);
             break;
         case POLYNOMIAL:
             k_precompute<POLYNOMIAL, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
-                                                                        c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
+                                                                        c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc, c.packed ? 1 : 0);
             break;
         default:
             k_precompute<RBF, T><<<c.ntiles, Engine<T>::THREADS, sm, c.s>>>(c.ops, g.mpad, g.dpad, c.tiles, c.q, c.nrm, c.kp,
-                                                                 c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc);
+                                                                 c.invC, c.scal, g.m1, g.band0, g.band1, c.Qc, c.packed ? 1 : 0);
     }
     PLS_CHECK_LAUNCH();
     ++c.launches;
@@ -532,7 +553,7 @@ void configure_product(Ctx<T> &c, Arena &A) {
     const Geometry &g = c.g;
     c.nsub_eff = c.tc ? 1 : Engine<T>::NSUB;
     c.nsplit = gemv_splits(g);
-    c.circ = g.P > 1 && !c.cached && !c.lowrank && comm_has_reduce_scatter(c.comm);
+    c.circ = g.P > 1 && !c.lowrank && (!c.cached || c.packed) && comm_has_reduce_scatter(c.comm);
     if (c.lowrank) {
         const int64_t r0 = g.g0, r1 = std::min<int64_t>(g.g0 + g.nb, c.m);
         const int64_t rows = std::max<int64_t>(r1 - r0, 1);
@@ -554,19 +575,31 @@ void configure_product(Ctx<T> &c, Arena &A) {
         c.Ypart = A.alloc<T>(static_cast<int64_t>(g.T) * c.nsub_eff * g.mpad);
         c.yfull = A.alloc<T>(g.mpad);
         c.ysc = A.alloc<T>(g.nb);
+    } else if (c.packed) {
+        c.Ypart = A.alloc<T>(static_cast<int64_t>(g.T) * g.nb);
     } else {
         c.Ypart = A.alloc<T>(static_cast<int64_t>(c.cached ? c.nsplit : g.T * c.nsub_eff) * g.nb);
     }
+    c.nstored = c.packed ? c.ntiles / c.nsub_eff : 0;
     c.Yfin = c.Ypart;
+}
+
+// Stored 128 x 128 tiles of the packed layout for this rank (upper triangle for one GPU, the
+// circulant pairs otherwise) -- computed without building the list, for the fit test.
+int64_t packed_tile_count(const Geometry &g) {
+    if (g.P == 1) return static_cast<int64_t>(g.T) * (g.T + 1) / 2;
+    int64_t n = 0;
+    const int half = g.T / 2;
+    for (int I = g.band0; I < g.band1; ++I) n += half + 1 - ((g.T % 2 == 0 && I >= half) ? 1 : 0);
+    return n;
 }
 
 // Mode selection (north_star: "mode picked by measurement"; SURVEY §8 decision 8): cached
 // whenever the Q~ band fits the budget -- the precompute costs about one implicit product and
 // every later product becomes an HBM stream (≈ 50-100x cheaper than a recompute).
 template <typename T>
-bool choose_cached(const Geometry &g, const plssvm_options_t &o, CommHandle *comm, cudaStream_t s) {
+bool choose_cached(const Geometry &g, const plssvm_options_t &o, CommHandle *comm, cudaStream_t s, int64_t need) {
     if (o.mode == PLSSVM_MODE_IMPLICIT) return false;
-    const int64_t need = g.nb * g.mpad * static_cast<int64_t>(sizeof(T));
     // memory this process' stream-ordered pool holds but does not use counts as free (it is
     // reused by the allocation below without re-mapping; trimming it would cost ~1 s per 100 GB)
     int dev = 0;
@@ -604,6 +637,18 @@ bool choose_cached(const Geometry &g, const plssvm_options_t &o, CommHandle *com
     return false;
 }
 
+// Mode: LOWRANK if asked; else cached when the Q~ storage fits (symmetric-packed tiles when one
+// GPU or a reduce-scatter is available: half the bytes of full rows), else implicit.
+template <typename T>
+void select_mode(Ctx<T> &c, const plssvm_options_t &o) {
+    const Geometry &g = c.g;
+    c.lowrank = o.mode == PLSSVM_MODE_LOWRANK;
+    const bool can_pack = g.P == 1 || (c.comm && comm_has_reduce_scatter(c.comm));
+    const int64_t need = (can_pack ? packed_tile_count(g) * kTile * kTile : g.nb * g.mpad) * static_cast<int64_t>(sizeof(T));
+    c.cached = !c.lowrank && choose_cached<T>(g, o, c.comm, c.s, need);
+    c.packed = c.cached && can_pack;
+}
+
 template <typename T>
 int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, void *b_out, plssvm_stats_t *st) {
     PLS_CUDA(cudaSetDevice(o.device));
@@ -629,10 +674,9 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     T *pband = c.p + g.g0;
 
-    c.lowrank = o.mode == PLSSVM_MODE_LOWRANK;
-    c.cached = !c.lowrank && choose_cached<T>(g, o, c.comm, c.s);
+    select_mode<T>(c, o);
     configure_product<T>(c, A);
-    if (c.cached) c.Qc = A.alloc<T>(g.nb * g.mpad);
+    if (c.cached) c.Qc = A.alloc<T>(c.packed ? c.nstored * kTile * kTile : g.nb * g.mpad);
     PLS_CUDA(cudaEventRecord(e_alloc, c.s));
     if (c.cached) launch_precompute<T>(c);
     PLS_CUDA(cudaEventRecord(e_pre, c.s));
@@ -803,12 +847,11 @@ int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, cons
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     const bool dev = o.device_pointers != 0;
     PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
-    c.lowrank = o.mode == PLSSVM_MODE_LOWRANK;
-    c.cached = !c.lowrank && choose_cached<T>(g, o, c.comm, c.s);  // throws E_OOM if CACHED does not fit
+    select_mode<T>(c, o);  // throws E_OOM if CACHED does not fit
     configure_product<T>(c, A);
     double t_pre = 0.0;
     if (c.cached) {
-        c.Qc = A.alloc<T>(g.nb * g.mpad);
+        c.Qc = A.alloc<T>(c.packed ? c.nstored * kTile * kTile : g.nb * g.mpad);
         PLS_CUDA(cudaEventRecord(e0, c.s));
         launch_precompute<T>(c);
         PLS_CUDA(cudaEventRecord(e1, c.s));

@@ -246,8 +246,12 @@ __global__ void __launch_bounds__(Tc::THREADS, 1)
         float rs = 0.f;
         float *qrow = nullptr, *qmir = nullptr;
         if constexpr (MODE == TC_PRECOMPUTE) {
-            qrow = Qc + (int64_t(I - band0) * T_tiles + J) * (kTile * kTile) + lr * kTile;
-            if (mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
+            if (T_tiles < 0) {  // packed symmetric layout: ordinal blockIdx.x, no mirror copy
+                qrow = Qc + int64_t(blockIdx.x) * (kTile * kTile) + lr * kTile;
+            } else {
+                qrow = Qc + (int64_t(I - band0) * T_tiles + J) * (kTile * kTile) + lr * kTile;
+                if (mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
+            }
         }
 #pragma unroll 1
         for (int c0 = 0; c0 < kTile; c0 += 16) {
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(Tc::THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 16; j += 4)
                         *reinterpret_cast<float4 *>(qrow + c0 + j) = make_float4(cs[j], cs[j + 1], cs[j + 2], cs[j + 3]);
-                    if (mirrored) {
+                    if (qmir) {
 #pragma unroll
                         for (int j = 0; j < 16; ++j) qmir[(c0 + j) * kTile] = cs[j];  // coalesced over lanes
                     }

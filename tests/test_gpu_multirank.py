@@ -58,9 +58,12 @@ def _worker(rank, world, port, path, kernel, mode, m, d, circ):
     (3, 0, 3, 1100, 30),    # linear LOWRANK, 3 ranks (all-reduce of X^T B p)
 ])
 def test_row_sharded_train_matches_oracle(tmp_path, world, kernel, mode, m, d, circ):
-    """circ=True: implicit products use circulant tile pairs + reduce-scatter; False: row bands."""
-    if mode in (2, 3) and not circ:
-        pytest.skip("cached / low-rank modes do not use the reduce-scatter")
+    """circ=True: implicit products use circulant tile pairs + reduce-scatter (cached: packed
+    circulant tiles); False: row bands (cached: full rows per rank)."""
+    if mode == 3 and not circ:
+        pytest.skip("the low-rank mode does not use the reduce-scatter")
+    # cached + circ: symmetric-packed tiles (circulant pairs) + reduce-scatter;
+    # cached without a reduce-scatter: full-row bands
     import oracle
     import synth
 
