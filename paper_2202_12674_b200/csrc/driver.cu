@@ -367,8 +367,9 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
         const int b0p = c.circ ? 0 : g.band0;
         const int64_t brows = c.circ ? g.mpad : g.nb;
         if (c.circ) PLS_CUDA(cudaMemsetAsync(c.Ypart, 0, static_cast<size_t>(g.T) * g.mpad * sizeof(T), c.s));
-        k_gemv_sym<T><<<static_cast<unsigned>(c.nstored), 256, 0, c.s>>>(c.Qc, c.tiles, c.nsub_eff, pfull, b0p, brows,
-                                                                        c.Ypart, c.cur_ctrl);
+        constexpr int per_cta = 4;  // stored tiles per CTA (amortises launch + reduction bubbles)
+        k_gemv_sym<T><<<static_cast<unsigned>(ceil_div(c.nstored, per_cta)), 256, 0, c.s>>>(
+            c.Qc, c.tiles, c.nsub_eff, c.nstored, per_cta, pfull, b0p, brows, c.Ypart, c.cur_ctrl);
         PLS_CHECK_LAUNCH();
         ++c.launches;
         if (!c.circ) {

@@ -350,77 +350,86 @@ __global__ void __launch_bounds__(256) k_gemv_tiled(const T *__restrict__ Qc, co
 // I != J, column sums Q~_IJ^T p_I -> rows of J (slot I) -- half the HBM bytes of full rows.
 // Warp w owns rows 16w..16w+15, lane l columns 4l..4l+3 (a row = 1 KiB / 512 B, coalesced).
 template <typename T>
-__global__ void __launch_bounds__(256) k_gemv_sym(const T *__restrict__ Qc, const int2 *__restrict__ tiles, int nsub,
-                                                  const T *__restrict__ p, int band0, int64_t brows,
-                                                  T *__restrict__ Ypart, const int *ctrl) {
+__global__ void __launch_bounds__(256, 4) k_gemv_sym(const T *__restrict__ Qc, const int2 *__restrict__ tiles, int nsub,
+                                                     int64_t nstored, int per_cta, const T *__restrict__ p, int band0,
+                                                     int64_t brows, T *__restrict__ Ypart, const int *ctrl) {
     using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
     constexpr int VEC = 16 / sizeof(T);
     constexpr int LPR = 4 / VEC;  // 16-byte loads per lane per row (2 fp64, 1 fp32)
-    __shared__ T redc[8][kTile];
-    __shared__ T redr[kTile];
+    __shared__ T redc[2][8][kTile + 4];
     if (cg_done(ctrl)) return;
-    const int2 tile = tiles[static_cast<int64_t>(blockIdx.x) * nsub];
-    const int I = tile.x, J = tile.y / nsub;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const T *blk = Qc + static_cast<int64_t>(blockIdx.x) * (kTile * kTile) + (w * 16) * kTile + lane * 4;
-    T pj[4], rs[16], cs[4];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        pj[v] = p[static_cast<int64_t>(J) * kTile + lane * 4 + v];
-        cs[v] = T(0);
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const T pi = p[static_cast<int64_t>(I) * kTile + w * 16 + r];
-        T a[4];
-#pragma unroll
-        for (int u = 0; u < LPR; ++u) {
-            const V *src = reinterpret_cast<const V *>(blk + r * kTile) + u;
-            V x;
-            if constexpr (sizeof(T) == 8) {
-                asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(x.x), "=d"(x.y) : "l"(src));
-            } else {
-                asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                             : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "l"(src));
-            }
-            const T *xe = reinterpret_cast<const T *>(&x);
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) a[u * VEC + v] = xe[v];
-        }
-        T s = T(0);
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * per_cta;
+    int nsync = 0;  // column partials double-buffered by barrier count: one barrier per mirrored tile
+    for (int64_t tt = t0; tt < t0 + per_cta && tt < nstored; ++tt) {
+        const int buf = nsync & 1;
+        const int2 tile = tiles[tt * nsub];
+        const int I = tile.x, J = tile.y / nsub;
+        const T *blk = Qc + tt * (kTile * kTile) + (w * 16) * kTile + lane * 4;
+        T pj[4], rs[16], cs[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-            s = fma(a[v], pj[v], s);
-            cs[v] = fma(a[v], pi, cs[v]);
+            pj[v] = p[static_cast<int64_t>(J) * kTile + lane * 4 + v];
+            cs[v] = T(0);
         }
-        rs[r] = s;
-    }
-    // row sums: 16 values x 32 lanes -> lane l holds row (l >> 1) of this warp (16 shuffles)
-    {
-        T w8[8], w4[4], w2[2];
-        const bool h1 = (lane >> 4) & 1, h2 = (lane >> 3) & 1, h3 = (lane >> 2) & 1, h4 = (lane >> 1) & 1;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) w8[i] = (h1 ? rs[i + 8] : rs[i]) + __shfl_xor_sync(0xffffffffu, h1 ? rs[i] : rs[i + 8], 16);
+        for (int r = 0; r < 16; ++r) {
+            const T pi = p[static_cast<int64_t>(I) * kTile + w * 16 + r];
+            T a[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w4[i] = (h2 ? w8[i + 4] : w8[i]) + __shfl_xor_sync(0xffffffffu, h2 ? w8[i] : w8[i + 4], 8);
+            for (int u = 0; u < LPR; ++u) {
+                const V *src = reinterpret_cast<const V *>(blk + r * kTile) + u;
+                V x;
+                if constexpr (sizeof(T) == 8) {
+                    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(x.x), "=d"(x.y) : "l"(src));
+                } else {
+                    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "l"(src));
+                }
+                const T *xe = reinterpret_cast<const T *>(&x);
 #pragma unroll
-        for (int i = 0; i < 2; ++i) w2[i] = (h3 ? w4[i + 2] : w4[i]) + __shfl_xor_sync(0xffffffffu, h3 ? w4[i] : w4[i + 2], 4);
-        T w1 = (h4 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? w2[0] : w2[1], 2);
-        w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
-        if ((lane & 1) == 0) redr[w * 16 + (lane >> 1)] = w1;
-    }
+                for (int v = 0; v < VEC; ++v) a[u * VEC + v] = xe[v];
+            }
+            T s = T(0);
 #pragma unroll
-    for (int v = 0; v < 4; ++v) redc[w][lane * 4 + v] = cs[v];
-    __syncthreads();
-    const int64_t lrow0 = static_cast<int64_t>(I - band0) * kTile, lcol0 = static_cast<int64_t>(J - band0) * kTile;
-    if (threadIdx.x < kTile) {
-        Ypart[static_cast<int64_t>(J) * brows + lrow0 + threadIdx.x] = redr[threadIdx.x];
-    } else if (I != J) {
-        const int t = threadIdx.x - kTile;
-        T s = T(0);
+            for (int v = 0; v < 4; ++v) {
+                s = fma(a[v], pj[v], s);
+                cs[v] = fma(a[v], pi, cs[v]);
+            }
+            rs[r] = s;
+        }
+        // row sums: 16 values x 32 lanes -> lane l holds row 16w + (l >> 1) (16 shuffles); each
+        // tile row belongs to exactly one warp, so it is written straight to its slot.
+        {
+            T w8[8], w4[4], w2[2];
+            const bool h1 = (lane >> 4) & 1, h2 = (lane >> 3) & 1, h3 = (lane >> 2) & 1, h4 = (lane >> 1) & 1;
 #pragma unroll
-        for (int ww = 0; ww < 8; ++ww) s += redc[ww][t];
-        Ypart[static_cast<int64_t>(I) * brows + lcol0 + t] = s;
+            for (int i = 0; i < 8; ++i)
+                w8[i] = (h1 ? rs[i + 8] : rs[i]) + __shfl_xor_sync(0xffffffffu, h1 ? rs[i] : rs[i + 8], 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                w4[i] = (h2 ? w8[i + 4] : w8[i]) + __shfl_xor_sync(0xffffffffu, h2 ? w8[i] : w8[i + 4], 8);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                w2[i] = (h3 ? w4[i + 2] : w4[i]) + __shfl_xor_sync(0xffffffffu, h3 ? w4[i] : w4[i + 2], 4);
+            T w1 = (h4 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? w2[0] : w2[1], 2);
+            w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
+            if ((lane & 1) == 0)
+                Ypart[static_cast<int64_t>(J) * brows + static_cast<int64_t>(I - band0) * kTile + w * 16 + (lane >> 1)] = w1;
+        }
+        if (I != J) {  // tile-uniform branch
+#pragma unroll
+            for (int v = 0; v < 4; ++v) redc[buf][w][lane * 4 + v] = cs[v];
+            __syncthreads();
+            ++nsync;
+            if (threadIdx.x < kTile) {
+                const int t = threadIdx.x;
+                T s = T(0);
+#pragma unroll
+                for (int ww = 0; ww < 8; ++ww) s += redc[buf][ww][t];
+                Ypart[static_cast<int64_t>(I) * brows + static_cast<int64_t>(J - band0) * kTile + t] = s;
+            }
+        }
     }
 }
 
