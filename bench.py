@@ -299,12 +299,12 @@ def main():
                 "avg_launch_s": avg_mv}
     else:
         s = 8 if cfg.dtype == "f64" else 4
-        mpad = int(math.ceil(cfg.m / (128 * world)) * 128 * world)
-        by = (mpad / world) * mpad * s
+        T = int(math.ceil(cfg.m / (128 * world)) * world)
+        by = T * (T + 1) / 2 / world * 128 * 128 * s  # symmetric-packed tiles, ~1/P per rank
         peak = measured_peaks().get("hbm_gbs", 6650.0)
         achieved = by / avg_mv / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic_for(f"{cfg.name}/cached/k_gemv_tiled") if world == 1 else None, "kernel": "k_gemv_tiled", "per_launch": f"{by:.4g} bytes of cached Q~ band",
+                "traffic": traffic_for(f"{cfg.name}/cached/k_gemv_sym") if world == 1 else None, "kernel": "k_gemv_sym", "per_launch": f"{by:.4g} bytes of stored (symmetric-packed) Q~ tiles per rank",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)", "avg_launch_s": avg_mv}
 
     line = {"metric": METRIC, "value": iters / t, "unit": UNIT, "n_gpus": world, "steps": args.steps,
