@@ -116,7 +116,7 @@ void launch_transform(const T *X, int64_t m, int64_t d, T *Xt, int64_t rows, int
 // 2-D row-major array [outer][inner] of 4- or 8-byte elements, box {box_inner, box_outer},
 // 128-byte swizzle (box_inner * elem = 128 B).
 CUtensorMap make_tmap_2d(void *base, int elem_bytes, int64_t inner, int64_t outer, uint32_t box_inner,
-                         uint32_t box_outer) {
+                         uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -131,7 +131,7 @@ CUtensorMap make_tmap_2d(void *base, int elem_bytes, int64_t inner, int64_t oute
     const cuuint32_t box[2] = {box_inner, box_outer};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&m, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base,
-                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
     return m;
@@ -232,6 +232,10 @@ struct Ctx {
     bool tc = false;             // fp32: tcgen05 3xTF32 contraction
     float *Xhi = nullptr, *Xlo = nullptr;
     CUtensorMap tm_hi, tm_lo;
+    CUtensorMap tw_ahi, tw_alo, tw_bhi, tw_blo;  // wide (128 x 256, SWIZZLE_64B) kernel
+    bool wide = false, wide_ok = true;
+    int2 *wtiles = nullptr;
+    int nwtiles = 0;
     int64_t dpad_tc = 0;
     int nsplit = 1;  // cached GEMV: column splits per row block
     int64_t launches = 0, launches_cg = 0;
@@ -291,6 +295,10 @@ void setup_tc(Ctx<T> &c, Arena &A, const T *Xs, int64_t m, int64_t d) {
         ++c.launches;
         c.tm_hi = make_tmap_2d_f32(c.Xhi, c.dpad_tc, g.mpad, Tc::BK, kTile);
         c.tm_lo = make_tmap_2d_f32(c.Xlo, c.dpad_tc, g.mpad, Tc::BK, kTile);
+        c.tw_ahi = make_tmap_2d(c.Xhi, 4, c.dpad_tc, g.mpad, TcW::BK, kTile, CU_TENSOR_MAP_SWIZZLE_64B);
+        c.tw_alo = make_tmap_2d(c.Xlo, 4, c.dpad_tc, g.mpad, TcW::BK, kTile, CU_TENSOR_MAP_SWIZZLE_64B);
+        c.tw_bhi = make_tmap_2d(c.Xhi, 4, c.dpad_tc, g.mpad, TcW::BK, 2 * kTile, CU_TENSOR_MAP_SWIZZLE_64B);
+        c.tw_blo = make_tmap_2d(c.Xlo, 4, c.dpad_tc, g.mpad, TcW::BK, 2 * kTile, CU_TENSOR_MAP_SWIZZLE_64B);
         tc_set_attrs();
     }
 }
@@ -323,12 +331,57 @@ void tc_set_attrs() {
     PLS_TC_ATTR(LINEAR, TC_PRECOMPUTE); PLS_TC_ATTR(POLYNOMIAL, TC_PRECOMPUTE); PLS_TC_ATTR(RBF, TC_PRECOMPUTE);
     PLS_TC_ATTR(LINEAR, TC_PREDICT); PLS_TC_ATTR(POLYNOMIAL, TC_PREDICT); PLS_TC_ATTR(RBF, TC_PREDICT);
 #undef PLS_TC_ATTR
+    const int wb = static_cast<int>(TcW::SMEM_BYTES);
+    PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<LINEAR, TC_MATVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
+    PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<POLYNOMIAL, TC_MATVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
+    PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<RBF, TC_MATVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
+    PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<LINEAR, TC_PREDICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
+    PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<POLYNOMIAL, TC_PREDICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
+    PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<RBF, TC_PREDICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
+}
+
+template <int KT, int MODE>
+void tcw_launch(int grid, cudaStream_t s, const CUtensorMap &ah, const CUtensorMap &al, const CUtensorMap &bh,
+                const CUtensorMap &bl, int64_t dpad, const int2 *tiles, int tilesI, int T_tiles, const float *qa,
+                const float *na, const float *qb, const float *nb_, const float *p, KParams<float> kp, float invC,
+                const double *scal, int64_t m1, float *Ypart, int64_t band_rows, const int *ctrl) {
+    k_tile_tc_wide<KT, MODE><<<grid, TcW::THREADS, TcW::SMEM_BYTES, s>>>(ah, al, bh, bl, dpad, tiles, tilesI, T_tiles, qa,
+                                                                        na, qb, nb_, p, kp, invC, scal, m1, Ypart,
+                                                                        band_rows, ctrl);
+    PLS_CHECK_LAUNCH();
+}
+
+template <int MODE, typename... Args>
+void tcw_dispatch(int kernel, Args &&...args) {
+    switch (kernel) {
+        case LINEAR: tcw_launch<LINEAR, MODE>(args...); break;
+        case POLYNOMIAL: tcw_launch<POLYNOMIAL, MODE>(args...); break;
+        default: tcw_launch<RBF, MODE>(args...);
+    }
+}
+
+// Wide tiles (I, Jw) of the upper triangle for one GPU: Jw from I/2 (grouped raster).
+std::vector<int2> wide_tiles(int T) {
+    std::vector<int2> t;
+    const int TW = (T + 1) / 2;
+    for (int I0 = 0; I0 < T; I0 += 8)
+        for (int Jw = 0; Jw < TW; ++Jw)
+            for (int I = I0; I < std::min(I0 + 8, T); ++I)
+                if (Jw >= I / 2) t.push_back(make_int2(I, Jw));
+    return t;
 }
 
 template <typename T>
 bool launch_tc(Ctx<T> &c, const T *pfull, int b0, int b1, int64_t brows) {
     if constexpr (std::is_same<T, float>::value) {
         const Geometry &g = c.g;
+        if (c.wide) {
+            tcw_dispatch<TC_MATVEC>(c.kp.kernel, c.nwtiles, c.s, c.tw_ahi, c.tw_alo, c.tw_bhi, c.tw_blo, c.dpad_tc,
+                                    c.wtiles, 0, g.T, c.q, c.nrm, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1,
+                                    c.Ypart, brows, c.cur_ctrl);
+            ++c.launches;
+            return true;
+        }
         tc_dispatch<TC_MATVEC>(c.kp.kernel, c.ntiles, c.s, c.tm_hi, c.tm_lo, c.tm_hi, c.tm_lo, c.dpad_tc, c.tiles, 0, c.q,
                                c.nrm, c.q, c.nrm, pfull, c.kp, c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows,
                                static_cast<float *>(nullptr), g.T, c.cur_ctrl);
@@ -583,6 +636,14 @@ void configure_product(Ctx<T> &c, Arena &A) {
     }
     c.nstored = c.packed ? c.ntiles / c.nsub_eff : 0;
     c.Yfin = c.Ypart;
+    c.wide = c.tc && g.P == 1 && !c.cached && !c.lowrank && !c.circ && c.wide_ok;
+    if (c.wide) {
+        std::vector<int2> wl = wide_tiles(g.T);
+        c.nwtiles = static_cast<int>(wl.size());
+        c.wtiles = A.alloc<int2>(c.nwtiles);
+        PLS_CUDA(cudaMemcpyAsync(c.wtiles, wl.data(), wl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
+        PLS_CUDA(cudaStreamSynchronize(c.s));
+    }
 }
 
 // Stored 128 x 128 tiles of the packed layout for this rank (upper triangle for one GPU, the
@@ -969,11 +1030,19 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
             const CUtensorMap xh = make_tmap_2d_f32(Xh, dtc, mpad, Tc::BK, kTile);
             const CUtensorMap xl = make_tmap_2d_f32(Xlo, dtc, mpad, Tc::BK, kTile);
             tc_set_attrs();
+            // 128 x 256 tiles (UMMA N = 256): test block I x two training blocks
+            const CUtensorMap zwh = make_tmap_2d(Zh, 4, dtc, npad, TcW::BK, kTile, CU_TENSOR_MAP_SWIZZLE_64B);
+            const CUtensorMap zwl = make_tmap_2d(Zlo, 4, dtc, npad, TcW::BK, kTile, CU_TENSOR_MAP_SWIZZLE_64B);
+            const CUtensorMap xwh = make_tmap_2d(Xh, 4, dtc, mpad, TcW::BK, 2 * kTile, CU_TENSOR_MAP_SWIZZLE_64B);
+            const CUtensorMap xwl = make_tmap_2d(Xlo, 4, dtc, mpad, TcW::BK, 2 * kTile, CU_TENSOR_MAP_SWIZZLE_64B);
+            (void)zh; (void)zl; (void)xh; (void)xl;
+            PLS_CUDA(cudaMemsetAsync(Fpart, 0, static_cast<size_t>(tilesJ) * npad * sizeof(T), s));
             PLS_CUDA(cudaEventRecord(e0, s));
-            tc_dispatch<TC_PREDICT>(pb.kernel, grid, s, zh, zl, xh, xl, dtc, static_cast<const int2 *>(nullptr), tilesI,
-                                    static_cast<const float *>(nullptr), nz, static_cast<const float *>(nullptr), nx,
-                                    alpha, kp, 0.f, static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,
-                                    static_cast<float *>(nullptr), 0, static_cast<const int *>(nullptr));
+            tcw_dispatch<TC_PREDICT>(pb.kernel, tilesI * static_cast<int>(ceil_div(tilesJ, 2)), s, zwh, zwl, xwh, xwl,
+                                     dtc, static_cast<const int2 *>(nullptr), tilesI, tilesJ,
+                                     static_cast<const float *>(nullptr), nz, static_cast<const float *>(nullptr), nx,
+                                     alpha, kp, 0.f, static_cast<const double *>(nullptr), int64_t(0), Fpart, npad,
+                                     static_cast<const int *>(nullptr));
         }
     }
     const Ops<T> pops = make_ops(Zl, zrows, Xl, xrows, EN::kPointMajor ? dpad : L);

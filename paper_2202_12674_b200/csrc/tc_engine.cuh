@@ -315,4 +315,188 @@ __global__ void __launch_bounds__(Tc::THREADS, 1)
     }
 }
 
+// =====================================================================================
+// Wide variant: 128 x 256 tiles (UMMA N = 256), 16-feature slabs in a 4-stage ring with the
+// 64-byte swizzle -- 25 % fewer operand bytes through L2 per useful flop than 128 x 128 (the
+// 3xTF32 path is L2-bandwidth bound, profiles/r01_ncu_matvec_c3_tc.txt).  A wide tile
+// (I, Jw) covers the two 128-blocks J = 2 Jw + h, h = 0, 1; a half is used iff J >= I and J < T
+// (upper triangle; the half below the diagonal of an odd I is computed and dropped), mirrored
+// iff J > I.  Slots as in k_tile_tc.  Used for the one-GPU implicit product and for predict.
+struct TcW {
+    static constexpr int BK = 16;                               // fp32 features per slab (64 B rows)
+    static constexpr int STAGES = 4;
+    static constexpr int TA = kTile * BK, TB = 2 * kTile * BK;  // floats per A / B operand tile
+    static constexpr uint32_t STAGE_BYTES = (2 * TA + 2 * TB) * 4;  // 48 KiB
+    static constexpr int THREADS = 192;
+    static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + 8192;
+    static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+};
+
+// K-major operand, 64-byte swizzle atoms (8 rows x 64 B): SBO = 512 B, layout type 4.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+    return (uint64_t((saddr >> 4) & 0x3FFFu)) | (uint64_t(512 >> 4) << 32) | (uint64_t(1) << 46) | (uint64_t(4) << 61);
+}
+__device__ __forceinline__ void umma_tf32_n256(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(TcW::IDESC), "r"(acc));
+}
+
+template <int KT, int MODE>
+__global__ void __launch_bounds__(TcW::THREADS, 1)
+    k_tile_tc_wide(const __grid_constant__ CUtensorMap tma_hi, const __grid_constant__ CUtensorMap tma_lo,
+                   const __grid_constant__ CUtensorMap tmb_hi, const __grid_constant__ CUtensorMap tmb_lo, int64_t dpad,
+                   const int2 *__restrict__ tiles, int tilesI, int T_tiles, const float *__restrict__ qa,
+                   const float *__restrict__ na, const float *__restrict__ qb, const float *__restrict__ nb_,
+                   const float *__restrict__ p, KParams<float> kp, float invC, const double *__restrict__ scal,
+                   int64_t m1, float *__restrict__ Ypart, int64_t band_rows, const int *ctrl) {
+    if (cg_done(ctrl)) return;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float *ring = reinterpret_cast<float *>(base);
+    unsigned char *misc = base + size_t(TcW::STAGES) * TcW::STAGE_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(misc);
+    uint64_t *empty = full + TcW::STAGES;
+    uint64_t *accf = empty + TcW::STAGES;
+    uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(accf + 1);
+    float *colq = reinterpret_cast<float *>(misc + 128);  // [256]
+    float *colp = colq + 2 * kTile;                       // [256] (alpha for predict)
+    float *coln = colp + 2 * kTile;                       // [256]
+    float *redc = coln + 2 * kTile;                       // [4][256]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int I, Jw;
+    if constexpr (MODE == TC_PREDICT) {
+        I = blockIdx.x % tilesI;
+        Jw = blockIdx.x / tilesI;
+    } else {
+        const int2 tile = tiles[blockIdx.x];
+        I = tile.x;
+        Jw = tile.y;
+    }
+    const int row0 = I * kTile, col0 = Jw * 2 * kTile;
+    const int nk = static_cast<int>(dpad / TcW::BK);
+
+    if (warp == 4 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_hi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_lo)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmb_hi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmb_lo)) : "memory");
+        for (int s = 0; s < TcW::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accf, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_addr(tmem_sh)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int c = threadIdx.x; c < 2 * kTile; c += TcW::THREADS) {
+        const int64_t gj = col0 + c;
+        const bool in = gj < int64_t(T_tiles) * kTile;
+        colq[c] = (MODE == TC_PREDICT || !in) ? 0.f : qb[gj];
+        colp[c] = in ? p[gj] : 0.f;
+        coln[c] = (KT == RBF && in) ? nb_[gj] : 0.f;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_sh;
+
+    if (warp == 4) {
+        if (lane == 0) {  // ---- TMA producer
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % TcW::STAGES;
+                if (kb >= TcW::STAGES) mbar_wait(&empty[s], ((kb / TcW::STAGES) - 1) & 1);
+                float *st = ring + size_t(s) * (2 * TcW::TA + 2 * TcW::TB);
+                mbar_expect_tx(&full[s], TcW::STAGE_BYTES);
+                const int x = kb * TcW::BK;
+                tma_load_2d(st, &tma_hi, &full[s], x, row0);
+                tma_load_2d(st + TcW::TA, &tma_lo, &full[s], x, row0);
+                tma_load_2d(st + 2 * TcW::TA, &tmb_hi, &full[s], x, col0);
+                tma_load_2d(st + 2 * TcW::TA + TcW::TB, &tmb_lo, &full[s], x, col0);
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {  // ---- MMA issuer: 2 K-steps x 3 products per slab
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % TcW::STAGES;
+                mbar_wait(&full[s], (kb / TcW::STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sa = smem_addr(ring + size_t(s) * (2 * TcW::TA + 2 * TcW::TB));
+                const uint64_t dah = umma_desc_sw64(sa), dal = umma_desc_sw64(sa + TcW::TA * 4);
+                const uint64_t dbh = umma_desc_sw64(sa + 2 * TcW::TA * 4);
+                const uint64_t dbl = umma_desc_sw64(sa + (2 * TcW::TA + TcW::TB) * 4);
+#pragma unroll
+                for (int kk = 0; kk < TcW::BK / 8; ++kk) {
+                    const uint64_t o = uint64_t(kk * 2);  // +32 B
+                    umma_tf32_n256(tmem, dah + o, dbh + o, (kb > 0 || kk > 0) ? 1u : 0u);
+                    umma_tf32_n256(tmem, dah + o, dbl + o, 1u);
+                    umma_tf32_n256(tmem, dal + o, dbh + o, 1u);
+                }
+                umma_commit(&empty[s]);
+            }
+            umma_commit(accf);
+        }
+    } else {  // ---- epilogue warps 0-3: thread = tile row 32w + lane, 256 columns (two halves)
+        const int lr = warp * 32 + lane;
+        const int64_t gi = row0 + lr;
+        const float qi = (MODE == TC_PREDICT) ? 0.f : qa[gi];
+        const float pi = (MODE == TC_MATVEC) ? p[gi] : 0.f;
+        const float ni = (KT == RBF) ? na[gi] : 0.f;
+        const float Qmm = (MODE == TC_PREDICT) ? 0.f : static_cast<float>(scal[S_QMM]);
+        mbar_wait(accf, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int J = 2 * Jw + h;
+            const bool use = (MODE == TC_PREDICT) ? (J < T_tiles) : (J >= I && J < T_tiles);  // warp-uniform
+            if (!use) continue;
+            const bool mirrored = (MODE == TC_MATVEC) && J > I;
+            float rs = 0.f;
+#pragma unroll 1
+            for (int c0 = h * kTile; c0 < (h + 1) * kTile; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
+                if constexpr (MODE == TC_PREDICT) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) rs = fmaf(colp[c0 + j], kernel_value<KT, float>(v[j], ni, coln[c0 + j], false, kp), rs);
+                } else {
+                    float cs[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int lc = c0 + j;
+                        const float qt = qtilde_value<KT, float>(v[j], gi, int64_t(col0 + lc), ni, coln[lc], qi,
+                                                                 colq[lc], Qmm, invC, m1, kp);
+                        rs = fmaf(qt, colp[lc], rs);
+                        cs[j] = qt * pi;
+                    }
+                    if (mirrored) {
+                        const float t = transpose_reduce16(cs, lane);
+                        if ((lane & 1) == 0) redc[warp * 2 * kTile + c0 + (lane >> 1)] = t;
+                    }
+                }
+            }
+            Ypart[int64_t(J) * band_rows + row0 + lr] = rs;
+            if (mirrored) {
+                asm volatile("bar.sync 1, 128;");
+                const int t = threadIdx.x;
+                const int c = h * kTile + t;
+                Ypart[int64_t(I) * band_rows + int64_t(J) * kTile + t] =
+                    (redc[c] + redc[2 * kTile + c]) + (redc[4 * kTile + c] + redc[6 * kTile + c]);
+                asm volatile("bar.sync 1, 128;");  // redc is reused by the next half
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 5) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    }
+}
+
 }  // namespace plssvm

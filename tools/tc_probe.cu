@@ -176,7 +176,119 @@ void run(int K) {
     cudaFree(dC);
 }
 
+
+// ---- SWIZZLE_64B, N = 256 variant: 16 fp32 (64 B) per row, A 128 rows, B 256 rows --------------
+// 64-byte swizzle atom (8 rows x 64 B = 512 B): 16-byte chunk c (0..3) of row r at c ^ ((r >> 1) & 3).
+__device__ __forceinline__ uint64_t make_desc_sw64(const void *smem_ptr) {
+    const uint64_t addr = smem_u32(smem_ptr);
+    return ((addr >> 4) & 0x3FFFull) | ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+__global__ void probe_n256(const float *A, const float *B, int K, float *C) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    float *sAh = reinterpret_cast<float *>(sm), *sAl = sAh + 128 * 16, *sBh = sAl + 128 * 16, *sBl = sBh + 256 * 16;
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base_sh;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_sh)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base_sh;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    uint32_t phase = 0;
+    for (int k0 = 0; k0 < K; k0 += 16) {
+        for (int rr = tid; rr < 256; rr += 128) {
+            for (int c = 0; c < 4; ++c) {
+                const int off = rr * 16 + ((c ^ ((rr >> 1) & 3)) * 4);
+                float4 b = *reinterpret_cast<const float4 *>(B + (size_t)rr * K + k0 + 4 * c);
+                float4 bh = make_float4(to_tf32(b.x), to_tf32(b.y), to_tf32(b.z), to_tf32(b.w));
+                float4 bl = make_float4(to_tf32(b.x - bh.x), to_tf32(b.y - bh.y), to_tf32(b.z - bh.z), to_tf32(b.w - bh.w));
+                *reinterpret_cast<float4 *>(sBh + off) = bh;
+                *reinterpret_cast<float4 *>(sBl + off) = bl;
+                if (rr < 128) {
+                    float4 a = *reinterpret_cast<const float4 *>(A + (size_t)rr * K + k0 + 4 * c);
+                    float4 ah = make_float4(to_tf32(a.x), to_tf32(a.y), to_tf32(a.z), to_tf32(a.w));
+                    float4 al = make_float4(to_tf32(a.x - ah.x), to_tf32(a.y - ah.y), to_tf32(a.z - ah.z), to_tf32(a.w - ah.w));
+                    *reinterpret_cast<float4 *>(sAh + off) = ah;
+                    *reinterpret_cast<float4 *>(sAl + off) = al;
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int kk = 0; kk < 2; ++kk) {
+                const uint64_t o = (uint64_t)(kk * 2);
+                const uint32_t acc0 = (k0 > 0 || kk > 0) ? 1u : 0u;
+                mma_tf32(tmem, make_desc_sw64(sAh) + o, make_desc_sw64(sBh) + o, idesc, acc0);
+                mma_tf32(tmem, make_desc_sw64(sAh) + o, make_desc_sw64(sBl) + o, idesc, 1u);
+                mma_tf32(tmem, make_desc_sw64(sAl) + o, make_desc_sw64(sBh) + o, idesc, 1u);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&mbar)));
+        }
+        asm volatile(
+            "{\n.reg .pred P1;\nWAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+            "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(&mbar)),
+            "r"(phase));
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        __syncthreads();
+    }
+    for (int c0 = 0; c0 < 256; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        for (int j = 0; j < 16; ++j) C[(size_t)(warp * 32 + lane) * 256 + c0 + j] = __uint_as_float(v[j]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+void run_n256(int K) {
+    std::vector<float> A(128 * K), B(256 * K), C(128 * 256);
+    srand(2);
+    for (auto &x : A) x = (rand() / (float)RAND_MAX) * 2 - 1;
+    for (auto &x : B) x = (rand() / (float)RAND_MAX) * 2 - 1;
+    float *dA, *dB, *dC;
+    CK(cudaMalloc(&dA, A.size() * 4));
+    CK(cudaMalloc(&dB, B.size() * 4));
+    CK(cudaMalloc(&dC, C.size() * 4));
+    CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaFuncSetAttribute(probe_n256, cudaFuncAttributeMaxDynamicSharedMemorySize, 49152 + 1024));
+    probe_n256<<<1, 128, 49152 + 1024>>>(dA, dB, K, dC);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("n256: kernel error %s\n", cudaGetErrorString(e)); exit(1); }
+    CK(cudaMemcpy(C.data(), dC, C.size() * 4, cudaMemcpyDeviceToHost));
+    double num = 0, den = 0;
+    for (int i = 0; i < 128; ++i)
+        for (int j = 0; j < 256; ++j) {
+            double s = 0;
+            for (int k = 0; k < K; ++k) s += (double)A[i * K + k] * (double)B[j * K + k];
+            num += (C[i * 256 + j] - s) * (C[i * 256 + j] - s);
+            den += s * s;
+        }
+    printf("SW64 N=256 K=%d 3xTF32: rel err %.3e\n", K, sqrt(num / den));
+}
+
 int main(int argc, char **argv) {
+    if (argc > 1 && atoi(argv[1]) == 256) { run_n256(256); return 0; }
     const int mbit = argc > 1 ? atoi(argv[1]) : 24;
     if (mbit == 23) run<23>(256);
     else run<24>(256);
