@@ -92,7 +92,14 @@ typedef struct {
                                 3xTF32 split) [0]; 1 = CUDA-core FFMA tiles */
     int32_t linear_w;        /* predict with the linear kernel through w = sum_i alpha_i x_i (Eq. 15,
                                 O((m+n)d)) [1]; 0 = evaluate the kernel matrix like the other kernels */
+    int32_t fp64_engine;     /* fp64 pairwise contraction (implicit Q~p, cached precompute, predict):
+                                PLSSVM_FP64_OZAKI = int8 tensor cores (tcgen05 kind::i8) on an exact
+                                8-digit split of each point, digit products summed exactly in int32
+                                and combined in fp64 [default]; PLSSVM_FP64_DMMA = fp64 DMMA tensor
+                                cores (mma.sync f64) */
 } plssvm_options_t;
+
+typedef enum { PLSSVM_FP64_OZAKI = 0, PLSSVM_FP64_DMMA = 1 } plssvm_fp64_engine_t;
 
 /* Statistics of one training call (all times are device-event seconds). */
 typedef struct {

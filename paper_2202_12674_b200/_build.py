@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libplssvm_b200.so")
 SOURCES = ["capi.cu", "driver.cu", "comm.cu"]
-HEADERS = ["common.cuh", "tile_engine.cuh", "kernels.cuh", "tc_engine.cuh", "driver.h"]
+HEADERS = ["common.cuh", "tile_engine.cuh", "kernels.cuh", "tc_engine.cuh", "ozaki_engine.cuh", "driver.h"]
 
 
 def nccl_dirs():

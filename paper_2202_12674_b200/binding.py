@@ -17,6 +17,7 @@ from . import _build
 LINEAR, POLYNOMIAL, RBF = 0, 1, 2
 F64, F32 = 0, 1
 MODE_AUTO, MODE_IMPLICIT, MODE_CACHED, MODE_LOWRANK = 0, 1, 2, 3
+FP64_OZAKI, FP64_DMMA = 0, 1
 OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED = range(8)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
                 6: "E_NUMERICAL", 7: "W_NOT_CONVERGED"}
@@ -31,7 +32,7 @@ class plssvm_options_t(ct.Structure):
     _fields_ = [("mode", ct.c_int32), ("x0", ct.c_int32), ("max_iter", ct.c_int64), ("replace_every", ct.c_int64),
                 ("fixed_iter", ct.c_int64), ("device", ct.c_int32), ("device_pointers", ct.c_int32),
                 ("stream", ct.c_void_p), ("comm", ct.c_void_p), ("cache_budget_bytes", ct.c_int64),
-                ("fp32_engine", ct.c_int32), ("linear_w", ct.c_int32)]
+                ("fp32_engine", ct.c_int32), ("linear_w", ct.c_int32), ("fp64_engine", ct.c_int32)]
 
 
 class plssvm_stats_t(ct.Structure):

@@ -22,6 +22,7 @@
 
 #include "driver.h"
 #include "kernels.cuh"
+#include "ozaki_engine.cuh"
 #include "tc_engine.cuh"
 
 namespace plssvm {
@@ -115,8 +116,7 @@ void launch_transform(const T *X, int64_t m, int64_t d, T *Xt, int64_t rows, int
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
 // 2-D row-major array [outer][inner] of 4- or 8-byte elements, box {box_inner, box_outer},
 // 128-byte swizzle (box_inner * elem = 128 B).
-CUtensorMap make_tmap_2d(void *base, int elem_bytes, int64_t inner, int64_t outer, uint32_t box_inner,
-                         uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -125,15 +125,36 @@ CUtensorMap make_tmap_2d(void *base, int elem_bytes, int64_t inner, int64_t oute
         if (!fn || q != cudaDriverEntryPointSuccess) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
+    return encode;
+}
+
+CUtensorMap make_tmap_2d(void *base, int elem_bytes, int64_t inner, int64_t outer, uint32_t box_inner,
+                         uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * elem_bytes)};
     const cuuint32_t box[2] = {box_inner, box_outer};
     const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(&m, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base,
-                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = tmap_encoder()(&m, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+// Digit planes D[planes][rows][dpad8] (int8) as a 3-D map; one box = 32 features x box_rows rows
+// x all planes, 32-byte swizzle (ozaki_engine.cuh).
+CUtensorMap make_tmap_digits(int8_t *base, int64_t dpad8, int64_t rows, int planes, uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(dpad8), static_cast<cuuint64_t>(rows),
+                                static_cast<cuuint64_t>(planes)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(dpad8), static_cast<cuuint64_t>(rows * dpad8)};
+    const cuuint32_t box[3] = {32u, box_rows, static_cast<cuuint32_t>(planes)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled (digits) failed: " + std::to_string(int(r)));
     return m;
 }
 CUtensorMap make_tmap_2d_f32(float *base, int64_t inner, int64_t outer, uint32_t box_inner, uint32_t box_outer) {
@@ -215,6 +236,15 @@ std::vector<int2> circulant_tiles(const Geometry &g, int nsub) {
     return t;
 }
 
+// Digit planes of a point-major padded fp64 array: TMA maps for the row (128) and column (64)
+// operand roles.
+struct OzOperand {
+    int8_t *D = nullptr;
+    double *sc = nullptr;
+    CUtensorMap ta, tb;
+    int nk = 0;
+};
+
 template <typename T>
 struct Ctx {
     Geometry g;
@@ -253,6 +283,8 @@ struct Ctx {
     T *yfull = nullptr, *ysc = nullptr, *Yfin = nullptr;
     int nsub_eff = 1;
     int *ctrl = nullptr;             // device CG control block (kernels.cuh Ctl)
+    bool oz = false;                 // fp64: int8 tensor-core digit engine (ozaki_engine.cuh)
+    OzOperand ozx;
     const int *cur_ctrl = nullptr;   // ctrl inside the CG loop (loop kernels early-exit when done)
 };
 
@@ -371,6 +403,85 @@ std::vector<int2> wide_tiles(int T) {
     return t;
 }
 
+// ---- fp64 on the int8 tensor cores (ozaki_engine.cuh) -------------------------------------
+constexpr int kOzS = 8;  // digits per point: fp64-level products
+using OzC = Oz<kOzS>;
+
+int num_sms() {
+    int dev = 0, n = 0;
+    PLS_CUDA(cudaGetDevice(&dev));
+    PLS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+}
+
+OzOperand oz_prepare(Arena &A, const double *Xp, int64_t rows, int64_t dpad, int64_t d, cudaStream_t s,
+                     int64_t &launches) {
+    OzOperand o;
+    const int64_t d8 = round_up(d, OzC::BK);
+    o.D = A.alloc<int8_t>(kOzS * rows * d8);
+    o.sc = A.alloc<double>(rows);
+    k_ozaki_split<kOzS><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, s>>>(Xp, rows, dpad, d8, o.D, o.sc);
+    PLS_CHECK_LAUNCH();
+    ++launches;
+    o.ta = make_tmap_digits(o.D, d8, rows, kOzS, kTile);
+    o.tb = make_tmap_digits(o.D, d8, rows, kOzS, OzC::TN);
+    o.nk = static_cast<int>(d8 / OzC::BK);
+    return o;
+}
+
+void oz_set_attrs() {
+    const int bytes = static_cast<int>(OzC::SMEM_BYTES);
+#define PLS_OZ_ATTR(K, M) \
+    PLS_CUDA(cudaFuncSetAttribute(k_tile_ozaki<K, kOzS, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
+    PLS_OZ_ATTR(LINEAR, OZ_MATVEC); PLS_OZ_ATTR(POLYNOMIAL, OZ_MATVEC); PLS_OZ_ATTR(RBF, OZ_MATVEC);
+    PLS_OZ_ATTR(LINEAR, OZ_PRECOMPUTE); PLS_OZ_ATTR(POLYNOMIAL, OZ_PRECOMPUTE); PLS_OZ_ATTR(RBF, OZ_PRECOMPUTE);
+    PLS_OZ_ATTR(LINEAR, OZ_PREDICT); PLS_OZ_ATTR(POLYNOMIAL, OZ_PREDICT); PLS_OZ_ATTR(RBF, OZ_PREDICT);
+#undef PLS_OZ_ATTR
+}
+
+// One persistent CTA per SM (the 512-column TMEM allocation admits one per SM anyway).
+template <int KT, int MODE>
+void oz_launch(int ntiles, cudaStream_t s, const OzOperand &ra, const OzOperand &cb, const int2 *tiles, int tilesI,
+               const double *qv, const double *na, const double *nb_, const double *p, KParams<double> kp, double invC,
+               const double *scal, int64_t m1, int band0, int band1, double *Ypart, int64_t band_rows, double *Qc,
+               int T_tiles, const int *ctrl) {
+    if (ntiles <= 0) return;
+    const int grid = std::min(ntiles, num_sms());
+    k_tile_ozaki<KT, kOzS, MODE><<<grid, OzC::THREADS, OzC::SMEM_BYTES, s>>>(
+        ra.ta, cb.tb, ra.nk, tiles, ntiles, tilesI, ra.sc, cb.sc, qv, na, nb_, p, kp, invC, scal, m1, band0, band1,
+        Ypart, band_rows, Qc, T_tiles, ctrl);
+    PLS_CHECK_LAUNCH();
+}
+
+template <int MODE, typename... Args>
+void oz_dispatch(int kernel, Args &&...args) {
+    switch (kernel) {
+        case LINEAR: oz_launch<LINEAR, MODE>(args...); break;
+        case POLYNOMIAL: oz_launch<POLYNOMIAL, MODE>(args...); break;
+        default: oz_launch<RBF, MODE>(args...);
+    }
+}
+
+template <typename T>
+bool launch_oz(Ctx<T> &c, const T *pfull, int b0, int b1, int64_t brows, bool precompute) {
+    if constexpr (std::is_same<T, double>::value) {
+        if (!c.oz) return false;
+        const Geometry &g = c.g;
+        if (precompute)
+            oz_dispatch<OZ_PRECOMPUTE>(c.kp.kernel, c.ntiles, c.s, c.ozx, c.ozx, c.tiles, 0, c.q, c.nrm, c.nrm,
+                                       static_cast<const double *>(nullptr), c.kp, c.invC, c.scal, g.m1, g.band0,
+                                       g.band1, static_cast<double *>(nullptr), g.nb, c.Qc, c.packed ? -1 : g.T,
+                                       static_cast<const int *>(nullptr));
+        else
+            oz_dispatch<OZ_MATVEC>(c.kp.kernel, c.ntiles, c.s, c.ozx, c.ozx, c.tiles, 0, c.q, c.nrm, c.nrm, pfull, c.kp,
+                                   c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows, static_cast<double *>(nullptr), g.T,
+                                   c.cur_ctrl);
+        ++c.launches;
+        return true;
+    }
+    return false;
+}
+
 template <typename T>
 bool launch_tc(Ctx<T> &c, const T *pfull, int b0, int b1, int64_t brows) {
     if constexpr (std::is_same<T, float>::value) {
@@ -473,6 +584,8 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
     if (c.circ) PLS_CUDA(cudaMemsetAsync(c.Ypart, 0, static_cast<size_t>(nslots) * g.mpad * sizeof(T), c.s));
     if (c.tc) {
         launch_tc<T>(c, pfull, b0, b1, brows);
+    } else if (launch_oz<T>(c, pfull, b0, b1, brows, false)) {
+        // fp64 on the int8 tensor cores
     } else {
         const size_t sm = Engine<T>::SMEM_BYTES;
         switch (c.kp.kernel) {
@@ -509,6 +622,7 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
 template <typename T>
 void launch_precompute(Ctx<T> &c) {
     if (c.tc && launch_tc_precompute<T>(c)) return;
+    if (launch_oz<T>(c, static_cast<const T *>(nullptr), 0, 0, 0, true)) return;
     const Geometry &g = c.g;
     const size_t sm = Engine<T>::SMEM_BYTES;
     switch (c.kp.kernel) {
@@ -578,6 +692,13 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.ops = make_ops(c.Xt, g.mpad, c.Xt, g.mpad, g.ld);
     c.tc = std::is_same<T, float>::value && o.fp32_engine == 0;
     if (c.tc) setup_tc<T>(c, A, Xs, pb.m, pb.d);
+    if constexpr (std::is_same<T, double>::value) {
+        c.oz = o.fp64_engine == PLSSVM_FP64_OZAKI;
+        if (c.oz) {
+            c.ozx = oz_prepare(A, c.Xt, g.mpad, g.dpad, pb.d, c.s, c.launches);
+            oz_set_attrs();
+        }
+    }
     PLS_CUDA(cudaEventRecord(e_tr, c.s));
     c.q = A.alloc<T>(g.mpad);
     c.nrm = A.alloc<T>(g.mpad);
@@ -1045,9 +1166,23 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
                                      static_cast<const int *>(nullptr));
         }
     }
+    bool oz = false;
+    if constexpr (std::is_same<T, double>::value) {
+        oz = o.fp64_engine == PLSSVM_FP64_OZAKI;
+        if (oz) {  // fp64 on the int8 tensor cores: test points = row operand, training points = columns
+            const OzOperand oz_z = oz_prepare(A, Zl, zrows, dpad, d, s, launches);
+            const OzOperand oz_x = oz_prepare(A, Xl, xrows, dpad, d, s, launches);
+            oz_set_attrs();
+            PLS_CUDA(cudaEventRecord(e0, s));
+            oz_dispatch<OZ_PREDICT>(pb.kernel, tilesI * tilesJ, s, oz_z, oz_x, static_cast<const int2 *>(nullptr),
+                                    tilesI, static_cast<const double *>(nullptr), nz, nx, alpha, kp, 0.0,
+                                    static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,
+                                    static_cast<double *>(nullptr), 0, static_cast<const int *>(nullptr));
+        }
+    }
     const Ops<T> pops = make_ops(Zl, zrows, Xl, xrows, EN::kPointMajor ? dpad : L);
-    if (!tc) PLS_CUDA(cudaEventRecord(e0, s));
-    if (!tc) switch (pb.kernel) {
+    if (!tc && !oz) PLS_CUDA(cudaEventRecord(e0, s));
+    if (!tc && !oz) switch (pb.kernel) {
         case LINEAR:
             k_predict_tiles<LINEAR, T><<<grid, Engine<T>::THREADS, sm, s>>>(pops, npad, dpad, nz, nx, alpha, kp, tilesI,
                                                                   Fpart);

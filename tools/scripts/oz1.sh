@@ -1,0 +1,7 @@
+set -x
+timeout 120 python tools/run_matvec.py --config C0 --compare --repeats 2
+timeout 120 python tools/run_matvec.py --config C1 --m 1000 --d 100 --compare --repeats 2
+timeout 120 python tools/run_matvec.py --config C1 --m 1000 --d 100 --kernel 0 --compare --repeats 2
+timeout 120 python tools/run_matvec.py --config C1 --m 1000 --d 100 --kernel 1 --compare --repeats 2
+timeout 180 python tools/run_matvec.py --config C1 --compare --repeats 5
+timeout 300 python tools/run_matvec.py --config C2 --compare --repeats 3
