@@ -92,14 +92,19 @@ typedef struct {
                                 3xTF32 split) [0]; 1 = CUDA-core FFMA tiles */
     int32_t linear_w;        /* predict with the linear kernel through w = sum_i alpha_i x_i (Eq. 15,
                                 O((m+n)d)) [1]; 0 = evaluate the kernel matrix like the other kernels */
-    int32_t fp64_engine;     /* fp64 pairwise contraction (implicit Q~p, cached precompute, predict):
-                                PLSSVM_FP64_OZAKI = int8 tensor cores (tcgen05 kind::i8) on an exact
-                                8-digit split of each point, digit products summed exactly in int32
-                                and combined in fp64 [default]; PLSSVM_FP64_DMMA = fp64 DMMA tensor
-                                cores (mma.sync f64) */
+    int32_t fp64_engine;     /* plssvm_fp64_engine_t: fp64 pairwise contraction of the implicit Q~p, the
+                                cached precompute and predict [AUTO] */
 } plssvm_options_t;
 
-typedef enum { PLSSVM_FP64_OZAKI = 0, PLSSVM_FP64_DMMA = 1 } plssvm_fp64_engine_t;
+/* fp64 contraction engines.
+ *  OZAKI: int8 tensor cores (tcgen05 kind::i8, 2-SM UMMA) on an EXACT split of every point into
+ *         8 int8 digits times a power of two (x = 2^E sum_a D_a 2^-7a); digit products summed
+ *         exactly in int32, combined in fp64.  Error of x_i.x_j <~ d 2^-56 ||x_i||_inf ||x_j||_inf
+ *         (an fp64-GEMM-type bound weighted by the row maxima instead of |x_ik||x_jk|).
+ *  DMMA:  fp64 tensor cores (mma.sync f64, error <~ d u sum_k |x_ik||x_jk|).
+ *  AUTO:  OZAKI unless some point has max_k |x_ik| > 64 * rms_k(x_ik) (a peaked row whose small
+ *         features would lose relative precision under the row-max scaling), then DMMA. */
+typedef enum { PLSSVM_FP64_AUTO = 0, PLSSVM_FP64_OZAKI = 1, PLSSVM_FP64_DMMA = 2 } plssvm_fp64_engine_t;
 
 /* Statistics of one training call (all times are device-event seconds). */
 typedef struct {
@@ -116,6 +121,8 @@ typedef struct {
     int64_t bytes_per_gpu;           /* device bytes allocated by this call on this GPU */
     int64_t gpu_launches;            /* kernels launched by this call (this rank) */
     int64_t launches_in_cg;          /* of which inside the CG loop */
+    int32_t fp64_engine_used;        /* PLSSVM_FP64_OZAKI or _DMMA for fp64 calls, 0 for fp32 */
+    int32_t reserved0;
 } plssvm_stats_t;
 
 PLSSVM_API void plssvm_default_options(plssvm_options_t *opts);

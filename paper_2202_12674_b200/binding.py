@@ -17,7 +17,7 @@ from . import _build
 LINEAR, POLYNOMIAL, RBF = 0, 1, 2
 F64, F32 = 0, 1
 MODE_AUTO, MODE_IMPLICIT, MODE_CACHED, MODE_LOWRANK = 0, 1, 2, 3
-FP64_OZAKI, FP64_DMMA = 0, 1
+FP64_AUTO, FP64_OZAKI, FP64_DMMA = 0, 1, 2
 OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED = range(8)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
                 6: "E_NUMERICAL", 7: "W_NOT_CONVERGED"}
@@ -42,7 +42,8 @@ class plssvm_stats_t(ct.Structure):
                 ("t_precompute", ct.c_double),
                 ("t_cg", ct.c_double), ("t_bias_d2h", ct.c_double), ("t_total", ct.c_double),
                 ("t_matvec", ct.c_double), ("t_matvec_min", ct.c_double), ("bytes_per_gpu", ct.c_int64),
-                ("gpu_launches", ct.c_int64), ("launches_in_cg", ct.c_int64)]
+                ("gpu_launches", ct.c_int64), ("launches_in_cg", ct.c_int64), ("fp64_engine_used", ct.c_int32),
+                ("reserved0", ct.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

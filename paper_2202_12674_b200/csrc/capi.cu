@@ -114,7 +114,7 @@ void plssvm_default_options(plssvm_options_t *o) {
     o->cache_budget_bytes = 0;
     o->fp32_engine = 0;
     o->linear_w = 1;
-    o->fp64_engine = PLSSVM_FP64_OZAKI;
+    o->fp64_engine = PLSSVM_FP64_AUTO;
 }
 
 int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtype, int kernel, double gamma, int degree,

@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -142,17 +143,16 @@ CUtensorMap make_tmap_2d(void *base, int elem_bytes, int64_t inner, int64_t oute
     return m;
 }
 
-// Digit planes D[planes][rows][dpad8] (int8) as a 3-D map; one box = 32 features x box_rows rows
-// x all planes, 32-byte swizzle (ozaki_engine.cuh).
-CUtensorMap make_tmap_digits(int8_t *base, int64_t dpad8, int64_t rows, int planes, uint32_t box_rows) {
+// Pre-swizzled digit blocks (ozaki_engine.cuh k_ozaki_split) as a 2-D byte array of 128-byte rows;
+// one box = box_rows rows (a whole digit-plane group of one slab block), no swizzle.
+CUtensorMap make_tmap_digit_blocks(int8_t *base, int64_t bytes, uint32_t box_rows) {
     CUtensorMap m;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(dpad8), static_cast<cuuint64_t>(rows),
-                                static_cast<cuuint64_t>(planes)};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(dpad8), static_cast<cuuint64_t>(rows * dpad8)};
-    const cuuint32_t box[3] = {32u, box_rows, static_cast<cuuint32_t>(planes)};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+    const cuuint64_t dims[2] = {128u, static_cast<cuuint64_t>(bytes / 128)};
+    const cuuint64_t strides[1] = {128u};
+    const cuuint32_t box[2] = {128u, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled (digits) failed: " + std::to_string(int(r)));
     return m;
@@ -236,12 +236,14 @@ std::vector<int2> circulant_tiles(const Geometry &g, int nsub) {
     return t;
 }
 
-// Digit planes of a point-major padded fp64 array: TMA maps for the row (128) and column (64)
-// operand roles.
+// Digit blocks of a point-major padded fp64 array (ozaki_engine.cuh): TMA maps whose boxes carry
+// the first 4 (pass 1) or all 8 (pass 0) planes of a slab block, in the row-operand layout DA
+// (128 points) and / or the column-operand layout DB (64 points).
 struct OzOperand {
-    int8_t *D = nullptr;
+    int8_t *DA = nullptr, *DB = nullptr;
     double *sc = nullptr;
-    CUtensorMap ta, tb;
+    CUtensorMap t4, t8;  // DA boxes
+    CUtensorMap h4, h8;  // DB boxes
     int nk = 0;
 };
 
@@ -285,6 +287,9 @@ struct Ctx {
     int *ctrl = nullptr;             // device CG control block (kernels.cuh Ctl)
     bool oz = false;                 // fp64: int8 tensor-core digit engine (ozaki_engine.cuh)
     OzOperand ozx;
+    int2 *oz_pt = nullptr;            // 2-SM pair-tiles (ozaki_engine.cuh)
+    int *oz_pk = nullptr;
+    int oz_npt = 0;
     const int *cur_ctrl = nullptr;   // ctrl inside the CG loop (loop kernels early-exit when done)
 };
 
@@ -414,19 +419,52 @@ int num_sms() {
     return n;
 }
 
-OzOperand oz_prepare(Arena &A, const double *Xp, int64_t rows, int64_t dpad, int64_t d, cudaStream_t s,
-                     int64_t &launches) {
+OzOperand oz_prepare(Arena &A, const double *Xp, int64_t rows, int64_t dpad, int64_t d, bool row_role, bool col_role,
+                     cudaStream_t s, int64_t &launches) {
     OzOperand o;
     const int64_t d8 = round_up(d, OzC::BK);
-    o.D = A.alloc<int8_t>(kOzS * rows * d8);
+    const int64_t bytes = kOzS * rows * d8;
+    if (row_role) o.DA = A.alloc<int8_t>(bytes);
+    if (col_role) o.DB = A.alloc<int8_t>(bytes);
     o.sc = A.alloc<double>(rows);
-    k_ozaki_split<kOzS><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, s>>>(Xp, rows, dpad, d8, o.D, o.sc);
+    k_ozaki_split<kOzS><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, s>>>(Xp, rows, dpad, d8, o.DA, o.DB,
+                                                                                       o.sc);
     PLS_CHECK_LAUNCH();
     ++launches;
-    o.ta = make_tmap_digits(o.D, d8, rows, kOzS, kTile);
-    o.tb = make_tmap_digits(o.D, d8, rows, kOzS, OzC::TN);
+    if (row_role) {
+        o.t4 = make_tmap_digit_blocks(o.DA, bytes, OzC::LV * 32);
+        o.t8 = make_tmap_digit_blocks(o.DA, bytes, kOzS * 32);
+    }
+    if (col_role) {
+        o.h4 = make_tmap_digit_blocks(o.DB, bytes, OzC::LV * 16);
+        o.h8 = make_tmap_digit_blocks(o.DB, bytes, kOzS * 16);
+    }
     o.nk = static_cast<int>(d8 / OzC::BK);
     return o;
+}
+
+// fp64 engine choice (plssvm.h plssvm_fp64_engine_t): OZAKI, DMMA, or AUTO = OZAKI unless a row
+// of any operand array peaks above kOzPeakMax x its RMS.
+constexpr double kOzPeakMax = 64.0;
+bool oz_choose(int engine, std::initializer_list<const double *> arrays, std::initializer_list<int64_t> rows,
+               int64_t dpad, int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
+    if (engine == PLSSVM_FP64_DMMA) return false;
+    if (engine == PLSSVM_FP64_OZAKI) return true;
+    unsigned *bits = A.alloc<unsigned>(1);
+    PLS_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned), s));
+    auto r = rows.begin();
+    for (const double *X : arrays) {
+        const int64_t n = *r++;
+        k_row_peak<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(X, n, dpad, d, bits);
+        PLS_CHECK_LAUNCH();
+        ++launches;
+    }
+    unsigned hb = 0;
+    PLS_CUDA(cudaMemcpyAsync(&hb, bits, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    PLS_CUDA(cudaStreamSynchronize(s));
+    float peak;
+    std::memcpy(&peak, &hb, sizeof(float));
+    return peak <= kOzPeakMax;
 }
 
 void oz_set_attrs() {
@@ -439,18 +477,51 @@ void oz_set_attrs() {
 #undef PLS_OZ_ATTR
 }
 
-// One persistent CTA per SM (the 512-column TMEM allocation admits one per SM anyway).
+// Experiments only (PLSSVM_OZ_DEBUG, results are wrong when set): 1 = no epilogue, 2 = no TMA,
+// 4 = no MMAs.  0 in production.
+int oz_debug_flags() {
+    static int f = [] {
+        const char *e = std::getenv("PLSSVM_OZ_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return f;
+}
+
+// One persistent CTA per SM (the 512-column TMEM allocation admits one per SM anyway), in
+// clusters of 2 (cta_group::2): the grid is an even number of CTAs, at most the SM count.
 template <int KT, int MODE>
-void oz_launch(int ntiles, cudaStream_t s, const OzOperand &ra, const OzOperand &cb, const int2 *tiles, int tilesI,
-               const double *qv, const double *na, const double *nb_, const double *p, KParams<double> kp, double invC,
-               const double *scal, int64_t m1, int band0, int band1, double *Ypart, int64_t band_rows, double *Qc,
-               int T_tiles, const int *ctrl) {
-    if (ntiles <= 0) return;
-    const int grid = std::min(ntiles, num_sms());
+void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb, const int2 *ptiles, const int *pk,
+               int rowsI, const double *qv, const double *na, const double *nb_, const double *p, KParams<double> kp,
+               double invC, const double *scal, int64_t m1, int band0, int band1, double *Ypart, int64_t band_rows,
+               double *Qc, int T_tiles, const int *ctrl) {
+    if (npt <= 0) return;
+    const int grid = 2 * std::min(npt, num_sms() / 2);
     k_tile_ozaki<KT, kOzS, MODE><<<grid, OzC::THREADS, OzC::SMEM_BYTES, s>>>(
-        ra.ta, cb.tb, ra.nk, tiles, ntiles, tilesI, ra.sc, cb.sc, qv, na, nb_, p, kp, invC, scal, m1, band0, band1,
-        Ypart, band_rows, Qc, T_tiles, ctrl);
+        ra.t4, ra.t8, cb.h4, cb.h8, ra.nk, ptiles, pk, npt, rowsI, ra.sc, cb.sc, qv, na, nb_, p, kp, invC, scal, m1,
+        band0, band1, Ypart, band_rows, Qc, T_tiles, ctrl, oz_debug_flags());
     PLS_CHECK_LAUNCH();
+}
+
+// Pair-tiles of the 2-SM kernel from a tile list (I, J) (NSUB = 1): row blocks b0, b0 + 2, ...
+// of [b0, b1) paired with the next one; entry (I0 | use << 24, J) where use bit r marks (I0 + r, J)
+// as a listed tile.  pk[2 t + r] = that tile's ordinal in the list (packed cached layout), -1
+// if unused.  Raster: groups of 4 row pairs, column blocks slowest inside a group (L2 reuse).
+void oz_pair_tiles(const std::vector<int2> &tl, int b0, int b1, int T, std::vector<int2> &pt, std::vector<int> &pk) {
+    std::vector<int> ord(static_cast<size_t>(b1 - b0) * T, -1);
+    for (size_t k = 0; k < tl.size(); ++k) ord[static_cast<size_t>(tl[k].x - b0) * T + tl[k].y] = static_cast<int>(k);
+    pt.clear();
+    pk.clear();
+    for (int P0 = b0; P0 < b1; P0 += 8)
+        for (int J = 0; J < T; ++J)
+            for (int I0 = P0; I0 < std::min(P0 + 8, b1); I0 += 2) {
+                const int o0 = ord[static_cast<size_t>(I0 - b0) * T + J];
+                const int o1 = (I0 + 1 < b1) ? ord[static_cast<size_t>(I0 + 1 - b0) * T + J] : -1;
+                if (o0 < 0 && o1 < 0) continue;
+                const int use = (o0 >= 0 ? 1 : 0) | (o1 >= 0 ? 2 : 0);
+                pt.push_back(make_int2(I0 | (use << 24), J));
+                pk.push_back(o0);
+                pk.push_back(o1);
+            }
 }
 
 template <int MODE, typename... Args>
@@ -468,18 +539,33 @@ bool launch_oz(Ctx<T> &c, const T *pfull, int b0, int b1, int64_t brows, bool pr
         if (!c.oz) return false;
         const Geometry &g = c.g;
         if (precompute)
-            oz_dispatch<OZ_PRECOMPUTE>(c.kp.kernel, c.ntiles, c.s, c.ozx, c.ozx, c.tiles, 0, c.q, c.nrm, c.nrm,
+            oz_dispatch<OZ_PRECOMPUTE>(c.kp.kernel, c.oz_npt, c.s, c.ozx, c.ozx, c.oz_pt, c.oz_pk, 0, c.q, c.nrm, c.nrm,
                                        static_cast<const double *>(nullptr), c.kp, c.invC, c.scal, g.m1, g.band0,
                                        g.band1, static_cast<double *>(nullptr), g.nb, c.Qc, c.packed ? -1 : g.T,
                                        static_cast<const int *>(nullptr));
         else
-            oz_dispatch<OZ_MATVEC>(c.kp.kernel, c.ntiles, c.s, c.ozx, c.ozx, c.tiles, 0, c.q, c.nrm, c.nrm, pfull, c.kp,
-                                   c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows, static_cast<double *>(nullptr), g.T,
-                                   c.cur_ctrl);
+            oz_dispatch<OZ_MATVEC>(c.kp.kernel, c.oz_npt, c.s, c.ozx, c.ozx, c.oz_pt, c.oz_pk, 0, c.q, c.nrm, c.nrm,
+                                   pfull, c.kp, c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows,
+                                   static_cast<double *>(nullptr), g.T, c.cur_ctrl);
         ++c.launches;
         return true;
     }
     return false;
+}
+
+// (Re)build the 2-SM pair-tile list from the current single-tile list.
+template <typename T>
+void oz_build_pairs(Ctx<T> &c, Arena &A, const std::vector<int2> &tl, int b0, int b1) {
+    if (!c.oz) return;
+    std::vector<int2> pt;
+    std::vector<int> pk;
+    oz_pair_tiles(tl, b0, b1, c.g.T, pt, pk);
+    c.oz_npt = static_cast<int>(pt.size());
+    c.oz_pt = A.alloc<int2>(c.oz_npt);
+    c.oz_pk = A.alloc<int>(2 * c.oz_npt);
+    PLS_CUDA(cudaMemcpyAsync(c.oz_pt, pt.data(), pt.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
+    PLS_CUDA(cudaMemcpyAsync(c.oz_pk, pk.data(), pk.size() * sizeof(int), cudaMemcpyHostToDevice, c.s));
+    PLS_CUDA(cudaStreamSynchronize(c.s));
 }
 
 template <typename T>
@@ -693,9 +779,9 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.tc = std::is_same<T, float>::value && o.fp32_engine == 0;
     if (c.tc) setup_tc<T>(c, A, Xs, pb.m, pb.d);
     if constexpr (std::is_same<T, double>::value) {
-        c.oz = o.fp64_engine == PLSSVM_FP64_OZAKI;
+        c.oz = oz_choose(o.fp64_engine, {c.Xt}, {g.mpad}, g.dpad, pb.d, A, c.s, c.launches);
         if (c.oz) {
-            c.ozx = oz_prepare(A, c.Xt, g.mpad, g.dpad, pb.d, c.s, c.launches);
+            c.ozx = oz_prepare(A, c.Xt, g.mpad, g.dpad, pb.d, true, true, c.s, c.launches);
             oz_set_attrs();
         }
     }
@@ -713,11 +799,12 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.partials = A.alloc<T>(kVecBlocks);
     c.counter = A.alloc<unsigned>(1);
     PLS_CUDA(cudaMemsetAsync(c.counter, 0, sizeof(unsigned), c.s));
-    std::vector<int2> tl = band_tiles(g, Engine<T>::NSUB);
+    std::vector<int2> tl = band_tiles(g, c.oz ? OzC::NSUB : Engine<T>::NSUB);
     c.ntiles = static_cast<int>(tl.size());
     c.tiles = A.alloc<int2>(c.ntiles);
     PLS_CUDA(cudaMemcpyAsync(c.tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
     PLS_CUDA(cudaStreamSynchronize(c.s));  // tl goes out of scope
+    oz_build_pairs<T>(c, A, tl, g.band0, g.band1);
     set_smem_attrs<T>();
 }
 
@@ -726,7 +813,7 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
 template <typename T>
 void configure_product(Ctx<T> &c, Arena &A) {
     const Geometry &g = c.g;
-    c.nsub_eff = c.tc ? 1 : Engine<T>::NSUB;
+    c.nsub_eff = c.tc ? 1 : c.oz ? OzC::NSUB : Engine<T>::NSUB;
     c.nsplit = gemv_splits(g);
     c.circ = g.P > 1 && !c.lowrank && (!c.cached || c.packed) && comm_has_reduce_scatter(c.comm);
     if (c.lowrank) {
@@ -747,6 +834,7 @@ void configure_product(Ctx<T> &c, Arena &A) {
         c.tiles = A.alloc<int2>(c.ntiles);
         PLS_CUDA(cudaMemcpyAsync(c.tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
         PLS_CUDA(cudaStreamSynchronize(c.s));
+        oz_build_pairs<T>(c, A, tl, g.band0, g.band1);
         c.Ypart = A.alloc<T>(static_cast<int64_t>(g.T) * c.nsub_eff * g.mpad);
         c.yfull = A.alloc<T>(g.mpad);
         c.ysc = A.alloc<T>(g.nb);
@@ -1007,6 +1095,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         st->bytes_per_gpu = A.bytes;
         st->gpu_launches = c.launches;
         st->launches_in_cg = c.launches_cg;
+        st->fp64_engine_used = std::is_same<T, double>::value ? (c.oz ? PLSSVM_FP64_OZAKI : PLSSVM_FP64_DMMA) : 0;
     }
     return status;
 }
@@ -1131,7 +1220,11 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
         launches += 2;
     }
     const bool tc = std::is_same<T, float>::value && o.fp32_engine == 0;
-    const int tilesI = static_cast<int>(npad / kTile), tilesJ = static_cast<int>(mpad / (tc ? kTile : EN::TN));
+    bool oz64 = false;
+    if constexpr (std::is_same<T, double>::value)
+        oz64 = oz_choose(o.fp64_engine, {Zl, Xl}, {zrows, xrows}, dpad, d, A, s, launches);
+    const int tilesI = static_cast<int>(npad / kTile),
+              tilesJ = static_cast<int>(mpad / (tc ? kTile : oz64 ? OzC::TN : EN::TN));
     T *Fpart = A.alloc<T>(static_cast<int64_t>(tilesJ) * npad);
     set_smem_attrs<T>();
     const size_t sm = EN::SMEM_BYTES;
@@ -1166,16 +1259,16 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
                                      static_cast<const int *>(nullptr));
         }
     }
-    bool oz = false;
+    const bool oz = oz64;
     if constexpr (std::is_same<T, double>::value) {
-        oz = o.fp64_engine == PLSSVM_FP64_OZAKI;
         if (oz) {  // fp64 on the int8 tensor cores: test points = row operand, training points = columns
-            const OzOperand oz_z = oz_prepare(A, Zl, zrows, dpad, d, s, launches);
-            const OzOperand oz_x = oz_prepare(A, Xl, xrows, dpad, d, s, launches);
+            const OzOperand oz_z = oz_prepare(A, Zl, zrows, dpad, d, true, false, s, launches);
+            const OzOperand oz_x = oz_prepare(A, Xl, xrows, dpad, d, false, true, s, launches);
             oz_set_attrs();
             PLS_CUDA(cudaEventRecord(e0, s));
-            oz_dispatch<OZ_PREDICT>(pb.kernel, tilesI * tilesJ, s, oz_z, oz_x, static_cast<const int2 *>(nullptr),
-                                    tilesI, static_cast<const double *>(nullptr), nz, nx, alpha, kp, 0.0,
+            oz_dispatch<OZ_PREDICT>(pb.kernel, ((tilesI + 1) / 2) * tilesJ, s, oz_z, oz_x,
+                                    static_cast<const int2 *>(nullptr), static_cast<const int *>(nullptr), tilesI,
+                                    static_cast<const double *>(nullptr), nz, nx, alpha, kp, 0.0,
                                     static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,
                                     static_cast<double *>(nullptr), 0, static_cast<const int *>(nullptr));
         }

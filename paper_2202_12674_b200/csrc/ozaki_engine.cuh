@@ -15,17 +15,26 @@
 // (Horner over l, one rounding per level), so the result is an fp64 dot product with a
 // different (shorter) rounding history, not a lower-precision one.
 //
-// Tile = 128 rows x 64 columns (UMMA M = 128, N = 64): S level accumulators of 64 int32 columns
-// each fill the 512-column TMEM (S = 8).  Persistent CTAs (one per SM), warp-specialised:
-//   warp 8 (one lane) : TMA producer -- per 32-feature slab ONE 3-D box per operand brings all S
-//                       digit planes (32 B x 128 rows x S, SWIZZLE_32B): S x 6 KiB per stage
-//   warp 9 (one lane) : TMEM owner + MMA issuer -- S(S+1)/2 UMMAs (K = 32) per slab into the
-//                       level accumulators; tcgen05.commit frees the stage / signals the tile
-//   warps 0-7         : epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows) and columns
-//                       32(w/4).. of every level (tcgen05.ld 32x32b.x32), Horner-combines them
-//                       in fp64, releases the accumulator (the MMA warp starts the next tile),
-//                       then applies the kernel function / Eq. 16 corrections and reduces.
-// Slot conventions are those of k_matvec_implicit (Engine<double>, TN = 64, NSUB = 2).
+// Tile = 128 x 128 per CTA, computed by CTA pairs as 256 x 128 UMMAs (cta_group::2, below).
+// The 8 level accumulators of a tile need 8 x 128 int32
+// TMEM columns, twice the 512 available, so a tile runs in TWO PASSES over the features:
+// pass 0 accumulates levels 4-7 (26 digit pairs, digit planes 0-7), pass 1 levels 0-3 (10
+// pairs, planes 0-3), each in 4 x 128 TMEM columns.  N = 128 halves the shared-memory operand
+// bytes per MMA cycle of an N = 64 tile (the SS-mode UMMA reads A and B from smem each time:
+// 128 B/clk at N = 128 = the smem bandwidth, 192 B/clk at N = 64 -- measured: tc pipe 84 %
+// busy, imma 46 % with 128 x 64 tiles), at the same L2 traffic per output element.
+// Persistent CTA pairs (one CTA per SM), warp-specialised:
+//   warp 8 (one lane) : TMA producer -- per 32-feature slab ONE 3-D box per operand brings the
+//                       pass's digit planes (32 B x 128 rows x 4|8 planes, SWIZZLE_32B)
+//   warp 9 (one lane) : TMEM owner; in the leader CTA the MMA issuer -- per slab the pass's digit pairs (K = 32 UMMAs)
+//                       into the level accumulators; tcgen05.commit frees the stage / signals
+//                       the pass
+//   warps 0-7         : epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows), columns
+//                       64(w/4).. of every level (tcgen05.ld 32x32b.x8), Horner-combines them in
+//                       fp64 (pass 0 -> w in fp32; pass 1 -> v + 2^-28 w, then the kernel
+//                       function / Eq. 16 corrections and the row / column contributions, 8
+//                       columns at a time), releasing the accumulators after each pass.
+// Slot conventions: those of k_matvec_implicit with 128-wide column blocks (NSUB = 1).
 #pragma once
 #include <cuda.h>
 
@@ -37,36 +46,29 @@ enum OzMode : int { OZ_MATVEC = 0, OZ_PRECOMPUTE = 1, OZ_PREDICT = 2 };
 
 template <int S>
 struct Oz {
+    static_assert(S == 8, "two passes of 4 levels");
     static constexpr int BK = 32;                                  // int8 features per slab (32 B rows)
-    static constexpr int TN = 64;                                  // tile columns (UMMA N)
-    static constexpr int NSUB = kTile / TN;                        // = Engine<double>::NSUB
+    static constexpr int TN = 128;                                 // tile columns (UMMA N)
+    static constexpr int NSUB = kTile / TN;                        // 1
+    static constexpr int LV = 4;                                   // levels per pass
     static constexpr int STAGES = 4;
-    static constexpr uint32_t A_PLANE = kTile * BK;                // 4 KiB per digit plane
-    static constexpr uint32_t B_PLANE = TN * BK;                   // 2 KiB
-    static constexpr uint32_t STAGE_BYTES = S * (A_PLANE + B_PLANE);
+    static constexpr uint32_t PLANE = kTile * BK;                  // 4 KiB: one A digit plane (B half: 2 KiB)
+    static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: 8 planes of A and of the B half
     static constexpr int EPI_WARPS = 8;
     static constexpr int THREADS = (EPI_WARPS + 2) * 32;
-    static constexpr int PAIRS = S * (S + 1) / 2;
     static constexpr int TMEM_COLS = 512;
-    static_assert(S * TN <= TMEM_COLS, "level accumulators must fit TMEM");
-    // misc: barriers (256 B) + column data 4 x 64 doubles + row partials 2 x 128 + col partials 4 x 64
+    static_assert(LV * TN <= TMEM_COLS, "a pass's level accumulators must fit TMEM");
+    // misc: barriers (256 B) + column data 4 x 128 doubles + row partials 2 x 128 + col partials 4 x 128
     static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN) * 8;
     static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + MISC;
-    // instruction descriptor: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 64, M = 128
-    static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TN >> 3) << 17) | ((128u >> 4) << 24);
+    // instruction descriptor: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 128, M = 256 (2 SMs)
+    static constexpr uint32_t IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TN >> 3) << 17) | ((256u >> 4) << 24);
 };
 
 // K-major operand in 32-byte swizzle atoms (8 rows x 32 B): LBO 1 (unused), SBO = 256 B, type 6.
 __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
     return (uint64_t((saddr >> 4) & 0x3FFFu)) | (uint64_t(1) << 16) | (uint64_t(256 >> 4) << 32) | (uint64_t(1) << 46) |
            (uint64_t(6) << 61);
-}
-template <int S>
-__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(Oz<S>::IDESC), "r"(acc));
 }
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y, int z) {
     asm volatile(
@@ -85,9 +87,27 @@ __device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32
           "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8_issue(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+
+// Exact int32 -> fp64 without the (slow, XU-pipe) I2F.F64: 2^52 + (r + 2^31) assembled from
+// bits, minus 2^52 + 2^31 -- one LOP3 + one DADD.
+__device__ __forceinline__ double i2d_exact(uint32_t r) {
+    return __hiloint2double(0x43300000, static_cast<int>(r ^ 0x80000000u)) - 4503601774854144.0;
 }
 
 // Sum of v[0..31] over the 32 lanes in 31 shuffles: afterwards lane l holds the total of
@@ -106,12 +126,43 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
     return v[0];
 }
 
-// Exact digit split of the point-major padded fp64 array Xp[rows][dpad] into S int8 planes
-// Dg[S][rows][dpad8] (dpad8 = multiple of 32, zero beyond dpad) and the row scales
-// sc_i = 2^{E_i - 7}.  One warp per row; 4 features per lane per step (char4 stores).
+// AUTO engine check: the largest row "peak" max_k |x_ik| / rms_k(x_ik) over the rows of a
+// point-major padded fp64 array (zero rows skipped), as float bits in *peak_bits (atomicMax on
+// the bits of a non-negative float orders like the value).  One warp per row.
+__global__ void k_row_peak(const double *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t d,
+                           unsigned *__restrict__ peak_bits) {
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= rows) return;
+    double mx = 0.0, ss = 0.0;
+    for (int64_t k = lane; k < d; k += 32) {
+        const double v = Xp[i * dpad + k];
+        mx = fmax(mx, fabs(v));
+        ss = fma(v, v, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    if (lane == 0 && ss > 0.0) {
+        const float r = static_cast<float>(mx / sqrt(ss / static_cast<double>(d)));
+        atomicMax(peak_bits, __float_as_uint(r));
+    }
+}
+
+// Exact digit split of the point-major padded fp64 array Xp[rows][dpad] (rows a multiple of
+// 128) into S int8 digit planes, stored PRE-SWIZZLED as the shared-memory images the UMMA reads:
+//   DA[rows/128][nk][S][128 x 32 B]  (row-operand role: 128-point blocks)
+//   DB[rows/64 ][nk][S][ 64 x 32 B]  (column-operand role: one CTA's half of a 2-SM B tile)
+// (nk = dpad8 / 32 feature slabs), each 32-byte row in the SWIZZLE_32B pattern (16-byte chunk
+// index XOR bit 2 of the row).  A stage of the tile kernel is then ONE contiguous block per
+// operand, moved by TMA in 128-byte rows with no swizzle (4x fewer, 4x larger requests than
+// a 32-byte-row box: the tile kernel was feed-bound with them).  Either pointer may be null.
+// Row scales sc_i = 2^{E_i - 7}.  One warp per row; 4 features per lane per step.
 template <int S>
 __global__ void k_ozaki_split(const double *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t dpad8,
-                              int8_t *__restrict__ Dg, double *__restrict__ sc) {
+                              int8_t *__restrict__ DA, int8_t *__restrict__ DB, double *__restrict__ sc) {
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= rows) return;
@@ -124,11 +175,18 @@ __global__ void k_ozaki_split(const double *__restrict__ Xp, int64_t rows, int64
     if (mx > 0.0) frexp(mx, &E);  // mx = f 2^E, f in [0.5, 1)  =>  |x_ik| < 2^E
     const double inv = ldexp(1.0, -E);
     if (lane == 0) sc[i] = ldexp(1.0, E - 7);
-    const int64_t plane = rows * dpad8;
+    const int64_t nk = dpad8 / 32;
+    const int r128 = static_cast<int>(i & 127), r64 = static_cast<int>(i & 63);
+    const int flip = (r128 >> 2) & 1;  // = (r64 >> 2) & 1
     for (int64_t k0 = 4 * lane; k0 < dpad8; k0 += 128) {
         double u[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) u[v] = (k0 + v < dpad) ? x[k0 + v] * inv : 0.0;  // |u| < 1, exact
+        const int64_t kb = k0 >> 5;
+        const int c = static_cast<int>(k0 & 31);
+        const int inrow = ((((c >> 4) ^ flip) << 4) | (c & 15));
+        int8_t *pa = DA ? DA + ((i >> 7) * nk + kb) * (S * 4096) + r128 * 32 + inrow : nullptr;
+        int8_t *pb = DB ? DB + ((i >> 6) * nk + kb) * (S * 2048) + r64 * 32 + inrow : nullptr;
 #pragma unroll
         for (int a = 0; a < S; ++a) {
             char4 dg;
@@ -140,134 +198,235 @@ __global__ void k_ozaki_split(const double *__restrict__ Xp, int64_t rows, int64
                 u[v] -= t;                        // exact
                 dv[v] = static_cast<signed char>(t);
             }
-            *reinterpret_cast<char4 *>(Dg + a * plane + i * dpad8 + k0) = dg;
+            if (pa) *reinterpret_cast<char4 *>(pa + a * 4096) = dg;
+            if (pb) *reinterpret_cast<char4 *>(pb + a * 2048) = dg;
         }
     }
 }
 
-// Persistent tile kernel.  Tiles: MATVEC / PRECOMPUTE take the (I, Jc) list of the DMMA engine
-// (Jc = 64-column sub-block); PREDICT enumerates tile t -> (t % tilesI, t / tilesI).
-//  OZ_MATVEC     : Q~ entries -> row sums Ypart[Jc] (rows of I), mirrored tiles also column sums
-//                  Ypart[I * NSUB] (rows of Jc) -- exactly k_matvec_implicit's slots
-//  OZ_PRECOMPUTE : Q~ entries -> cached tiled array Qc (packed: ordinal t / NSUB; else band rows,
-//                  with the mirrored transposed copy) -- k_precompute's layout
-//  OZ_PREDICT    : alpha_j k(z_i, x_j) -> Fpart[Jc][npad]
+__device__ __forceinline__ void tma_load_2d_2sm(void *dst, const CUtensorMap *map, uint32_t bar_cluster, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
+
+// ---- cluster helpers (CTA pair of a cta_group::2 MMA) ----------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA of this CTA's half of a 2-SM operand; completion bytes go to the leader CTA's barrier.
+__device__ __forceinline__ void tma_load_3d_2sm(void *dst, const CUtensorMap *map, uint32_t bar_cluster, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+template <int S>
+__device__ __forceinline__ void umma_i8_2sm(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(Oz<S>::IDESC2), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_2sm_mc(uint64_t *bar) {  // arrive on bar in both CTAs of the pair
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_addr(bar)),
+        "h"(uint16_t(3))
+        : "memory");
+}
+
+// Persistent 2-SM tile kernel (cluster of 2 CTAs, tcgen05 cta_group::2).  A CTA pair owns the
+// 256 x 128 pair-tile (row blocks I0, I0 + 1) x (column block J): CTA rank r stages the digit
+// planes of its row block I0 + r (A, 128 rows) and of HALF the column block (B, rows
+// J*128 + 64 r .. +63); the leader's single MMA thread issues M = 256, N = 128 UMMAs that read A
+// and B from both CTAs' shared memory and accumulate each CTA's 128 rows in its own TMEM.  Per SM
+// the MMA reads 6 KiB of operands per 64-cycle UMMA instead of 8 (A 4 KiB + half of B), and the
+// pair loads each B plane once -- the 1-SM kernel was bound by shared-memory bandwidth
+// (operand reads + TMA writes ~1.3x the 128 B/clk an SM has).
+// Pair-tiles: MATVEC / PRECOMPUTE take a list of int2 (I0 | use << 24, J), use bit r = tile
+// (I0 + r, J) is one of this rank's (others are computed and dropped: only the diagonal pair's
+// lower block and odd band ends); PREDICT enumerates t -> (2 (t % pairsI), t / pairsI).
+//  OZ_MATVEC     : Q~ entries -> row sums Ypart[J] (rows of I), mirrored tiles also column sums
+//                  Ypart[I] (rows of J) -- k_matvec_implicit's slots with 128-wide blocks
+//  OZ_PRECOMPUTE : Q~ entries -> cached tiled array Qc (packed: ordinal pk[2 t + r]; else band
+//                  rows, with the mirrored transposed copy) -- k_precompute's layout
+//  OZ_PREDICT    : alpha_j k(z_i, x_j) -> Fpart[J][npad]
+// ta4/ta8: maps over the pre-swizzled row-operand digits DA (boxes of 4 / 8 planes of a 128-point
+// slab block, 128-byte rows); tb4/tb8: the same over DB (64-point half blocks).
 template <int KT, int S, int MODE>
-__global__ void __launch_bounds__(Oz<S>::THREADS, 1)
-    k_tile_ozaki(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int nk,
-                 const int2 *__restrict__ tiles, int ntiles, int tilesI, const double *__restrict__ sca,
-                 const double *__restrict__ scb, const double *__restrict__ qv, const double *__restrict__ na,
-                 const double *__restrict__ nb_, const double *__restrict__ p, KParams<double> kp, double invC,
-                 const double *__restrict__ scal, int64_t m1, int band0, int band1, double *__restrict__ Ypart,
-                 int64_t band_rows, double *__restrict__ Qc, int T_tiles, const int *ctrl) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
+    k_tile_ozaki(const __grid_constant__ CUtensorMap ta4, const __grid_constant__ CUtensorMap ta8,
+                 const __grid_constant__ CUtensorMap tb4, const __grid_constant__ CUtensorMap tb8, int nk,
+                 const int2 *__restrict__ tiles, const int *__restrict__ pk, int ntiles, int rowsI,
+                 const double *__restrict__ sca, const double *__restrict__ scb, const double *__restrict__ qv,
+                 const double *__restrict__ na, const double *__restrict__ nb_, const double *__restrict__ p,
+                 KParams<double> kp, double invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
+                 double *__restrict__ Ypart, int64_t band_rows, double *__restrict__ Qc, int T_tiles, const int *ctrl,
+                 int dbg) {
     using O = Oz<S>;
-    if (cg_done(ctrl)) return;
+    constexpr int TN = O::TN, LV = O::LV;
+    if (cg_done(ctrl)) return;  // uniform across the cluster
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char *ring = base;
     unsigned char *misc = base + size_t(O::STAGES) * O::STAGE_BYTES;
-    uint64_t *full = reinterpret_cast<uint64_t *>(misc);  // [STAGES]
-    uint64_t *empty = full + O::STAGES;                   // [STAGES]
-    uint64_t *tfull = empty + O::STAGES;                  // accumulators ready
-    uint64_t *tempty = tfull + 1;                         // accumulators drained
+    uint64_t *full = reinterpret_cast<uint64_t *>(misc);  // [STAGES] (leader's are used)
+    uint64_t *empty = full + O::STAGES;                   // [STAGES] (each CTA's own)
+    uint64_t *tfull = empty + O::STAGES;                  // a pass's accumulators ready (each CTA)
+    uint64_t *tempty = tfull + 1;                         // a pass's accumulators drained (leader: 16 warps)
     uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(tempty + 1);
-    double *colsc = reinterpret_cast<double *>(misc + 256);  // [64]
-    double *colq = colsc + O::TN;                            // [64]
-    double *colp = colq + O::TN;                             // [64] (alpha for predict)
-    double *coln = colp + O::TN;                             // [64]
-    double *redr = coln + O::TN;                             // [2][128]
-    double *redc = redr + 2 * kTile;                         // [4][64]
+    double *colsc = reinterpret_cast<double *>(misc + 256);  // [128]
+    double *colq = colsc + TN;                               // [128]
+    double *colp = colq + TN;                                // [128] (alpha for predict)
+    double *coln = colp + TN;                                // [128]
+    double *redr = coln + TN;                                // [2][128]
+    double *redc = redr + 2 * kTile;                         // [4][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     if (warp == 8 && lane == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmb)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta4)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta8)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb4)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb8)) : "memory");
         for (int s = 0; s < O::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
-        mbar_init(tempty, O::EPI_WARPS);
+        mbar_init(tempty, 2 * O::EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     if (warp == 9) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_sh)),
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_sh)),
                      "n"(O::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_sh;
+    const uint32_t full0 = mapa_shared(smem_addr(full), 0);     // leader's full[0] (cluster window)
+    const uint32_t tempty0 = mapa_shared(smem_addr(tempty), 0);  // leader's tempty
 
-    auto tile_of = [&](int t, int &I, int &Jc) {
+    // pair-tile t -> first row block, column block, use bits
+    auto tile_of = [&](int t, int &I0, int &J, int &use) {
         if constexpr (MODE == OZ_PREDICT) {
-            I = t % tilesI;
-            Jc = t / tilesI;
+            const int pairsI = (rowsI + 1) / 2;
+            I0 = 2 * (t % pairsI);
+            J = t / pairsI;
+            use = (I0 + 1 < rowsI) ? 3 : 1;
         } else {
             const int2 tl = tiles[t];
-            I = tl.x;
-            Jc = tl.y;
+            I0 = tl.x & 0xFFFFFF;
+            J = tl.y;
+            use = tl.x >> 24;
         }
     };
 
     if (warp == 8) {
-        if (lane == 0) {  // ---- TMA producer: all S digit planes of a slab in one box per operand
+        if (lane == 0) {  // ---- TMA producer (both CTAs): this CTA's A block and B half
             uint32_t g = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                int I, Jc;
-                tile_of(t, I, Jc);
-                for (int kb = 0; kb < nk; ++kb, ++g) {
-                    const uint32_t s = g % O::STAGES;
-                    if (g >= O::STAGES) mbar_wait(&empty[s], ((g / O::STAGES) - 1) & 1);
-                    unsigned char *st = ring + size_t(s) * O::STAGE_BYTES;
-                    mbar_expect_tx(&full[s], O::STAGE_BYTES);
-                    tma_load_3d(st, &tma, &full[s], kb * O::BK, I * kTile, 0);
-                    tma_load_3d(st + S * O::A_PLANE, &tmb, &full[s], kb * O::BK, Jc * O::TN, 0);
+            for (int t = pair; t < ntiles; t += npairs) {
+                int I0, J, use;
+                tile_of(t, I0, J, use);
+#pragma unroll 1
+                for (int pass = 0; pass < 2; ++pass) {
+                    const int np = pass == 0 ? S : LV;
+                    for (int kb = 0; kb < nk; ++kb, ++g) {
+                        const uint32_t s = g % O::STAGES;
+                        if (g >= O::STAGES) mbar_wait(&empty[s], ((g / O::STAGES) - 1) & 1);
+                        unsigned char *st = ring + size_t(s) * O::STAGE_BYTES;
+                        if (dbg & 2) {  // experiment: no data movement
+                            if (leader) mbar_arrive(&full[s]);
+                            continue;
+                        }
+                        if (leader) mbar_expect_tx(&full[s], 2u * np * (O::PLANE + O::PLANE / 2));  // both CTAs' bytes
+                        const uint32_t fb = full0 + s * 8;
+                        // pre-swizzled blocks: A (row block I0 + r, slab kb) = S x 4 KiB at 128-B row
+                        // (I * nk + kb) * 256; B (64-row block 2 J + r, slab kb) = S x 2 KiB at (.) * 128
+                        tma_load_2d_2sm(st, pass == 0 ? &ta8 : &ta4, fb, 0, ((I0 + int(rank)) * nk + kb) * (S * 32));
+                        tma_load_2d_2sm(st + np * O::PLANE, pass == 0 ? &tb8 : &tb4, fb, 0,
+                                        ((2 * J + int(rank)) * nk + kb) * (S * 16));
+                    }
                 }
             }
         }
     } else if (warp == 9) {
-        if (lane == 0) {  // ---- MMA issuer: level l = a + b accumulates D_a(x_I) D_b(x_J)^T
-            uint32_t g = 0;
-            int n = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
-                if (n > 0) {
-                    mbar_wait(tempty, (n - 1) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                }
-                for (int kb = 0; kb < nk; ++kb, ++g) {
-                    const uint32_t s = g % O::STAGES;
-                    mbar_wait(&full[s], (g / O::STAGES) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t sa = smem_addr(ring + size_t(s) * O::STAGE_BYTES);
-                    const uint32_t sb = sa + S * O::A_PLANE;
-#pragma unroll
-                    for (int a = 0; a < S; ++a) {
-                        const uint64_t da = umma_desc_sw32(sa + a * O::A_PLANE);
-#pragma unroll
-                        for (int b = 0; b < S - a; ++b) {
-                            const uint64_t db = umma_desc_sw32(sb + b * O::B_PLANE);
-                            umma_i8<S>(tmem + uint32_t((a + b) * O::TN), da, db, (kb > 0 || a > 0) ? 1u : 0u);
-                        }
+        if (leader && lane == 0) {  // ---- MMA issuer (leader only): level l = a + b
+            uint32_t g = 0, e = 0;  // e: accumulator events (two per pair-tile)
+            for (int t = pair; t < ntiles; t += npairs) {
+#pragma unroll 1
+                for (int pass = 0; pass < 2; ++pass, ++e) {
+                    if (e > 0) {  // both CTAs' epilogues have drained the previous pass
+                        mbar_wait(tempty, (e - 1) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
                     }
-                    umma_commit(&empty[s]);
+                    const int np = pass == 0 ? S : LV;
+                    for (int kb = 0; kb < nk; ++kb, ++g) {
+                        const uint32_t s = g % O::STAGES;
+                        mbar_wait(&full[s], (g / O::STAGES) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        const uint32_t sa = smem_addr(ring + size_t(s) * O::STAGE_BYTES);
+                        const uint32_t sb = sa + np * O::PLANE;
+                        if (dbg & 4) {  // experiment: data movement only
+                        } else if (pass == 0) {  // levels 4..7 (26 pairs), TMEM column block l - 4
+#pragma unroll
+                            for (int a = 0; a < S; ++a)
+#pragma unroll
+                                for (int b = 0; b < S; ++b) {
+                                    const int l = a + b;
+                                    if (l < LV || l >= S) continue;  // compile-time after unrolling
+                                    // the first MMA into level l (at kb = 0) is the one with a = 0
+                                    umma_i8_2sm<S>(tmem + uint32_t((l - LV) * TN), umma_desc_sw32(sa + a * O::PLANE),
+                                                   umma_desc_sw32(sb + b * (O::PLANE / 2)), (kb > 0 || a > 0) ? 1u : 0u);
+                                }
+                        } else {  // levels 0..3 (10 pairs)
+#pragma unroll
+                            for (int a = 0; a < LV; ++a)
+#pragma unroll
+                                for (int b = 0; a + b < LV; ++b)
+                                    umma_i8_2sm<S>(tmem + uint32_t((a + b) * TN), umma_desc_sw32(sa + a * O::PLANE),
+                                                   umma_desc_sw32(sb + b * (O::PLANE / 2)), (kb > 0 || a > 0) ? 1u : 0u);
+                        }
+                        umma_commit_2sm_mc(&empty[s]);  // frees stage s in both CTAs
+                    }
+                    umma_commit_2sm_mc(tfull);  // this pass's accumulators ready in both CTAs
                 }
-                umma_commit(tfull);
             }
         }
-    } else {  // ---- epilogue warps 0-7: row 32(w%4) + lane, columns 32(w/4) .. +31
+    } else {  // ---- epilogue warps 0-7 (both CTAs): row 32(w%4) + lane, columns 64(w/4) .. +63
         const int quarter = warp & 3, grp = warp >> 2;
         const int lr = quarter * 32 + lane;
         const int et = threadIdx.x;  // 0..255
         const double Qmm = (MODE == OZ_PREDICT) ? 0.0 : scal[S_QMM];
-        int n = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
-            int I, Jc;
-            tile_of(t, I, Jc);
-            const int64_t row0 = int64_t(I) * kTile, col0 = int64_t(Jc) * O::TN;
-            const int J = Jc / O::NSUB;
-            if (et < O::TN) {  // column data of this tile (the previous tile's readers are done: B3)
+        uint32_t e = 0;
+        for (int t = pair; t < ntiles; t += npairs) {
+            int I0, J, use;
+            tile_of(t, I0, J, use);
+            const int I = I0 + int(rank);
+            const bool used = (use >> rank) & 1;  // CTA-uniform
+            const int64_t row0 = int64_t(I) * kTile, col0 = int64_t(J) * TN;
+            if (et < TN) {  // column data of this tile (the previous tile's readers are done: B3)
                 const int64_t gj = col0 + et;
                 colsc[et] = scb[gj];
                 colq[et] = (MODE == OZ_PREDICT) ? 0.0 : qv[gj];
@@ -275,95 +434,143 @@ __global__ void __launch_bounds__(Oz<S>::THREADS, 1)
                 coln[et] = (KT == RBF) ? nb_[gj] : 0.0;
             }
             const int64_t gi = row0 + lr;
-            const double sci = sca[gi];
-            const double qi = (MODE == OZ_PREDICT) ? 0.0 : qv[gi];
-            const double pi = (MODE == OZ_MATVEC) ? p[gi] : 0.0;
-            const double ni = (KT == RBF) ? na[gi] : 0.0;
+            const double sci = used ? sca[gi] : 0.0;
+            const double qi = (MODE == OZ_PREDICT || !used) ? 0.0 : qv[gi];
+            const double pi = (MODE == OZ_MATVEC && used) ? p[gi] : 0.0;
+            const double ni = (KT == RBF && used) ? na[gi] : 0.0;
             asm volatile("bar.sync 1, 256;" ::: "memory");  // B1
 
-            // drain: Horner over the levels, highest first:  v = sum_l 2^{-7l} acc_l
-            mbar_wait(tfull, n & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(grp * 32);
-            double v[32];
-            uint32_t r[32];
-            tmem_ld32_issue(tbase + uint32_t((S - 1) * O::TN), r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = static_cast<double>(static_cast<int>(r[j]));
-#pragma unroll 1
-            for (int l = S - 2; l >= 0; --l) {
-                tmem_ld32_issue(tbase + uint32_t(l * O::TN), r);
-                tmem_ld_wait();
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = fma(v[j], 0.0078125, static_cast<double>(static_cast<int>(r[j])));
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty);  // the MMA warp may overwrite the accumulators now
-
+            // Pass 0 (levels 4-7) -> the low-order part w = sum_{l<4} 2^{-7l} acc_{4+l}, kept in
+            // fp32: it enters as 2^{-28} w, so its rounding is ~2^{-52} relative to the leading
+            // digit products, and 64 columns cost 64 registers.  Pass 1 (levels 0-3), 8 columns at
+            // a time: v = sum_{l<4} 2^{-7l} acc_l + 2^{-28} w in fp64, then at once the Q~ entry /
+            // kernel value and its row and column contributions -- the accumulators are released
+            // after the last chunk (64 fp64 values per thread would not fit the 168-register
+            // budget of a 10-warp CTA).
+            const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(grp * 64);
+            const bool mirrored = used && (MODE != OZ_PREDICT) && (I != J) && (J >= band0) && (J < band1);
+            float wl[64];
             double rs = 0.0;
-            if constexpr (MODE == OZ_PREDICT) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int lc = grp * 32 + j;
-                    const double sv = v[j] * (sci * colsc[lc]);
-                    rs = fma(colp[lc], kernel_value<KT, double>(sv, ni, coln[lc], false, kp), rs);
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int lc = grp * 32 + j;
-                    const double sv = v[j] * (sci * colsc[lc]);
-                    v[j] = qtilde_value<KT, double>(sv, gi, col0 + lc, ni, coln[lc], qi, colq[lc], Qmm, invC, m1, kp);
+            double *qdst = nullptr, *qmir = nullptr;
+            if constexpr (MODE == OZ_PRECOMPUTE) {
+                if (used) {
+                    qdst = ((T_tiles < 0) ? Qc + int64_t(pk[2 * t + int(rank)]) * (kTile * kTile)
+                                          : Qc + (int64_t(I - band0) * T_tiles + J) * (kTile * kTile)) +
+                           int64_t(lr) * kTile + grp * 64;
+                    if (T_tiles >= 0 && mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
                 }
             }
-            if constexpr (MODE == OZ_MATVEC) {
-                const bool mirrored = (I != J) && (J >= band0) && (J < band1);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) rs = fma(v[j], colp[grp * 32 + j], rs);
-                redr[grp * kTile + lr] = rs;
-                if (mirrored) {  // tile-uniform
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] *= pi;
-                    redc[quarter * O::TN + grp * 32 + lane] = transpose_reduce32(v, lane);
+            for (int pass = 0; pass < 2; ++pass, ++e) {
+                mbar_wait(tfull, e & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (dbg & 1) {  // experiment: no epilogue
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty0);
+                    continue;
                 }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {  // 8-column chunks
+                    uint32_t r0[8], r1[8], r2[8], r3[8];
+                    tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
+                    tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
+                    tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
+                    tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
+                    tmem_ld_wait();
+                    double w[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        double h = i2d_exact(r3[j]);
+                        h = fma(h, 0.0078125, i2d_exact(r2[j]));
+                        h = fma(h, 0.0078125, i2d_exact(r1[j]));
+                        w[j] = fma(h, 0.0078125, i2d_exact(r0[j]));
+                    }
+                    if (pass == 0) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) wl[c * 8 + j] = static_cast<float>(w[j]);
+                        continue;
+                    }
+                    // ---- pass 1: finished contractions of columns c*8 .. c*8+7 of this thread's 64
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int lc = grp * 64 + c * 8 + j;
+                        const double sv = fma(static_cast<double>(wl[c * 8 + j]), 0x1p-28, w[j]) * (sci * colsc[lc]);
+                        if constexpr (MODE == OZ_PREDICT) {
+                            rs = fma(colp[lc], kernel_value<KT, double>(sv, ni, coln[lc], false, kp), rs);
+                        } else {
+                            w[j] = qtilde_value<KT, double>(sv, gi, col0 + lc, ni, coln[lc], qi, colq[lc], Qmm, invC, m1, kp);
+                        }
+                    }
+                    if constexpr (MODE == OZ_MATVEC) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            rs = fma(w[j], colp[grp * 64 + c * 8 + j], rs);
+                            w[j] *= pi;
+                        }
+                        if (mirrored) {  // CTA-uniform: column sums over the warp's 32 rows
+                            // transpose-reduce 8 values over 32 lanes: lanes l with (l & 3) == 0 end
+                            // with column 4 b4 + 2 b3 + b2 (b_k = bit k of l); fixed order
+#pragma unroll
+                            for (int o = 16, n = 4; o >= 4; o >>= 1, n >>= 1) {
+                                const bool up = (lane & o) != 0;
+#pragma unroll
+                                for (int i = 0; i < n; ++i) {
+                                    const double send = up ? w[i] : w[i + n];
+                                    const double keep = up ? w[i + n] : w[i];
+                                    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                                }
+                            }
+                            double tot = w[0] + __shfl_xor_sync(0xffffffffu, w[0], 2);
+                            tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+                            if ((lane & 3) == 0) {
+                                const int cc = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                                redc[quarter * TN + grp * 64 + c * 8 + cc] = tot;
+                            }
+                        }
+                    } else if constexpr (MODE == OZ_PRECOMPUTE) {
+                        if (qdst) {
+#pragma unroll
+                            for (int j = 0; j < 8; j += 2)
+                                *reinterpret_cast<double2 *>(qdst + c * 8 + j) = make_double2(w[j], w[j + 1]);
+                        }
+                        if (qmir) {  // transposed copy: column lc of this tile = row lc of tile (J, I)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) qmir[int64_t(grp * 64 + c * 8 + j) * kTile] = w[j];  // coalesced
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty0);  // the leader's MMA may overwrite the accumulators
+            }
+
+            if constexpr (MODE == OZ_MATVEC) {
+                redr[grp * kTile + lr] = rs;
                 asm volatile("bar.sync 1, 256;" ::: "memory");  // B2
-                const int64_t lrow0 = row0 - int64_t(band0) * kTile;
-                if (et < kTile) Ypart[int64_t(Jc) * band_rows + lrow0 + et] = redr[et] + redr[kTile + et];
-                if (mirrored && et >= kTile && et < kTile + O::TN) {
-                    const int c = et - kTile;
-                    const int64_t lcol0 = col0 - int64_t(band0) * kTile;
-                    Ypart[int64_t(I) * O::NSUB * band_rows + lcol0 + c] =
-                        (redc[c] + redc[O::TN + c]) + (redc[2 * O::TN + c] + redc[3 * O::TN + c]);
+                if (used) {
+                    const int64_t lrow0 = row0 - int64_t(band0) * kTile;
+                    if (et < kTile) {
+                        Ypart[int64_t(J) * band_rows + lrow0 + et] = redr[et] + redr[kTile + et];
+                    } else if (mirrored) {
+                        const int cidx = et - kTile;
+                        const int64_t lcol0 = col0 - int64_t(band0) * kTile;
+                        Ypart[int64_t(I) * band_rows + lcol0 + cidx] =
+                            (redc[cidx] + redc[TN + cidx]) + (redc[2 * TN + cidx] + redc[3 * TN + cidx]);
+                    }
                 }
             } else if constexpr (MODE == OZ_PREDICT) {
                 redr[grp * kTile + lr] = rs;
                 asm volatile("bar.sync 1, 256;" ::: "memory");  // B2
-                if (et < kTile) Ypart[int64_t(Jc) * band_rows + row0 + et] = redr[et] + redr[kTile + et];
-            } else {  // OZ_PRECOMPUTE: row-major 128 x 128 tiles, this tile is the 64-column half h
-                const int h = Jc % O::NSUB;
-                double *dst;
-                if (T_tiles < 0) dst = Qc + int64_t(t / O::NSUB) * (kTile * kTile) + h * O::TN;
-                else dst = Qc + (int64_t(I - band0) * T_tiles + J) * (kTile * kTile) + h * O::TN;
-                double *drow = dst + int64_t(lr) * kTile + grp * 32;
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2 *>(drow + j) = make_double2(v[j], v[j + 1]);
-                const bool mirrored = (I != J) && (J >= band0) && (J < band1);
-                if (T_tiles >= 0 && mirrored) {  // transposed copy: column lc of this tile = row of tile (J, I)
-                    double *mdst = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + int64_t(h * O::TN) * kTile;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) mdst[int64_t(grp * 32 + j) * kTile + lr] = v[j];  // coalesced over lanes
-                }
+                if (used && et < kTile) Ypart[int64_t(J) * band_rows + row0 + et] = redr[et] + redr[kTile + et];
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");  // B3: smem partials / column data reusable
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    cluster_sync_all();  // no more MMAs into either CTA's TMEM, no more remote arrives
     if (warp == 9) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(O::TMEM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(O::TMEM_COLS));
     }
 }
 
