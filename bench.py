@@ -45,6 +45,18 @@ def tf32x3_peak_tflops():
     return measured_peaks().get("bf16_tflops", 1590.0) * (1.1 / 2.25) / 3.0
 
 
+OZAKI_DIGIT_PAIRS = 36  # 8 digits per point, digit pairs (a, b) with a + b <= 7 (ozaki_engine.cuh)
+
+
+def int8_peak_tops(sustained=True):
+    """Dense int8 tensor peak: the measured bf16 dense peak x the guide's nominal int8/bf16 ratio
+    (4.5 / 2.25 POPS).  The Q~p kernel runs back to back inside the CG loop at the power cap, so the
+    roofline uses the SUSTAINED bf16 figure (MEASURED_PEAKS.json bf16_tflops_sustained)."""
+    pk = measured_peaks()
+    bf = pk.get("bf16_tflops_sustained", 1392.0) if sustained else pk.get("bf16_tflops", 1645.0)
+    return 2.0 * bf
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -285,7 +297,27 @@ def main():
 
     # ---- roofline of the dominant kernel (the Q~p product), timed with CUDA events on its stream
     avg_mv = t_mv / max(1, matvecs)
-    if mode_used == "implicit":
+    engine = {1: "ozaki", 2: "dmma"}.get(stats0.fp64_engine_used, "tcgen05-3xtf32")
+    if mode_used == "implicit" and engine == "ozaki":
+        # int8 digit products per launch: 36 pairs x 2 d8 ops per distinct Q~ entry (d8 = d rounded up to
+        # the 32-feature slab), this rank's ~1/P share; fp64-equivalent rate reported beside it
+        fl = matvec_flops(cfg.m, cfg.d) / world
+        d8 = -(-cfg.d // 32) * 32
+        ops = OZAKI_DIGIT_PAIRS * fl * d8 / cfg.d
+        peak = int8_peak_tops(sustained=True)
+        achieved = ops / avg_mv / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)", "frac": achieved / peak,
+                "traffic": traffic_for(f"{cfg.name}/implicit/k_tile_ozaki") if world == 1 else None,
+                "traffic_unit": "bytes per launch (ncu dram read+write)", "kernel": "k_tile_ozaki (OZ_MATVEC)",
+                "per_launch": f"36 digit pairs x 2*d8 int8 ops per distinct Q~ entry, E = m'(m'+1)/2 "
+                              f"({ops:.4g} int8 ops per launch per rank)",
+                "peak_source": "int8 dense = 2 x MEASURED_PEAKS.json bf16_tflops_sustained (guide ratio 4.5/2.25; "
+                               "the kernel runs back to back at the 1 kW power cap)",
+                "frac_of_burst_peak": achieved / int8_peak_tops(sustained=False),
+                "fp64_equivalent": {"achieved_tflops": fl / avg_mv / 1e12, "dmma_peak_tflops": FP64_PEAK_TFLOPS,
+                                    "ratio": fl / avg_mv / 1e12 / FP64_PEAK_TFLOPS},
+                "avg_launch_s": avg_mv}
+    elif mode_used == "implicit":
         fl = matvec_flops(cfg.m, cfg.d) / world  # this rank's share (symmetric work split)
         peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else tf32x3_peak_tflops()
         achieved = fl / avg_mv / 1e12
@@ -310,7 +342,10 @@ def main():
     line = {"metric": METRIC, "value": iters / t, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (sklearn make_classification planes, seeded)",
-            "config": config_dict(cfg, args, mode_used), "gpu_launches": launches, "clocks": clocks,
+            "config": dict(config_dict(cfg, args, mode_used), fp64_engine=engine if cfg.dtype == "f64" else None,
+                           contraction=("int8 digit products (exact int32 sums) combined in f64" if engine == "ozaki"
+                                        else None)),
+            "gpu_launches": launches, "clocks": clocks,
             "roofline": roof,
             "train": {"iterations_per_step": iters / args.steps, "t_train_s": stats0.t_total,
                       "t_cg_s": stats0.t_cg, "t_precompute_s": stats0.t_precompute,
