@@ -30,6 +30,10 @@ def tf32x3_peak():
 
 
 FP32_PEAK = tf32x3_peak()
+try:  # int8 dense = 2 x the measured sustained bf16 dense rate (bench.py int8_peak_tops)
+    INT8_PEAK = 2.0 * json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"]
+except (OSError, KeyError, ValueError):
+    INT8_PEAK = 2784.4
 
 
 def hbm_peak():
@@ -39,12 +43,16 @@ def hbm_peak():
         return 6650.0
 
 
-MODES = {"C0": ["implicit"], "C1": ["implicit", "cached"], "C2": ["cached", "implicit", "lowrank"],
-         "C3": ["cached", "implicit"],
-         "C4": ["cached"]}
+# (mode, fp64 engine) per config; engine "auto" = the default (Ozaki on these data), "dmma" = fp64
+# tensor cores for comparison
+MODES = {"C0": [("implicit", "auto")], "C1": [("implicit", "auto"), ("implicit", "dmma"), ("cached", "auto")],
+         "C2": [("cached", "auto"), ("implicit", "auto"), ("lowrank", "auto")],
+         "C3": [("cached", "auto"), ("implicit", "auto")],
+         "C4": [("cached", "auto"), ("implicit", "auto")]}
+ENGINES = {"auto": pl.FP64_AUTO, "dmma": pl.FP64_DMMA}
 
 
-def run(cfg, mode, repeat=2):
+def run(cfg, mode, engine="auto", repeat=2):
     X, y, Z, yz = synth.config_data(cfg)
     dev = torch.device("cuda", 0)
     tX, ty, tZ = (torch.from_numpy(a).to(dev) for a in (X, y, Z))
@@ -54,13 +62,14 @@ def run(cfg, mode, repeat=2):
     for _ in range(repeat):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        alpha, b, st, s = pl.plssvm_train_ex(tX, ty, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=pl.options(mode=md), **kw)
+        alpha, b, st, s = pl.plssvm_train_ex(tX, ty, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=pl.options(mode=md, fp64_engine=ENGINES[engine]), **kw)
         torch.cuda.synchronize()
         tt = time.perf_counter() - t0
         if best is None or tt < best[0]:
             best = (tt, s, alpha, b, st)
     tt, s, alpha, b, st = best
-    f, lab, (tk, _) = pl.plssvm_predict_ex(tX, alpha, float(b.item()), tZ, cfg.kernel, **kw)
+    f, lab, (tk, _) = pl.plssvm_predict_ex(tX, alpha, float(b.item()), tZ, cfg.kernel,
+                                           opts=pl.options(fp64_engine=ENGINES[engine]), **kw)
     acc = float((lab.cpu().numpy() == yz.astype(np.int32)).mean()) if len(yz) else None
     m1 = cfg.m - 1
     fl = 2.0 * cfg.d * m1 * (m1 + 1) / 2
@@ -70,12 +79,19 @@ def run(cfg, mode, repeat=2):
            "status": st, "iterations": s.iterations, "rel_residual": s.rel_residual, "train_s": tt,
            "cg_s": s.t_cg, "precompute_s": s.t_precompute, "cg_iterations_per_s": s.iterations / s.t_cg,
            "matvec_ms": 1e3 * mv, "bytes_per_gpu": s.bytes_per_gpu,
-           "predict_s": tk, "n_test": cfg.n_test, "test_accuracy": acc}
+           "predict_s": tk, "n_test": cfg.n_test, "test_accuracy": acc,
+           "fp64_engine": {1: "ozaki", 2: "dmma"}.get(s.fp64_engine_used)}
     if mode == "lowrank":  # two streams over X per product (a different cost model, NEXT-2)
         sz = 8 if cfg.dtype == "f64" else 4
         row["matvec_gbs"] = 2.0 * cfg.m * cfg.d * sz / mv / 1e9
         row["frac_of_peak"] = row["matvec_gbs"] / hbm_peak()
         row["peak_gbs"] = hbm_peak()
+    elif mode == "implicit" and row["fp64_engine"] == "ozaki":
+        d8 = -(-cfg.d // 32) * 32
+        row["matvec_tflops"] = fl / mv / 1e12  # fp64-equivalent
+        row["matvec_int8_tops"] = 36 * fl * d8 / cfg.d / mv / 1e12
+        row["peak_int8_tops_sustained"] = INT8_PEAK
+        row["frac_of_peak"] = row["matvec_int8_tops"] / INT8_PEAK
     elif mode == "implicit":
         row["matvec_tflops"] = fl / mv / 1e12
         row["frac_of_peak"] = row["matvec_tflops"] / peak_f
@@ -103,8 +119,10 @@ def main():
     cfgs = synth.configs()
     out = open(a.out, "w") if a.out else None
     for name in a.configs.split(","):
-        for mode in MODES[name]:
-            row = run(cfgs[name], mode)
+        for mode, engine in MODES[name]:
+            if cfgs[name].dtype == "f32" and engine != "auto":
+                continue
+            row = run(cfgs[name], mode, engine, repeat=1 if name == "C4" else 2)
             line = json.dumps(row)
             print(line, flush=True)
             if out:
