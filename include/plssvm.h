@@ -29,6 +29,9 @@
  * Layout: X is point-major (row i = point i), m x d, C-contiguous (numpy/torch default);
  * Z is n x d, same layout.  The device transposes to the paper's feature-major layout
  * itself.
+ * Validation: scalar arguments on the host; X, Z, alpha, p (finite) and y (every y_i in
+ * {-1, +1}, both present) on the device right after they are staged, for host and device
+ * pointers alike (one small read-back; no host-side scan of the caller's arrays).
  * Errors: every entry point returns a plssvm_status_t; on any error the outputs are left
  * untouched (except PLSSVM_W_NOT_CONVERGED, which fills alpha and b) and
  * plssvm_last_error() returns a thread-local message valid until the next call on the thread.
@@ -57,7 +60,7 @@ typedef enum { PLSSVM_LINEAR = 0, PLSSVM_POLYNOMIAL = 1, PLSSVM_RBF = 2 } plssvm
 typedef enum {
     PLSSVM_OK = 0,
     PLSSVM_E_INVALID_ARG = 1,  /* m < 2, d < 1, C <= 0, gamma <= 0 (poly/rbf), degree < 1,
-                                  eps <= 0, unknown kernel, non-finite X/Z, NULL pointer */
+                                  eps <= 0, unknown kernel, non-finite X/Z/alpha/p, NULL pointer */
     PLSSVM_E_LABELS = 2,       /* a y_i not in {-1,+1}, or only one class present */
     PLSSVM_E_OOM = 3,          /* device allocation failed */
     PLSSVM_E_CUDA = 4,         /* CUDA runtime error / no device */

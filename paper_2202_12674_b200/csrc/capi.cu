@@ -2,7 +2,8 @@
 // conventions (status codes + thread-local message), dispatch to the device driver.
 // Validation rules (plssvm.h): m >= 2, d >= 1; y_i in {-1,+1}
 // with both classes present; C > 0; gamma > 0 for poly/rbf and degree >= 1
-// (P:248-249); eps > 0; kernel in {0,1,2}; finite X / Z.
+// (P:248-249); eps > 0; kernel in {0,1,2}.  Finite X / Z / alpha / p and the labels are checked
+// on the device after staging (driver.cu validate_inputs), for host and device pointers alike.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -62,37 +63,10 @@ int check_params(int64_t m, int64_t d, int kernel, double gamma, int degree, dou
     return PLSSVM_OK;
 }
 
-// Host-side checks of host buffers only (device buffers are the caller's responsibility).
-template <typename T>
-int check_finite(const T *a, int64_t n, const char *what) {
-    for (int64_t i = 0; i < n; ++i)
-        if (!std::isfinite(static_cast<double>(a[i]))) return fail(PLSSVM_E_INVALID_ARG, std::string(what) + " is not finite");
-    return PLSSVM_OK;
-}
-
-template <typename T>
-int check_labels(const T *y, int64_t m) {
-    bool pos = false, neg = false;
-    for (int64_t i = 0; i < m; ++i) {
-        if (y[i] == T(1)) pos = true;
-        else if (y[i] == T(-1)) neg = true;
-        else return fail(PLSSVM_E_LABELS, "labels must be +1 or -1");
-    }
-    if (!pos || !neg) return fail(PLSSVM_E_LABELS, "both classes (+1 and -1) must be present");
-    return PLSSVM_OK;
-}
-
 plssvm_options_t defaults() {
     plssvm_options_t o;
     plssvm_default_options(&o);
     return o;
-}
-
-template <typename T>
-int host_checks_train(const void *X, const void *y, int64_t m, int64_t d) {
-    int s = check_finite(static_cast<const T *>(X), m * d, "X");
-    if (s) return s;
-    return check_labels(static_cast<const T *>(y), m);
 }
 
 }  // namespace
@@ -131,10 +105,6 @@ int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtyp
     if (o.mode == PLSSVM_MODE_LOWRANK && kernel != PLSSVM_LINEAR)
         return fail(PLSSVM_E_INVALID_ARG, "options.mode LOWRANK needs the linear kernel");
     if (o.x0 != 0 && o.x0 != 1) return fail(PLSSVM_E_INVALID_ARG, "options.x0 must be 0 or 1");
-    if (!o.device_pointers) {
-        s = dtype == PLSSVM_F64 ? host_checks_train<double>(X, y, m, d) : host_checks_train<float>(X, y, m, d);
-        if (s) return s;
-    }
     if ((s = device_ok(o.device))) return s;
     if (stats) std::memset(stats, 0, sizeof(*stats));
     plssvm::Problem pb{X, y, m, d, dtype, kernel, gamma, degree, coef0, C, eps};
@@ -164,17 +134,6 @@ int plssvm_predict_ex(const void *X, const void *alpha, double b, int64_t m, int
     if (n < 0) return fail(PLSSVM_E_INVALID_ARG, "n must be >= 0");
     if (n == 0) return PLSSVM_OK;
     if (!std::isfinite(b)) return fail(PLSSVM_E_INVALID_ARG, "b is not finite");
-    if (!o.device_pointers) {
-        if (dtype == PLSSVM_F64) {
-            if ((s = check_finite(static_cast<const double *>(X), m * d, "X"))) return s;
-            if ((s = check_finite(static_cast<const double *>(Z), n * d, "Z"))) return s;
-            if ((s = check_finite(static_cast<const double *>(alpha), m, "alpha"))) return s;
-        } else {
-            if ((s = check_finite(static_cast<const float *>(X), m * d, "X"))) return s;
-            if ((s = check_finite(static_cast<const float *>(Z), n * d, "Z"))) return s;
-            if ((s = check_finite(static_cast<const float *>(alpha), m, "alpha"))) return s;
-        }
-    }
     if ((s = device_ok(o.device))) return s;
     plssvm::Problem pb{X, nullptr, m, d, dtype, kernel, gamma, degree, coef0, 1.0, 1.0};
     return guarded([&] { return plssvm::predict(pb, alpha, b, Z, n, o, decision, labels, t_kernel); });
@@ -201,11 +160,6 @@ int plssvm_qtilde_matvec(const void *X, const void *p, int64_t m, int64_t d, int
     if (dtype != PLSSVM_F64 && dtype != PLSSVM_F32) return fail(PLSSVM_E_INVALID_ARG, "dtype must be 0 (f64) or 1 (f32)");
     int s = check_params(m, d, kernel, gamma, degree, C);
     if (s) return s;
-    if (!o.device_pointers) {
-        s = dtype == PLSSVM_F64 ? check_finite(static_cast<const double *>(X), m * d, "X")
-                                : check_finite(static_cast<const float *>(X), m * d, "X");
-        if (s) return s;
-    }
     if ((s = device_ok(o.device))) return s;
     if (o.mode < 0 || o.mode > 3) return fail(PLSSVM_E_INVALID_ARG, "options.mode must be 0, 1, 2 or 3");
     if (o.mode == PLSSVM_MODE_LOWRANK && kernel != PLSSVM_LINEAR)

@@ -104,6 +104,40 @@ const T *stage_input(Arena &A, const void *src, int64_t n, bool device_ptr, cuda
     return d;
 }
 
+// Device-side input validation (replaces host scans of the caller's arrays): every listed array
+// is checked for non-finite values, labels for {-1, +1} with both classes.  One sync; throws the
+// plssvm.h status with a message.  Outputs are untouched (nothing is written before this).
+template <typename T>
+struct VCheck {
+    const T *a;
+    int64_t n;
+    unsigned bit;
+};
+template <typename T>
+void validate_inputs(Arena &A, std::initializer_list<VCheck<T>> arrays, const T *y, int64_t m, cudaStream_t s,
+                     int64_t &launches) {
+    unsigned *flags = A.alloc<unsigned>(1);
+    PLS_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned), s));
+    bool first = true;
+    for (const VCheck<T> &v : arrays) {
+        k_validate<T><<<4 * 148, 256, 0, s>>>(v.a, v.n, v.bit, first ? y : nullptr, m, flags);
+        PLS_CHECK_LAUNCH();
+        ++launches;
+        first = false;
+    }
+    unsigned h = 0;
+    PLS_CUDA(cudaMemcpyAsync(&h, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    PLS_CUDA(cudaStreamSynchronize(s));
+    if (h & V_NONFINITE_X) throw Error(PLSSVM_E_INVALID_ARG, "X is not finite");
+    if (h & V_NONFINITE_Z) throw Error(PLSSVM_E_INVALID_ARG, "Z is not finite");
+    if (h & V_NONFINITE_ALPHA) throw Error(PLSSVM_E_INVALID_ARG, "alpha is not finite");
+    if (h & V_NONFINITE_P) throw Error(PLSSVM_E_INVALID_ARG, "p is not finite");
+    if (y) {
+        if (h & V_BADLABEL) throw Error(PLSSVM_E_LABELS, "labels must be +1 or -1");
+        if (!(h & V_POS) || !(h & V_NEG)) throw Error(PLSSVM_E_LABELS, "both classes (+1 and -1) must be present");
+    }
+}
+
 // rows = padded point count of the destination array (its column count is dpad).
 template <typename T>
 void launch_transform(const T *X, int64_t m, int64_t d, T *Xt, int64_t rows, int64_t dpad, cudaStream_t s,
@@ -768,9 +802,12 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.d = pb.d;
     if (need_labels) {
         c.ylab = const_cast<T *>(stage_input<T>(A, pb.y, pb.m, dev, c.s));
+        validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * pb.d, V_NONFINITE_X}}, c.ylab, pb.m, c.s, c.launches);
     } else {
         c.ylab = A.alloc<T>(pb.m);
         PLS_CUDA(cudaMemsetAsync(c.ylab, 0, pb.m * sizeof(T), c.s));
+        validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * pb.d, V_NONFINITE_X}}, static_cast<const T *>(nullptr), 0, c.s,
+                           c.launches);
     }
     PLS_CUDA(cudaEventRecord(e_h2d, c.s));
     c.Xt = A.alloc<T>(g.dpad * g.mpad);
@@ -1119,6 +1156,7 @@ int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, cons
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     const bool dev = o.device_pointers != 0;
     PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
+    validate_inputs<T>(A, {VCheck<T>{c.p, g.m1, V_NONFINITE_P}}, static_cast<const T *>(nullptr), 0, c.s, c.launches);
     select_mode<T>(c, o);  // throws E_OOM if CACHED does not fit
     configure_product<T>(c, A);
     double t_pre = 0.0;
@@ -1177,9 +1215,12 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     const int64_t xrows = EN::kPointMajor ? mpad : L, zrows = EN::kPointMajor ? npad : L;
     const T *Xs = stage_input<T>(A, pb.X, m * d, dev, s);
     const T *Zs = stage_input<T>(A, Zin, n * d, dev, s);
+    const T *al = stage_input<T>(A, alpha_in, m, dev, s);
+    validate_inputs<T>(A, {VCheck<T>{Xs, m * d, V_NONFINITE_X}, VCheck<T>{Zs, n * d, V_NONFINITE_Z},
+                           VCheck<T>{al, m, V_NONFINITE_ALPHA}},
+                       static_cast<const T *>(nullptr), 0, s, launches);
     if (pb.kernel == LINEAR && o.linear_w) {
         // f(z) = <w, z> + b with w = sum_i alpha_i x_i (Eq. 15): O((m + n) d)
-        const T *al = stage_input<T>(A, alpha_in, m, dev, s);
         const int64_t rpb = std::max<int64_t>(1, ceil_div(m, 4 * 148));
         const int parts = static_cast<int>(ceil_div(m, rpb));
         T *wpart = A.alloc<T>(static_cast<int64_t>(parts) * d), *w = A.alloc<T>(d);
@@ -1210,7 +1251,7 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     launch_transform<T>(Zs, n, d, Zl, zrows, dpad, s, launches);
     T *alpha = A.alloc<T>(xrows);
     PLS_CUDA(cudaMemsetAsync(alpha, 0, xrows * sizeof(T), s));
-    PLS_CUDA(cudaMemcpyAsync(alpha, alpha_in, m * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    PLS_CUDA(cudaMemcpyAsync(alpha, al, m * sizeof(T), cudaMemcpyDeviceToDevice, s));
     T *nx = A.alloc<T>(xrows), *nz = A.alloc<T>(zrows);
     KParams<T> kp{pb.kernel, static_cast<T>(pb.gamma), pb.degree, static_cast<T>(pb.coef0)};
     if (pb.kernel == RBF) {

@@ -75,6 +75,28 @@ __device__ __forceinline__ void grid_reduce(T v, T *partials, unsigned *counter,
 }
 
 // ---------------------------------------------------------------------------------------
+// Input validation on the device (plssvm.h "Validation"): non-finite values of an array set its
+// bit; labels must be +1 / -1 with both present.  One flag word, OR-reduced per warp.
+enum VFlag : unsigned { V_BADLABEL = 1u, V_POS = 2u, V_NEG = 4u, V_NONFINITE_X = 8u, V_NONFINITE_Z = 16u,
+                        V_NONFINITE_ALPHA = 32u, V_NONFINITE_P = 64u };
+template <typename T>
+__global__ void k_validate(const T *__restrict__ a, int64_t n, unsigned bit, const T *__restrict__ y, int64_t m,
+                           unsigned *__restrict__ flags) {
+    unsigned f = 0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        if (!isfinite(a[i])) f |= bit;
+    if (y) {
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+            const T v = y[i];
+            f |= (v == T(1)) ? V_POS : (v == T(-1)) ? V_NEG : V_BADLABEL;
+        }
+    }
+    f = __reduce_or_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+// ---------------------------------------------------------------------------------------
 // Layout transform (paper "transform"): X[m][d] point-major (host order) ->
 //   feature-major X^T[dpad][ld] (fp32 FFMA engine, the paper's column-major layout), or
 //   point-major   Xp[ld][dpad]  (fp64 DMMA engine, features contiguous),

@@ -95,16 +95,50 @@ def test_validation_errors_leave_outputs_untouched():
         st, msg, alpha, b = _train_status(X, y, **kw)
         assert st == code and msg, (kw, st, msg)
         assert np.all(alpha == 7.0) and b[0] == 7.0
-    st, msg, _, _ = _train_status(X, np.ones(10))
-    assert st == binding.E_LABELS and "both classes" in msg
-    st, msg, _, _ = _train_status(X, np.array([1, -1, 2, 1, 1, 1, -1, -1, 1, 1.0]))
-    assert st == binding.E_LABELS
-    Xn = X.copy()
-    Xn[3, 1] = np.nan
-    st, msg, _, _ = _train_status(Xn, y)
-    assert st == binding.E_INVALID_ARG and "finite" in msg
     st, msg, _, _ = _train_status(X[:1], y[:1])
     assert st == binding.E_INVALID_ARG
+
+
+def _data_validation_cases():
+    """Array contents (labels, finiteness) are validated on the device after staging
+    (driver.cu validate_inputs): E_LABELS / E_INVALID_ARG with a GPU, E_CUDA without one."""
+    X = np.random.default_rng(0).standard_normal((10, 3))
+    y = np.array([1, -1] * 5, dtype=float)
+    Xn = X.copy()
+    Xn[3, 1] = np.nan
+    return [((X, np.ones(10)), binding.E_LABELS, "both classes"),
+            ((X, np.array([1, -1, 2, 1, 1, 1, -1, -1, 1, 1.0])), binding.E_LABELS, "+1 or -1"),
+            ((Xn, y), binding.E_INVALID_ARG, "finite")]
+
+
+@pytest.mark.skipif(pl.plssvm_device_count() > 0, reason="GPU present")
+def test_data_validation_needs_the_device():
+    for (X, y), _, _ in _data_validation_cases():
+        st, msg, alpha, b = _train_status(X, y)
+        assert st == binding.E_CUDA and np.all(alpha == 7.0) and b[0] == 7.0
+
+
+@pytest.mark.gpu
+def test_data_validation_on_device_leaves_outputs_untouched():
+    for (X, y), code, text in _data_validation_cases():
+        st, msg, alpha, b = _train_status(X, y)
+        assert st == code and text in msg, (st, msg)
+        assert np.all(alpha == 7.0) and b[0] == 7.0
+    X = np.random.default_rng(1).standard_normal((10, 3))
+    Z = X.copy()
+    Z[2, 2] = np.inf
+    with pytest.raises(pl.PlssvmError, match="Z is not finite"):
+        pl.plssvm_predict(X, np.zeros(10), 0.0, Z, pl.RBF, 0.5)
+    with pytest.raises(pl.PlssvmError, match="alpha is not finite"):
+        pl.plssvm_predict(X, np.full(10, np.nan), 0.0, X, pl.RBF, 0.5)
+    with pytest.raises(pl.PlssvmError, match="p is not finite"):
+        pl.plssvm_qtilde_matvec(X, np.full(9, np.inf), pl.RBF, 0.5)
+    import torch  # device pointers are validated too
+
+    tX = torch.from_numpy(X).cuda()
+    ty = torch.from_numpy(np.ones(10)).cuda()
+    with pytest.raises(pl.PlssvmError, match="both classes"):
+        pl.plssvm_train_ex(tX, ty, pl.RBF, 0.5)
 
 
 def test_linear_kernel_ignores_gamma_validation():
