@@ -105,8 +105,10 @@ typedef struct {
  *         exactly in int32, combined in fp64.  Error of x_i.x_j <~ d 2^-56 ||x_i||_inf ||x_j||_inf
  *         (an fp64-GEMM-type bound weighted by the row maxima instead of |x_ik||x_jk|).
  *  DMMA:  fp64 tensor cores (mma.sync f64, error <~ d u sum_k |x_ik||x_jk|).
+ *         Needs d <= 16384 (the int32 level sums; larger d with OZAKI -> PLSSVM_E_INVALID_ARG).
  *  AUTO:  OZAKI unless some point has max_k |x_ik| > 64 * rms_k(x_ik) (a peaked row whose small
- *         features would lose relative precision under the row-max scaling), then DMMA. */
+ *         features would lose relative precision under the row-max scaling) or d > 16384,
+ *         then DMMA. */
 typedef enum { PLSSVM_FP64_AUTO = 0, PLSSVM_FP64_OZAKI = 1, PLSSVM_FP64_DMMA = 2 } plssvm_fp64_engine_t;
 
 /* Statistics of one training call (all times are device-event seconds). */

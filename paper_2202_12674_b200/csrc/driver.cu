@@ -480,10 +480,19 @@ OzOperand oz_prepare(Arena &A, const double *Xp, int64_t rows, int64_t dpad, int
 // fp64 engine choice (plssvm.h plssvm_fp64_engine_t): OZAKI, DMMA, or AUTO = OZAKI unless a row
 // of any operand array peaks above kOzPeakMax x its RMS.
 constexpr double kOzPeakMax = 64.0;
+constexpr int64_t kOzMaxD = 16384;
 bool oz_choose(int engine, std::initializer_list<const double *> arrays, std::initializer_list<int64_t> rows,
                int64_t dpad, int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
     if (engine == PLSSVM_FP64_DMMA) return false;
-    if (engine == PLSSVM_FP64_OZAKI) return true;
+    // int32 level sums: |acc_l| <= 8 d8 127^2 < 2^31 needs d8 <= 16384 (ozaki_engine.cuh)
+    const bool fits = round_up(d, OzC::BK) <= kOzMaxD;
+    if (engine == PLSSVM_FP64_OZAKI) {
+        if (!fits)
+            throw Error(PLSSVM_E_INVALID_ARG, "fp64_engine OZAKI supports d <= " + std::to_string(kOzMaxD) +
+                                                  " (int32 digit-product sums); use AUTO or DMMA");
+        return true;
+    }
+    if (!fits) return false;
     unsigned *bits = A.alloc<unsigned>(1);
     PLS_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned), s));
     auto r = rows.begin();

@@ -156,3 +156,22 @@ def test_engines_agree_on_planes_c1_slice():
     a, _ = pl.plssvm_qtilde_matvec(X, p, cfg.kernel, cfg.gamma, opts=pl.options(fp64_engine=pl.FP64_OZAKI))
     b, _ = pl.plssvm_qtilde_matvec(X, p, cfg.kernel, cfg.gamma, opts=pl.options(fp64_engine=pl.FP64_DMMA))
     assert rel(a, b) <= 1e-14
+
+
+def test_wide_d_limit():
+    """int32 level sums bound d (<= 16384): AUTO switches to DMMA beyond it, forced OZAKI refuses."""
+    rng = np.random.default_rng(8)
+    m, d = 40, 16400
+    X = rng.standard_normal((m, d)) * 0.05
+    y = np.where(np.arange(m) % 2 == 0, 1.0, -1.0)
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, pl.RBF, 1.0 / d, eps=1e-10)
+    assert st == 0 and stats.fp64_engine_used == pl.FP64_DMMA
+    a_ref, _, _, _ = oracle.train(X, y, pl.RBF, 1.0 / d, eps=1e-10)
+    assert rel(alpha, a_ref) <= 1e-7
+    with pytest.raises(pl.PlssvmError, match="d <= 16384"):
+        pl.plssvm_train_ex(X, y, pl.RBF, 1.0 / d, eps=1e-10, opts=pl.options(fp64_engine=pl.FP64_OZAKI))
+    X2 = X[:, :16384].copy()
+    alpha, b, st, stats = pl.plssvm_train_ex(X2, y, pl.RBF, 1.0 / 16384, eps=1e-10)
+    assert st == 0 and stats.fp64_engine_used == pl.FP64_OZAKI
+    a_ref, _, _, _ = oracle.train(X2, y, pl.RBF, 1.0 / 16384, eps=1e-10)
+    assert rel(alpha, a_ref) <= 1e-7
