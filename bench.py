@@ -45,7 +45,7 @@ def tf32x3_peak_tflops():
     return measured_peaks().get("bf16_tflops", 1590.0) * (1.1 / 2.25) / 3.0
 
 
-OZAKI_DIGIT_PAIRS = 36  # 8 digits per point, digit pairs (a, b) with a + b <= 7 (ozaki_engine.cuh)
+OZAKI_DIGIT_PAIRS = 28  # 7 balanced base-256 digits per point, digit pairs (a, b) with a + b <= 6 (ozaki_engine.cuh)
 
 
 def int8_peak_tops(sustained=True):
@@ -299,7 +299,7 @@ def main():
     avg_mv = t_mv / max(1, matvecs)
     engine = {1: "ozaki", 2: "dmma"}.get(stats0.fp64_engine_used, "tcgen05-3xtf32")
     if mode_used == "implicit" and engine == "ozaki":
-        # int8 digit products per launch: 36 pairs x 2 d8 ops per distinct Q~ entry (d8 = d rounded up to
+        # int8 digit products per launch: 28 pairs x 2 d8 ops per distinct Q~ entry (d8 = d rounded up to
         # the 32-feature slab), this rank's ~1/P share; fp64-equivalent rate reported beside it
         fl = matvec_flops(cfg.m, cfg.d) / world
         d8 = -(-cfg.d // 32) * 32
@@ -309,7 +309,7 @@ def main():
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)", "frac": achieved / peak,
                 "traffic": traffic_for(f"{cfg.name}/implicit/k_tile_ozaki") if world == 1 else None,
                 "traffic_unit": "bytes per launch (ncu dram read+write)", "kernel": "k_tile_ozaki (OZ_MATVEC)",
-                "per_launch": f"36 digit pairs x 2*d8 int8 ops per distinct Q~ entry, E = m'(m'+1)/2 "
+                "per_launch": f"{OZAKI_DIGIT_PAIRS} digit pairs x 2*d8 int8 ops per distinct Q~ entry, E = m'(m'+1)/2 "
                               f"({ops:.4g} int8 ops per launch per rank)",
                 "peak_source": "int8 dense = 2 x MEASURED_PEAKS.json bf16_tflops_sustained (guide ratio 4.5/2.25; "
                                "the kernel runs back to back at the 1 kW power cap)",

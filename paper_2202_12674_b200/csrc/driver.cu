@@ -443,7 +443,7 @@ std::vector<int2> wide_tiles(int T) {
 }
 
 // ---- fp64 on the int8 tensor cores (ozaki_engine.cuh) -------------------------------------
-constexpr int kOzS = 8;  // digits per point: fp64-level products
+constexpr int kOzS = 7;  // balanced base-256 digits per point: fp64-level products
 using OzC = Oz<kOzS>;
 
 int num_sms() {
@@ -484,7 +484,7 @@ constexpr int64_t kOzMaxD = 16384;
 bool oz_choose(int engine, std::initializer_list<const double *> arrays, std::initializer_list<int64_t> rows,
                int64_t dpad, int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
     if (engine == PLSSVM_FP64_DMMA) return false;
-    // int32 level sums: |acc_l| <= 8 d8 127^2 < 2^31 needs d8 <= 16384 (ozaki_engine.cuh)
+    // int32 level sums: |acc_l| <= 7 d8 2^14 < 2^31 needs d8 <= 18724; limit 16384 (ozaki_engine.cuh)
     const bool fits = round_up(d, OzC::BK) <= kOzMaxD;
     if (engine == PLSSVM_FP64_OZAKI) {
         if (!fits)

@@ -3,23 +3,23 @@
 // (Eq. 16), the cached-mode precompute and the predict (Eq. 10).
 //
 // Why: a B200 runs fp64 at 37 TFLOP/s (DMMA, profiles/r01_fp64_peak.txt) but int8 MMAs at
-// ~4.5 POPS.  Each point x_i is written EXACTLY as
-//     x_i = 2^{E_i} * sum_{a=1..S} D_a(x_i) 2^{-7a},   D_a in [-127, 127] (int8 digits),
-// E_i = the row's exponent (max_k |x_ik| < 2^{E_i}); the remainder after S digits is < 2^{E_i-7S}.
-// Then  x_i . x_j = 2^{E_i+E_j-14} * sum_{l=0..S-1} 2^{-7l} * acc_l,
-//       acc_l = sum_{a+b=l} D_a(x_i) . D_b(x_j)       (0-based digit indices a, b)
-// keeps every digit product of order <= S-1 (the dropped ones are < S 2^{-7S} relative to
-// 2^{E_i+E_j} each: S = 8 gives 1e-16-level products, i.e. fp64 accuracy; SURVEY App. A style
-// check in DESIGN.md).  Every acc_l is an EXACT int32 sum (|acc_l| <= S d 127^2 < 2^31 for
-// d < 16384), accumulated in TMEM by tcgen05.mma.kind::i8; the combination runs in fp64
-// (Horner over l, one rounding per level), so the result is an fp64 dot product with a
-// different (shorter) rounding history, not a lower-precision one.
+// ~4.5 POPS.  Each point x_i is written EXACTLY as a 54-bit integer N_i = x_i 2^{54-E_i}
+// (E_i = the row's exponent, max_k |x_ik| < 2^{E_i}; exact because x's ulp is >= 2^{E_i-53})
+// in 7 BALANCED base-256 digits:
+//     N_i = sum_{a=0..6} D_a 256^{6-a},   D_a in [-128, 127]  (int8; |N| < 2^54 < the 7-digit range)
+// so  x_i . x_j = 2^{E_i+E_j-12} * sum_{l=0..12} 2^{-8l} acc_l,   acc_l = sum_{a+b=l} D_a(x_i) . D_b(x_j).
+// Levels l <= 6 are kept (28 digit pairs); the dropped ones are < 7 * 2^{-56} relative to
+// 2^{E_i+E_j} each (8 bits per digit: an 8 x 7-bit split needed 36 pairs for the same bound).
+// Every acc_l is an EXACT int32 sum (|acc_l| <= 7 d 2^14 < 2^31 for d <= 16384), accumulated in
+// TMEM by tcgen05.mma.kind::i8; the combination runs in fp64 (Horner over l, one rounding per
+// level), so the result is an fp64 dot product with a different (shorter) rounding history,
+// not a lower-precision one.
 //
 // Tile = 128 x 128 per CTA, computed by CTA pairs as 256 x 128 UMMAs (cta_group::2, below).
-// The 8 level accumulators of a tile need 8 x 128 int32
-// TMEM columns, twice the 512 available, so a tile runs in TWO PASSES over the features:
-// pass 0 accumulates levels 4-7 (26 digit pairs, digit planes 0-7), pass 1 levels 0-3 (10
-// pairs, planes 0-3), each in 4 x 128 TMEM columns.  N = 128 halves the shared-memory operand
+// The 7 level accumulators of a tile need 7 x 128 int32
+// TMEM columns, more than the 512 available, so a tile runs in TWO PASSES over the features:
+// pass 0 accumulates levels 4-6 (18 digit pairs, digit planes 0-6), pass 1 levels 0-3 (10
+// pairs, planes 0-3), each in <= 4 x 128 TMEM columns.  N = 128 halves the shared-memory operand
 // bytes per MMA cycle of an N = 64 tile (the SS-mode UMMA reads A and B from smem each time:
 // 128 B/clk at N = 128 = the smem bandwidth, 192 B/clk at N = 64 -- measured: tc pipe 84 %
 // busy, imma 46 % with 128 x 64 tiles), at the same L2 traffic per output element.
@@ -31,7 +31,7 @@
 //                       the pass
 //   warps 0-7         : epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows), columns
 //                       64(w/4).. of every level (tcgen05.ld 32x32b.x8), Horner-combines them in
-//                       fp64 (pass 0 -> w in fp32; pass 1 -> v + 2^-28 w, then the kernel
+//                       fp64 (pass 0 -> w in fp32; pass 1 -> v + 2^-32 w, then the kernel
 //                       function / Eq. 16 corrections and the row / column contributions, 8
 //                       columns at a time), releasing the accumulators after each pass.
 // Slot conventions: those of k_matvec_implicit with 128-wide column blocks (NSUB = 1).
@@ -46,18 +46,19 @@ enum OzMode : int { OZ_MATVEC = 0, OZ_PRECOMPUTE = 1, OZ_PREDICT = 2 };
 
 template <int S>
 struct Oz {
-    static_assert(S == 8, "two passes of 4 levels");
+    static_assert(S == 7, "7 balanced base-256 digits: pass 0 = levels 4..6, pass 1 = levels 0..3");
     static constexpr int BK = 32;                                  // int8 features per slab (32 B rows)
     static constexpr int TN = 128;                                 // tile columns (UMMA N)
     static constexpr int NSUB = kTile / TN;                        // 1
-    static constexpr int LV = 4;                                   // levels per pass
+    static constexpr int LV = 4;                                   // levels of pass 1 (0..3)
+    static constexpr int LV0 = S - LV;                             // levels of pass 0 (4..S-1)
     static constexpr int STAGES = 4;
     static constexpr uint32_t PLANE = kTile * BK;                  // 4 KiB: one A digit plane (B half: 2 KiB)
-    static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: 8 planes of A and of the B half
+    static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: S planes of A and of the B half
     static constexpr int EPI_WARPS = 8;
     static constexpr int THREADS = (EPI_WARPS + 2) * 32;
     static constexpr int TMEM_COLS = 512;
-    static_assert(LV * TN <= TMEM_COLS, "a pass's level accumulators must fit TMEM");
+    static_assert(LV * TN <= TMEM_COLS && LV0 * TN <= TMEM_COLS, "a pass's level accumulators must fit TMEM");
     // misc: barriers (256 B) + column data 4 x 128 doubles + row partials 2 x 128 + col partials 4 x 128
     static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN) * 8;
     static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + MISC;
@@ -152,17 +153,20 @@ __global__ void k_row_peak(const double *__restrict__ Xp, int64_t rows, int64_t 
 }
 
 // Exact digit split of the point-major padded fp64 array Xp[rows][dpad] (rows a multiple of
-// 128) into S int8 digit planes, stored PRE-SWIZZLED as the shared-memory images the UMMA reads:
+// 128) into S balanced base-256 int8 digit planes (plane 0 = most significant), stored
+// PRE-SWIZZLED as the shared-memory images the UMMA reads:
 //   DA[rows/128][nk][S][128 x 32 B]  (row-operand role: 128-point blocks)
 //   DB[rows/64 ][nk][S][ 64 x 32 B]  (column-operand role: one CTA's half of a 2-SM B tile)
 // (nk = dpad8 / 32 feature slabs), each 32-byte row in the SWIZZLE_32B pattern (16-byte chunk
 // index XOR bit 2 of the row).  A stage of the tile kernel is then ONE contiguous block per
 // operand, moved by TMA in 128-byte rows with no swizzle (4x fewer, 4x larger requests than
 // a 32-byte-row box: the tile kernel was feed-bound with them).  Either pointer may be null.
-// Row scales sc_i = 2^{E_i - 7}.  One warp per row; 4 features per lane per step.
+// Row scales sc_i = 2^{E_i - 6} (x_i . x_j = sc_i sc_j sum_l 2^{-8l} acc_l).  One warp per row;
+// 4 features per lane per step.
 template <int S>
 __global__ void k_ozaki_split(const double *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t dpad8,
                               int8_t *__restrict__ DA, int8_t *__restrict__ DB, double *__restrict__ sc) {
+    static_assert(8 * S >= 55, "S balanced base-256 digits must hold a 54-bit integer");
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= rows) return;
@@ -173,30 +177,29 @@ __global__ void k_ozaki_split(const double *__restrict__ Xp, int64_t rows, int64
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     int E = 0;
     if (mx > 0.0) frexp(mx, &E);  // mx = f 2^E, f in [0.5, 1)  =>  |x_ik| < 2^E
-    const double inv = ldexp(1.0, -E);
-    if (lane == 0) sc[i] = ldexp(1.0, E - 7);
+    if (lane == 0) sc[i] = ldexp(1.0, E - 6);
     const int64_t nk = dpad8 / 32;
     const int r128 = static_cast<int>(i & 127), r64 = static_cast<int>(i & 63);
     const int flip = (r128 >> 2) & 1;  // = (r64 >> 2) & 1
     for (int64_t k0 = 4 * lane; k0 < dpad8; k0 += 128) {
-        double u[4];
+        long long N[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) u[v] = (k0 + v < dpad) ? x[k0 + v] * inv : 0.0;  // |u| < 1, exact
+        for (int v = 0; v < 4; ++v)  // |N| < 2^54, an exact integer (x's ulp >= 2^{E-53})
+            N[v] = (k0 + v < dpad) ? __double2ll_rn(ldexp(x[k0 + v], 54 - E)) : 0ll;
         const int64_t kb = k0 >> 5;
         const int c = static_cast<int>(k0 & 31);
         const int inrow = ((((c >> 4) ^ flip) << 4) | (c & 15));
         int8_t *pa = DA ? DA + ((i >> 7) * nk + kb) * (S * 4096) + r128 * 32 + inrow : nullptr;
         int8_t *pb = DB ? DB + ((i >> 6) * nk + kb) * (S * 2048) + r64 * 32 + inrow : nullptr;
 #pragma unroll
-        for (int a = 0; a < S; ++a) {
+        for (int a = S - 1; a >= 0; --a) {  // least significant digit first
             char4 dg;
             signed char *dv = reinterpret_cast<signed char *>(&dg);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                u[v] *= 128.0;                    // exact (power of two)
-                const double t = trunc(u[v]);     // |t| <= 127
-                u[v] -= t;                        // exact
-                dv[v] = static_cast<signed char>(t);
+                const signed char dd = static_cast<signed char>(N[v] & 0xFF);  // N = dd (mod 256), dd in [-128, 127]
+                N[v] = (N[v] - dd) >> 8;                                       // exact
+                dv[v] = dd;
             }
             if (pa) *reinterpret_cast<char4 *>(pa + a * 4096) = dg;
             if (pb) *reinterpret_cast<char4 *>(pb + a * 2048) = dg;
@@ -281,7 +284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                  double *__restrict__ Ypart, int64_t band_rows, double *__restrict__ Qc, int T_tiles, const int *ctrl,
                  int dbg) {
     using O = Oz<S>;
-    constexpr int TN = O::TN, LV = O::LV;
+    constexpr int TN = O::TN, LV = O::LV, LV0 = O::LV0;
     if (cg_done(ctrl)) return;  // uniform across the cluster
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -364,7 +367,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         const uint32_t fb = full0 + s * 8;
                         // pre-swizzled blocks: A (row block I0 + r, slab kb) = S x 4 KiB at 128-B row
                         // (I * nk + kb) * 256; B (64-row block 2 J + r, slab kb) = S x 2 KiB at (.) * 128
-                        tma_load_2d_2sm(st, pass == 0 ? &ta8 : &ta4, fb, 0, ((I0 + int(rank)) * nk + kb) * (S * 32));
+                        tma_load_2d_2sm(st, pass == 0 ? &ta8 : &ta4, fb, 0, ((I0 + int(rank)) * nk + kb) * (S * 32));  // ta8: all S planes
                         tma_load_2d_2sm(st + np * O::PLANE, pass == 0 ? &tb8 : &tb4, fb, 0,
                                         ((2 * J + int(rank)) * nk + kb) * (S * 16));
                     }
@@ -389,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         const uint32_t sa = smem_addr(ring + size_t(s) * O::STAGE_BYTES);
                         const uint32_t sb = sa + np * O::PLANE;
                         if (dbg & 4) {  // experiment: data movement only
-                        } else if (pass == 0) {  // levels 4..7 (26 pairs), TMEM column block l - 4
+                        } else if (pass == 0) {  // levels 4..6 (18 pairs), TMEM column block l - 4
 #pragma unroll
                             for (int a = 0; a < S; ++a)
 #pragma unroll
@@ -440,10 +443,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             const double ni = (KT == RBF && used) ? na[gi] : 0.0;
             asm volatile("bar.sync 1, 256;" ::: "memory");  // B1
 
-            // Pass 0 (levels 4-7) -> the low-order part w = sum_{l<4} 2^{-7l} acc_{4+l}, kept in
-            // fp32: it enters as 2^{-28} w, so its rounding is ~2^{-52} relative to the leading
+            // Pass 0 (levels 4-6) -> the low-order part w = sum_{l<3} 2^{-8l} acc_{4+l}, kept in
+            // fp32: it enters as 2^{-32} w, so its rounding is ~2^{-56} relative to the leading
             // digit products, and 64 columns cost 64 registers.  Pass 1 (levels 0-3), 8 columns at
-            // a time: v = sum_{l<4} 2^{-7l} acc_l + 2^{-28} w in fp64, then at once the Q~ entry /
+            // a time: v = sum_{l<4} 2^{-8l} acc_l + 2^{-32} w in fp64, then at once the Q~ entry /
             // kernel value and its row and column contributions -- the accumulators are released
             // after the last chunk (64 fp64 values per thread would not fit the 168-register
             // budget of a 10-warp CTA).
@@ -472,18 +475,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {  // 8-column chunks
                     uint32_t r0[8], r1[8], r2[8], r3[8];
-                    tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
+                    const int nl = pass == 0 ? LV0 : LV;  // levels of this pass (TMEM blocks 0..nl-1)
+                    if (nl > 3) tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
                     tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
                     tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
                     tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
                     tmem_ld_wait();
                     double w[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        double h = i2d_exact(r3[j]);
-                        h = fma(h, 0.0078125, i2d_exact(r2[j]));
-                        h = fma(h, 0.0078125, i2d_exact(r1[j]));
-                        w[j] = fma(h, 0.0078125, i2d_exact(r0[j]));
+                    for (int j = 0; j < 8; ++j) {  // Horner in base 2^-8, highest level first
+                        double h = i2d_exact(r2[j]);
+                        if (nl > 3) h = fma(i2d_exact(r3[j]), 0.00390625, h);
+                        h = fma(h, 0.00390625, i2d_exact(r1[j]));
+                        w[j] = fma(h, 0.00390625, i2d_exact(r0[j]));
                     }
                     if (pass == 0) {
 #pragma unroll
@@ -494,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int lc = grp * 64 + c * 8 + j;
-                        const double sv = fma(static_cast<double>(wl[c * 8 + j]), 0x1p-28, w[j]) * (sci * colsc[lc]);
+                        const double sv = fma(static_cast<double>(wl[c * 8 + j]), 0x1p-32, w[j]) * (sci * colsc[lc]);
                         if constexpr (MODE == OZ_PREDICT) {
                             rs = fma(colp[lc], kernel_value<KT, double>(sv, ni, coln[lc], false, kp), rs);
                         } else {

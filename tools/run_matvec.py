@@ -20,8 +20,8 @@ ap.add_argument("--m", type=int, default=0)
 ap.add_argument("--d", type=int, default=0)
 ap.add_argument("--kernel", type=int, default=-1)
 ap.add_argument("--fp32-engine", type=int, default=0)
-ap.add_argument("--fp64-engine", type=int, default=0)
-ap.add_argument("--compare", action="store_true", help="also run the other fp64 engine and compare")
+ap.add_argument("--fp64-engine", type=int, default=0, help="0 AUTO, 1 OZAKI, 2 DMMA")
+ap.add_argument("--compare", action="store_true", help="also run the DMMA fp64 engine (OZAKI if --fp64-engine 2) and compare")
 a = ap.parse_args()
 cfg = synth.configs()[a.config]
 m, d = a.m or cfg.m, a.d or cfg.d
@@ -40,6 +40,6 @@ print(f"{a.config} m={m} d={d} kernel={kern} mode={a.mode}: mean {t[0]*1e3:.3f} 
       f" -> {fl/t[1]/1e12:.2f} TFLOP/s (implicit-equivalent), cached stream {m1*m1*s/t[1]/1e9:.1f} GB/s")
 if a.compare and dt == np.float64:
     ref, t2 = pl.plssvm_qtilde_matvec(X, p, kern, 1.0 / d, cfg.degree, cfg.coef0, cfg.C, repeats=a.repeats,
-                                      opts=pl.options(mode=mode, fp64_engine=1 - a.fp64_engine))
+                                      opts=pl.options(mode=mode, fp64_engine=pl.FP64_OZAKI if a.fp64_engine == pl.FP64_DMMA else pl.FP64_DMMA))
     err = np.linalg.norm(out - ref) / np.linalg.norm(ref)
     print(f"  other fp64 engine: min {t2[1]*1e3:.3f} ms ({fl/t2[1]/1e12:.2f} TFLOP/s); rel diff {err:.3e}, max abs {np.abs(out-ref).max():.3e}")
