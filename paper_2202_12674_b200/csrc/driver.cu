@@ -538,7 +538,20 @@ void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb
                double invC, const double *scal, int64_t m1, int band0, int band1, double *Ypart, int64_t band_rows,
                double *Qc, int T_tiles, const int *ctrl) {
     if (npt <= 0) return;
-    const int grid = 2 * std::min(npt, num_sms() / 2);
+    // Only co-resident clusters (a pair must fit in one GPC): a statically scheduled grid with one
+    // cluster too many would run that cluster's tiles as a second wave.
+    static int max_clusters[3][3] = {};
+    int &mc = max_clusters[KT][MODE];
+    if (mc == 0) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(num_sms()), 1, 1);
+        cfg.blockDim = dim3(OzC::THREADS, 1, 1);
+        cfg.dynamicSmemBytes = OzC::SMEM_BYTES;
+        PLS_CUDA(cudaOccupancyMaxActiveClusters(&mc, k_tile_ozaki<KT, kOzS, MODE>, &cfg));
+        if (mc <= 0) mc = num_sms() / 2;
+        if (std::getenv("PLSSVM_DEBUG")) std::fprintf(stderr, "[plssvm] k_tile_ozaki co-resident pairs: %d\n", mc);
+    }
+    const int grid = 2 * std::min(npt, mc);
     k_tile_ozaki<KT, kOzS, MODE><<<grid, OzC::THREADS, OzC::SMEM_BYTES, s>>>(
         ra.t4, ra.t8, cb.h4, cb.h8, ra.nk, ptiles, pk, npt, rowsI, ra.sc, cb.sc, qv, na, nb_, p, kp, invC, scal, m1,
         band0, band1, Ypart, band_rows, Qc, T_tiles, ctrl, oz_debug_flags());
