@@ -97,12 +97,39 @@ typedef struct {
                                 O((m+n)d)) [1]; 0 = evaluate the kernel matrix like the other kernels */
     int32_t fp64_engine;     /* plssvm_fp64_engine_t: fp64 pairwise contraction of the implicit Q~p, the
                                 cached precompute and predict [AUTO] */
+    int32_t cg_loop;         /* plssvm_cg_loop_t: how the CG iterations are issued [AUTO] */
+    int32_t multi_gpu;       /* plssvm_multi_gpu_t: how `comm`'s ranks share the work [ROWS] */
 } plssvm_options_t;
+
+/* CG loop issue.  The convergence test always runs on the device
+ * (Shewchuk's loop condition, evaluated by the last block of the p update).
+ *  BATCHED: the host enqueues iterations in batches of 8 and reads the control block once per
+ *           batch; per-product CUDA events give stats.t_matvec.
+ *  GRAPH:   one CUDA graph whose device-side WHILE conditional node runs the iteration body
+ *           until the device sets the condition to 0 -- a single launch, no host round trip;
+ *           stats.t_matvec stays 0 (no events inside conditional bodies).  Single GPU only, and
+ *           not with replace_every > 0 (its period is a host-side branch).
+ *  AUTO:    GRAPH when it applies and one product is latency-sized (cached / low-rank products,
+ *           or m <= 8192), else BATCHED (launch overhead < 0.1 % of a multi-ms product). */
+typedef enum { PLSSVM_CG_AUTO = 0, PLSSVM_CG_BATCHED = 1, PLSSVM_CG_GRAPH = 2 } plssvm_cg_loop_t;
+
+/* Multi-GPU work split when options.comm has P > 1 ranks.
+ *  ROWS:     Q~ rows are sharded (cached: row bands; implicit: circulant symmetric tile pairs +
+ *            reduce-scatter), all kernels; p all-gathered, CG scalars all-reduced.
+ *  FEATURES: the paper's own multi-GPU scheme (§III-C5): every rank holds all points
+ *            but only its feature slice [f0, f1) (plssvm_feature_partition), computes the
+ *            partial Q~^(g) p of Eq. 16 restricted to those features (the 1/C terms on rank 0
+ *            only), and the partial products are summed by one all-reduce of the m-1 vector per
+ *            iteration; the CG vectors are replicated.  Valid for the LINEAR kernel only (the
+ *            kernel must be a sum over features), fp64, implicit products (mode AUTO or
+ *            IMPLICIT); needs d >= P.  Otherwise PLSSVM_E_INVALID_ARG. */
+typedef enum { PLSSVM_MULTI_GPU_ROWS = 0, PLSSVM_MULTI_GPU_FEATURES = 1 } plssvm_multi_gpu_t;
 
 /* fp64 contraction engines.
  *  OZAKI: int8 tensor cores (tcgen05 kind::i8, 2-SM UMMA) on an EXACT split of every point into
- *         8 int8 digits times a power of two (x = 2^E sum_a D_a 2^-7a); digit products summed
- *         exactly in int32, combined in fp64.  Error of x_i.x_j <~ d 2^-56 ||x_i||_inf ||x_j||_inf
+ *         7 balanced base-256 int8 digits times a power of two (x_i = 2^(E_i-54) sum_a D_a 256^(6-a),
+ *         D_a in [-128, 127]); the 28 digit-pair products of levels a+b <= 6 are summed exactly in
+ *         int32 and combined in fp64.  Error of x_i.x_j <~ 7 d 2^-56 ||x_i||_inf ||x_j||_inf
  *         (an fp64-GEMM-type bound weighted by the row maxima instead of |x_ik||x_jk|).
  *  DMMA:  fp64 tensor cores (mma.sync f64, error <~ d u sum_k |x_ik||x_jk|).
  *         Needs d <= 16384 (the int32 level sums; larger d with OZAKI -> PLSSVM_E_INVALID_ARG).
@@ -127,7 +154,7 @@ typedef struct {
     int64_t gpu_launches;            /* kernels launched by this call (this rank) */
     int64_t launches_in_cg;          /* of which inside the CG loop */
     int32_t fp64_engine_used;        /* PLSSVM_FP64_OZAKI or _DMMA for fp64 calls, 0 for fp32 */
-    int32_t reserved0;
+    int32_t cg_loop_used;            /* PLSSVM_CG_BATCHED or PLSSVM_CG_GRAPH */
 } plssvm_stats_t;
 
 PLSSVM_API void plssvm_default_options(plssvm_options_t *opts);
@@ -206,6 +233,11 @@ PLSSVM_API int plssvm_comm_init_callbacks(const plssvm_comm_callbacks_t *cb, int
  * 128 * nranks).  Rows >= m-1 are padding (masked). */
 PLSSVM_API int plssvm_partition(int64_t m, int32_t nranks, int32_t rank, int64_t *row_begin, int64_t *row_end,
                      int64_t *m_pad);
+
+/* Host-side feature split of PLSSVM_MULTI_GPU_FEATURES (no GPU needed): rank `rank` of `nranks`
+ * owns features [f_begin, f_end) = [rank*d/nranks, (rank+1)*d/nranks) (integer division, so the
+ * slices differ by at most one feature).  d >= nranks >= 1. */
+PLSSVM_API int plssvm_feature_partition(int64_t d, int32_t nranks, int32_t rank, int64_t *f_begin, int64_t *f_end);
 
 /* ---- misc ------------------------------------------------------------------------------ */
 PLSSVM_API const char *plssvm_last_error(void); /* thread-local; "" when the last call succeeded */

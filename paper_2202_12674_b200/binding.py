@@ -18,21 +18,24 @@ LINEAR, POLYNOMIAL, RBF = 0, 1, 2
 F64, F32 = 0, 1
 MODE_AUTO, MODE_IMPLICIT, MODE_CACHED, MODE_LOWRANK = 0, 1, 2, 3
 FP64_AUTO, FP64_OZAKI, FP64_DMMA = 0, 1, 2
+CG_AUTO, CG_BATCHED, CG_GRAPH = 0, 1, 2
+MULTI_GPU_ROWS, MULTI_GPU_FEATURES = 0, 1
 OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED = range(8)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
                 6: "E_NUMERICAL", 7: "W_NOT_CONVERGED"}
 
 EXPORTS = ["plssvm_default_options", "plssvm_train", "plssvm_train_f32", "plssvm_train_ex", "plssvm_predict",
            "plssvm_predict_f32", "plssvm_predict_ex", "plssvm_qtilde_matvec", "plssvm_comm_unique_id",
-           "plssvm_comm_init", "plssvm_comm_init_callbacks", "plssvm_comm_destroy", "plssvm_partition", "plssvm_last_error", "plssvm_version",
-           "plssvm_device_count"]
+           "plssvm_comm_init", "plssvm_comm_init_callbacks", "plssvm_comm_destroy", "plssvm_partition",
+           "plssvm_feature_partition", "plssvm_last_error", "plssvm_version", "plssvm_device_count"]
 
 
 class plssvm_options_t(ct.Structure):
     _fields_ = [("mode", ct.c_int32), ("x0", ct.c_int32), ("max_iter", ct.c_int64), ("replace_every", ct.c_int64),
                 ("fixed_iter", ct.c_int64), ("device", ct.c_int32), ("device_pointers", ct.c_int32),
                 ("stream", ct.c_void_p), ("comm", ct.c_void_p), ("cache_budget_bytes", ct.c_int64),
-                ("fp32_engine", ct.c_int32), ("linear_w", ct.c_int32), ("fp64_engine", ct.c_int32)]
+                ("fp32_engine", ct.c_int32), ("linear_w", ct.c_int32), ("fp64_engine", ct.c_int32),
+                ("cg_loop", ct.c_int32), ("multi_gpu", ct.c_int32)]
 
 
 class plssvm_stats_t(ct.Structure):
@@ -43,7 +46,7 @@ class plssvm_stats_t(ct.Structure):
                 ("t_cg", ct.c_double), ("t_bias_d2h", ct.c_double), ("t_total", ct.c_double),
                 ("t_matvec", ct.c_double), ("t_matvec_min", ct.c_double), ("bytes_per_gpu", ct.c_int64),
                 ("gpu_launches", ct.c_int64), ("launches_in_cg", ct.c_int64), ("fp64_engine_used", ct.c_int32),
-                ("reserved0", ct.c_int32)]
+                ("cg_loop_used", ct.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -100,6 +103,7 @@ def load(build_if_missing: bool = True):
     L.plssvm_comm_destroy.argtypes = [vp]
     L.plssvm_comm_init_callbacks.argtypes = [ct.POINTER(plssvm_comm_callbacks_t), i32, i32, i32, ct.POINTER(vp)]
     L.plssvm_partition.argtypes = [i64, i32, i32, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
+    L.plssvm_feature_partition.argtypes = [i64, i32, i32, ct.POINTER(i64), ct.POINTER(i64)]
     L.plssvm_last_error.restype = ct.c_char_p
     L.plssvm_version.restype = ct.c_char_p
     L.plssvm_device_count.restype = ct.c_int
@@ -168,6 +172,13 @@ def plssvm_partition(m: int, nranks: int, rank: int):
     b, e, mp = ct.c_int64(), ct.c_int64(), ct.c_int64()
     _check(load().plssvm_partition(m, nranks, rank, ct.byref(b), ct.byref(e), ct.byref(mp)))
     return b.value, e.value, mp.value
+
+
+def plssvm_feature_partition(d: int, nranks: int, rank: int):
+    """(f_begin, f_end): the feature slice of `rank` under MULTI_GPU_FEATURES (host logic, no GPU)."""
+    b, e = ct.c_int64(), ct.c_int64()
+    _check(load().plssvm_feature_partition(d, nranks, rank, ct.byref(b), ct.byref(e)))
+    return b.value, e.value
 
 
 def plssvm_train(X, y, kernel, gamma=1.0, degree=3, coef0=0.0, C=1.0, eps=1e-10):

@@ -69,6 +69,21 @@ plssvm_options_t defaults() {
     return o;
 }
 
+// PLSSVM_MULTI_GPU_FEATURES (paper §III-C5): linear kernel, fp64, implicit, d >= P.
+int check_multi_gpu(const plssvm_options_t &o, int kernel, int dtype, int64_t d) {
+    if (o.multi_gpu != PLSSVM_MULTI_GPU_ROWS && o.multi_gpu != PLSSVM_MULTI_GPU_FEATURES)
+        return fail(PLSSVM_E_INVALID_ARG, "options.multi_gpu must be 0 (ROWS) or 1 (FEATURES)");
+    if (o.multi_gpu != PLSSVM_MULTI_GPU_FEATURES) return PLSSVM_OK;
+    if (kernel != PLSSVM_LINEAR)
+        return fail(PLSSVM_E_INVALID_ARG, "multi_gpu FEATURES needs the linear kernel (P:421-425)");
+    if (dtype != PLSSVM_F64) return fail(PLSSVM_E_INVALID_ARG, "multi_gpu FEATURES is fp64 only");
+    if (o.mode != PLSSVM_MODE_AUTO && o.mode != PLSSVM_MODE_IMPLICIT)
+        return fail(PLSSVM_E_INVALID_ARG, "multi_gpu FEATURES computes implicit products (mode AUTO or IMPLICIT)");
+    if (o.comm && d < plssvm::comm_size(static_cast<plssvm::CommHandle *>(o.comm)))
+        return fail(PLSSVM_E_INVALID_ARG, "multi_gpu FEATURES needs d >= number of ranks");
+    return PLSSVM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -89,6 +104,8 @@ void plssvm_default_options(plssvm_options_t *o) {
     o->fp32_engine = 0;
     o->linear_w = 1;
     o->fp64_engine = PLSSVM_FP64_AUTO;
+    o->cg_loop = PLSSVM_CG_AUTO;
+    o->multi_gpu = PLSSVM_MULTI_GPU_ROWS;
 }
 
 int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtype, int kernel, double gamma, int degree,
@@ -105,6 +122,8 @@ int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtyp
     if (o.mode == PLSSVM_MODE_LOWRANK && kernel != PLSSVM_LINEAR)
         return fail(PLSSVM_E_INVALID_ARG, "options.mode LOWRANK needs the linear kernel");
     if (o.x0 != 0 && o.x0 != 1) return fail(PLSSVM_E_INVALID_ARG, "options.x0 must be 0 or 1");
+    if (o.cg_loop < 0 || o.cg_loop > 2) return fail(PLSSVM_E_INVALID_ARG, "options.cg_loop must be 0, 1 or 2");
+    if ((s = check_multi_gpu(o, kernel, dtype, d))) return s;
     if ((s = device_ok(o.device))) return s;
     if (stats) std::memset(stats, 0, sizeof(*stats));
     plssvm::Problem pb{X, y, m, d, dtype, kernel, gamma, degree, coef0, C, eps};
@@ -164,6 +183,7 @@ int plssvm_qtilde_matvec(const void *X, const void *p, int64_t m, int64_t d, int
     if (o.mode < 0 || o.mode > 3) return fail(PLSSVM_E_INVALID_ARG, "options.mode must be 0, 1, 2 or 3");
     if (o.mode == PLSSVM_MODE_LOWRANK && kernel != PLSSVM_LINEAR)
         return fail(PLSSVM_E_INVALID_ARG, "options.mode LOWRANK needs the linear kernel");
+    if ((s = check_multi_gpu(o, kernel, dtype, d))) return s;
     plssvm::Problem pb{X, nullptr, m, d, dtype, kernel, gamma, degree, coef0, C, 1.0};
     return guarded([&] { return plssvm::qtilde_matvec(pb, p, repeats, o, out, t_kernel); });
 }
@@ -205,6 +225,15 @@ int plssvm_partition(int64_t m, int32_t nranks, int32_t rank, int64_t *row_begin
     *m_pad = mpad;
     *row_begin = static_cast<int64_t>(rank) * nb;
     *row_end = *row_begin + nb;
+    return PLSSVM_OK;
+}
+
+int plssvm_feature_partition(int64_t d, int32_t nranks, int32_t rank, int64_t *f_begin, int64_t *f_end) {
+    g_last_error.clear();
+    if (d < 1 || nranks < 1 || d < nranks || rank < 0 || rank >= nranks || !f_begin || !f_end)
+        return fail(PLSSVM_E_INVALID_ARG, "bad feature partition arguments");
+    *f_begin = plssvm::feature_begin(d, nranks, rank);
+    *f_end = plssvm::feature_begin(d, nranks, rank + 1);
     return PLSSVM_OK;
 }
 

@@ -325,6 +325,11 @@ struct Ctx {
     int *oz_pk = nullptr;
     int oz_npt = 0;
     const int *cur_ctrl = nullptr;   // ctrl inside the CG loop (loop kernels early-exit when done)
+    bool fsplit = false;             // PLSSVM_MULTI_GPU_FEATURES: this rank's feature slice only,
+                                     // partial products summed by an all-reduce
+    int nranks = 1;                  // communicator size (g.P is the row-shard count)
+    T *yred = nullptr;               // fsplit: the all-reduced product
+    bool graph_used = false;         // the CG loop ran as one CUDA graph (WHILE node)
 };
 
 template <typename T>
@@ -787,21 +792,38 @@ void launch_precompute(Ctx<T> &c) {
 template <typename T>
 void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par, int set_delta0) {
     const Geometry &g = c.g;
-    k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Yfin, nslots, (c.cached || c.circ) ? 1 : c.nsub_eff, g.band0,
-                                                       g.nb, g.g0, g.m1, pband, c.y, mode, c.ylab,
-                                                       c.r, pout, c.scal, par, set_delta0, c.partials, c.counter, 1,
-                                                       c.cur_ctrl);
+    const T *Y = c.Yfin;
+    int nsub = (c.cached || c.circ) ? 1 : c.nsub_eff;
+    if constexpr (std::is_same<T, double>::value) {
+        if (c.fsplit) {
+            // this rank's partial product (its feature slice) -> sum over the ranks,
+            // then the usual finalize on the summed vector (one slot)
+            k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(Y, nslots, nsub, g.band0, g.nb, g.g0, g.m1, c.p + g.g0,
+                                                               c.yred, 0, c.ylab, c.r, nullptr, c.scal, 0, 0,
+                                                               c.partials, c.counter, 0, c.cur_ctrl);
+            PLS_CHECK_LAUNCH();
+            ++c.launches;
+            comm_allreduce_sum_f64(c.comm, c.yred, c.yred, g.nb, c.s);
+            Y = c.yred;
+            nslots = 1;
+            nsub = 1;
+        }
+    }
+    k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(Y, nslots, nsub, g.band0, g.nb, g.g0, g.m1, pband, c.y, mode,
+                                                       c.ylab, c.r, pout, c.scal, par, set_delta0, c.partials,
+                                                       c.counter, 1, c.cur_ctrl);
     PLS_CHECK_LAUNCH();
     ++c.launches;
 }
 
+// Row-sharded exchanges; with the feature split the CG vectors and scalars are replicated.
 template <typename T>
 void allreduce(Ctx<T> &c, int slot, int count) {
-    if (c.comm) comm_allreduce_sum_f64(c.comm, c.scal + slot + S_L, c.scal + slot, count, c.s);
+    if (c.comm && !c.fsplit) comm_allreduce_sum_f64(c.comm, c.scal + slot + S_L, c.scal + slot, count, c.s);
 }
 template <typename T>
 void allgather(Ctx<T> &c, T *full) {
-    if (c.comm) comm_allgather(c.comm, full, c.g.nb, dtype_of(T()), c.s);
+    if (c.comm && !c.fsplit) comm_allgather(c.comm, full, c.g.nb, dtype_of(T()), c.s);
 }
 
 // Common setup: geometry, buffers, H2D, transform, q.  Returns the context.
@@ -809,38 +831,59 @@ template <typename T>
 void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bool need_labels, Events &E,
            cudaEvent_t e_h2d, cudaEvent_t e_tr, cudaEvent_t e_q) {
     int P = 1, rank = 0;
-    if (c.comm) {
+    c.nranks = c.comm ? comm_size(c.comm) : 1;
+    c.fsplit = c.nranks > 1 && o.multi_gpu == PLSSVM_MULTI_GPU_FEATURES;
+    if (c.comm && !c.fsplit) {
         P = comm_size(c.comm);
         rank = comm_rank(c.comm);
     }
-    c.g = geometry<T>(pb.m, pb.d, P, rank);
+    // Feature split (paper §III-C5): all points, features [f0, f0 + dl) of this rank; the 1/C
+    // terms of Eq. 16 (delta_ij/C and the 1/C inside Q_mm) are added by rank 0 only, so the sum
+    // of the ranks' partial products is Q~p exactly once.
+    int64_t f0 = 0, dl = pb.d;
+    bool root = true;
+    if (c.fsplit) {
+        const int fr = comm_rank(c.comm);
+        f0 = feature_begin(pb.d, c.nranks, fr);
+        dl = feature_begin(pb.d, c.nranks, fr + 1) - f0;
+        root = fr == 0;
+    }
+    c.g = geometry<T>(pb.m, dl, P, rank);
     const Geometry &g = c.g;
     c.kp = KParams<T>{pb.kernel, static_cast<T>(pb.gamma), pb.degree, static_cast<T>(pb.coef0)};
-    c.invC = static_cast<T>(1.0 / pb.C);
+    c.invC = root ? static_cast<T>(1.0 / pb.C) : T(0);
     const bool dev = o.device_pointers != 0;
-    const T *Xs = stage_input<T>(A, pb.X, pb.m * pb.d, dev, c.s);
+    const T *Xs = nullptr;
+    if (c.fsplit) {  // strided copy of the column slice X[:, f0:f0+dl]
+        T *sl = A.alloc<T>(pb.m * dl);
+        PLS_CUDA(cudaMemcpy2DAsync(sl, dl * sizeof(T), static_cast<const T *>(pb.X) + f0, pb.d * sizeof(T),
+                                   dl * sizeof(T), pb.m, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
+        Xs = sl;
+    } else {
+        Xs = stage_input<T>(A, pb.X, pb.m * pb.d, dev, c.s);
+    }
     c.Xraw = Xs;
     c.m = pb.m;
-    c.d = pb.d;
+    c.d = dl;
     if (need_labels) {
         c.ylab = const_cast<T *>(stage_input<T>(A, pb.y, pb.m, dev, c.s));
-        validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * pb.d, V_NONFINITE_X}}, c.ylab, pb.m, c.s, c.launches);
+        validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * dl, V_NONFINITE_X}}, c.ylab, pb.m, c.s, c.launches);
     } else {
         c.ylab = A.alloc<T>(pb.m);
         PLS_CUDA(cudaMemsetAsync(c.ylab, 0, pb.m * sizeof(T), c.s));
-        validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * pb.d, V_NONFINITE_X}}, static_cast<const T *>(nullptr), 0, c.s,
+        validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * dl, V_NONFINITE_X}}, static_cast<const T *>(nullptr), 0, c.s,
                            c.launches);
     }
     PLS_CUDA(cudaEventRecord(e_h2d, c.s));
     c.Xt = A.alloc<T>(g.dpad * g.mpad);
-    launch_transform<T>(Xs, pb.m, pb.d, c.Xt, g.mpad, g.dpad, c.s, c.launches);
+    launch_transform<T>(Xs, pb.m, dl, c.Xt, g.mpad, g.dpad, c.s, c.launches);
     c.ops = make_ops(c.Xt, g.mpad, c.Xt, g.mpad, g.ld);
     c.tc = std::is_same<T, float>::value && o.fp32_engine == 0;
-    if (c.tc) setup_tc<T>(c, A, Xs, pb.m, pb.d);
+    if (c.tc) setup_tc<T>(c, A, Xs, pb.m, dl);
     if constexpr (std::is_same<T, double>::value) {
-        c.oz = oz_choose(o.fp64_engine, {c.Xt}, {g.mpad}, g.dpad, pb.d, A, c.s, c.launches);
+        c.oz = oz_choose(o.fp64_engine, {c.Xt}, {g.mpad}, g.dpad, dl, A, c.s, c.launches);
         if (c.oz) {
-            c.ozx = oz_prepare(A, c.Xt, g.mpad, g.dpad, pb.d, true, true, c.s, c.launches);
+            c.ozx = oz_prepare(A, c.Xt, g.mpad, g.dpad, dl, true, true, c.s, c.launches);
             oz_set_attrs();
         }
     }
@@ -849,7 +892,7 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.nrm = A.alloc<T>(g.mpad);
     c.scal = A.alloc<double>(S_COUNT);
     PLS_CUDA(cudaMemsetAsync(c.scal, 0, S_COUNT * sizeof(double), c.s));
-    k_q_norms<T><<<static_cast<unsigned>(ceil_div(g.mpad * 32, 256)), 256, 0, c.s>>>(c.Xt, g.mpad, g.dpad, pb.m, pb.d,
+    k_q_norms<T><<<static_cast<unsigned>(ceil_div(g.mpad * 32, 256)), 256, 0, c.s>>>(c.Xt, g.mpad, g.dpad, pb.m, dl,
                                                                                       c.kp, c.invC, c.ylab, c.q, c.nrm,
                                                                                       c.scal);
     PLS_CHECK_LAUNCH();
@@ -875,6 +918,7 @@ void configure_product(Ctx<T> &c, Arena &A) {
     c.nsub_eff = c.tc ? 1 : c.oz ? OzC::NSUB : Engine<T>::NSUB;
     c.nsplit = gemv_splits(g);
     c.circ = g.P > 1 && !c.lowrank && (!c.cached || c.packed) && comm_has_reduce_scatter(c.comm);
+    if (c.fsplit) c.yred = A.alloc<T>(g.nb);
     if (c.lowrank) {
         const int64_t r0 = g.g0, r1 = std::min<int64_t>(g.g0 + g.nb, c.m);
         const int64_t rows = std::max<int64_t>(r1 - r0, 1);
@@ -973,6 +1017,10 @@ template <typename T>
 void select_mode(Ctx<T> &c, const plssvm_options_t &o) {
     const Geometry &g = c.g;
     c.lowrank = o.mode == PLSSVM_MODE_LOWRANK;
+    if (c.fsplit) {  // the paper's feature split recomputes the partial entries
+        c.lowrank = c.cached = c.packed = false;
+        return;
+    }
     const bool can_pack = g.P == 1 || (c.comm && comm_has_reduce_scatter(c.comm));
     const int64_t need = (can_pack ? packed_tile_count(g) * kTile * kTile : g.nb * g.mpad) * static_cast<int64_t>(sizeof(T));
     c.cached = !c.lowrank && choose_cached<T>(g, o, c.comm, c.s, need);
@@ -1058,47 +1106,121 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     double t_mv = 0.0, t_mv_min = 1e30;
     int64_t it = 0;
     c.cur_ctrl = c.ctrl;
-    while (true) {
-        for (int b = 0; b < kBatch; ++b) {
-            const int64_t k = it + b;  // iteration index if the loop is still running
-            const int par = static_cast<int>(k & 1);
-            PLS_CUDA(cudaEventRecord(mv0[b], c.s));
-            const int ns = launch_qtilde_product<T>(c, c.p);
-            PLS_CUDA(cudaEventRecord(mv1[b], c.s));
-            finalize<T>(c, ns, pband, 0, nullptr, 0, 0);
-            allreduce(c, S_PAP, 1);
-            k_update_xr<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.y, g.nb, c.scal, c.ctrl, c.partials,
-                                                                c.counter);
-            PLS_CHECK_LAUNCH();
-            ++c.launches;
+    // One CG iteration (a3 product, a4 fused updates, a5 test in k_update_p, a8 exchanges).
+    // k = host-side iteration index (only the residual-replacement period uses it); `loop` /
+    // `use_loop`: the CUDA-graph WHILE condition k_update_p sets.
+    auto enqueue_iteration = [&](int64_t k, cudaEvent_t ev0, cudaEvent_t ev1, cudaGraphConditionalHandle loop,
+                                 int use_loop) {
+        const int par = static_cast<int>(k & 1);
+        if (ev0) PLS_CUDA(cudaEventRecord(ev0, c.s));
+        const int ns = launch_qtilde_product<T>(c, c.p);
+        if (ev1) PLS_CUDA(cudaEventRecord(ev1, c.s));
+        finalize<T>(c, ns, pband, 0, nullptr, 0, 0);
+        allreduce(c, S_PAP, 1);
+        k_update_xr<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.y, g.nb, c.scal, c.ctrl, c.partials,
+                                                            c.counter);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        allreduce(c, S_DELTA + (par ^ 1), 1);
+        if (o.replace_every > 0 && k > 0 && k % o.replace_every == 0) {
+            // explicit residual r = rhs - Q~x (Shewchuk B2 replacement, option R > 0)
+            PLS_CUDA(cudaMemcpyAsync(c.xfull + g.g0, c.x, g.nb * sizeof(T), cudaMemcpyDeviceToDevice, c.s));
+            allgather(c, c.xfull);
+            const int ns2 = launch_qtilde_product<T>(c, c.xfull);
+            finalize<T>(c, ns2, nullptr, 1, nullptr, -1, 0);
             allreduce(c, S_DELTA + (par ^ 1), 1);
-            if (o.replace_every > 0 && k > 0 && k % o.replace_every == 0) {
-                // explicit residual r = rhs - Q~x (Shewchuk B2 replacement, option R > 0)
-                PLS_CUDA(cudaMemcpyAsync(c.xfull + g.g0, c.x, g.nb * sizeof(T), cudaMemcpyDeviceToDevice, c.s));
-                allgather(c, c.xfull);
-                const int ns2 = launch_qtilde_product<T>(c, c.xfull);
-                finalize<T>(c, ns2, nullptr, 1, nullptr, -1, 0);
-                allreduce(c, S_DELTA + (par ^ 1), 1);
-            }
-            k_update_p<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter);
-            PLS_CHECK_LAUNCH();
-            ++c.launches;
-            allgather(c, c.p);
         }
+        k_update_p<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter, loop,
+                                                           use_loop);
+        PLS_CHECK_LAUNCH();
+        ++c.launches;
+        allgather(c, c.p);
+    };
+    const bool graph_ok = c.comm == nullptr && o.replace_every <= 0;
+    const bool use_graph = graph_ok && (o.cg_loop == PLSSVM_CG_GRAPH ||
+                                        (o.cg_loop == PLSSVM_CG_AUTO && (c.cached || c.lowrank || g.m1 <= 8192)));
+    if (o.cg_loop == PLSSVM_CG_GRAPH && !graph_ok)
+        throw Error(PLSSVM_E_INVALID_ARG, "cg_loop GRAPH needs a single GPU (no comm) and replace_every = 0");
+    if (use_graph) {
+        // The whole loop as ONE graph launch: entry kernel sets the WHILE
+        // condition from the control block, the body (captured once) is one iteration, and
+        // k_update_p's last block clears the condition when Shewchuk's loop condition fails.
+        cudaStream_t cap = nullptr;
+        cudaGraph_t G = nullptr;
+        cudaGraphExec_t GE = nullptr;
+        struct GraphFree {
+            cudaStream_t &s;
+            cudaGraph_t &g;
+            cudaGraphExec_t &e;
+            ~GraphFree() {
+                if (e) cudaGraphExecDestroy(e);
+                if (g) cudaGraphDestroy(g);
+                if (s) cudaStreamDestroy(s);
+            }
+        } gf{cap, G, GE};
+        PLS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        PLS_CUDA(cudaGraphCreate(&G, 0));
+        cudaGraphConditionalHandle loop;
+        PLS_CUDA(cudaGraphConditionalHandleCreate(&loop, G, 0u, 0u));
+        cudaKernelNodeParams kn = {};
+        const int *ctrl_c = c.ctrl;
+        void *kargs[] = {&loop, &ctrl_c};
+        kn.func = reinterpret_cast<void *>(k_cg_loop_init);
+        kn.gridDim = dim3(1);
+        kn.blockDim = dim3(1);
+        kn.kernelParams = kargs;
+        cudaGraphNode_t n0, nw;
+        PLS_CUDA(cudaGraphAddKernelNode(&n0, G, nullptr, 0, &kn));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = loop;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        PLS_CUDA(cudaGraphAddNode(&nw, G, &n0, 1, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        const int64_t l0 = c.launches;
+        cudaStream_t s_run = c.s;
+        c.s = cap;
+        PLS_CUDA(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_iteration(0, nullptr, nullptr, loop, 1);
+        } catch (...) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(cap, &junk);
+            c.s = s_run;
+            throw;
+        }
+        PLS_CUDA(cudaStreamEndCapture(cap, &body));
+        c.s = s_run;
+        const int64_t per_it = c.launches - l0;
+        c.launches = l0;
+        PLS_CUDA(cudaGraphInstantiate(&GE, G, 0ull));
+        PLS_CUDA(cudaGraphLaunch(GE, c.s));
         PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
         PLS_CUDA(cudaMemcpyAsync(hctrl, c.ctrl, C_COUNT * sizeof(int), cudaMemcpyDeviceToHost, c.s));
         PLS_CUDA(cudaStreamSynchronize(c.s));
-        const int64_t ran = hctrl[C_IT] - it;  // iterations of this batch that did work
-        for (int b = 0; b < ran && b < kBatch; ++b) {
-            const double tm = elapsed(mv0[b], mv1[b]);
-            t_mv += tm;
-            t_mv_min = std::min(t_mv_min, tm);
-        }
         it = hctrl[C_IT];
-        if (std::getenv("PLSSVM_DEBUG"))
-            std::fprintf(stderr, "[plssvm] batch: it=%d done=%d d0=%.6e d[0]=%.6e d[1]=%.6e thr=%.6e pap=%.6e\n",
-                         hctrl[C_IT], hctrl[C_DONE], hs[S_DELTA0], hs[S_DELTA], hs[S_DELTA + 1], hs[S_THR], hs[S_PAP]);
-        if (hctrl[C_DONE] != 0 || ran < kBatch) break;
+        c.launches += 1 + per_it * it;
+        c.graph_used = true;
+    } else {
+        while (true) {
+            for (int b = 0; b < kBatch; ++b) enqueue_iteration(it + b, mv0[b], mv1[b], 0ull, 0);
+            PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+            PLS_CUDA(cudaMemcpyAsync(hctrl, c.ctrl, C_COUNT * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+            PLS_CUDA(cudaStreamSynchronize(c.s));
+            const int64_t ran = hctrl[C_IT] - it;  // iterations of this batch that did work
+            for (int b = 0; b < ran && b < kBatch; ++b) {
+                const double tm = elapsed(mv0[b], mv1[b]);
+                t_mv += tm;
+                t_mv_min = std::min(t_mv_min, tm);
+            }
+            it = hctrl[C_IT];
+            if (std::getenv("PLSSVM_DEBUG"))
+                std::fprintf(stderr, "[plssvm] batch: it=%d done=%d d0=%.6e d[0]=%.6e d[1]=%.6e thr=%.6e pap=%.6e\n",
+                             hctrl[C_IT], hctrl[C_DONE], hs[S_DELTA0], hs[S_DELTA], hs[S_DELTA + 1], hs[S_THR],
+                             hs[S_PAP]);
+            if (hctrl[C_DONE] != 0 || ran < kBatch) break;
+        }
     }
     c.cur_ctrl = nullptr;
     int64_t matvecs = it + ((o.x0 == 0) ? 0 : 1);
@@ -1114,6 +1236,12 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
 
     if (status != PLSSVM_E_NUMERICAL) {
         // ---- bias + alpha (a6) ----
+        if constexpr (std::is_same<T, double>::value) {
+            if (c.fsplit) {  // Eq. 15 needs the full q and Q_mm: sum the ranks' feature-slice partials
+                comm_allreduce_sum_f64(c.comm, c.q, c.q, g.mpad, c.s);
+                comm_allreduce_sum_f64(c.comm, c.scal + S_QMM, c.scal + S_QMM, 1, c.s);
+            }
+        }
         k_bias_sums<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.q, g.nb, g.g0, c.scal, 0, c.partials, c.counter);
         PLS_CHECK_LAUNCH();
         k_bias_sums<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.q, g.nb, g.g0, c.scal, 1, c.partials, c.counter);
@@ -1140,7 +1268,8 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         st->matvecs = matvecs;
         st->rel_residual = delta0 > 0 ? std::sqrt(delta / delta0) : 0.0;
         st->mode_used = c.lowrank ? PLSSVM_MODE_LOWRANK : (c.cached ? PLSSVM_MODE_CACHED : PLSSVM_MODE_IMPLICIT);
-        st->num_ranks = g.P;
+        st->num_ranks = c.nranks;
+        st->cg_loop_used = c.graph_used ? PLSSVM_CG_GRAPH : PLSSVM_CG_BATCHED;
         st->t_h2d = elapsed(e0, e_h2d);
         st->t_transform = elapsed(e_h2d, e_tr);
         st->t_q = elapsed(e_tr, e_q);

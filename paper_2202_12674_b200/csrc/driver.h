@@ -20,6 +20,9 @@ struct Problem {
 
 struct CommHandle;  // comm.cu
 
+// Feature split of PLSSVM_MULTI_GPU_FEATURES: rank r owns features [feature_begin(r), feature_begin(r+1)).
+inline int64_t feature_begin(int64_t d, int nranks, int rank) { return d * rank / nranks; }
+
 // Each returns a plssvm_status_t and throws plssvm::Error for CUDA / NCCL failures.
 int train(const Problem &pb, const plssvm_options_t &o, void *alpha, void *b, plssvm_stats_t *st);
 int predict(const Problem &pb, const void *alpha, double b, const void *Z, int64_t n, const plssvm_options_t &o,

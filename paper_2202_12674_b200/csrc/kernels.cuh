@@ -7,7 +7,7 @@
 //   k_gemv_tiled       y_band = Q~_band p streamed from HBM (tiled layout)
 //   k_finalize         y = sum_slots Ypart ; p.y  (deterministic)
 //   k_update_xr        x += a p ; r -= a y ; r.r  (fused axpy + norm)
-//   k_update_p         p = r + b p
+//   k_update_p         p = r + b p ; loop condition (and the CUDA-graph WHILE condition)
 //   k_init / k_bias    CG start, Eq. 15 bias + alpha assembly
 //   k_predict          f(z) = sum_i alpha_i k(x_i, z) + b                (Eq. 10)
 #pragma once
@@ -654,8 +654,11 @@ __global__ void __launch_bounds__(kVecThreads)
 template <typename T>
 __global__ void __launch_bounds__(kVecThreads)
     k_update_p(T *__restrict__ p, const T *__restrict__ r, int64_t nb, const double *scal, int *ctrl,
-               unsigned *counter) {
-    if (cg_done(ctrl)) return;
+               unsigned *counter, cudaGraphConditionalHandle loop, int use_loop) {
+    if (cg_done(ctrl)) {
+        if (use_loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0u);
+        return;
+    }
     const int par = ctrl[C_IT] & 1;
     const T b = static_cast<T>(scal[S_DELTA + (par ^ 1)] / scal[S_DELTA + par]);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
@@ -679,7 +682,14 @@ __global__ void __launch_bounds__(kVecThreads)
         ctrl[C_IT] = it;
         ctrl[C_DONE] = done;
         *counter = 0u;
+        // CUDA-graph CG loop (plssvm_cg_loop_t GRAPH): the WHILE node repeats while not done
+        if (use_loop) cudaGraphSetConditional(loop, done == 0 ? 1u : 0u);
     }
+}
+
+// Entry node of the CUDA-graph CG loop: the WHILE condition = "not done" (k_cg_start's verdict).
+__global__ void k_cg_loop_init(cudaGraphConditionalHandle loop, const int *ctrl) {
+    cudaGraphSetConditional(loop, ctrl[C_DONE] == 0 ? 1u : 0u);
 }
 
 // Loop entry (after delta_0 is final on every rank): threshold and control block.

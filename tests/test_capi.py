@@ -29,7 +29,7 @@ def exported_symbols():
 def test_library_loads_and_exports_every_declared_symbol():
     L = pl.load()
     decl = declared_symbols()
-    assert len(decl) == 16
+    assert len(decl) == 17
     for name in decl:
         assert hasattr(L, name), name
     assert exported_symbols() == decl  # nothing else is public
@@ -46,6 +46,7 @@ def test_default_options():
     o = pl.options()
     assert (o.mode, o.x0, o.max_iter, o.replace_every, o.fixed_iter, o.device, o.device_pointers) == (0, 0, 0, 0, 0, 0, 0)
     assert o.stream is None and o.comm is None
+    assert (o.cg_loop, o.multi_gpu) == (pl.CG_AUTO, pl.MULTI_GPU_ROWS)
 
 
 @pytest.mark.parametrize("m,P", [(2, 1), (256, 1), (16384, 1), (16384, 8), (1000, 3), (65536, 8), (131072, 8)])
@@ -58,6 +59,25 @@ def test_partition_rule(m, P):
         assert e0 == b1
     sizes = {e - b for b, e, _ in bands}
     assert len(sizes) == 1 and sizes.pop() % 128 == 0
+
+
+@pytest.mark.parametrize("d,P", [(1, 1), (16, 1), (17, 2), (1024, 8), (4096, 8), (30, 4), (8, 8), (13, 3)])
+def test_feature_partition_rule(d, P):
+    """MULTI_GPU_FEATURES (paper §III-C5): contiguous feature slices covering [0, d)
+    exactly once, sizes differing by at most one, none empty."""
+    sl = [pl.plssvm_feature_partition(d, P, r) for r in range(P)]
+    assert sl[0][0] == 0 and sl[-1][1] == d
+    for (b0, e0), (b1, e1) in zip(sl, sl[1:]):
+        assert e0 == b1
+    sizes = [e - b for b, e in sl]
+    assert min(sizes) >= 1 and max(sizes) - min(sizes) <= 1 and sum(sizes) == d
+
+
+def test_feature_partition_invalid():
+    with pytest.raises(pl.PlssvmError):
+        pl.plssvm_feature_partition(3, 4, 0)  # d < P
+    with pytest.raises(pl.PlssvmError):
+        pl.plssvm_feature_partition(8, 2, 2)
 
 
 def test_partition_invalid():

@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, path, kernel, mode, m, d, circ):
+def _worker(rank, world, port, path, kernel, mode, m, d, circ, mg=0, x0=0):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -36,10 +36,10 @@ def _worker(rank, world, port, path, kernel, mode, m, d, circ):
     comm = pl.comm_host_staged(0, circulant=circ)
     X, y, Z, _ = synth.planes(m, d, 64, seed=21 + kernel)
     p = np.random.default_rng(5).standard_normal(m - 1)
-    opts = pl.options(mode=mode, comm=comm)
+    opts = pl.options(mode=mode, comm=comm, multi_gpu=mg)
     out, _ = pl.plssvm_qtilde_matvec(X, p, kernel, 1.0 / d, 3, 0.5, 1.0, opts=opts)
     alpha, b, st, stats = pl.plssvm_train_ex(X, y, kernel, 1.0 / d, 3, 0.5, 1.0, 1e-10,
-                                             opts=pl.options(mode=mode, comm=comm))
+                                             opts=pl.options(mode=mode, comm=comm, multi_gpu=mg, x0=x0))
     if rank == 0:
         np.savez(path, out=out, alpha=alpha, b=b, st=st, it=stats.iterations, ranks=stats.num_ranks,
                  mode_used=stats.mode_used)
@@ -77,5 +77,30 @@ def test_row_sharded_train_matches_oracle(tmp_path, world, kernel, mode, m, d, c
     assert np.linalg.norm(r["out"] - ref) <= 1e-12 * np.linalg.norm(ref)
     a_ref, b_ref, it_ref, _ = oracle.train(X, y, kernel, 1.0 / d, 3, 0.5, 1.0, 1e-10)
     assert int(r["st"]) == 0 and int(r["ranks"]) == world and int(r["mode_used"]) == mode
+    assert np.linalg.norm(r["alpha"] - a_ref) <= 1e-7 * np.linalg.norm(a_ref)
+    assert abs(float(r["b"]) - b_ref) <= 1e-7 * max(abs(b_ref), np.abs(a_ref).max())
+
+
+@pytest.mark.parametrize("world,m,d,x0", [
+    (2, 1000, 33, 0),   # ragged features (17 + 16), ragged points
+    (3, 700, 20, 0),    # 3 ranks: 6 + 7 + 7 features
+    (4, 1500, 9, 0),    # 4 ranks, 2-3 features each (smaller than one 32-feature slab)
+    (2, 900, 64, 1),    # x0 = ones: initial product through the all-reduce too
+])
+def test_feature_split_train_matches_oracle(tmp_path, world, m, d, x0):
+    """MULTI_GPU_FEATURES (paper §III-C5): every rank computes the partial Q~p of its
+    feature slice (1/C terms on rank 0 only), one all-reduce per product; linear kernel."""
+    import oracle
+    import synth
+
+    path = str(tmp_path / "r.npz")
+    mp.spawn(_worker, args=(world, _free_port(), path, 0, 0, m, d, True, 1, x0), nprocs=world, join=True)
+    r = np.load(path)
+    X, y, _, _ = synth.planes(m, d, 64, seed=21)
+    p = np.random.default_rng(5).standard_normal(m - 1)
+    ref = oracle.qtilde(X, 0, 1.0 / d, 3, 0.5, 1.0) @ p
+    assert np.linalg.norm(r["out"] - ref) <= 1e-12 * np.linalg.norm(ref)
+    a_ref, b_ref, _, _ = oracle.train(X, y, 0, 1.0 / d, 3, 0.5, 1.0, 1e-10, x0=x0)
+    assert int(r["st"]) == 0 and int(r["ranks"]) == world and int(r["mode_used"]) == 1
     assert np.linalg.norm(r["alpha"] - a_ref) <= 1e-7 * np.linalg.norm(a_ref)
     assert abs(float(r["b"]) - b_ref) <= 1e-7 * max(abs(b_ref), np.abs(a_ref).max())

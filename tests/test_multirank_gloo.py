@@ -133,3 +133,63 @@ def test_circulant_pairs_cover_each_unordered_pair_once_and_balance(T, P):
     assert len(seen) == T * (T + 1) // 2 and set(seen.values()) == {1}
     loads = [len(t) for t in ranks]
     assert max(loads) / min(loads) <= 1 + 2.0 / T + 1e-12 or T < 16
+
+
+def _worker_features(rank, world, port, result_path):
+    """MULTI_GPU_FEATURES host logic (paper §III-C5): rank g holds the feature slice
+    from plssvm_feature_partition and forms its partial Q~^(g) of Eq. 16 on that slice, with
+    the 1/C terms on rank 0 only (C = inf elsewhere); one all-reduce of the partial products per
+    iteration, replicated CG vectors.  Must reproduce the single-process Q~p and CG solution."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    import paper_2202_12674_b200 as pl
+    import synth
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, y, _, _ = synth.planes(260, 11, seed=4)
+    m1 = X.shape[0] - 1
+    f0, f1 = pl.plssvm_feature_partition(X.shape[1], world, rank)
+    Qg = oracle.qtilde(np.ascontiguousarray(X[:, f0:f1]), oracle.LINEAR, C=2.0 if rank == 0 else np.inf)
+
+    def product(p):  # partial product of this slice, summed over the ranks
+        t = torch.from_numpy(Qg @ p)
+        dist.all_reduce(t)
+        return t.numpy()
+
+    p = np.random.default_rng(2).standard_normal(m1)
+    yfull = product(p)
+    rhs = y[:-1] - y[-1]
+    x = np.zeros(m1)
+    r = rhs.copy()
+    pv = r.copy()
+    delta = delta0 = r @ r
+    it = 0
+    while it < m1 and delta > 1e-20 * delta0:
+        yv = product(pv)
+        a = delta / (pv @ yv)
+        x += a * pv
+        r -= a * yv
+        dnew = r @ r
+        pv = r + (dnew / delta) * pv
+        delta = dnew
+        it += 1
+    if rank == 0:
+        Qt = oracle.qtilde(X, oracle.LINEAR, C=2.0)
+        xo, ito, _ = oracle.cg(Qt, rhs, eps=1e-10)
+        np.savez(result_path, y=yfull, ref_y=Qt @ p, x=x, ref_x=xo, it=it, ito=ito)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_feature_split_cg_gloo(tmp_path, world):
+    path = str(tmp_path / "res.npz")
+    mp.spawn(_worker_features, args=(world, _free_port(), path), nprocs=world, join=True)
+    res = np.load(path)
+    assert np.linalg.norm(res["y"] - res["ref_y"]) <= 1e-13 * np.linalg.norm(res["ref_y"])
+    assert np.linalg.norm(res["x"] - res["ref_x"]) <= 1e-8 * np.linalg.norm(res["ref_x"])
+    assert abs(int(res["it"]) - int(res["ito"])) <= 2

@@ -16,7 +16,7 @@ for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     a, b, st, s = pl.plssvm_train_ex(tX, ty, cfg.kernel, cfg.gamma, C=cfg.C, eps=cfg.eps,
-                                     opts=pl.options(mode=pl.MODE_IMPLICIT))
+                                     opts=pl.options(mode=pl.MODE_IMPLICIT, cg_loop=int(os.environ.get("CG_LOOP", "0"))))
     torch.cuda.synchronize()
     t = time.perf_counter() - t0
     if rep % 5 == 4:
