@@ -24,16 +24,18 @@
 // 128 B/clk at N = 128 = the smem bandwidth, 192 B/clk at N = 64 -- measured: tc pipe 84 %
 // busy, imma 46 % with 128 x 64 tiles), at the same L2 traffic per output element.
 // Persistent CTA pairs (one CTA per SM), warp-specialised:
-//   warp 8 (one lane) : TMA producer -- per 32-feature slab ONE 3-D box per operand brings the
+//   warp 0 (one lane) : TMA producer -- per 32-feature slab ONE 3-D box per operand brings the
 //                       pass's digit planes (32 B x 128 rows x 4|8 planes, SWIZZLE_32B)
-//   warp 9 (one lane) : TMEM owner; in the leader CTA the MMA issuer -- per slab the pass's digit pairs (K = 32 UMMAs)
+//   warp 1 (one lane) : TMEM owner; in the leader CTA the MMA issuer -- per slab the pass's digit pairs (K = 32 UMMAs)
 //                       into the level accumulators; tcgen05.commit frees the stage / signals
 //                       the pass
-//   warps 0-7         : epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows), columns
-//                       64(w/4).. of every level (tcgen05.ld 32x32b.x8), Horner-combines them in
-//                       fp64 (pass 0 -> w in fp32; pass 1 -> v + 2^-32 w, then the kernel
-//                       function / Eq. 16 corrections and the row / column contributions, 8
-//                       columns at a time), releasing the accumulators after each pass.
+//   warps 2-3         : idle (warpgroup 0 gives its registers to the epilogue: setmaxnreg 40 / 232)
+//   warps 4-11        : epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows), columns
+//                       64((w-4)/4).. of every level (tcgen05.ld 32x32b.x8), Horner-combines them
+//                       in fp64 (pass 0 -> w in fp32; pass 1 -> the 64 contractions v + 2^-32 w in
+//                       registers), releases the accumulators after each pass, and only then runs
+//                       the kernel function / Eq. 16 corrections and the row / column contributions
+//                       -- overlapped with the next pair-tile's MMAs.
 // Slot conventions: those of k_matvec_implicit with 128-wide column blocks (NSUB = 1).
 #pragma once
 #include <cuda.h>
@@ -56,7 +58,8 @@ struct Oz {
     static constexpr uint32_t PLANE = kTile * BK;                  // 4 KiB: one A digit plane (B half: 2 KiB)
     static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: S planes of A and of the B half
     static constexpr int EPI_WARPS = 8;
-    static constexpr int THREADS = (EPI_WARPS + 2) * 32;
+    static constexpr int THREADS = (EPI_WARPS + 4) * 32;             // warpgroup 0: control, 1-2: epilogue
+    static constexpr int CTRL_REGS = 40, EPI_REGS = 232;            // setmaxnreg split (4x40 + 8x232 <= 512 per lane)
     static constexpr int TMEM_COLS = 512;
     static_assert(LV * TN <= TMEM_COLS && LV0 * TN <= TMEM_COLS, "a pass's level accumulators must fit TMEM");
     // misc: barriers (256 B) + column data 4 x 128 doubles + row partials 2 x 128 + col partials 4 x 128
@@ -306,7 +309,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    if (warp == 8 && lane == 0) {
+    if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta4)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta8)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb4)) : "memory");
@@ -319,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
         mbar_init(tempty, 2 * O::EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
-    if (warp == 9) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_sh)),
                      "n"(O::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -346,7 +349,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
         }
     };
 
-    if (warp == 8) {
+    // Register split by warpgroup: the control warps need few, the epilogue keeps a pass's 64
+    // fp64 contractions in registers (so the accumulators are released before the fp64 work).
+    // (each role branch starts with its setmaxnreg, so the allocator sees the new budget)
+    if (warp == 0) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(O::CTRL_REGS));
         if (lane == 0) {  // ---- TMA producer (both CTAs): this CTA's A block and B half
             uint32_t g = 0;
             for (int t = pair; t < ntiles; t += npairs) {
@@ -374,7 +381,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 }
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == 1) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(O::CTRL_REGS));
         if (leader && lane == 0) {  // ---- MMA issuer (leader only): level l = a + b
             uint32_t g = 0, e = 0;  // e: accumulator events (two per pair-tile)
             for (int t = pair; t < ntiles; t += npairs) {
@@ -417,10 +425,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 }
             }
         }
-    } else {  // ---- epilogue warps 0-7 (both CTAs): row 32(w%4) + lane, columns 64(w/4) .. +63
-        const int quarter = warp & 3, grp = warp >> 2;
+    } else if (warp < 4) {  // idle warps 2-3
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(O::CTRL_REGS));
+    } else {  // ---- epilogue warps 4-11 (both CTAs): row 32(w%4) + lane, columns 64((w-4)/4) .. +63
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(O::EPI_REGS));
+        const int quarter = warp & 3, grp = (warp - 4) >> 2;
         const int lr = quarter * 32 + lane;
-        const int et = threadIdx.x;  // 0..255
+        const int et = threadIdx.x - 128;  // 0..255
         const double Qmm = (MODE == OZ_PREDICT) ? 0.0 : scal[S_QMM];
         uint32_t e = 0;
         for (int t = pair; t < ntiles; t += npairs) {
@@ -463,46 +474,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     if (T_tiles >= 0 && mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
                 }
             }
+            // Pass 0: drain levels 4-6 into wl (fp32), release the accumulators.
+            mbar_wait(tfull, e & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            ++e;
+            if (!(dbg & 1)) {
 #pragma unroll
-            for (int pass = 0; pass < 2; ++pass, ++e) {
-                mbar_wait(tfull, e & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                if (dbg & 1) {  // experiment: no epilogue
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(tempty0);
-                    continue;
-                }
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {  // 8-column chunks
-                    uint32_t r0[8], r1[8], r2[8], r3[8];
-                    const int nl = pass == 0 ? LV0 : LV;  // levels of this pass (TMEM blocks 0..nl-1)
-                    if (nl > 3) tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t r0[8], r1[8], r2[8];
                     tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
                     tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
                     tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
                     tmem_ld_wait();
-                    double w[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {  // Horner in base 2^-8, highest level first
-                        double h = i2d_exact(r2[j]);
-                        if (nl > 3) h = fma(i2d_exact(r3[j]), 0.00390625, h);
-                        h = fma(h, 0.00390625, i2d_exact(r1[j]));
-                        w[j] = fma(h, 0.00390625, i2d_exact(r0[j]));
+                        const double h = fma(i2d_exact(r2[j]), 0.00390625, i2d_exact(r1[j]));
+                        wl[c * 8 + j] = static_cast<float>(fma(h, 0.00390625, i2d_exact(r0[j])));
                     }
-                    if (pass == 0) {
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty0);  // the MMA may start pass 1
+            // Pass 1: drain levels 0-3 and finish the contraction sv (fp64, 64 columns in registers),
+            // then release the accumulators BEFORE the kernel function / Eq. 16 / row and column
+            // sums, so the MMAs of the next pair-tile's pass 0 overlap this fp64 work (the epilogue
+            // is fp64-pipe bound: ~40 DP ops per entry, ~20 % of a C1 tile when serialised).
+            mbar_wait(tfull, e & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            ++e;
+            double sv[64];
+            if (!(dbg & 1)) {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) wl[c * 8 + j] = static_cast<float>(w[j]);
-                        continue;
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t r0[8], r1[8], r2[8], r3[8];
+                    tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
+                    tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
+                    tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
+                    tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        double h = fma(i2d_exact(r3[j]), 0.00390625, i2d_exact(r2[j]));
+                        h = fma(h, 0.00390625, i2d_exact(r1[j]));
+                        h = fma(h, 0.00390625, i2d_exact(r0[j]));
+                        const int lc = grp * 64 + c * 8 + j;
+                        sv[c * 8 + j] = fma(static_cast<double>(wl[c * 8 + j]), 0x1p-32, h) * (sci * colsc[lc]);
                     }
-                    // ---- pass 1: finished contractions of columns c*8 .. c*8+7 of this thread's 64
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty0);  // the next pair-tile's MMAs may start
+            if (!(dbg & 1)) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {  // 8-column chunks of this thread's 64 columns
+                    double w[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int lc = grp * 64 + c * 8 + j;
-                        const double sv = fma(static_cast<double>(wl[c * 8 + j]), 0x1p-32, w[j]) * (sci * colsc[lc]);
                         if constexpr (MODE == OZ_PREDICT) {
-                            rs = fma(colp[lc], kernel_value<KT, double>(sv, ni, coln[lc], false, kp), rs);
+                            rs = fma(colp[lc], kernel_value<KT, double>(sv[c * 8 + j], ni, coln[lc], false, kp), rs);
                         } else {
-                            w[j] = qtilde_value<KT, double>(sv, gi, col0 + lc, ni, coln[lc], qi, colq[lc], Qmm, invC, m1, kp);
+                            w[j] = qtilde_value<KT, double>(sv[c * 8 + j], gi, col0 + lc, ni, coln[lc], qi, colq[lc], Qmm,
+                                                            invC, m1, kp);
                         }
                     }
                     if constexpr (MODE == OZ_MATVEC) {
@@ -543,9 +578,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         }
                     }
                 }
-                asm volatile("tcgen05.fence::before_thread_sync;");
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(tempty0);  // the leader's MMA may overwrite the accumulators
             }
 
             if constexpr (MODE == OZ_MATVEC) {
@@ -572,7 +604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     cluster_sync_all();  // no more MMAs into either CTA's TMEM, no more remote arrives
-    if (warp == 9) {
+    if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;");
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(O::TMEM_COLS));
     }
