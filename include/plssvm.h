@@ -66,7 +66,8 @@ typedef enum {
     PLSSVM_E_CUDA = 4,         /* CUDA runtime error / no device */
     PLSSVM_E_NCCL = 5,         /* NCCL error in row-sharded mode */
     PLSSVM_E_NUMERICAL = 6,    /* CG breakdown: p.Q~p <= 0 or non-finite */
-    PLSSVM_W_NOT_CONVERGED = 7 /* max_iter reached before ||r|| <= eps ||r0||; alpha, b filled */
+    PLSSVM_W_NOT_CONVERGED = 7, /* max_iter reached before ||r|| <= eps ||r0||; alpha, b filled */
+    PLSSVM_E_IO = 8            /* file open / read / write failure or malformed file (message names the line) */
 } plssvm_status_t;
 
 typedef enum { PLSSVM_F64 = 0, PLSSVM_F32 = 1 } plssvm_dtype_t;
@@ -238,6 +239,46 @@ PLSSVM_API int plssvm_partition(int64_t m, int32_t nranks, int32_t rank, int64_t
  * owns features [f_begin, f_end) = [rank*d/nranks, (rank+1)*d/nranks) (integer division, so the
  * slices differ by at most one feature).  d >= nranks >= 1. */
 PLSSVM_API int plssvm_feature_partition(int64_t d, int32_t nranks, int32_t rank, int64_t *f_begin, int64_t *f_end);
+
+/* ---- LIBSVM files and scaling -----------------------------------
+ * The read / write steps around the hot path (the paper's runtime components, Fig. 2,
+ * P:624-632) and the LIBSVM drop-in formats.  Host-only, no GPU needed; native
+ * C++ (io.cpp), multi-threaded parse.  Paths are NUL-terminated file names.  Numbers are
+ * parsed correctly rounded and written as %.17g, so files round-trip bit-exactly.
+ *
+ * plssvm_libsvm_read: data file, one point per line "<label> <index>:<value> ...", 1-based
+ *   strictly ascending indices, blank / '#' lines skipped, LF or CRLF.  Sparse
+ *   input becomes dense (absent features are 0).  Outputs: m points, d = the
+ *   largest index, labels[0..nlabels) = the distinct label values in first-seen order
+ *   (nlabels 1 or 2; a third label -> PLSSVM_E_LABELS).  Query mode: X or y NULL -> only m, d,
+ *   labels, nlabels are written.  Otherwise needs cap_m >= m, cap_d >= max(d, 1): X[i*cap_d + k]
+ *   (row stride cap_d, features >= d set to 0) and y[i] = the RAW label of point i (map it to
+ *   +1 / -1 yourself, e.g. labels[0] -> +1 as the CLI does). */
+PLSSVM_API int plssvm_libsvm_read(const char *path, double *X, double *y, int64_t cap_m, int64_t cap_d, int64_t *m,
+                                  int64_t *d, double *labels /* [2] */, int32_t *nlabels);
+/* X [m*d] point-major, y [m] labels: "<y_i> <k+1>:<x_ik> ..." per point, zero features omitted. */
+PLSSVM_API int plssvm_libsvm_write(const char *path, const double *X, const double *y, int64_t m, int64_t d);
+/* LIBSVM c_svc model file of a trained LS-SVM: header svm_type c_svc, kernel_type,
+ * degree (poly) / gamma (poly, rbf) / coef0 (poly), nr_class 2, total_sv m, rho = -b, label
+ * labels[0] labels[1] (the original labels of y = +1 and y = -1), nr_sv n+ n-, SV; then one line
+ * per training point "<alpha_i> <k>:<x_ik> ..." -- every LS-SVM point is a support vector, the
+ * y = +1 points first (LIBSVM's class grouping), each group in input order.  y [m] = +1 / -1. */
+PLSSVM_API int plssvm_model_write(const char *path, int kernel, double gamma, int degree, double coef0,
+                                  const double *X, const double *alpha, double b, int64_t m, int64_t d,
+                                  const double *y, const double *labels /* [2] */);
+/* Reads a model written by plssvm_model_write or an equivalent LIBSVM c_svc model:
+ * unknown kernel_type, nr_class != 2, or a missing mandatory field -> PLSSVM_E_IO with the field
+ * named.  b = -rho; labels[0] is predicted for f >= 0.  Query mode: X or alpha NULL.  Otherwise
+ * cap_m >= m, cap_d >= max(d, 1), X row stride cap_d. */
+PLSSVM_API int plssvm_model_read(const char *path, int32_t *kernel, double *gamma, int32_t *degree, double *coef0,
+                                 double *X, double *alpha, double *b, int64_t cap_m, int64_t cap_d, int64_t *m,
+                                 int64_t *d, double *labels /* [2] */);
+/* svm-scale: per-feature ranges over all m points (zeros included) ... */
+PLSSVM_API int plssvm_scale_fit(const double *X, int64_t m, int64_t d, double *fmin /* [d] */, double *fmax /* [d] */);
+/* ... and the affine map x -> lo + (hi - lo) (x - min) / (max - min), constant features -> lo, no
+ * clamping (values outside the fitted range map outside [lo, hi]).  In place.  lo < hi. */
+PLSSVM_API int plssvm_scale_apply(double *X, int64_t m, int64_t d, const double *fmin, const double *fmax, double lo,
+                                  double hi);
 
 /* ---- misc ------------------------------------------------------------------------------ */
 PLSSVM_API const char *plssvm_last_error(void); /* thread-local; "" when the last call succeeded */

@@ -9,4 +9,6 @@ from .binding import (  # noqa: F401
     plssvm_feature_partition,
     plssvm_version, plssvm_device_count, plssvm_last_error, plssvm_comm_unique_id, plssvm_comm_init,
     plssvm_comm_destroy, plssvm_comm_init_callbacks, comm_from_torch_distributed, comm_host_staged,
+    plssvm_libsvm_read, plssvm_libsvm_write, plssvm_model_write, plssvm_model_read, plssvm_scale_fit,
+    plssvm_scale_apply, cli_path,
 )

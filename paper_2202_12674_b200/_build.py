@@ -13,8 +13,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libplssvm_b200.so")
-SOURCES = ["capi.cu", "driver.cu", "comm.cu"]
-HEADERS = ["common.cuh", "tile_engine.cuh", "kernels.cuh", "tc_engine.cuh", "ozaki_engine.cuh", "driver.h"]
+BINDIR = os.path.join(PKG, "bin")
+CLI = os.path.join(BINDIR, "plssvm")
+SOURCES = ["capi.cu", "driver.cu", "comm.cu", "io.cpp"]
+HEADERS = ["common.cuh", "tile_engine.cuh", "kernels.cuh", "tc_engine.cuh", "ozaki_engine.cuh", "driver.h", "io.h"]
 
 
 def nccl_dirs():
@@ -32,8 +34,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def build_cli(force: bool = False) -> str:
+    """The LIBSVM-style CLI (csrc/cli.cpp, host C++ over the C ABI) -> bin/plssvm and the
+    plssvm-train / plssvm-predict / plssvm-scale links."""
+    src = os.path.join(CSRC, "cli.cpp")
+    if force or not os.path.exists(CLI) or os.path.getmtime(CLI) < max(os.path.getmtime(src), os.path.getmtime(LIB)):
+        os.makedirs(BINDIR, exist_ok=True)
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-Wall", "-o", CLI, src, "-I", os.path.join(ROOT, "include"),
+                               "-L", LIBDIR, "-l:libplssvm_b200.so", "-Wl,-rpath,$ORIGIN/../lib"])
+    for name in ("plssvm-train", "plssvm-predict", "plssvm-scale"):
+        link = os.path.join(BINDIR, name)
+        if not os.path.islink(link):
+            if os.path.exists(link):
+                os.remove(link)
+            os.symlink("plssvm", link)
+    return CLI
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
+        build_cli()
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     inc, libd = nccl_dirs()
@@ -48,6 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    build_cli(force=True)
     return LIB
 
 

@@ -20,14 +20,16 @@ MODE_AUTO, MODE_IMPLICIT, MODE_CACHED, MODE_LOWRANK = 0, 1, 2, 3
 FP64_AUTO, FP64_OZAKI, FP64_DMMA = 0, 1, 2
 CG_AUTO, CG_BATCHED, CG_GRAPH = 0, 1, 2
 MULTI_GPU_ROWS, MULTI_GPU_FEATURES = 0, 1
-OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED = range(8)
+OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED, E_IO = range(9)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
-                6: "E_NUMERICAL", 7: "W_NOT_CONVERGED"}
+                6: "E_NUMERICAL", 7: "W_NOT_CONVERGED", 8: "E_IO"}
 
 EXPORTS = ["plssvm_default_options", "plssvm_train", "plssvm_train_f32", "plssvm_train_ex", "plssvm_predict",
            "plssvm_predict_f32", "plssvm_predict_ex", "plssvm_qtilde_matvec", "plssvm_comm_unique_id",
            "plssvm_comm_init", "plssvm_comm_init_callbacks", "plssvm_comm_destroy", "plssvm_partition",
-           "plssvm_feature_partition", "plssvm_last_error", "plssvm_version", "plssvm_device_count"]
+           "plssvm_feature_partition", "plssvm_last_error", "plssvm_version", "plssvm_device_count",
+           "plssvm_libsvm_read", "plssvm_libsvm_write", "plssvm_model_write", "plssvm_model_read", "plssvm_scale_fit",
+           "plssvm_scale_apply"]
 
 
 class plssvm_options_t(ct.Structure):
@@ -104,6 +106,15 @@ def load(build_if_missing: bool = True):
     L.plssvm_comm_init_callbacks.argtypes = [ct.POINTER(plssvm_comm_callbacks_t), i32, i32, i32, ct.POINTER(vp)]
     L.plssvm_partition.argtypes = [i64, i32, i32, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
     L.plssvm_feature_partition.argtypes = [i64, i32, i32, ct.POINTER(i64), ct.POINTER(i64)]
+    pd = ct.POINTER(ct.c_double)
+    L.plssvm_libsvm_read.argtypes = [ct.c_char_p, vp, vp, i64, i64, ct.POINTER(i64), ct.POINTER(i64), pd,
+                                     ct.POINTER(i32)]
+    L.plssvm_libsvm_write.argtypes = [ct.c_char_p, vp, vp, i64, i64]
+    L.plssvm_model_write.argtypes = [ct.c_char_p, i, d, i, d, vp, vp, d, i64, i64, vp, pd]
+    L.plssvm_model_read.argtypes = [ct.c_char_p, ct.POINTER(i32), pd, ct.POINTER(i32), pd, vp, vp, pd, i64, i64,
+                                    ct.POINTER(i64), ct.POINTER(i64), pd]
+    L.plssvm_scale_fit.argtypes = [vp, i64, i64, vp, vp]
+    L.plssvm_scale_apply.argtypes = [vp, i64, i64, vp, vp, d, d]
     L.plssvm_last_error.restype = ct.c_char_p
     L.plssvm_version.restype = ct.c_char_p
     L.plssvm_device_count.restype = ct.c_int
@@ -413,3 +424,72 @@ def comm_from_torch_distributed(device: int):
         t = t.cuda(device)
     dist.broadcast(t, 0)
     return plssvm_comm_init(bytes(t.cpu().tolist()), world, rank, device)
+
+
+# ------------------------------------------------------------------- LIBSVM files (NEXT-4)
+def _path(p) -> bytes:
+    return os.fsencode(p)
+
+
+def plssvm_libsvm_read(path, min_d: int = 0):
+    """-> (X [m, max(d, min_d)] float64, y_raw [m], labels (distinct, first-seen order))."""
+    L = load()
+    m, d, nl = ct.c_int64(), ct.c_int64(), ct.c_int32()
+    labs = (ct.c_double * 2)()
+    _check(L.plssvm_libsvm_read(_path(path), None, None, 0, 0, ct.byref(m), ct.byref(d), labs, ct.byref(nl)))
+    D = max(d.value, min_d, 1)
+    X = np.zeros((m.value, D))
+    y = np.zeros(m.value)
+    _check(L.plssvm_libsvm_read(_path(path), X.ctypes.data, y.ctypes.data, m.value, D, ct.byref(m), ct.byref(d), labs,
+                                ct.byref(nl)))
+    return X, y, [labs[k] for k in range(nl.value)]
+
+
+def plssvm_libsvm_write(path, X, y):
+    X, y = _host(X, F64), _host(y, F64)
+    _check(load().plssvm_libsvm_write(_path(path), X.ctypes.data, y.ctypes.data, X.shape[0], X.shape[1]))
+
+
+def plssvm_model_write(path, kernel, gamma, degree, coef0, X, alpha, b, y, labels):
+    X, alpha, y = _host(X, F64), _host(alpha, F64), _host(y, F64)
+    labs = (ct.c_double * 2)(float(labels[0]), float(labels[1]))
+    _check(load().plssvm_model_write(_path(path), kernel, gamma, degree, coef0, X.ctypes.data, alpha.ctypes.data,
+                                     float(b), X.shape[0], X.shape[1], y.ctypes.data, labs))
+
+
+def plssvm_model_read(path, min_d: int = 0):
+    """-> dict(kernel, gamma, degree, coef0, X, alpha, b, labels)."""
+    L = load()
+    k, dg = ct.c_int32(), ct.c_int32()
+    g, r, b = ct.c_double(), ct.c_double(), ct.c_double()
+    m, d = ct.c_int64(), ct.c_int64()
+    labs = (ct.c_double * 2)()
+    args = (ct.byref(k), ct.byref(g), ct.byref(dg), ct.byref(r))
+    _check(L.plssvm_model_read(_path(path), *args, None, None, ct.byref(b), 0, 0, ct.byref(m), ct.byref(d), labs))
+    D = max(d.value, min_d, 1)
+    X = np.zeros((m.value, D))
+    alpha = np.zeros(m.value)
+    _check(L.plssvm_model_read(_path(path), *args, X.ctypes.data, alpha.ctypes.data, ct.byref(b), m.value, D,
+                               ct.byref(m), ct.byref(d), labs))
+    return dict(kernel=k.value, gamma=g.value, degree=dg.value, coef0=r.value, X=X, alpha=alpha, b=b.value,
+                labels=[labs[0], labs[1]])
+
+
+def plssvm_scale_fit(X):
+    X = _host(X, F64)
+    fmin, fmax = np.zeros(X.shape[1]), np.zeros(X.shape[1])
+    _check(load().plssvm_scale_fit(X.ctypes.data, X.shape[0], X.shape[1], fmin.ctypes.data, fmax.ctypes.data))
+    return fmin, fmax
+
+
+def plssvm_scale_apply(X, fmin, fmax, lo=-1.0, hi=1.0):
+    """Returns a scaled copy (the C call works in place)."""
+    X = np.array(X, dtype=np.float64, order="C", copy=True)
+    fmin, fmax = _host(fmin, F64), _host(fmax, F64)
+    _check(load().plssvm_scale_apply(X.ctypes.data, X.shape[0], X.shape[1], fmin.ctypes.data, fmax.ctypes.data, lo, hi))
+    return X
+
+
+def cli_path() -> str:
+    """bin/plssvm (the LIBSVM-style CLI; plssvm-train / -predict / -scale link to it)."""
+    return _build.CLI

@@ -13,6 +13,7 @@
 #include "../../include/plssvm.h"
 #include "common.cuh"
 #include "driver.h"
+#include "io.h"
 
 #ifndef PLSSVM_VERSION
 #define PLSSVM_VERSION "0.1.0"
@@ -234,6 +235,54 @@ int plssvm_feature_partition(int64_t d, int32_t nranks, int32_t rank, int64_t *f
         return fail(PLSSVM_E_INVALID_ARG, "bad feature partition arguments");
     *f_begin = plssvm::feature_begin(d, nranks, rank);
     *f_end = plssvm::feature_begin(d, nranks, rank + 1);
+    return PLSSVM_OK;
+}
+
+int plssvm_libsvm_read(const char *path, double *X, double *y, int64_t cap_m, int64_t cap_d, int64_t *m, int64_t *d,
+                       double *labels, int32_t *nlabels) {
+    return guarded([&] {
+        plssvm::io::libsvm_read(path, X, y, cap_m, cap_d, m, d, labels, nlabels);
+        return PLSSVM_OK;
+    });
+}
+
+int plssvm_libsvm_write(const char *path, const double *X, const double *y, int64_t m, int64_t d) {
+    if (!X || !y || m < 0 || d < 0) return fail(PLSSVM_E_INVALID_ARG, "bad libsvm_write arguments");
+    return guarded([&] {
+        plssvm::io::libsvm_write(path, X, y, m, d);
+        return PLSSVM_OK;
+    });
+}
+
+int plssvm_model_write(const char *path, int kernel, double gamma, int degree, double coef0, const double *X,
+                       const double *alpha, double b, int64_t m, int64_t d, const double *y, const double *labels) {
+    if (!X || !alpha || !y || !labels || m < 1 || d < 1) return fail(PLSSVM_E_INVALID_ARG, "bad model_write arguments");
+    return guarded([&] {
+        plssvm::io::model_write(path, kernel, gamma, degree, coef0, X, alpha, b, m, d, y, labels);
+        return PLSSVM_OK;
+    });
+}
+
+int plssvm_model_read(const char *path, int32_t *kernel, double *gamma, int32_t *degree, double *coef0, double *X,
+                      double *alpha, double *b, int64_t cap_m, int64_t cap_d, int64_t *m, int64_t *d, double *labels) {
+    return guarded([&] {
+        plssvm::io::model_read(path, kernel, gamma, degree, coef0, X, alpha, b, cap_m, cap_d, m, d, labels);
+        return PLSSVM_OK;
+    });
+}
+
+int plssvm_scale_fit(const double *X, int64_t m, int64_t d, double *fmin, double *fmax) {
+    g_last_error.clear();
+    if (!X || !fmin || !fmax || m < 1 || d < 1) return fail(PLSSVM_E_INVALID_ARG, "bad scale_fit arguments");
+    plssvm::io::scale_fit(X, m, d, fmin, fmax);
+    return PLSSVM_OK;
+}
+
+int plssvm_scale_apply(double *X, int64_t m, int64_t d, const double *fmin, const double *fmax, double lo, double hi) {
+    g_last_error.clear();
+    if (!X || !fmin || !fmax || m < 0 || d < 1) return fail(PLSSVM_E_INVALID_ARG, "bad scale_apply arguments");
+    if (!(lo < hi)) return fail(PLSSVM_E_INVALID_ARG, "scale_apply: lower bound must be < upper bound");
+    plssvm::io::scale_apply(X, m, d, fmin, fmax, lo, hi);
     return PLSSVM_OK;
 }
 

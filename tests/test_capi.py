@@ -29,7 +29,7 @@ def exported_symbols():
 def test_library_loads_and_exports_every_declared_symbol():
     L = pl.load()
     decl = declared_symbols()
-    assert len(decl) == 17
+    assert len(decl) == 23
     for name in decl:
         assert hasattr(L, name), name
     assert exported_symbols() == decl  # nothing else is public
