@@ -63,7 +63,8 @@ struct Oz {
     static constexpr int TMEM_COLS = 512;
     static_assert(LV * TN <= TMEM_COLS && LV0 * TN <= TMEM_COLS, "a pass's level accumulators must fit TMEM");
     // misc: barriers (256 B) + column data 4 x 128 doubles + row partials 2 x 128 + col partials 4 x 128
-    static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN) * 8;
+    // + the 64-entry exp table
+    static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN + 64) * 8;
     static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + MISC;
     // instruction descriptor: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 128, M = 256 (2 SMs)
     static constexpr uint32_t IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TN >> 3) << 17) | ((256u >> 4) << 24);
@@ -108,11 +109,71 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
 }
 
+// 2^(j/64), j = 0..63, correctly rounded (Decimal, 60 digits) -- the table of exp_tab.
+__constant__ double kExp2Tab64[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+// e^t for t <= 0 (the RBF kernel, t = -gamma ||x_i - x_j||^2) with ~1 ulp error and 10 DP
+// operations instead of exp()'s ~17 (the fp64 epilogue is the energy that separates C1 from
+// the MMA-only bound):  t = (64 k + j) ln2/64 + r, |r| <= ln2/128, so
+// e^t = 2^k * 2^(j/64) * e^r with e^r = 1 + q(r), q the degree-5 Taylor polynomial
+// (truncation |r|^6/720 < 4e-17).  n = 64 k + j by the 1.5 * 2^52 rounding trick; ln2/64 split
+// into a 36-bit head (n * head exact for |n| < 2^17) and a tail.  t < -708 (e^t < 1e-307,
+// below the normal range the exponent shift can reach) returns 0.  tab = kExp2Tab64 in smem.
+__device__ __forceinline__ double exp_tab(double t, const double *__restrict__ tab) {
+    constexpr double kInvL = 92.33248261689366;         // 64 / ln 2
+    constexpr double kLhi = 0.010830424696223417;       // ln2/64, 36-bit head
+    constexpr double kLlo = 2.572804622327669e-14;      // ln2/64 - kLhi
+    constexpr double kShift = 6755399441055744.0;       // 1.5 * 2^52
+    const double kd = fma(t, kInvL, kShift);
+    const int n = __double2loint(kd);                   // round(t * 64 / ln2), two's complement
+    const double kf = kd - kShift;
+    double r = fma(kf, -kLhi, t);
+    r = fma(kf, -kLlo, r);
+    double c = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    c = fma(r, c, 1.0 / 6.0);
+    c = fma(r, c, 0.5);
+    c = fma(r, c, 1.0);
+    const double T = tab[n & 63];
+    const double e = fma(T, r * c, T);                  // 2^(j/64) e^r, in [0.99, 2)
+    const double v = __hiloint2double(__double2hiint(e) + ((n >> 6) << 20), __double2loint(e));
+    return t < -708.0 ? 0.0 : v;
+}
+
 // Exact int32 -> fp64 without the (slow, XU-pipe) I2F.F64: 2^52 + (r + 2^31) assembled from
 // bits, minus 2^52 + 2^31 -- one LOP3 + one DADD.
 __device__ __forceinline__ double i2d_exact(uint32_t r) {
     return __hiloint2double(0x43300000, static_cast<int>(r ^ 0x80000000u)) - 4503601774854144.0;
 }
+
+// Exact int64 -> fp64 for |v| < 2^53: v = hi 2^32 + lo (lo unsigned), both halves by the bias
+// trick, one fma (exact: the sum is representable).  3 DP ops.
+__device__ __forceinline__ double i64_to_f64_exact(long long v) {
+    const uint32_t hi = static_cast<uint32_t>(static_cast<unsigned long long>(v) >> 32);
+    const uint32_t lo = static_cast<uint32_t>(v);
+    return fma(i2d_exact(hi), 4294967296.0, __hiloint2double(0x43300000, static_cast<int>(lo)) - 4503599627370496.0);
+}
+
+// Level sums combined in INTEGER arithmetic (exact), one conversion per group instead of one per
+// level: pass 0 W = acc_4 2^16 + acc_5 2^8 + acc_6, pass 1 V = acc_0 2^24 + acc_1 2^16 + acc_2 2^8
+// + acc_3.  |acc_l| <= (l+1) d 2^14, so |V| <= d 2^38.01 < 2^53 for d <= 16384 (the engine's
+// limit) -- exactly representable, converted without rounding.
+__device__ __forceinline__ long long lv(uint32_t r) { return static_cast<long long>(static_cast<int>(r)); }
 
 // Sum of v[0..31] over the 32 lanes in 31 shuffles: afterwards lane l holds the total of
 // element l.  Fixed order (deterministic).
@@ -304,6 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     double *coln = colp + TN;                                // [128]
     double *redr = coln + TN;                                // [2][128]
     double *redc = redr + 2 * kTile;                         // [4][128]
+    double *etab = redc + 4 * TN;                            // [64] 2^(j/64) (RBF, exp_tab)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -429,6 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(O::CTRL_REGS));
     } else {  // ---- epilogue warps 4-11 (both CTAs): row 32(w%4) + lane, columns 64((w-4)/4) .. +63
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(O::EPI_REGS));
+        if (KT == RBF && threadIdx.x - 128 < 64) etab[threadIdx.x - 128] = kExp2Tab64[threadIdx.x - 128];  // read after B1
         const int quarter = warp & 3, grp = (warp - 4) >> 2;
         const int lr = quarter * 32 + lane;
         const int et = threadIdx.x - 128;  // 0..255
@@ -448,19 +511,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 coln[et] = (KT == RBF) ? nb_[gj] : 0.0;
             }
             const int64_t gi = row0 + lr;
-            const double sci = used ? sca[gi] : 0.0;
+            const double sci = used ? sca[gi] * 0x1p-24 : 0.0;  // row scale, with V's 2^-24 folded in
             const double qi = (MODE == OZ_PREDICT || !used) ? 0.0 : qv[gi];
             const double pi = (MODE == OZ_MATVEC && used) ? p[gi] : 0.0;
             const double ni = (KT == RBF && used) ? na[gi] : 0.0;
+            const double cqi = Qmm - qi;  // Eq. 16 row constant
             asm volatile("bar.sync 1, 256;" ::: "memory");  // B1
 
-            // Pass 0 (levels 4-6) -> the low-order part w = sum_{l<3} 2^{-8l} acc_{4+l}, kept in
-            // fp32: it enters as 2^{-32} w, so its rounding is ~2^{-56} relative to the leading
-            // digit products, and 64 columns cost 64 registers.  Pass 1 (levels 0-3), 8 columns at
-            // a time: v = sum_{l<4} 2^{-8l} acc_l + 2^{-32} w in fp64, then at once the Q~ entry /
-            // kernel value and its row and column contributions -- the accumulators are released
-            // after the last chunk (64 fp64 values per thread would not fit the 168-register
-            // budget of a 10-warp CTA).
+            // Pass 0 (levels 4-6) -> the low-order part W = 2^16 sum_{l<3} 2^{-8l} acc_{4+l} (exact
+            // int64), kept in fp32: it enters 2^{-48} below V, so its rounding is ~2^{-56}
+            // relative to the leading digit products, and 64 columns cost 64 registers.  Pass 1
+            // (levels 0-3): V = 2^24 sum_{l<4} 2^{-8l} acc_l (exact int64) + 2^{-24} W in fp64 for
+            // all 64 columns (registers), accumulators released, then the Q~ entry / kernel value
+            // and its row and column contributions (under the next pair-tile's MMAs).
             const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(grp * 64);
             const bool mirrored = used && (MODE != OZ_PREDICT) && (I != J) && (J >= band0) && (J < band1);
             float wl[64];
@@ -487,9 +550,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {  // Horner in base 2^-8, highest level first
-                        const double h = fma(i2d_exact(r2[j]), 0.00390625, i2d_exact(r1[j]));
-                        wl[c * 8 + j] = static_cast<float>(fma(h, 0.00390625, i2d_exact(r0[j])));
+                    for (int j = 0; j < 8; ++j) {  // W = acc_4 2^16 + acc_5 2^8 + acc_6 (exact), rounded to fp32
+                        const long long W = (lv(r0[j]) << 16) + (lv(r1[j]) << 8) + lv(r2[j]);
+                        wl[c * 8 + j] = static_cast<float>(i64_to_f64_exact(W));
                     }
                 }
             }
@@ -515,11 +578,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        double h = fma(i2d_exact(r3[j]), 0.00390625, i2d_exact(r2[j]));
-                        h = fma(h, 0.00390625, i2d_exact(r1[j]));
-                        h = fma(h, 0.00390625, i2d_exact(r0[j]));
+                        // x_i.x_j = sc_i sc_j (V + 2^-24 W) 2^-24: level 4 is 2^-32 below level 0, W
+                        // carries 2^16 of it (the 2^-24 of V sits in sci)
+                        const long long V = (lv(r0[j]) << 24) + (lv(r1[j]) << 16) + (lv(r2[j]) << 8) + lv(r3[j]);
                         const int lc = grp * 64 + c * 8 + j;
-                        sv[c * 8 + j] = fma(static_cast<double>(wl[c * 8 + j]), 0x1p-32, h) * (sci * colsc[lc]);
+                        sv[c * 8 + j] = fma(static_cast<double>(wl[c * 8 + j]), 0x1p-24, i64_to_f64_exact(V)) *
+                                        (sci * colsc[lc]);
                     }
                 }
             }
@@ -533,11 +597,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int lc = grp * 64 + c * 8 + j;
-                        if constexpr (MODE == OZ_PREDICT) {
-                            rs = fma(colp[lc], kernel_value<KT, double>(sv[c * 8 + j], ni, coln[lc], false, kp), rs);
+                        const int64_t gj = col0 + lc;
+                        const bool diag = (MODE != OZ_PREDICT) && gi == gj;
+                        double kv;
+                        if constexpr (KT == RBF) {  // kernel_value's RBF with the table exp
+                            double dist = ni + coln[lc] - 2.0 * sv[c * 8 + j];
+                            dist = dist > 0.0 ? dist : 0.0;
+                            if (diag) dist = 0.0;
+                            kv = exp_tab(-kp.gamma * dist, etab);
                         } else {
-                            w[j] = qtilde_value<KT, double>(sv[c * 8 + j], gi, col0 + lc, ni, coln[lc], qi, colq[lc], Qmm,
-                                                            invC, m1, kp);
+                            kv = kernel_value<KT, double>(sv[c * 8 + j], ni, coln[lc], diag, kp);
+                        }
+                        if constexpr (MODE == OZ_PREDICT) {
+                            rs = fma(colp[lc], kv, rs);
+                        } else {  // qtilde_value (Eq. 16) with the row constant Q_mm - q_i hoisted
+                            const double v = (kv + (diag ? invC : 0.0)) - colq[lc] + cqi;
+                            w[j] = (gi < m1 && gj < m1) ? v : 0.0;
                         }
                     }
                     if constexpr (MODE == OZ_MATVEC) {

@@ -175,3 +175,24 @@ def test_wide_d_limit():
     assert st == 0 and stats.fp64_engine_used == pl.FP64_OZAKI
     a_ref, _, _, _ = oracle.train(X2, y, pl.RBF, 1.0 / 16384, eps=1e-10)
     assert rel(alpha, a_ref) <= 1e-7
+
+
+@pytest.mark.parametrize("gamma", [1e-7, 1.0 / 64, 0.3, 2.0, 40.0])
+def test_ozaki_rbf_table_exp_across_the_exponent_range(gamma):
+    """The Ozaki epilogue evaluates exp(-gamma ||x_i - x_j||^2) with a 64-entry 2^(j/64) table and a
+    degree-5 polynomial (ozaki_engine.cuh exp_tab): kernel values from ~1 down through the
+    2^-1022 cut-off (gamma = 40 on 64-feature N(0,1) data gives exponents far below -708) must
+    still give the oracle's product within 1e-12, in implicit, cached and predict paths."""
+    rng = np.random.default_rng(int(gamma * 1000) + 5)
+    m, d = 600, 64
+    X = rng.standard_normal((m, d))
+    X[5] = X[4] + 1e-9  # near-duplicate point: exponent ~ -gamma 1e-16, kernel ~ 1
+    p = rng.standard_normal(m - 1)
+    for mode in (pl.MODE_IMPLICIT, pl.MODE_CACHED):
+        check(X, p, pl.RBF, gamma, engine=pl.FP64_OZAKI, mode=mode)
+    Z = rng.standard_normal((300, d)) * 0.5
+    alpha = rng.standard_normal(m)
+    f, _, _ = pl.plssvm_predict_ex(X, alpha, 0.25, Z, pl.RBF, gamma=gamma, opts=pl.options(fp64_engine=pl.FP64_OZAKI))
+    f_ref, _ = oracle.predict(X, alpha, 0.25, Z, pl.RBF, gamma)
+    K = np.exp(-gamma * ((Z[:, None, :] - X[None, :, :]) ** 2).sum(-1))
+    assert np.all(np.abs(f - f_ref) <= 1e-12 * (np.abs(K) @ np.abs(alpha) + 0.25))
