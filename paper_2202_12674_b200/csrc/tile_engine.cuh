@@ -356,9 +356,15 @@ __device__ __forceinline__ T kernel_value(T s, T ni, T nj, bool diag, const KPar
     if constexpr (KT == LINEAR) {
         return s;
     } else if constexpr (KT == POLYNOMIAL) {
-        const T base = kp.gamma * s + kp.coef0;
-        T r = T(1);
-        for (int t = 0; t < kp.degree; ++t) r *= base;
+        // integer power by repeated multiplication (R-6).  Degrees 1-4 as a fixed
+        // product sequence selected by the (warp-uniform, loop-invariant) degree: no per-entry loop
+        // in the unrolled epilogues (the loop cost C3 12 %); b^3 = (b b) b as the oracle's order.
+        const T b = kp.gamma * s + kp.coef0;
+        const T b2 = b * b;
+        const T b3 = b2 * b;
+        if (kp.degree <= 4) return kp.degree == 1 ? b : kp.degree == 2 ? b2 : kp.degree == 3 ? b3 : b2 * b2;
+        T r = b3;
+        for (int t = 3; t < kp.degree; ++t) r *= b;
         return r;
     } else {
         T dist = ni + nj - T(2) * s;

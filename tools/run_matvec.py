@@ -21,6 +21,7 @@ ap.add_argument("--d", type=int, default=0)
 ap.add_argument("--kernel", type=int, default=-1)
 ap.add_argument("--fp32-engine", type=int, default=0)
 ap.add_argument("--fp64-engine", type=int, default=0, help="0 AUTO, 1 OZAKI, 2 DMMA")
+ap.add_argument("--synth", action="store_true", help="use the config's seeded make_classification data (as bench.py) instead of N(0,1)")
 ap.add_argument("--compare", action="store_true", help="also run the DMMA fp64 engine (OZAKI if --fp64-engine 2) and compare")
 a = ap.parse_args()
 cfg = synth.configs()[a.config]
@@ -28,6 +29,8 @@ m, d = a.m or cfg.m, a.d or cfg.d
 dt = np.float32 if cfg.dtype == "f32" else np.float64
 rng = np.random.default_rng(0)
 X = rng.standard_normal((m, d)).astype(dt)
+if a.synth:
+    X = synth.config_data(cfg)[0].astype(dt)
 p = rng.standard_normal(m - 1).astype(dt)
 mode = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED, "lowrank": pl.MODE_LOWRANK}[a.mode]
 kern = cfg.kernel if a.kernel < 0 else a.kernel
