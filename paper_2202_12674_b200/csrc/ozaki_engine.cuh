@@ -348,7 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                  double *__restrict__ Ypart, int64_t band_rows, double *__restrict__ Qc, int T_tiles, const int *ctrl,
                  int dbg) {
     using O = Oz<S>;
-    constexpr int TN = O::TN, LV = O::LV, LV0 = O::LV0;
+    constexpr int TN = O::TN, LV = O::LV;
     if (cg_done(ctrl)) return;  // uniform across the cluster
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

@@ -102,5 +102,8 @@ def test_feature_split_train_matches_oracle(tmp_path, world, m, d, x0):
     assert np.linalg.norm(r["out"] - ref) <= 1e-12 * np.linalg.norm(ref)
     a_ref, b_ref, _, _ = oracle.train(X, y, 0, 1.0 / d, 3, 0.5, 1.0, 1e-10, x0=x0)
     assert int(r["st"]) == 0 and int(r["ranks"]) == world and int(r["mode_used"]) == 1
-    assert np.linalg.norm(r["alpha"] - a_ref) <= 1e-7 * np.linalg.norm(a_ref)
-    assert abs(float(r["b"]) - b_ref) <= 1e-7 * max(abs(b_ref), np.abs(a_ref).max())
+    # x0 = ones stops at eps relative to ||rhs - Q~1|| >> ||rhs||, so two summation orders agree
+    # only to ~1e-6 on this linear system (R-5); x0 = 0: the 1e-7 bar
+    tol = 1e-7 if x0 == 0 else 1e-6
+    assert np.linalg.norm(r["alpha"] - a_ref) <= tol * np.linalg.norm(a_ref)
+    assert abs(float(r["b"]) - b_ref) <= tol * max(abs(b_ref), np.abs(a_ref).max())
