@@ -258,7 +258,9 @@ def main():
     kw = dict(gamma=cfg.gamma, degree=cfg.degree, coef0=cfg.coef0)
 
     def opts():
-        return pl.options(mode=mode, comm=comm, device=local)
+        # the batched CG loop (AUTO's choice at the bench workload): per-launch CUDA events on the
+        # product's stream give roofline.achieved (no events inside a CUDA-graph loop body)
+        return pl.options(mode=mode, comm=comm, device=local, cg_loop=pl.CG_BATCHED)
 
     def step():
         alpha, b, st, stats = pl.plssvm_train_ex(tX, ty, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=opts(), **kw)

@@ -100,7 +100,16 @@ typedef struct {
                                 cached precompute and predict [AUTO] */
     int32_t cg_loop;         /* plssvm_cg_loop_t: how the CG iterations are issued [AUTO] */
     int32_t multi_gpu;       /* plssvm_multi_gpu_t: how `comm`'s ranks share the work [ROWS] */
+    int32_t cg_variant;      /* plssvm_cg_variant_t [SHEWCHUK] */
 } plssvm_options_t;
+
+/* CG formulation.  SHEWCHUK: the paper's loop (two inner products per iteration, each
+ * its own reduction / all-reduce).  SINGLE_REDUCTION: Chronopoulos-Gear CG:
+ * the product is taken of r, s = Q~p is carried by recurrence, and gamma = r.r, delta = (Q~r).r
+ * share ONE reduction point (one all-reduce of a scalar pair per iteration on several GPUs, three
+ * kernels per iteration instead of four).  Same iterates in exact arithmetic, same stopping rule
+ * (||r|| <= eps ||r0||); one extra product at exit.  Not with replace_every > 0. */
+typedef enum { PLSSVM_CG_SHEWCHUK = 0, PLSSVM_CG_SINGLE_REDUCTION = 1 } plssvm_cg_variant_t;
 
 /* CG loop issue.  The convergence test always runs on the device
  * (Shewchuk's loop condition, evaluated by the last block of the p update).

@@ -20,6 +20,7 @@ MODE_AUTO, MODE_IMPLICIT, MODE_CACHED, MODE_LOWRANK = 0, 1, 2, 3
 FP64_AUTO, FP64_OZAKI, FP64_DMMA = 0, 1, 2
 CG_AUTO, CG_BATCHED, CG_GRAPH = 0, 1, 2
 MULTI_GPU_ROWS, MULTI_GPU_FEATURES = 0, 1
+CG_SHEWCHUK, CG_SINGLE_REDUCTION = 0, 1
 OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED, E_IO = range(9)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
                 6: "E_NUMERICAL", 7: "W_NOT_CONVERGED", 8: "E_IO"}
@@ -37,7 +38,7 @@ class plssvm_options_t(ct.Structure):
                 ("fixed_iter", ct.c_int64), ("device", ct.c_int32), ("device_pointers", ct.c_int32),
                 ("stream", ct.c_void_p), ("comm", ct.c_void_p), ("cache_budget_bytes", ct.c_int64),
                 ("fp32_engine", ct.c_int32), ("linear_w", ct.c_int32), ("fp64_engine", ct.c_int32),
-                ("cg_loop", ct.c_int32), ("multi_gpu", ct.c_int32)]
+                ("cg_loop", ct.c_int32), ("multi_gpu", ct.c_int32), ("cg_variant", ct.c_int32)]
 
 
 class plssvm_stats_t(ct.Structure):

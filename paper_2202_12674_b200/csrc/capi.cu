@@ -107,6 +107,7 @@ void plssvm_default_options(plssvm_options_t *o) {
     o->fp64_engine = PLSSVM_FP64_AUTO;
     o->cg_loop = PLSSVM_CG_AUTO;
     o->multi_gpu = PLSSVM_MULTI_GPU_ROWS;
+    o->cg_variant = PLSSVM_CG_SHEWCHUK;
 }
 
 int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtype, int kernel, double gamma, int degree,
@@ -124,6 +125,10 @@ int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtyp
         return fail(PLSSVM_E_INVALID_ARG, "options.mode LOWRANK needs the linear kernel");
     if (o.x0 != 0 && o.x0 != 1) return fail(PLSSVM_E_INVALID_ARG, "options.x0 must be 0 or 1");
     if (o.cg_loop < 0 || o.cg_loop > 2) return fail(PLSSVM_E_INVALID_ARG, "options.cg_loop must be 0, 1 or 2");
+    if (o.cg_variant != PLSSVM_CG_SHEWCHUK && o.cg_variant != PLSSVM_CG_SINGLE_REDUCTION)
+        return fail(PLSSVM_E_INVALID_ARG, "options.cg_variant must be 0 (SHEWCHUK) or 1 (SINGLE_REDUCTION)");
+    if (o.cg_variant == PLSSVM_CG_SINGLE_REDUCTION && o.replace_every > 0)
+        return fail(PLSSVM_E_INVALID_ARG, "cg_variant SINGLE_REDUCTION does not support replace_every");
     if ((s = check_multi_gpu(o, kernel, dtype, d))) return s;
     if ((s = device_ok(o.device))) return s;
     if (stats) std::memset(stats, 0, sizeof(*stats));

@@ -330,6 +330,7 @@ struct Ctx {
     int nranks = 1;                  // communicator size (g.P is the row-shard count)
     T *yred = nullptr;               // fsplit: the all-reduced product
     bool graph_used = false;         // the CG loop ran as one CUDA graph (WHILE node)
+    int pap_slot = S_PAP;            // scalar slot of finalize's p.Q~p (Chronopoulos-Gear: S_CG_DELTA)
 };
 
 template <typename T>
@@ -818,7 +819,7 @@ void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par,
             // then the usual finalize on the summed vector (one slot)
             k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(Y, nslots, nsub, g.band0, g.nb, g.g0, g.m1, c.p + g.g0,
                                                                c.yred, 0, c.ylab, c.r, nullptr, c.scal, 0, 0,
-                                                               c.partials, c.counter, 0, c.cur_ctrl);
+                                                               c.partials, c.counter, 0, c.cur_ctrl, S_PAP);
             PLS_CHECK_LAUNCH();
             ++c.launches;
             comm_allreduce_sum_f64(c.comm, c.yred, c.yred, g.nb, c.s);
@@ -829,7 +830,7 @@ void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par,
     }
     k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(Y, nslots, nsub, g.band0, g.nb, g.g0, g.m1, pband, c.y, mode,
                                                        c.ylab, c.r, pout, c.scal, par, set_delta0, c.partials,
-                                                       c.counter, 1, c.cur_ctrl);
+                                                       c.counter, 1, c.cur_ctrl, c.pap_slot);
     PLS_CHECK_LAUNCH();
     ++c.launches;
 }
@@ -1127,8 +1128,30 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     // One CG iteration (a3 product, a4 fused updates, a5 test in k_update_p, a8 exchanges).
     // k = host-side iteration index (only the residual-replacement period uses it); `loop` /
     // `use_loop`: the CUDA-graph WHILE condition k_update_p sets.
+    // Chronopoulos-Gear variant: c.p (full) carries r (the product's operand), c.r (band) the
+    // search direction p, scg the recurrence s = Q~ p; one all-reduce of (gamma, delta).
+    const bool cgcg = o.cg_variant == PLSSVM_CG_SINGLE_REDUCTION;
+    T *scg = nullptr;
+    if (cgcg) {
+        scg = A.alloc<T>(g.nb);
+        PLS_CUDA(cudaMemsetAsync(scg, 0, g.nb * sizeof(T), c.s));
+        c.pap_slot = S_CG_DELTA;
+    }
     auto enqueue_iteration = [&](int64_t k, cudaEvent_t ev0, cudaEvent_t ev1, cudaGraphConditionalHandle loop,
                                  int use_loop) {
+        if (cgcg) {
+            if (ev0) PLS_CUDA(cudaEventRecord(ev0, c.s));
+            const int ns = launch_qtilde_product<T>(c, c.p);  // w = Q~ r
+            if (ev1) PLS_CUDA(cudaEventRecord(ev1, c.s));
+            finalize<T>(c, ns, pband, 0, nullptr, 0, 0);  // w -> c.y, delta = w.r (partial)
+            allreduce(c, S_CG_GAMMA, 2);                   // (gamma, delta): the one reduction
+            k_cgcg_update<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, pband, c.r, scg, c.y, g.nb, c.scal, c.ctrl,
+                                                                  c.partials, c.counter, loop, use_loop);
+            PLS_CHECK_LAUNCH();
+            ++c.launches;
+            allgather(c, c.p);
+            return;
+        }
         const int par = static_cast<int>(k & 1);
         if (ev0) PLS_CUDA(cudaEventRecord(ev0, c.s));
         const int ns = launch_qtilde_product<T>(c, c.p);
@@ -1241,10 +1264,10 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         }
     }
     c.cur_ctrl = nullptr;
-    int64_t matvecs = it + ((o.x0 == 0) ? 0 : 1);
+    int64_t matvecs = it + ((o.x0 == 0) ? 0 : 1) + (cgcg ? 1 : 0);  // CG-CG: the product of the final r
     if (o.replace_every > 0 && it > 1) matvecs += (it - 1) / o.replace_every;
     const double delta0 = hs[S_DELTA0];
-    const double delta = hs[S_DELTA + (it & 1)];
+    const double delta = cgcg ? hs[S_CG_GAMMA] : hs[S_DELTA + (it & 1)];
     const double eps2 = pb.eps * pb.eps;
     int status = PLSSVM_OK;
     if (hctrl[C_DONE] == 2) status = PLSSVM_E_NUMERICAL;

@@ -28,6 +28,10 @@ enum Scal : int {
     S_B = 9,        // bias b
     S_THR = 10,     // eps^2 delta_0 (the CG stopping threshold on delta)
     S_SP = 11,      // sum of p (linear low-rank product)
+    S_CG_GAMMA = 12,  // Chronopoulos-Gear: gamma_i = r_i.r_i      } contiguous: one all-reduce
+    S_CG_DELTA = 13,  //                    delta_i = (Q~ r_i).r_i }   of the pair per iteration
+    S_CG_GPREV = 14,  //                    gamma_{i-1}
+    S_CG_APREV = 15,  //                    alpha_{i-1}
     S_L = 16,       // slot s + S_L holds this rank's local partial of slot s; the multi-GPU
                     // all-reduce is out of place (local -> global), hence idempotent: iterations
                     // enqueued after convergence cannot corrupt the global scalars
@@ -580,7 +584,7 @@ __global__ void __launch_bounds__(kVecThreads)
     k_finalize(const T *__restrict__ Ypart, int nslots, int nsub, int band0, int64_t nb, int64_t g0, int64_t m1,
                const T *__restrict__ pband, T *__restrict__ y, int mode, const T *__restrict__ yl, T *__restrict__ r,
                T *__restrict__ pout, double *scal, int par, int set_delta0, T *partials, unsigned *counter,
-               int write_scalar, const int *ctrl) {
+               int write_scalar, const int *ctrl, int pap_slot) {
     if (cg_done(ctrl)) return;
     if (par < 0) par = (ctrl[C_IT] & 1) ^ 1;  // residual replacement: the slot of delta_{k+1}
     T part = T(0);
@@ -616,7 +620,7 @@ __global__ void __launch_bounds__(kVecThreads)
     grid_reduce<T>(part, partials, counter, [&](T tot) {
         if (!write_scalar) return;
         if (mode == 0) {
-            scal[S_PAP] = scal[S_PAP + S_L] = static_cast<double>(tot);
+            scal[pap_slot] = scal[pap_slot + S_L] = static_cast<double>(tot);
         } else {
             scal[S_DELTA + par] = scal[S_DELTA + par + S_L] = static_cast<double>(tot);
             if (set_delta0) scal[S_DELTA0] = scal[S_DELTA0 + S_L] = static_cast<double>(tot);
@@ -692,9 +696,71 @@ __global__ void k_cg_loop_init(cudaGraphConditionalHandle loop, const int *ctrl)
     cudaGraphSetConditional(loop, ctrl[C_DONE] == 0 ? 1u : 0u);
 }
 
+// Chronopoulos-Gear CG (options.cg_variant SINGLE_REDUCTION; Chronopoulos & Gear 1989): the
+// product is taken of r instead of p (w = Q~ r), and s = Q~ p is carried by recurrence, so both
+// inner products of an iteration, gamma = r.r and delta = w.r, come from ONE reduction point
+// (one all-reduce of the pair on several GPUs instead of two).  Mathematically the CG iterates
+// of Shewchuk's loop.  Entry: r_i, w_i = Q~ r_i (band), gamma_i, delta_i global.
+// Loop condition on gamma_i (same threshold eps^2 delta_0 as the Shewchuk loop), breakdown if
+// the p.Q~p equivalent delta_i - beta gamma_i / alpha_{i-1} <= 0; otherwise
+//   beta = gamma_i / gamma_{i-1}, alpha = gamma_i / (delta_i - beta gamma_i / alpha_{i-1})
+//   p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s ; gamma_{i+1} = r.r (partial)
+// Every block takes the same verdict from the same scalars; block 0 records it.
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_cgcg_update(T *__restrict__ x, T *__restrict__ r, T *__restrict__ p, T *__restrict__ s, const T *__restrict__ w,
+                  int64_t nb, double *scal, int *ctrl, T *partials, unsigned *counter, cudaGraphConditionalHandle loop,
+                  int use_loop) {
+    if (cg_done(ctrl)) {
+        if (use_loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0u);
+        return;
+    }
+    const int it = ctrl[C_IT];
+    const double g = scal[S_CG_GAMMA], dl = scal[S_CG_DELTA];
+    double beta = 0.0, den = dl;
+    if (it > 0) {
+        beta = g / scal[S_CG_GPREV];
+        den = dl - beta * g / scal[S_CG_APREV];
+    }
+    int done = 0;
+    if (ctrl[C_FIXED] > 0 ? (it >= ctrl[C_FIXED] || g == 0.0) : (g <= scal[S_THR])) done = 1;
+    else if (it >= ctrl[C_IMAX]) done = 1;
+    else if (!(den > 0.0) || !isfinite(den) || !isfinite(g)) done = 2;
+    if (done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctrl[C_DONE] = done;
+            if (use_loop) cudaGraphSetConditional(loop, 0u);
+        }
+        return;
+    }
+    const double alpha = g / den;
+    const T a = static_cast<T>(alpha), b = static_cast<T>(beta);
+    T part = T(0);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const T pi = fma(b, p[i], r[i]);
+        const T si = fma(b, s[i], w[i]);
+        p[i] = pi;
+        s[i] = si;
+        x[i] = fma(a, pi, x[i]);
+        const T ri = fma(-a, si, r[i]);
+        r[i] = ri;
+        part = fma(ri, ri, part);
+    }
+    grid_reduce<T>(part, partials, counter, [&](T tot) {
+        scal[S_CG_GAMMA] = scal[S_CG_GAMMA + S_L] = static_cast<double>(tot);
+        scal[S_CG_GPREV] = g;
+        scal[S_CG_APREV] = alpha;
+        scal[S_ALPHA] = alpha;
+        ctrl[C_IT] = it + 1;
+    });
+}
+
 // Loop entry (after delta_0 is final on every rank): threshold and control block.
 __global__ void k_cg_start(double *scal, int *ctrl, double eps2, int imax, int fixed) {
     const double d0 = scal[S_DELTA0];
+    scal[S_CG_GAMMA] = d0;  // Chronopoulos-Gear: gamma_0 = r_0.r_0 (global and this rank's partial)
+    scal[S_CG_GAMMA + S_L] = scal[S_DELTA0 + S_L];
     scal[S_THR] = eps2 * d0;
     ctrl[C_IT] = 0;
     ctrl[C_IMAX] = imax;

@@ -193,3 +193,77 @@ def test_feature_split_cg_gloo(tmp_path, world):
     assert np.linalg.norm(res["y"] - res["ref_y"]) <= 1e-13 * np.linalg.norm(res["ref_y"])
     assert np.linalg.norm(res["x"] - res["ref_x"]) <= 1e-8 * np.linalg.norm(res["ref_x"])
     assert abs(int(res["it"]) - int(res["ito"])) <= 2
+
+
+def _worker_cgcg(rank, world, port, result_path):
+    """Chronopoulos-Gear CG with the driver's exchange sequence (kernels.cuh k_cgcg_update): per
+    iteration ONE all-gather of r, the band product w = (Q~ r)_band, and ONE all-reduce of the
+    pair (gamma, delta).  Must reach the single-process oracle CG solution."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    import paper_2202_12674_b200 as pl
+    import synth
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, y, _, _ = synth.planes(300, 7, seed=3)
+    m = X.shape[0]
+    m1 = m - 1
+    b0, b1, mpad = pl.plssvm_partition(m, world, rank)
+    nb = b1 - b0
+    rows = np.arange(b0, b1)
+    valid = rows < m1
+    R = np.zeros((nb, m1))
+    R[valid] = oracle.qtilde_rows(X, rows[valid], oracle.RBF, 0.2, C=1.0)
+
+    def allgather(band):
+        out = [torch.zeros(nb, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(out, torch.from_numpy(band.copy()))
+        return torch.cat(out).numpy()
+
+    def allreduce_pair(a, b):
+        t = torch.tensor([a, b], dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t[0]), float(t[1])
+
+    reductions = 0
+    r = np.where(valid, y[np.minimum(rows, m - 1)] - y[m - 1], 0.0)
+    x = np.zeros(nb)
+    p = np.zeros(nb)
+    s = np.zeros(nb)
+    gamma, _ = allreduce_pair(r @ r, 0.0)
+    thr = 1e-20 * gamma
+    it, g_prev, a_prev = 0, 0.0, 0.0
+    while True:
+        w = R @ allgather(r)[:m1]
+        gamma, delta = allreduce_pair(r @ r, w @ r)  # the one reduction point
+        reductions += 1
+        if gamma <= thr or it >= m1:
+            break
+        beta = gamma / g_prev if it > 0 else 0.0
+        alpha = gamma / (delta - beta * gamma / a_prev) if it > 0 else gamma / delta
+        p = r + beta * p
+        s = w + beta * s
+        x += alpha * p
+        r = r - alpha * s
+        g_prev, a_prev = gamma, alpha
+        it += 1
+    xfull = allgather(x)[:m1]
+    if rank == 0:
+        Qt = oracle.qtilde(X, oracle.RBF, 0.2, C=1.0)
+        xo, ito, _ = oracle.cg(Qt, y[:-1] - y[-1], eps=1e-10)
+        np.savez(result_path, x=xfull, ref_x=xo, it=it, ito=ito, red=reductions)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_single_reduction_cg_gloo(tmp_path):
+    path = str(tmp_path / "res.npz")
+    mp.spawn(_worker_cgcg, args=(2, _free_port(), path), nprocs=2, join=True)
+    res = np.load(path)
+    assert np.linalg.norm(res["x"] - res["ref_x"]) <= 1e-8 * np.linalg.norm(res["ref_x"])
+    assert abs(int(res["it"]) - int(res["ito"])) <= 2
+    assert int(res["red"]) == int(res["it"]) + 1  # one all-reduce per iteration (+ the final test)

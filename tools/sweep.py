@@ -62,7 +62,7 @@ def run(cfg, mode, engine="auto", repeat=2):
     for _ in range(repeat):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        alpha, b, st, s = pl.plssvm_train_ex(tX, ty, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=pl.options(mode=md, fp64_engine=ENGINES[engine]), **kw)
+        alpha, b, st, s = pl.plssvm_train_ex(tX, ty, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=pl.options(mode=md, fp64_engine=ENGINES[engine], cg_loop=pl.CG_BATCHED), **kw)
         torch.cuda.synchronize()
         tt = time.perf_counter() - t0
         if best is None or tt < best[0]:
