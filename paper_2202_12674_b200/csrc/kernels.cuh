@@ -374,7 +374,10 @@ __global__ void __launch_bounds__(256) k_gemv_tiled(const T *__restrict__ Qc, co
 // row-major block at ordinal t (the tile list order, NSUB entries per pair).  One CTA per stored
 // tile streams it once and uses it twice: row sums Q~_IJ p_J -> rows of I (slot J) and, for
 // I != J, column sums Q~_IJ^T p_I -> rows of J (slot I) -- half the HBM bytes of full rows.
-// Warp w owns rows 16w..16w+15, lane l columns 4l..4l+3 (a row = 1 KiB / 512 B, coalesced).
+// Warp w owns rows 16w..16w+15; lane l holds 4 columns of each row, taken as LPR 16-byte
+// vectors that are each contiguous across the warp: column u*32*VEC + l*VEC + v (fp64: 2l, 2l+1,
+// 64+2l, 65+2l; fp32: 4l..4l+3) -- every load instruction of a warp covers 512 contiguous bytes,
+// so no 32-byte sector is fetched twice through the no-allocate L1 path.
 template <typename T>
 __global__ void __launch_bounds__(256, 4) k_gemv_sym(const T *__restrict__ Qc, const int2 *__restrict__ tiles, int nsub,
                                                      int64_t nstored, int per_cta, const T *__restrict__ p, int band0,
@@ -391,11 +394,11 @@ __global__ void __launch_bounds__(256, 4) k_gemv_sym(const T *__restrict__ Qc, c
         const int buf = nsync & 1;
         const int2 tile = tiles[tt * nsub];
         const int I = tile.x, J = tile.y / nsub;
-        const T *blk = Qc + tt * (kTile * kTile) + (w * 16) * kTile + lane * 4;
+        const T *blk = Qc + tt * (kTile * kTile) + (w * 16) * kTile + lane * VEC;
         T pj[4], rs[16], cs[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-            pj[v] = p[static_cast<int64_t>(J) * kTile + lane * 4 + v];
+            pj[v] = p[static_cast<int64_t>(J) * kTile + (v / VEC) * (32 * VEC) + lane * VEC + (v % VEC)];
             cs[v] = T(0);
         }
 #pragma unroll
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(256, 4) k_gemv_sym(const T *__restrict__ Qc, c
             T a[4];
 #pragma unroll
             for (int u = 0; u < LPR; ++u) {
-                const V *src = reinterpret_cast<const V *>(blk + r * kTile) + u;
+                const V *src = reinterpret_cast<const V *>(blk + r * kTile + u * (32 * VEC));
                 V x;
                 if constexpr (sizeof(T) == 8) {
                     asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(x.x), "=d"(x.y) : "l"(src));
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(256, 4) k_gemv_sym(const T *__restrict__ Qc, c
         }
         if (I != J) {  // tile-uniform branch
 #pragma unroll
-            for (int v = 0; v < 4; ++v) redc[buf][w][lane * 4 + v] = cs[v];
+            for (int v = 0; v < 4; ++v) redc[buf][w][(v / VEC) * (32 * VEC) + lane * VEC + (v % VEC)] = cs[v];
             __syncthreads();
             ++nsync;
             if (threadIdx.x < kTile) {
