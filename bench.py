@@ -299,26 +299,35 @@ def main():
 
     # ---- roofline of the dominant kernel (the Q~p product), timed with CUDA events on its stream
     avg_mv = t_mv / max(1, matvecs)
-    engine = {1: "ozaki", 2: "dmma"}.get(stats0.fp64_engine_used, "tcgen05-3xtf32")
+    if cfg.dtype == "f64":
+        engine = {1: "ozaki", 2: "dmma"}.get(stats0.fp64_engine_used, "dmma")
+    else:
+        engine = {0: "tcgen05-3xtf32", 1: "ffma", 2: "ozaki"}.get(stats0.fp32_engine_used, "tcgen05-3xtf32")
     if mode_used == "implicit" and engine == "ozaki":
         # int8 digit products per launch: 28 pairs x 2 d8 ops per distinct Q~ entry (d8 = d rounded up to
         # the 32-feature slab), this rank's ~1/P share; fp64-equivalent rate reported beside it
         fl = matvec_flops(cfg.m, cfg.d) / world
         d8 = -(-cfg.d // 32) * 32
-        ops = OZAKI_DIGIT_PAIRS * fl * d8 / cfg.d
+        pairs = OZAKI_DIGIT_PAIRS if cfg.dtype == "f64" else 6  # fp32 engine: 3 digits, levels <= 2
+        ops = pairs * fl * d8 / cfg.d
         peak = int8_peak_tops(sustained=True)
         achieved = ops / avg_mv / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)", "frac": achieved / peak,
                 "traffic": traffic_for(f"{cfg.name}/implicit/k_tile_ozaki") if world == 1 else None,
                 "traffic_unit": "bytes per launch (ncu dram read+write)", "kernel": "k_tile_ozaki (OZ_MATVEC)",
-                "per_launch": f"{OZAKI_DIGIT_PAIRS} digit pairs x 2*d8 int8 ops per distinct Q~ entry, E = m'(m'+1)/2 "
+                "per_launch": f"{pairs} digit pairs x 2*d8 int8 ops per distinct Q~ entry, E = m'(m'+1)/2 "
                               f"({ops:.4g} int8 ops per launch per rank)",
                 "peak_source": "int8 dense = 2 x MEASURED_PEAKS.json bf16_tflops_sustained (guide ratio 4.5/2.25; "
                                "the kernel runs back to back at the 1 kW power cap)",
                 "frac_of_burst_peak": achieved / int8_peak_tops(sustained=False),
-                "fp64_equivalent": {"achieved_tflops": fl / avg_mv / 1e12, "dmma_peak_tflops": FP64_PEAK_TFLOPS,
-                                    "ratio": fl / avg_mv / 1e12 / FP64_PEAK_TFLOPS},
                 "avg_launch_s": avg_mv}
+        if cfg.dtype == "f64":
+            roof["fp64_equivalent"] = {"achieved_tflops": fl / avg_mv / 1e12, "dmma_peak_tflops": FP64_PEAK_TFLOPS,
+                                       "ratio": fl / avg_mv / 1e12 / FP64_PEAK_TFLOPS}
+        else:
+            roof["fp32_equivalent"] = {"achieved_tflops": fl / avg_mv / 1e12,
+                                       "tf32x3_peak_tflops": tf32x3_peak_tflops(),
+                                       "ratio": fl / avg_mv / 1e12 / tf32x3_peak_tflops()}
     elif mode_used == "implicit":
         fl = matvec_flops(cfg.m, cfg.d) / world  # this rank's share (symmetric work split)
         peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else tf32x3_peak_tflops()
@@ -345,7 +354,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (sklearn make_classification planes, seeded)",
             "config": dict(config_dict(cfg, args, mode_used), fp64_engine=engine if cfg.dtype == "f64" else None,
-                           contraction=("int8 digit products (exact int32 sums) combined in f64" if engine == "ozaki"
+                           fp32_engine=engine if cfg.dtype == "f32" else None,
+                           contraction=(("int8 digit products (exact int32 sums) combined in f64" if cfg.dtype == "f64" else
+                                         "int8 digit products of a 3-digit (22-bit) split, exact int32 sums, "
+                                         "f32 epilogue") if engine == "ozaki"
                                         else None)),
             "gpu_launches": launches, "clocks": clocks,
             "roofline": roof,

@@ -92,8 +92,8 @@ typedef struct {
                                 one process per GPU); NULL = single GPU [NULL] */
     int64_t cache_budget_bytes; /* AUTO/CACHED: max bytes for the cached Q~ band;
                                    <= 0 means 90 % of free HBM after the other buffers [0] */
-    int32_t fp32_engine;     /* fp32 implicit Q~p contraction: 0 = tensor cores (tcgen05 kind::tf32,
-                                3xTF32 split) [0]; 1 = CUDA-core FFMA tiles */
+    int32_t fp32_engine;     /* plssvm_fp32_engine_t: fp32 contraction of the implicit Q~p, the cached
+                                precompute and predict [AUTO] */
     int32_t linear_w;        /* predict with the linear kernel through w = sum_i alpha_i x_i (Eq. 15,
                                 O((m+n)d)) [1]; 0 = evaluate the kernel matrix like the other kernels */
     int32_t fp64_engine;     /* plssvm_fp64_engine_t: fp64 pairwise contraction of the implicit Q~p, the
@@ -135,6 +135,15 @@ typedef enum { PLSSVM_CG_AUTO = 0, PLSSVM_CG_BATCHED = 1, PLSSVM_CG_GRAPH = 2 } 
  *            IMPLICIT); needs d >= P.  Otherwise PLSSVM_E_INVALID_ARG. */
 typedef enum { PLSSVM_MULTI_GPU_ROWS = 0, PLSSVM_MULTI_GPU_FEATURES = 1 } plssvm_multi_gpu_t;
 
+/* fp32 contraction engines.
+ *  TCGEN05: tcgen05 kind::tf32 tensor cores, 3xTF32 hi/lo split (21 + 21 bits per operand).
+ *  FFMA:    CUDA-core fp32 FMA tiles.
+ *  OZAKI:   int8 tensor cores (tcgen05 kind::i8, 2-SM UMMA) on a 3-digit balanced base-256 split of
+ *           every point, rounded to 22 bits below its row maximum (6 digit pairs, exact int32 sums,
+ *           one TMEM pass): error of x_i.x_j <~ d 2^-22 ||x_i||_inf ||x_j||_inf.  d <= 16384.
+ *  AUTO:    OZAKI unless some point has max_k |x_ik| > 8 * rms_k(x_ik) or d > 16384, then TCGEN05. */
+typedef enum { PLSSVM_FP32_TCGEN05 = 0, PLSSVM_FP32_FFMA = 1, PLSSVM_FP32_OZAKI = 2, PLSSVM_FP32_AUTO = 3 } plssvm_fp32_engine_t;
+
 /* fp64 contraction engines.
  *  OZAKI: int8 tensor cores (tcgen05 kind::i8, 2-SM UMMA) on an EXACT split of every point into
  *         7 balanced base-256 int8 digits times a power of two (x_i = 2^(E_i-54) sum_a D_a 256^(6-a),
@@ -165,6 +174,8 @@ typedef struct {
     int64_t launches_in_cg;          /* of which inside the CG loop */
     int32_t fp64_engine_used;        /* PLSSVM_FP64_OZAKI or _DMMA for fp64 calls, 0 for fp32 */
     int32_t cg_loop_used;            /* PLSSVM_CG_BATCHED or PLSSVM_CG_GRAPH */
+    int32_t fp32_engine_used;        /* fp32 calls: PLSSVM_FP32_OZAKI, _TCGEN05 or _FFMA; 0 for fp64 */
+    int32_t reserved1;
 } plssvm_stats_t;
 
 PLSSVM_API void plssvm_default_options(plssvm_options_t *opts);

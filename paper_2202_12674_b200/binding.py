@@ -21,6 +21,7 @@ FP64_AUTO, FP64_OZAKI, FP64_DMMA = 0, 1, 2
 CG_AUTO, CG_BATCHED, CG_GRAPH = 0, 1, 2
 MULTI_GPU_ROWS, MULTI_GPU_FEATURES = 0, 1
 CG_SHEWCHUK, CG_SINGLE_REDUCTION = 0, 1
+FP32_TCGEN05, FP32_FFMA, FP32_OZAKI, FP32_AUTO = 0, 1, 2, 3
 OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED, E_IO = range(9)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
                 6: "E_NUMERICAL", 7: "W_NOT_CONVERGED", 8: "E_IO"}
@@ -49,7 +50,7 @@ class plssvm_stats_t(ct.Structure):
                 ("t_cg", ct.c_double), ("t_bias_d2h", ct.c_double), ("t_total", ct.c_double),
                 ("t_matvec", ct.c_double), ("t_matvec_min", ct.c_double), ("bytes_per_gpu", ct.c_int64),
                 ("gpu_launches", ct.c_int64), ("launches_in_cg", ct.c_int64), ("fp64_engine_used", ct.c_int32),
-                ("cg_loop_used", ct.c_int32)]
+                ("cg_loop_used", ct.c_int32), ("fp32_engine_used", ct.c_int32), ("reserved1", ct.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

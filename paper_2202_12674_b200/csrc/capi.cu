@@ -72,6 +72,8 @@ plssvm_options_t defaults() {
 
 // PLSSVM_MULTI_GPU_FEATURES (paper §III-C5): linear kernel, fp64, implicit, d >= P.
 int check_multi_gpu(const plssvm_options_t &o, int kernel, int dtype, int64_t d) {
+    if (o.fp32_engine < PLSSVM_FP32_TCGEN05 || o.fp32_engine > PLSSVM_FP32_AUTO)
+        return fail(PLSSVM_E_INVALID_ARG, "options.fp32_engine must be 0 (TCGEN05), 1 (FFMA), 2 (OZAKI) or 3 (AUTO)");
     if (o.multi_gpu != PLSSVM_MULTI_GPU_ROWS && o.multi_gpu != PLSSVM_MULTI_GPU_FEATURES)
         return fail(PLSSVM_E_INVALID_ARG, "options.multi_gpu must be 0 (ROWS) or 1 (FEATURES)");
     if (o.multi_gpu != PLSSVM_MULTI_GPU_FEATURES) return PLSSVM_OK;
@@ -102,7 +104,7 @@ void plssvm_default_options(plssvm_options_t *o) {
     o->stream = nullptr;
     o->comm = nullptr;
     o->cache_budget_bytes = 0;
-    o->fp32_engine = 0;
+    o->fp32_engine = PLSSVM_FP32_AUTO;
     o->linear_w = 1;
     o->fp64_engine = PLSSVM_FP64_AUTO;
     o->cg_loop = PLSSVM_CG_AUTO;

@@ -451,6 +451,9 @@ std::vector<int2> wide_tiles(int T) {
 // ---- fp64 on the int8 tensor cores (ozaki_engine.cuh) -------------------------------------
 constexpr int kOzS = 7;  // balanced base-256 digits per point: fp64-level products
 using OzC = Oz<kOzS>;
+// digits of the engine for value type T: 7 for fp64, 3 for fp32 (PLSSVM_FP32_OZAKI)
+template <typename T>
+constexpr int oz_digits() { return std::is_same<T, double>::value ? 7 : 3; }
 
 int num_sms() {
     int dev = 0, n = 0;
@@ -459,34 +462,71 @@ int num_sms() {
     return n;
 }
 
-OzOperand oz_prepare(Arena &A, const double *Xp, int64_t rows, int64_t dpad, int64_t d, bool row_role, bool col_role,
+// S digit planes of the point-major padded array Xp (fp64 with S = 7, fp32 with S = 3).  Maps:
+// t8 / h8 carry all S planes of a slab block, t4 / h4 the first LV planes (S = 7's pass 1).
+template <int S, typename TIN>
+OzOperand oz_prepare(Arena &A, const TIN *Xp, int64_t rows, int64_t dpad, int64_t d, bool row_role, bool col_role,
                      cudaStream_t s, int64_t &launches) {
+    using O = Oz<S>;
     OzOperand o;
-    const int64_t d8 = round_up(d, OzC::BK);
-    const int64_t bytes = kOzS * rows * d8;
+    const int64_t d8 = round_up(d, O::BK);
+    const int64_t bytes = S * rows * d8;
     if (row_role) o.DA = A.alloc<int8_t>(bytes);
     if (col_role) o.DB = A.alloc<int8_t>(bytes);
     o.sc = A.alloc<double>(rows);
-    k_ozaki_split<kOzS><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, s>>>(Xp, rows, dpad, d8, o.DA, o.DB,
-                                                                                       o.sc);
+    k_ozaki_split<S, TIN><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, s>>>(Xp, rows, dpad, d8, o.DA,
+                                                                                         o.DB, o.sc);
     PLS_CHECK_LAUNCH();
     ++launches;
     if (row_role) {
-        o.t4 = make_tmap_digit_blocks(o.DA, bytes, OzC::LV * 32);
-        o.t8 = make_tmap_digit_blocks(o.DA, bytes, kOzS * 32);
+        o.t4 = make_tmap_digit_blocks(o.DA, bytes, O::LV * 32);
+        o.t8 = make_tmap_digit_blocks(o.DA, bytes, S * 32);
     }
     if (col_role) {
-        o.h4 = make_tmap_digit_blocks(o.DB, bytes, OzC::LV * 16);
-        o.h8 = make_tmap_digit_blocks(o.DB, bytes, kOzS * 16);
+        o.h4 = make_tmap_digit_blocks(o.DB, bytes, O::LV * 16);
+        o.h8 = make_tmap_digit_blocks(o.DB, bytes, S * 16);
     }
-    o.nk = static_cast<int>(d8 / OzC::BK);
+    o.nk = static_cast<int>(d8 / O::BK);
     return o;
+}
+
+// Point-major padded fp32 copy [rows][d8] of the caller's row-major X (zero padding) -- the
+// layout k_ozaki_split reads; the fp32 engines otherwise use the feature-major one.
+float *oz_point_major(Arena &A, const float *Xs, int64_t m, int64_t d, int64_t rows, int64_t d8, cudaStream_t s,
+                      int64_t &launches) {
+    float *Xp = A.alloc<float>(rows * d8);
+    dim3 grid(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(ceil_div(d8, 32)));
+    k_transform<float><<<grid, dim3(32, 8), 0, s>>>(Xs, m, d, Xp, rows, d8, 1);
+    PLS_CHECK_LAUNCH();
+    ++launches;
+    return Xp;
 }
 
 // fp64 engine choice (plssvm.h plssvm_fp64_engine_t): OZAKI, DMMA, or AUTO = OZAKI unless a row
 // of any operand array peaks above kOzPeakMax x its RMS.
 constexpr double kOzPeakMax = 64.0;
 constexpr int64_t kOzMaxD = 16384;
+// The largest row peak max_k |x_ik| / rms_k(x_ik) over the given point-major arrays (one sync).
+template <typename TIN>
+float oz_row_peak(std::initializer_list<const TIN *> arrays, std::initializer_list<int64_t> rows, int64_t dpad,
+                  int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
+    unsigned *bits = A.alloc<unsigned>(1);
+    PLS_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned), s));
+    auto r = rows.begin();
+    for (const TIN *X : arrays) {
+        const int64_t n = *r++;
+        k_row_peak<TIN><<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(X, n, dpad, d, bits);
+        PLS_CHECK_LAUNCH();
+        ++launches;
+    }
+    unsigned hb = 0;
+    PLS_CUDA(cudaMemcpyAsync(&hb, bits, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    PLS_CUDA(cudaStreamSynchronize(s));
+    float peak;
+    std::memcpy(&peak, &hb, sizeof(float));
+    return peak;
+}
+
 bool oz_choose(int engine, std::initializer_list<const double *> arrays, std::initializer_list<int64_t> rows,
                int64_t dpad, int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
     if (engine == PLSSVM_FP64_DMMA) return false;
@@ -499,27 +539,31 @@ bool oz_choose(int engine, std::initializer_list<const double *> arrays, std::in
         return true;
     }
     if (!fits) return false;
-    unsigned *bits = A.alloc<unsigned>(1);
-    PLS_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned), s));
-    auto r = rows.begin();
-    for (const double *X : arrays) {
-        const int64_t n = *r++;
-        k_row_peak<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(X, n, dpad, d, bits);
-        PLS_CHECK_LAUNCH();
-        ++launches;
-    }
-    unsigned hb = 0;
-    PLS_CUDA(cudaMemcpyAsync(&hb, bits, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    PLS_CUDA(cudaStreamSynchronize(s));
-    float peak;
-    std::memcpy(&peak, &hb, sizeof(float));
-    return peak <= kOzPeakMax;
+    return oz_row_peak<double>(arrays, rows, dpad, d, A, s, launches) <= kOzPeakMax;
 }
 
+// fp32 engine choice (plssvm.h plssvm_fp32_engine_t): AUTO = OZAKI (3 digits, error <~ d 2^-22
+// ||x_i||_inf ||x_j||_inf) unless a row peaks above kOzPeakMax32 x its RMS (its small features
+// would lose relative accuracy against the fp32 bar) or d > 16384; then TCGEN05 (3xTF32).
+constexpr double kOzPeakMax32 = 8.0;
+bool oz_choose_f32(int engine, std::initializer_list<const float *> arrays, std::initializer_list<int64_t> rows,
+                   int64_t dpad, int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
+    if (engine == PLSSVM_FP32_TCGEN05 || engine == PLSSVM_FP32_FFMA) return false;
+    const bool fits = round_up(d, Oz<3>::BK) <= kOzMaxD;
+    if (engine == PLSSVM_FP32_OZAKI) {
+        if (!fits) throw Error(PLSSVM_E_INVALID_ARG, "fp32_engine OZAKI supports d <= " + std::to_string(kOzMaxD));
+        return true;
+    }
+    if (!fits) return false;
+    return oz_row_peak<float>(arrays, rows, dpad, d, A, s, launches) <= kOzPeakMax32;
+}
+
+template <typename T>
 void oz_set_attrs() {
-    const int bytes = static_cast<int>(OzC::SMEM_BYTES);
+    constexpr int S = oz_digits<T>();
+    const int bytes = static_cast<int>(Oz<S>::SMEM_BYTES);
 #define PLS_OZ_ATTR(K, M) \
-    PLS_CUDA(cudaFuncSetAttribute(k_tile_ozaki<K, kOzS, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
+    PLS_CUDA(cudaFuncSetAttribute(k_tile_ozaki<K, S, M, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
     PLS_OZ_ATTR(LINEAR, OZ_MATVEC); PLS_OZ_ATTR(POLYNOMIAL, OZ_MATVEC); PLS_OZ_ATTR(RBF, OZ_MATVEC);
     PLS_OZ_ATTR(LINEAR, OZ_PRECOMPUTE); PLS_OZ_ATTR(POLYNOMIAL, OZ_PRECOMPUTE); PLS_OZ_ATTR(RBF, OZ_PRECOMPUTE);
     PLS_OZ_ATTR(LINEAR, OZ_PREDICT); PLS_OZ_ATTR(POLYNOMIAL, OZ_PREDICT); PLS_OZ_ATTR(RBF, OZ_PREDICT);
@@ -538,11 +582,13 @@ int oz_debug_flags() {
 
 // One persistent CTA per SM (the 512-column TMEM allocation admits one per SM anyway), in
 // clusters of 2 (cta_group::2): the grid is an even number of CTAs, at most the SM count.
-template <int KT, int MODE>
+template <int KT, int MODE, typename T>
 void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb, const int2 *ptiles, const int *pk,
-               int rowsI, const double *qv, const double *na, const double *nb_, const double *p, KParams<double> kp,
-               double invC, const double *scal, int64_t m1, int band0, int band1, double *Ypart, int64_t band_rows,
-               double *Qc, int T_tiles, const int *ctrl) {
+               int rowsI, const T *qv, const T *na, const T *nb_, const T *p, KParams<T> kp, T invC,
+               const double *scal, int64_t m1, int band0, int band1, T *Ypart, int64_t band_rows, T *Qc, int T_tiles,
+               const int *ctrl) {
+    constexpr int S = oz_digits<T>();
+    using O = Oz<S>;
     if (npt <= 0) return;
     // Only co-resident clusters (a pair must fit in one GPC): a statically scheduled grid with one
     // cluster too many would run that cluster's tiles as a second wave.
@@ -551,14 +597,14 @@ void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb
     if (mc == 0) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(num_sms()), 1, 1);
-        cfg.blockDim = dim3(OzC::THREADS, 1, 1);
-        cfg.dynamicSmemBytes = OzC::SMEM_BYTES;
-        PLS_CUDA(cudaOccupancyMaxActiveClusters(&mc, k_tile_ozaki<KT, kOzS, MODE>, &cfg));
+        cfg.blockDim = dim3(O::THREADS, 1, 1);
+        cfg.dynamicSmemBytes = O::SMEM_BYTES;
+        PLS_CUDA(cudaOccupancyMaxActiveClusters(&mc, k_tile_ozaki<KT, S, MODE, T>, &cfg));
         if (mc <= 0) mc = num_sms() / 2;
         if (std::getenv("PLSSVM_DEBUG")) std::fprintf(stderr, "[plssvm] k_tile_ozaki co-resident pairs: %d\n", mc);
     }
     const int grid = 2 * std::min(npt, mc);
-    k_tile_ozaki<KT, kOzS, MODE><<<grid, OzC::THREADS, OzC::SMEM_BYTES, s>>>(
+    k_tile_ozaki<KT, S, MODE, T><<<grid, O::THREADS, O::SMEM_BYTES, s>>>(
         ra.t4, ra.t8, cb.h4, cb.h8, ra.nk, ptiles, pk, npt, rowsI, ra.sc, cb.sc, qv, na, nb_, p, kp, invC, scal, m1,
         band0, band1, Ypart, band_rows, Qc, T_tiles, ctrl, oz_debug_flags());
     PLS_CHECK_LAUNCH();
@@ -604,33 +650,31 @@ void oz_pair_tiles(const std::vector<int2> &tl, int b0, int b1, int T, int64_t d
             }
 }
 
-template <int MODE, typename... Args>
+template <int MODE, typename T, typename... Args>
 void oz_dispatch(int kernel, Args &&...args) {
     switch (kernel) {
-        case LINEAR: oz_launch<LINEAR, MODE>(args...); break;
-        case POLYNOMIAL: oz_launch<POLYNOMIAL, MODE>(args...); break;
-        default: oz_launch<RBF, MODE>(args...);
+        case LINEAR: oz_launch<LINEAR, MODE, T>(args...); break;
+        case POLYNOMIAL: oz_launch<POLYNOMIAL, MODE, T>(args...); break;
+        default: oz_launch<RBF, MODE, T>(args...);
     }
 }
 
 template <typename T>
 bool launch_oz(Ctx<T> &c, const T *pfull, int b0, int b1, int64_t brows, bool precompute) {
-    if constexpr (std::is_same<T, double>::value) {
-        if (!c.oz) return false;
-        const Geometry &g = c.g;
-        if (precompute)
-            oz_dispatch<OZ_PRECOMPUTE>(c.kp.kernel, c.oz_npt, c.s, c.ozx, c.ozx, c.oz_pt, c.oz_pk, 0, c.q, c.nrm, c.nrm,
-                                       static_cast<const double *>(nullptr), c.kp, c.invC, c.scal, g.m1, g.band0,
-                                       g.band1, static_cast<double *>(nullptr), g.nb, c.Qc, c.packed ? -1 : g.T,
-                                       static_cast<const int *>(nullptr));
-        else
-            oz_dispatch<OZ_MATVEC>(c.kp.kernel, c.oz_npt, c.s, c.ozx, c.ozx, c.oz_pt, c.oz_pk, 0, c.q, c.nrm, c.nrm,
-                                   pfull, c.kp, c.invC, c.scal, g.m1, b0, b1, c.Ypart, brows,
-                                   static_cast<double *>(nullptr), g.T, c.cur_ctrl);
-        ++c.launches;
-        return true;
-    }
-    return false;
+    if (!c.oz) return false;
+    const Geometry &g = c.g;
+    const T *cq = c.q, *cn = c.nrm;
+    if (precompute)
+        oz_dispatch<OZ_PRECOMPUTE, T>(c.kp.kernel, c.oz_npt, c.s, c.ozx, c.ozx, c.oz_pt, c.oz_pk, 0, cq, cn, cn,
+                                      static_cast<const T *>(nullptr), c.kp, c.invC, static_cast<const double *>(c.scal),
+                                      g.m1, g.band0, g.band1, static_cast<T *>(nullptr), g.nb, c.Qc,
+                                      c.packed ? -1 : g.T, static_cast<const int *>(nullptr));
+    else
+        oz_dispatch<OZ_MATVEC, T>(c.kp.kernel, c.oz_npt, c.s, c.ozx, c.ozx, c.oz_pt, c.oz_pk, 0, cq, cn, cn, pfull,
+                                  c.kp, c.invC, static_cast<const double *>(c.scal), g.m1, b0, b1, c.Ypart, brows,
+                                  static_cast<T *>(nullptr), g.T, c.cur_ctrl);
+    ++c.launches;
+    return true;
 }
 
 // (Re)build the 2-SM pair-tile list from the current single-tile list.
@@ -897,14 +941,25 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.Xt = A.alloc<T>(g.dpad * g.mpad);
     launch_transform<T>(Xs, pb.m, dl, c.Xt, g.mpad, g.dpad, c.s, c.launches);
     c.ops = make_ops(c.Xt, g.mpad, c.Xt, g.mpad, g.ld);
-    c.tc = std::is_same<T, float>::value && o.fp32_engine == 0;
-    if (c.tc) setup_tc<T>(c, A, Xs, pb.m, dl);
     if constexpr (std::is_same<T, double>::value) {
         c.oz = oz_choose(o.fp64_engine, {c.Xt}, {g.mpad}, g.dpad, dl, A, c.s, c.launches);
         if (c.oz) {
-            c.ozx = oz_prepare(A, c.Xt, g.mpad, g.dpad, dl, true, true, c.s, c.launches);
-            oz_set_attrs();
+            c.ozx = oz_prepare<7, double>(A, c.Xt, g.mpad, g.dpad, dl, true, true, c.s, c.launches);
+            oz_set_attrs<double>();
         }
+    } else {
+        if (o.fp32_engine == PLSSVM_FP32_OZAKI || o.fp32_engine == PLSSVM_FP32_AUTO) {
+            // fp32 on the int8 tensor cores (3 digits): a point-major padded copy to split
+            const int64_t d8 = round_up(dl, Oz<3>::BK);
+            float *Xp = oz_point_major(A, Xs, pb.m, dl, g.mpad, d8, c.s, c.launches);
+            c.oz = oz_choose_f32(o.fp32_engine, {Xp}, {g.mpad}, d8, dl, A, c.s, c.launches);
+            if (c.oz) {
+                c.ozx = oz_prepare<3, float>(A, Xp, g.mpad, d8, dl, true, true, c.s, c.launches);
+                oz_set_attrs<float>();
+            }
+        }
+        c.tc = !c.oz && o.fp32_engine != PLSSVM_FP32_FFMA;
+        if (c.tc) setup_tc<T>(c, A, Xs, pb.m, dl);
     }
     PLS_CUDA(cudaEventRecord(e_tr, c.s));
     c.q = A.alloc<T>(g.mpad);
@@ -1311,6 +1366,9 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         st->mode_used = c.lowrank ? PLSSVM_MODE_LOWRANK : (c.cached ? PLSSVM_MODE_CACHED : PLSSVM_MODE_IMPLICIT);
         st->num_ranks = c.nranks;
         st->cg_loop_used = c.graph_used ? PLSSVM_CG_GRAPH : PLSSVM_CG_BATCHED;
+        st->fp32_engine_used = std::is_same<T, float>::value
+                                   ? (c.oz ? PLSSVM_FP32_OZAKI : c.tc ? PLSSVM_FP32_TCGEN05 : PLSSVM_FP32_FFMA)
+                                   : 0;
         st->t_h2d = elapsed(e0, e_h2d);
         st->t_transform = elapsed(e_h2d, e_tr);
         st->t_q = elapsed(e_tr, e_q);
@@ -1452,10 +1510,17 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
         PLS_CHECK_LAUNCH();
         launches += 2;
     }
-    const bool tc = std::is_same<T, float>::value && o.fp32_engine == 0;
-    bool oz64 = false;
-    if constexpr (std::is_same<T, double>::value)
+    bool oz64 = false;  // (the name: the Ozaki engine of either precision)
+    const T *Xoz = nullptr, *Zoz = nullptr;  // fp32: point-major padded copies for the split
+    if constexpr (std::is_same<T, double>::value) {
         oz64 = oz_choose(o.fp64_engine, {Zl, Xl}, {zrows, xrows}, dpad, d, A, s, launches);
+    } else if (o.fp32_engine == PLSSVM_FP32_OZAKI || o.fp32_engine == PLSSVM_FP32_AUTO) {
+        const int64_t d8 = round_up(d, Oz<3>::BK);
+        Zoz = oz_point_major(A, Zs, n, d, npad, d8, s, launches);
+        Xoz = oz_point_major(A, Xs, m, d, mpad, d8, s, launches);
+        oz64 = oz_choose_f32(o.fp32_engine, {Zoz, Xoz}, {npad, mpad}, d8, d, A, s, launches);
+    }
+    const bool tc = std::is_same<T, float>::value && !oz64 && o.fp32_engine != PLSSVM_FP32_FFMA;
     const int tilesI = static_cast<int>(npad / kTile),
               tilesJ = static_cast<int>(mpad / (tc ? kTile : oz64 ? OzC::TN : EN::TN));
     T *Fpart = A.alloc<T>(static_cast<int64_t>(tilesJ) * npad);
@@ -1493,18 +1558,24 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
         }
     }
     const bool oz = oz64;
-    if constexpr (std::is_same<T, double>::value) {
-        if (oz) {  // fp64 on the int8 tensor cores: test points = row operand, training points = columns
-            const OzOperand oz_z = oz_prepare(A, Zl, zrows, dpad, d, true, false, s, launches);
-            const OzOperand oz_x = oz_prepare(A, Xl, xrows, dpad, d, false, true, s, launches);
-            oz_set_attrs();
-            PLS_CUDA(cudaEventRecord(e0, s));
-            oz_dispatch<OZ_PREDICT>(pb.kernel, ((tilesI + 1) / 2) * tilesJ, s, oz_z, oz_x,
-                                    static_cast<const int2 *>(nullptr), static_cast<const int *>(nullptr), tilesI,
-                                    static_cast<const double *>(nullptr), nz, nx, alpha, kp, 0.0,
-                                    static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,
-                                    static_cast<double *>(nullptr), 0, static_cast<const int *>(nullptr));
+    if (oz) {  // int8 tensor cores: test points = row operand, training points = columns
+        OzOperand oz_z, oz_x;
+        if constexpr (std::is_same<T, double>::value) {
+            oz_z = oz_prepare<7, double>(A, Zl, zrows, dpad, d, true, false, s, launches);
+            oz_x = oz_prepare<7, double>(A, Xl, xrows, dpad, d, false, true, s, launches);
+        } else {
+            const int64_t d8 = round_up(d, Oz<3>::BK);
+            oz_z = oz_prepare<3, float>(A, Zoz, npad, d8, d, true, false, s, launches);
+            oz_x = oz_prepare<3, float>(A, Xoz, mpad, d8, d, false, true, s, launches);
         }
+        oz_set_attrs<T>();
+        PLS_CUDA(cudaEventRecord(e0, s));
+        oz_dispatch<OZ_PREDICT, T>(pb.kernel, ((tilesI + 1) / 2) * tilesJ, s, oz_z, oz_x,
+                                   static_cast<const int2 *>(nullptr), static_cast<const int *>(nullptr), tilesI,
+                                   static_cast<const T *>(nullptr), static_cast<const T *>(nz),
+                                   static_cast<const T *>(nx), static_cast<const T *>(alpha), kp, T(0),
+                                   static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,
+                                   static_cast<T *>(nullptr), 0, static_cast<const int *>(nullptr));
     }
     const Ops<T> pops = make_ops(Zl, zrows, Xl, xrows, EN::kPointMajor ? dpad : L);
     if (!tc && !oz) PLS_CUDA(cudaEventRecord(e0, s));

@@ -46,17 +46,24 @@ namespace plssvm {
 
 enum OzMode : int { OZ_MATVEC = 0, OZ_PRECOMPUTE = 1, OZ_PREDICT = 2 };
 
+// S = 7 (fp64 engine): pass 0 = levels 4..6 (all 7 planes), pass 1 = levels 0..3 (planes 0..3).
+// S = 3 (fp32 engine, plssvm.h PLSSVM_FP32_OZAKI): one pass, levels 0..2 (6 digit pairs, planes
+// 0..2) -- x rounded to 22 bits below its row maximum, i.e. the fp32 products of the inputs to
+// ~2^-22 relative to ||x_i||_inf ||x_j||_inf (the 3xTF32 split carries 21 + 21 bits).
 template <int S>
 struct Oz {
-    static_assert(S == 7, "7 balanced base-256 digits: pass 0 = levels 4..6, pass 1 = levels 0..3");
+    static_assert(S == 7 || S == 3, "7 digits (fp64, two passes) or 3 digits (fp32, one pass)");
+    static constexpr int NPASS = S == 7 ? 2 : 1;
+    static constexpr int BITS = 8 * S - 2;                         // N_i = round(x_i 2^{BITS - E_i})
+    static constexpr int SC_SHIFT = S == 7 ? 6 : 14;               // sc_i = 2^{E_i - SC_SHIFT}
     static constexpr int BK = 32;                                  // int8 features per slab (32 B rows)
     static constexpr int TN = 128;                                 // tile columns (UMMA N)
     static constexpr int NSUB = kTile / TN;                        // 1
-    static constexpr int LV = 4;                                   // levels of pass 1 (0..3)
-    static constexpr int LV0 = S - LV;                             // levels of pass 0 (4..S-1)
-    static constexpr int STAGES = 4;
+    static constexpr int LV = S == 7 ? 4 : 3;                      // levels of the last pass (0..LV-1)
+    static constexpr int LV0 = S == 7 ? S - LV : LV;               // levels of pass 0
+    static constexpr int STAGES = S == 7 ? 4 : 8;
     static constexpr uint32_t PLANE = kTile * BK;                  // 4 KiB: one A digit plane (B half: 2 KiB)
-    static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: S planes of A and of the B half
+    static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: all S planes of A and of the B half
     static constexpr int EPI_WARPS = 8;
     static constexpr int THREADS = (EPI_WARPS + 4) * 32;             // warpgroup 0: control, 1-2: epilogue
     static constexpr int CTRL_REGS = 40, EPI_REGS = 232;            // setmaxnreg split (4x40 + 8x232 <= 512 per lane)
@@ -69,6 +76,10 @@ struct Oz {
     // instruction descriptor: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 128, M = 256 (2 SMs)
     static constexpr uint32_t IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TN >> 3) << 17) | ((256u >> 4) << 24);
 };
+
+// Digit planes a pass loads (S = 7: 7 then 4; S = 3: 3).
+template <int S>
+__host__ __device__ constexpr int oz_planes(int pass) { return (S == 7 && pass == 1) ? Oz<S>::LV : S; }
 
 // K-major operand in 32-byte swizzle atoms (8 rows x 32 B): LBO 1 (unused), SBO = 256 B, type 6.
 __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
@@ -194,14 +205,15 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
 // AUTO engine check: the largest row "peak" max_k |x_ik| / rms_k(x_ik) over the rows of a
 // point-major padded fp64 array (zero rows skipped), as float bits in *peak_bits (atomicMax on
 // the bits of a non-negative float orders like the value).  One warp per row.
-__global__ void k_row_peak(const double *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t d,
+template <typename TIN>
+__global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t d,
                            unsigned *__restrict__ peak_bits) {
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= rows) return;
     double mx = 0.0, ss = 0.0;
     for (int64_t k = lane; k < d; k += 32) {
-        const double v = Xp[i * dpad + k];
+        const double v = static_cast<double>(Xp[i * dpad + k]);
         mx = fmax(mx, fabs(v));
         ss = fma(v, v, ss);
     }
@@ -225,31 +237,33 @@ __global__ void k_row_peak(const double *__restrict__ Xp, int64_t rows, int64_t 
 // index XOR bit 2 of the row).  A stage of the tile kernel is then ONE contiguous block per
 // operand, moved by TMA in 128-byte rows with no swizzle (4x fewer, 4x larger requests than
 // a 32-byte-row box: the tile kernel was feed-bound with them).  Either pointer may be null.
-// Row scales sc_i = 2^{E_i - 6} (x_i . x_j = sc_i sc_j sum_l 2^{-8l} acc_l).  One warp per row;
-// 4 features per lane per step.
-template <int S>
-__global__ void k_ozaki_split(const double *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t dpad8,
+// Row scales sc_i = 2^{E_i - SC_SHIFT} (S = 7: x_i . x_j = sc_i sc_j sum_l 2^{-8l} acc_l;
+// S = 3: sc_i sc_j (acc_0 2^16 + acc_1 2^8 + acc_2)).  S = 7 splits the fp64 value exactly
+// (N = x 2^{54-E}, |N| < 2^54); S = 3 rounds the (fp32) value to N = rint(x 2^{22-E}), |N| <= 2^22,
+// which three balanced digits hold.  One warp per row; 4 features per lane per step.
+template <int S, typename TIN>
+__global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t dpad8,
                               int8_t *__restrict__ DA, int8_t *__restrict__ DB, double *__restrict__ sc) {
-    static_assert(8 * S >= 55, "S balanced base-256 digits must hold a 54-bit integer");
+    static_assert(8 * S >= Oz<S>::BITS + 1, "S balanced base-256 digits must hold the split integer");
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= rows) return;
-    const double *x = Xp + i * dpad;
+    const TIN *x = Xp + i * dpad;
     double mx = 0.0;
-    for (int64_t k = lane; k < dpad; k += 32) mx = fmax(mx, fabs(x[k]));
+    for (int64_t k = lane; k < dpad; k += 32) mx = fmax(mx, fabs(static_cast<double>(x[k])));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     int E = 0;
     if (mx > 0.0) frexp(mx, &E);  // mx = f 2^E, f in [0.5, 1)  =>  |x_ik| < 2^E
-    if (lane == 0) sc[i] = ldexp(1.0, E - 6);
+    if (lane == 0) sc[i] = ldexp(1.0, E - Oz<S>::SC_SHIFT);
     const int64_t nk = dpad8 / 32;
     const int r128 = static_cast<int>(i & 127), r64 = static_cast<int>(i & 63);
     const int flip = (r128 >> 2) & 1;  // = (r64 >> 2) & 1
     for (int64_t k0 = 4 * lane; k0 < dpad8; k0 += 128) {
         long long N[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v)  // |N| < 2^54, an exact integer (x's ulp >= 2^{E-53})
-            N[v] = (k0 + v < dpad) ? __double2ll_rn(ldexp(x[k0 + v], 54 - E)) : 0ll;
+        for (int v = 0; v < 4; ++v)  // S = 7: |N| < 2^54, exact (x's ulp >= 2^{E-53}); S = 3: rounded
+            N[v] = (k0 + v < dpad) ? __double2ll_rn(ldexp(static_cast<double>(x[k0 + v]), Oz<S>::BITS - E)) : 0ll;
         const int64_t kb = k0 >> 5;
         const int c = static_cast<int>(k0 & 31);
         const int inrow = ((((c >> 4) ^ flip) << 4) | (c & 15));
@@ -337,16 +351,18 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t *bar) {  // arrive o
 //  OZ_PREDICT    : alpha_j k(z_i, x_j) -> Fpart[J][npad]
 // ta4/ta8: maps over the pre-swizzled row-operand digits DA (boxes of 4 / 8 planes of a 128-point
 // slab block, 128-byte rows); tb4/tb8: the same over DB (64-point half blocks).
-template <int KT, int S, int MODE>
+// T: the value type of the epilogue and of q, norms, p, the products and Q~ (double with S = 7,
+// float with S = 3); the digit scales are fp64 either way.
+template <int KT, int S, int MODE, typename T>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     k_tile_ozaki(const __grid_constant__ CUtensorMap ta4, const __grid_constant__ CUtensorMap ta8,
                  const __grid_constant__ CUtensorMap tb4, const __grid_constant__ CUtensorMap tb8, int nk,
                  const int2 *__restrict__ tiles, const int *__restrict__ pk, int ntiles, int rowsI,
-                 const double *__restrict__ sca, const double *__restrict__ scb, const double *__restrict__ qv,
-                 const double *__restrict__ na, const double *__restrict__ nb_, const double *__restrict__ p,
-                 KParams<double> kp, double invC, const double *__restrict__ scal, int64_t m1, int band0, int band1,
-                 double *__restrict__ Ypart, int64_t band_rows, double *__restrict__ Qc, int T_tiles, const int *ctrl,
-                 int dbg) {
+                 const double *__restrict__ sca, const double *__restrict__ scb, const T *__restrict__ qv,
+                 const T *__restrict__ na, const T *__restrict__ nb_, const T *__restrict__ p, KParams<T> kp, T invC,
+                 const double *__restrict__ scal, int64_t m1, int band0, int band1, T *__restrict__ Ypart,
+                 int64_t band_rows, T *__restrict__ Qc, int T_tiles, const int *ctrl, int dbg) {
+    static_assert((S == 7) == std::is_same<T, double>::value, "S = 7 computes fp64, S = 3 fp32");
     using O = Oz<S>;
     constexpr int TN = O::TN, LV = O::LV;
     if (cg_done(ctrl)) return;  // uniform across the cluster
@@ -360,12 +376,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     uint64_t *tempty = tfull + 1;                         // a pass's accumulators drained (leader: 16 warps)
     uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(tempty + 1);
     double *colsc = reinterpret_cast<double *>(misc + 256);  // [128]
-    double *colq = colsc + TN;                               // [128]
-    double *colp = colq + TN;                                // [128] (alpha for predict)
-    double *coln = colp + TN;                                // [128]
-    double *redr = coln + TN;                                // [2][128]
-    double *redc = redr + 2 * kTile;                         // [4][128]
-    double *etab = redc + 4 * TN;                            // [64] 2^(j/64) (RBF, exp_tab)
+    T *colq = reinterpret_cast<T *>(colsc + TN);             // [128] (8-byte slots for either T)
+    T *colp = reinterpret_cast<T *>(colsc + 2 * TN);         // [128] (alpha for predict)
+    T *coln = reinterpret_cast<T *>(colsc + 3 * TN);         // [128]
+    T *redr = reinterpret_cast<T *>(colsc + 4 * TN);         // [2][128]
+    T *redc = reinterpret_cast<T *>(colsc + 4 * TN + 2 * kTile);  // [4][128]
+    double *etab = colsc + 8 * TN + 2 * kTile;               // [64] 2^(j/64) (fp64 RBF, exp_tab)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -422,8 +438,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 int I0, J, use;
                 tile_of(t, I0, J, use);
 #pragma unroll 1
-                for (int pass = 0; pass < 2; ++pass) {
-                    const int np = pass == 0 ? S : LV;
+                for (int pass = 0; pass < O::NPASS; ++pass) {
+                    const int np = oz_planes<S>(pass);
                     for (int kb = 0; kb < nk; ++kb, ++g) {
                         const uint32_t s = g % O::STAGES;
                         if (g >= O::STAGES) mbar_wait(&empty[s], ((g / O::STAGES) - 1) & 1);
@@ -436,8 +452,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         const uint32_t fb = full0 + s * 8;
                         // pre-swizzled blocks: A (row block I0 + r, slab kb) = S x 4 KiB at 128-B row
                         // (I * nk + kb) * 256; B (64-row block 2 J + r, slab kb) = S x 2 KiB at (.) * 128
-                        tma_load_2d_2sm(st, pass == 0 ? &ta8 : &ta4, fb, 0, ((I0 + int(rank)) * nk + kb) * (S * 32));  // ta8: all S planes
-                        tma_load_2d_2sm(st + np * O::PLANE, pass == 0 ? &tb8 : &tb4, fb, 0,
+                        tma_load_2d_2sm(st, np == S ? &ta8 : &ta4, fb, 0, ((I0 + int(rank)) * nk + kb) * (S * 32));  // ta8: all S planes
+                        tma_load_2d_2sm(st + np * O::PLANE, np == S ? &tb8 : &tb4, fb, 0,
                                         ((2 * J + int(rank)) * nk + kb) * (S * 16));
                     }
                 }
@@ -449,12 +465,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             uint32_t g = 0, e = 0;  // e: accumulator events (two per pair-tile)
             for (int t = pair; t < ntiles; t += npairs) {
 #pragma unroll 1
-                for (int pass = 0; pass < 2; ++pass, ++e) {
+                for (int pass = 0; pass < O::NPASS; ++pass, ++e) {
                     if (e > 0) {  // both CTAs' epilogues have drained the previous pass
                         mbar_wait(tempty, (e - 1) & 1);
                         asm volatile("tcgen05.fence::after_thread_sync;");
                     }
-                    const int np = pass == 0 ? S : LV;
+                    const int np = oz_planes<S>(pass);
                     for (int kb = 0; kb < nk; ++kb, ++g) {
                         const uint32_t s = g % O::STAGES;
                         mbar_wait(&full[s], (g / O::STAGES) & 1);
@@ -462,7 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         const uint32_t sa = smem_addr(ring + size_t(s) * O::STAGE_BYTES);
                         const uint32_t sb = sa + np * O::PLANE;
                         if (dbg & 4) {  // experiment: data movement only
-                        } else if (pass == 0) {  // levels 4..6 (18 pairs), TMEM column block l - 4
+                        } else if (S == 7 && pass == 0) {  // levels 4..6 (18 pairs), TMEM column block l - 4
 #pragma unroll
                             for (int a = 0; a < S; ++a)
 #pragma unroll
@@ -473,7 +489,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                                     umma_i8_2sm<S>(tmem + uint32_t((l - LV) * TN), umma_desc_sw32(sa + a * O::PLANE),
                                                    umma_desc_sw32(sb + b * (O::PLANE / 2)), (kb > 0 || a > 0) ? 1u : 0u);
                                 }
-                        } else {  // levels 0..3 (10 pairs)
+                        } else {  // levels 0..LV-1 (S = 7: 10 pairs; S = 3: 6 pairs)
 #pragma unroll
                             for (int a = 0; a < LV; ++a)
 #pragma unroll
@@ -491,11 +507,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(O::CTRL_REGS));
     } else {  // ---- epilogue warps 4-11 (both CTAs): row 32(w%4) + lane, columns 64((w-4)/4) .. +63
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(O::EPI_REGS));
-        if (KT == RBF && threadIdx.x - 128 < 64) etab[threadIdx.x - 128] = kExp2Tab64[threadIdx.x - 128];  // read after B1
+        constexpr bool kTabExp = KT == RBF && S == 7;
+        if (kTabExp && threadIdx.x - 128 < 64) etab[threadIdx.x - 128] = kExp2Tab64[threadIdx.x - 128];  // read after B1
         const int quarter = warp & 3, grp = (warp - 4) >> 2;
         const int lr = quarter * 32 + lane;
         const int et = threadIdx.x - 128;  // 0..255
-        const double Qmm = (MODE == OZ_PREDICT) ? 0.0 : scal[S_QMM];
+        const T Qmm = (MODE == OZ_PREDICT) ? T(0) : static_cast<T>(scal[S_QMM]);
         uint32_t e = 0;
         for (int t = pair; t < ntiles; t += npairs) {
             int I0, J, use;
@@ -506,16 +523,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             if (et < TN) {  // column data of this tile (the previous tile's readers are done: B3)
                 const int64_t gj = col0 + et;
                 colsc[et] = scb[gj];
-                colq[et] = (MODE == OZ_PREDICT) ? 0.0 : qv[gj];
-                colp[et] = (MODE == OZ_PRECOMPUTE) ? 0.0 : p[gj];
-                coln[et] = (KT == RBF) ? nb_[gj] : 0.0;
+                colq[et] = (MODE == OZ_PREDICT) ? T(0) : qv[gj];
+                colp[et] = (MODE == OZ_PRECOMPUTE) ? T(0) : p[gj];
+                coln[et] = (KT == RBF) ? nb_[gj] : T(0);
             }
             const int64_t gi = row0 + lr;
-            const double sci = used ? sca[gi] * 0x1p-24 : 0.0;  // row scale, with V's 2^-24 folded in
-            const double qi = (MODE == OZ_PREDICT || !used) ? 0.0 : qv[gi];
-            const double pi = (MODE == OZ_MATVEC && used) ? p[gi] : 0.0;
-            const double ni = (KT == RBF && used) ? na[gi] : 0.0;
-            const double cqi = Qmm - qi;  // Eq. 16 row constant
+            // row scale (S = 7: with V's 2^-24 folded in)
+            const double sci = used ? sca[gi] * (S == 7 ? 0x1p-24 : 1.0) : 0.0;
+            const T qi = (MODE == OZ_PREDICT || !used) ? T(0) : qv[gi];
+            const T pi = (MODE == OZ_MATVEC && used) ? p[gi] : T(0);
+            const T ni = (KT == RBF && used) ? na[gi] : T(0);
+            const T cqi = Qmm - qi;  // Eq. 16 row constant
             asm volatile("bar.sync 1, 256;" ::: "memory");  // B1
 
             // Pass 0 (levels 4-6) -> the low-order part W = 2^16 sum_{l<3} 2^{-8l} acc_{4+l} (exact
@@ -527,8 +545,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(grp * 64);
             const bool mirrored = used && (MODE != OZ_PREDICT) && (I != J) && (J >= band0) && (J < band1);
             float wl[64];
-            double rs = 0.0;
-            double *qdst = nullptr, *qmir = nullptr;
+            T rs = T(0);
+            T *qdst = nullptr, *qmir = nullptr;
             if constexpr (MODE == OZ_PRECOMPUTE) {
                 if (used) {
                     qdst = ((T_tiles < 0) ? Qc + int64_t(pk[2 * t + int(rank)]) * (kTile * kTile)
@@ -537,7 +555,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     if (T_tiles >= 0 && mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
                 }
             }
-            // Pass 0: drain levels 4-6 into wl (fp32), release the accumulators.
+            // Pass 0 of S = 7: drain levels 4-6 into wl (fp32), release the accumulators.
+            if constexpr (S == 7) {
             mbar_wait(tfull, e & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             ++e;
@@ -559,6 +578,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty0);  // the MMA may start pass 1
+            }
             // Pass 1: drain levels 0-3 and finish the contraction sv (fp64, 64 columns in registers),
             // then release the accumulators BEFORE the kernel function / Eq. 16 / row and column
             // sums, so the MMAs of the next pair-tile's pass 0 overlap this fp64 work (the epilogue
@@ -566,8 +586,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             mbar_wait(tfull, e & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             ++e;
-            double sv[64];
-            if (!(dbg & 1)) {
+            T sv[64];
+            if (S == 3 && !(dbg & 1)) {  // the single pass of S = 3: V = acc_0 2^16 + acc_1 2^8 + acc_2
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t r0[8], r1[8], r2[8];
+                    tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
+                    tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
+                    tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const long long V = (lv(r0[j]) << 16) + (lv(r1[j]) << 8) + lv(r2[j]);
+                        sv[c * 8 + j] = static_cast<T>(i64_to_f64_exact(V) * (sci * colsc[grp * 64 + c * 8 + j]));
+                    }
+                }
+            } else if (S == 7 && !(dbg & 1)) {
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     uint32_t r0[8], r1[8], r2[8], r3[8];
@@ -582,8 +616,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         // carries 2^16 of it (the 2^-24 of V sits in sci)
                         const long long V = (lv(r0[j]) << 24) + (lv(r1[j]) << 16) + (lv(r2[j]) << 8) + lv(r3[j]);
                         const int lc = grp * 64 + c * 8 + j;
-                        sv[c * 8 + j] = fma(static_cast<double>(wl[c * 8 + j]), 0x1p-24, i64_to_f64_exact(V)) *
-                                        (sci * colsc[lc]);
+                        sv[c * 8 + j] = static_cast<T>(fma(static_cast<double>(wl[c * 8 + j]), 0x1p-24,
+                                                           i64_to_f64_exact(V)) * (sci * colsc[lc]));
                     }
                 }
             }
@@ -593,26 +627,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             if (!(dbg & 1)) {
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {  // 8-column chunks of this thread's 64 columns
-                    double w[8];
+                    T w[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int lc = grp * 64 + c * 8 + j;
                         const int64_t gj = col0 + lc;
                         const bool diag = (MODE != OZ_PREDICT) && gi == gj;
-                        double kv;
-                        if constexpr (KT == RBF) {  // kernel_value's RBF with the table exp
+                        T kv;
+                        if constexpr (kTabExp) {  // kernel_value's RBF with the table exp
                             double dist = ni + coln[lc] - 2.0 * sv[c * 8 + j];
                             dist = dist > 0.0 ? dist : 0.0;
                             if (diag) dist = 0.0;
                             kv = exp_tab(-kp.gamma * dist, etab);
                         } else {
-                            kv = kernel_value<KT, double>(sv[c * 8 + j], ni, coln[lc], diag, kp);
+                            kv = kernel_value<KT, T>(sv[c * 8 + j], ni, coln[lc], diag, kp);
                         }
                         if constexpr (MODE == OZ_PREDICT) {
                             rs = fma(colp[lc], kv, rs);
                         } else {  // qtilde_value (Eq. 16) with the row constant Q_mm - q_i hoisted
-                            const double v = (kv + (diag ? invC : 0.0)) - colq[lc] + cqi;
-                            w[j] = (gi < m1 && gj < m1) ? v : 0.0;
+                            const T v = (kv + (diag ? invC : T(0))) - colq[lc] + cqi;
+                            w[j] = (gi < m1 && gj < m1) ? v : T(0);
                         }
                     }
                     if constexpr (MODE == OZ_MATVEC) {
@@ -629,12 +663,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                                 const bool up = (lane & o) != 0;
 #pragma unroll
                                 for (int i = 0; i < n; ++i) {
-                                    const double send = up ? w[i] : w[i + n];
-                                    const double keep = up ? w[i + n] : w[i];
+                                    const T send = up ? w[i] : w[i + n];
+                                    const T keep = up ? w[i + n] : w[i];
                                     w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                                 }
                             }
-                            double tot = w[0] + __shfl_xor_sync(0xffffffffu, w[0], 2);
+                            T tot = w[0] + __shfl_xor_sync(0xffffffffu, w[0], 2);
                             tot += __shfl_xor_sync(0xffffffffu, tot, 1);
                             if ((lane & 3) == 0) {
                                 const int cc = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
@@ -644,8 +678,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     } else if constexpr (MODE == OZ_PRECOMPUTE) {
                         if (qdst) {
 #pragma unroll
-                            for (int j = 0; j < 8; j += 2)
-                                *reinterpret_cast<double2 *>(qdst + c * 8 + j) = make_double2(w[j], w[j + 1]);
+                            for (int j = 0; j < 8; j += 2) {
+                                if constexpr (sizeof(T) == 8)
+                                    *reinterpret_cast<double2 *>(qdst + c * 8 + j) = make_double2(w[j], w[j + 1]);
+                                else
+                                    *reinterpret_cast<float2 *>(qdst + c * 8 + j) = make_float2(w[j], w[j + 1]);
+                            }
                         }
                         if (qmir) {  // transposed copy: column lc of this tile = row lc of tile (J, I)
 #pragma unroll

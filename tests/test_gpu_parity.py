@@ -61,7 +61,8 @@ def test_matvec_implicit_small(m, d, kernel, dtype):
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("m,d", [(129, 3), (1000, 33), (2177, 70), (4097, 300)])
 def test_matvec_fp32_ffma_engine(m, d, kernel):
-    """fp32 on the CUDA-core FFMA engine (options.fp32_engine = 1); default is tcgen05 3xTF32."""
+    """fp32 on the tcgen05 3xTF32 engine (fp32_engine = 0) and the CUDA-core FFMA engine (1); the
+    default AUTO takes the int8 Ozaki engine on these data (tests/test_gpu_fp32_ozaki.py)."""
     rng = np.random.default_rng(3000 * m + d + kernel)
     X = rng.standard_normal((m, d)).astype(np.float32)
     p = rng.standard_normal(m - 1).astype(np.float32)

@@ -80,16 +80,19 @@ def run(cfg, mode, engine="auto", repeat=2):
            "cg_s": s.t_cg, "precompute_s": s.t_precompute, "cg_iterations_per_s": s.iterations / s.t_cg,
            "matvec_ms": 1e3 * mv, "bytes_per_gpu": s.bytes_per_gpu,
            "predict_s": tk, "n_test": cfg.n_test, "test_accuracy": acc,
-           "fp64_engine": {1: "ozaki", 2: "dmma"}.get(s.fp64_engine_used)}
+           "fp64_engine": {1: "ozaki", 2: "dmma"}.get(s.fp64_engine_used),
+           "fp32_engine": {0: "tcgen05", 1: "ffma", 2: "ozaki"}.get(s.fp32_engine_used)
+           if cfg.dtype == "f32" else None}
     if mode == "lowrank":  # two streams over X per product (a different cost model, NEXT-2)
         sz = 8 if cfg.dtype == "f64" else 4
         row["matvec_gbs"] = 2.0 * cfg.m * cfg.d * sz / mv / 1e9
         row["frac_of_peak"] = row["matvec_gbs"] / hbm_peak()
         row["peak_gbs"] = hbm_peak()
-    elif mode == "implicit" and row["fp64_engine"] == "ozaki":
+    elif mode == "implicit" and "ozaki" in (row["fp64_engine"], row["fp32_engine"]):
         d8 = -(-cfg.d // 32) * 32
-        row["matvec_tflops"] = fl / mv / 1e12  # fp64-equivalent
-        row["matvec_int8_tops"] = 28 * fl * d8 / cfg.d / mv / 1e12  # 28 digit pairs (ozaki_engine.cuh)
+        pairs = 28 if cfg.dtype == "f64" else 6  # digit pairs per entry (ozaki_engine.cuh: 7 / 3 digits)
+        row["matvec_tflops"] = fl / mv / 1e12  # fp64- / fp32-equivalent
+        row["matvec_int8_tops"] = pairs * fl * d8 / cfg.d / mv / 1e12
         row["peak_int8_tops_sustained"] = INT8_PEAK
         row["frac_of_peak"] = row["matvec_int8_tops"] / INT8_PEAK
     elif mode == "implicit":
