@@ -582,43 +582,61 @@ __global__ void __launch_bounds__(kVecThreads)
 // y_i = sum_s Ypart[s][i] (fixed slot order), then pAp = p . y  (mode 0), or for the initial
 // / replaced residual (mode 1): r_i = rhs_i - y_i, r.r -> S_DELTA+par (and S_DELTA0 if init);
 // par < 0: take the slot from the device iteration counter.
+// Layout: a block takes 32-row chunks; thread (row lane r = tid % 32, slot group q = tid / 32) sums
+// slots q, q + 8, q + 16, ... of its row (8 independent load streams per row: the slot sum is
+// bandwidth-, not latency-bound; C2 cached reads 512 slots), then warp 0 adds the 8 group
+// partials in fixed order -- deterministic.
 template <typename T>
 __global__ void __launch_bounds__(kVecThreads)
     k_finalize(const T *__restrict__ Ypart, int nslots, int nsub, int band0, int64_t nb, int64_t g0, int64_t m1,
                const T *__restrict__ pband, T *__restrict__ y, int mode, const T *__restrict__ yl, T *__restrict__ r,
                T *__restrict__ pout, double *scal, int par, int set_delta0, T *partials, unsigned *counter,
                int write_scalar, const int *ctrl, int pap_slot) {
+    constexpr int G = kVecThreads / 32;  // slot groups
+    __shared__ T grp[G][33];
     if (cg_done(ctrl)) return;
     if (par < 0) par = (ctrl[C_IT] & 1) ^ 1;  // residual replacement: the slot of delta_{k+1}
     T part = T(0);
     const double ym = scal[S_YM];
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const int64_t nchunks = (nb + 31) / 32;
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const int64_t i = ch * 32 + lane;
         // Slot validity (k_matvec_implicit): with NSUB = 2 column sub-blocks, the odd slot of an
         // in-band column block J below this row block R carries nothing (mirrored column sums
-        // go to the even slot).  Fixed slot order -> deterministic.
-        const int R = static_cast<int>((g0 + i) / kTile);
-        T s = T(0);
-        for (int k = 0; k < nslots; ++k) {
-            if (nsub == 2 && (k & 1)) {
-                const int J = k >> 1;
-                if (J >= band0 && J < R) continue;
+        // go to the even slot).  R is uniform over a 32-row chunk.
+        const int R = static_cast<int>((g0 + ch * 32) / kTile);
+        T sg = T(0);
+        if (i < nb) {
+            for (int k = q; k < nslots; k += G) {
+                if (nsub == 2 && (k & 1)) {
+                    const int J = k >> 1;
+                    if (J >= band0 && J < R) continue;
+                }
+                sg += Ypart[static_cast<int64_t>(k) * nb + i];
             }
-            s += Ypart[static_cast<int64_t>(k) * nb + i];
         }
-        const bool valid = (g0 + i) < m1;
-        s = valid ? s : T(0);
-        if (mode == 0) {
-            y[i] = s;
-            part = fma(pband[i], s, part);
-        } else {
-            // rhs_i = y_i - y_m (Eq. 14)
-            const T rhs = valid ? static_cast<T>(static_cast<double>(yl[g0 + i]) - ym) : T(0);
-            const T ri = valid ? rhs - s : T(0);
-            r[i] = ri;
-            if (pout) pout[i] = ri;
-            part = fma(ri, ri, part);
+        grp[q][lane] = sg;
+        __syncthreads();
+        if (q == 0 && i < nb) {
+            T s = T(0);
+#pragma unroll
+            for (int g = 0; g < G; ++g) s += grp[g][lane];
+            const bool valid = (g0 + i) < m1;
+            s = valid ? s : T(0);
+            if (mode == 0) {
+                y[i] = s;
+                part = fma(pband[i], s, part);
+            } else {
+                // rhs_i = y_i - y_m (Eq. 14)
+                const T rhs = valid ? static_cast<T>(static_cast<double>(yl[g0 + i]) - ym) : T(0);
+                const T ri = valid ? rhs - s : T(0);
+                r[i] = ri;
+                if (pout) pout[i] = ri;
+                part = fma(ri, ri, part);
+            }
         }
+        __syncthreads();
     }
     grid_reduce<T>(part, partials, counter, [&](T tot) {
         if (!write_scalar) return;

@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, path, kernel, mode, m, d, circ, mg=0, x0=0):
+def _worker(rank, world, port, path, kernel, mode, m, d, circ, mg=0, x0=0, f32=0):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -36,9 +36,11 @@ def _worker(rank, world, port, path, kernel, mode, m, d, circ, mg=0, x0=0):
     comm = pl.comm_host_staged(0, circulant=circ)
     X, y, Z, _ = synth.planes(m, d, 64, seed=21 + kernel)
     p = np.random.default_rng(5).standard_normal(m - 1)
+    if f32:
+        X, y, p = X.astype(np.float32), y.astype(np.float32), p.astype(np.float32)
     opts = pl.options(mode=mode, comm=comm, multi_gpu=mg)
     out, _ = pl.plssvm_qtilde_matvec(X, p, kernel, 1.0 / d, 3, 0.5, 1.0, opts=opts)
-    alpha, b, st, stats = pl.plssvm_train_ex(X, y, kernel, 1.0 / d, 3, 0.5, 1.0, 1e-10,
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, kernel, 1.0 / d, 3, 0.5, 1.0, 1e-6 if f32 else 1e-10,
                                              opts=pl.options(mode=mode, comm=comm, multi_gpu=mg, x0=x0))
     if rank == 0:
         np.savez(path, out=out, alpha=alpha, b=b, st=st, it=stats.iterations, ranks=stats.num_ranks,
@@ -107,3 +109,26 @@ def test_feature_split_train_matches_oracle(tmp_path, world, m, d, x0):
     tol = 1e-7 if x0 == 0 else 1e-6
     assert np.linalg.norm(r["alpha"] - a_ref) <= tol * np.linalg.norm(a_ref)
     assert abs(float(r["b"]) - b_ref) <= tol * max(abs(b_ref), np.abs(a_ref).max())
+
+
+@pytest.mark.parametrize("world,kernel,mode", [(2, 1, 1), (3, 2, 1), (2, 2, 2)])
+def test_fp32_int8_engine_multirank(tmp_path, world, kernel, mode):
+    """fp32 (default AUTO -> the int8 3-digit engine) on several ranks: the gathered product vs the
+    oracle (<= 1e-5) and the model vs the same engine on one rank (fp32 CG accuracy)."""
+    import oracle
+    import paper_2202_12674_b200 as pl
+    import synth
+
+    m, d = 1100, 37
+    path = str(tmp_path / "r.npz")
+    mp.spawn(_worker, args=(world, _free_port(), path, kernel, mode, m, d, True, 0, 0, 1), nprocs=world, join=True)
+    r = np.load(path)
+    X, y, _, _ = synth.planes(m, d, 64, seed=21 + kernel)
+    X, y = X.astype(np.float32), y.astype(np.float32)
+    p = np.random.default_rng(5).standard_normal(m - 1).astype(np.float32)
+    gamma = float(np.float32(1.0 / d))
+    ref = oracle.qtilde(X.astype(np.float64), kernel, gamma, 3, 0.5, 1.0) @ p.astype(np.float64)
+    assert np.linalg.norm(r["out"] - ref) <= 1e-5 * np.linalg.norm(ref)
+    a1, b1, st1, _ = pl.plssvm_train_ex(X, y, kernel, 1.0 / d, 3, 0.5, 1.0, 1e-6, opts=pl.options(mode=mode))
+    assert int(r["st"]) == 0 and st1 == 0 and int(r["ranks"]) == world
+    assert np.linalg.norm(r["alpha"] - a1) <= 1e-3 * np.linalg.norm(a1)
