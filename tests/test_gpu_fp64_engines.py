@@ -1,5 +1,5 @@
 """GPU parity of the two fp64 contraction engines (include/plssvm.h plssvm_fp64_engine_t):
-OZAKI (int8 tensor cores on an exact 8-digit split of every point, 2-SM UMMA) and DMMA (fp64
+OZAKI (int8 tensor cores on an exact 7-digit split of every point, 2-SM UMMA) and DMMA (fp64
 tensor cores), plus the AUTO rule, against the CPU oracle.  Bars as in test_gpu_parity.py:
 product <= 1e-12 norm-wise and |y_i - y*_i| <= 1e-12 (|Q~||p|)_i element-wise; alpha, b <= 1e-7.
 
