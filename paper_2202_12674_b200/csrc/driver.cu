@@ -1163,27 +1163,19 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     k_cg_start<<<1, 1, 0, c.s>>>(c.scal, c.ctrl, pb.eps * pb.eps, imax_i, fixed_i);
     PLS_CHECK_LAUNCH();
     ++c.launches;
-    // two pinned snapshots of (scalars, control block): the batched loop reads batch k's while
-    // batch k+1 is already queued
-    constexpr size_t kSnap = S_COUNT * sizeof(double) + C_COUNT * sizeof(int);
     double *hs = nullptr;
-    PLS_CUDA(cudaMallocHost(&hs, 2 * kSnap));
+    PLS_CUDA(cudaMallocHost(&hs, S_COUNT * sizeof(double) + C_COUNT * sizeof(int)));
     struct HostFree {
         double *p;
         ~HostFree() { cudaFreeHost(p); }
     } hf{hs};
-    double *hsb[2] = {hs, reinterpret_cast<double *>(reinterpret_cast<char *>(hs) + kSnap)};
-    int *hcb[2] = {reinterpret_cast<int *>(hsb[0] + S_COUNT), reinterpret_cast<int *>(hsb[1] + S_COUNT)};
-    int *hctrl = hcb[0];
+    int *hctrl = reinterpret_cast<int *>(hs + S_COUNT);
     const int64_t launches_before_cg = c.launches;
     constexpr int kBatch = 8;
-    cudaEvent_t mv0[2][kBatch], mv1[2][kBatch], bdone[2];
-    for (int q = 0; q < 2; ++q) {
-        bdone[q] = E.make();
-        for (int b = 0; b < kBatch; ++b) {
-            mv0[q][b] = E.make();
-            mv1[q][b] = E.make();
-        }
+    cudaEvent_t mv0[kBatch], mv1[kBatch];
+    for (int b = 0; b < kBatch; ++b) {
+        mv0[b] = E.make();
+        mv1[b] = E.make();
     }
     double t_mv = 0.0, t_mv_min = 1e30;
     int64_t it = 0;
@@ -1307,26 +1299,14 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         c.launches += 1 + per_it * it;
         c.graph_used = true;
     } else {
-        // one batch of look-ahead: batch k+1 is queued before the host waits for batch k's
-        // snapshot, so the GPU does not idle during the host's enqueue (iterations queued after
-        // convergence are no-ops)
-        int64_t next = 0;  // host index of the next iteration to enqueue
-        auto enqueue_batch = [&](int q) {
-            for (int b = 0; b < kBatch; ++b) enqueue_iteration(next++, mv0[q][b], mv1[q][b], 0ull, 0);
-            PLS_CUDA(cudaMemcpyAsync(hsb[q], c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
-            PLS_CUDA(cudaMemcpyAsync(hcb[q], c.ctrl, C_COUNT * sizeof(int), cudaMemcpyDeviceToHost, c.s));
-            PLS_CUDA(cudaEventRecord(bdone[q], c.s));
-        };
-        enqueue_batch(0);
-        for (int k = 0;; ++k) {
-            const int q = k & 1;
-            enqueue_batch(q ^ 1);
-            PLS_CUDA(cudaEventSynchronize(bdone[q]));
-            hs = hsb[q];
-            hctrl = hcb[q];
+        while (true) {
+            for (int b = 0; b < kBatch; ++b) enqueue_iteration(it + b, mv0[b], mv1[b], 0ull, 0);
+            PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+            PLS_CUDA(cudaMemcpyAsync(hctrl, c.ctrl, C_COUNT * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+            PLS_CUDA(cudaStreamSynchronize(c.s));
             const int64_t ran = hctrl[C_IT] - it;  // iterations of this batch that did work
             for (int b = 0; b < ran && b < kBatch; ++b) {
-                const double tm = elapsed(mv0[q][b], mv1[q][b]);
+                const double tm = elapsed(mv0[b], mv1[b]);
                 t_mv += tm;
                 t_mv_min = std::min(t_mv_min, tm);
             }
