@@ -88,6 +88,28 @@ double elapsed(cudaEvent_t a, cudaEvent_t b) {
     return 1e-3 * ms;
 }
 
+// Pinned host buffer for the CG control snapshots, allocated once per host thread and grown on
+// demand: cudaMallocHost costs ~1 ms and sat inside every training call's CG phase (the GPU idles
+// meanwhile).  Calls on one thread are sequential (plssvm.h thread-safety rule), so one buffer
+// per thread suffices; portable across devices.
+char *pinned_scratch(size_t bytes) {
+    thread_local struct Buf {
+        char *p = nullptr;
+        size_t n = 0;
+        ~Buf() {
+            if (p) cudaFreeHost(p);
+        }
+    } b;
+    if (b.n < bytes) {
+        if (b.p) cudaFreeHost(b.p);
+        b.p = nullptr;
+        b.n = 0;
+        PLS_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&b.p), bytes, cudaHostAllocPortable));
+        b.n = bytes;
+    }
+    return b.p;
+}
+
 void setup_mempool(int dev) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -1163,12 +1185,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     k_cg_start<<<1, 1, 0, c.s>>>(c.scal, c.ctrl, pb.eps * pb.eps, imax_i, fixed_i);
     PLS_CHECK_LAUNCH();
     ++c.launches;
-    double *hs = nullptr;
-    PLS_CUDA(cudaMallocHost(&hs, S_COUNT * sizeof(double) + C_COUNT * sizeof(int)));
-    struct HostFree {
-        double *p;
-        ~HostFree() { cudaFreeHost(p); }
-    } hf{hs};
+    double *hs = reinterpret_cast<double *>(pinned_scratch(S_COUNT * sizeof(double) + C_COUNT * sizeof(int)));
     int *hctrl = reinterpret_cast<int *>(hs + S_COUNT);
     const int64_t launches_before_cg = c.launches;
     constexpr int kBatch = 8;
