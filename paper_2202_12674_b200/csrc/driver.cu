@@ -640,25 +640,25 @@ void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb
 // block) should stay L2-resident while the co-resident pairs sweep the column blocks -- 32 blocks
 // up to ~40 MB (C1: DRAM reads per product 902 -> 405 MB, ncu), fewer for wide points (C2 at 32:
 // 117 MB, L2 thrash, +4 % time).  PLSSVM_OZ_GROUP overrides (experiments).
-int oz_group_rows(int64_t d8) {
+int oz_group_rows(int64_t d8, int S) {
     static int forced = [] {
         const char *e = std::getenv("PLSSVM_OZ_GROUP");
         const int v = e ? std::atoi(e) : 0;
         return v >= 2 ? (v & ~1) : 0;
     }();
     if (forced) return forced;
-    const int64_t per_block = int64_t(kOzS) * 128 * d8;
+    const int64_t per_block = int64_t(S) * 128 * d8;
     const int64_t budget = int64_t(40) << 20;
     return per_block * 32 <= budget ? 32 : per_block * 16 <= budget ? 16 : 8;
 }
 
-void oz_pair_tiles(const std::vector<int2> &tl, int b0, int b1, int T, int64_t d8, std::vector<int2> &pt,
+void oz_pair_tiles(const std::vector<int2> &tl, int b0, int b1, int T, int64_t d8, int S, std::vector<int2> &pt,
                    std::vector<int> &pk) {
     std::vector<int> ord(static_cast<size_t>(b1 - b0) * T, -1);
     for (size_t k = 0; k < tl.size(); ++k) ord[static_cast<size_t>(tl[k].x - b0) * T + tl[k].y] = static_cast<int>(k);
     pt.clear();
     pk.clear();
-    const int G = oz_group_rows(d8);
+    const int G = oz_group_rows(d8, S);
     for (int P0 = b0; P0 < b1; P0 += G)
         for (int J = 0; J < T; ++J)
             for (int I0 = P0; I0 < std::min(P0 + G, b1); I0 += 2) {
@@ -705,7 +705,7 @@ void oz_build_pairs(Ctx<T> &c, Arena &A, const std::vector<int2> &tl, int b0, in
     if (!c.oz) return;
     std::vector<int2> pt;
     std::vector<int> pk;
-    oz_pair_tiles(tl, b0, b1, c.g.T, int64_t(c.ozx.nk) * 32, pt, pk);
+    oz_pair_tiles(tl, b0, b1, c.g.T, int64_t(c.ozx.nk) * 32, oz_digits<T>(), pt, pk);
     c.oz_npt = static_cast<int>(pt.size());
     c.oz_pt = A.alloc<int2>(c.oz_npt);
     c.oz_pk = A.alloc<int>(2 * c.oz_npt);
