@@ -365,7 +365,10 @@ def main():
                       "t_cg_s": stats0.t_cg, "t_precompute_s": stats0.t_precompute,
                       "t_transform_s": stats0.t_transform, "t_q_s": stats0.t_q, "rel_residual": stats0.rel_residual,
                       "bytes_per_gpu": stats0.bytes_per_gpu, "launches_in_cg": stats0.launches_in_cg,
-                      "matvec_ms_avg": 1e3 * avg_mv, "matvec_ms_min": 1e3 * stats0.t_matvec_min}}
+                      "matvec_ms_avg": 1e3 * avg_mv, "matvec_ms_min": 1e3 * stats0.t_matvec_min,
+                      # the paper's variability measure: coefficient of variation over the K steps
+                      "t_train_cov": float(np.std([st.t_total for st, *_ in per]) /
+                                           max(np.mean([st.t_total for st, *_ in per]), 1e-30))}}
 
     # ---- e2e: same metric through the public API with HOST buffers (pinned), copies inside
     if not args.no_e2e:
