@@ -70,10 +70,18 @@ plssvm_options_t defaults() {
     return o;
 }
 
-// PLSSVM_MULTI_GPU_FEATURES (paper §III-C5, P:418-427): linear kernel, fp64, implicit, d >= P.
-int check_multi_gpu(const plssvm_options_t &o, int kernel, int dtype, int64_t d) {
+// Engine options (plssvm.h plssvm_fp64_engine_t / plssvm_fp32_engine_t).
+int check_engines(const plssvm_options_t &o) {
+    if (o.fp64_engine < PLSSVM_FP64_AUTO || o.fp64_engine > PLSSVM_FP64_DMMA)
+        return fail(PLSSVM_E_INVALID_ARG, "options.fp64_engine must be 0 (AUTO), 1 (OZAKI) or 2 (DMMA)");
     if (o.fp32_engine < PLSSVM_FP32_TCGEN05 || o.fp32_engine > PLSSVM_FP32_AUTO)
         return fail(PLSSVM_E_INVALID_ARG, "options.fp32_engine must be 0 (TCGEN05), 1 (FFMA), 2 (OZAKI) or 3 (AUTO)");
+    return PLSSVM_OK;
+}
+
+// PLSSVM_MULTI_GPU_FEATURES (paper §III-C5, P:418-427): linear kernel, fp64, implicit, d >= P.
+int check_multi_gpu(const plssvm_options_t &o, int kernel, int dtype, int64_t d) {
+    if (int s = check_engines(o)) return s;
     if (o.multi_gpu != PLSSVM_MULTI_GPU_ROWS && o.multi_gpu != PLSSVM_MULTI_GPU_FEATURES)
         return fail(PLSSVM_E_INVALID_ARG, "options.multi_gpu must be 0 (ROWS) or 1 (FEATURES)");
     if (o.multi_gpu != PLSSVM_MULTI_GPU_FEATURES) return PLSSVM_OK;
@@ -161,6 +169,7 @@ int plssvm_predict_ex(const void *X, const void *alpha, double b, int64_t m, int
     if (n < 0) return fail(PLSSVM_E_INVALID_ARG, "n must be >= 0");
     if (n == 0) return PLSSVM_OK;
     if (!std::isfinite(b)) return fail(PLSSVM_E_INVALID_ARG, "b is not finite");
+    if ((s = check_engines(o))) return s;
     if ((s = device_ok(o.device))) return s;
     plssvm::Problem pb{X, nullptr, m, d, dtype, kernel, gamma, degree, coef0, 1.0, 1.0};
     return guarded([&] { return plssvm::predict(pb, alpha, b, Z, n, o, decision, labels, t_kernel); });

@@ -80,6 +80,20 @@ def test_feature_partition_invalid():
         pl.plssvm_feature_partition(8, 2, 2)
 
 
+def test_engine_options_validated():
+    """Out-of-range engine / loop / variant options are rejected before any device work."""
+    L = pl.load()
+    X = np.random.default_rng(0).standard_normal((10, 3))
+    y = np.array([1, -1] * 5, dtype=float)
+    alpha, b = np.zeros(10), np.zeros(1)
+    for kw in (dict(fp64_engine=3), dict(fp32_engine=4), dict(cg_loop=3), dict(cg_variant=2), dict(multi_gpu=2)):
+        o = pl.options(**kw)
+        st = L.plssvm_train_ex(X.ctypes.data, y.ctypes.data, 10, 3, 0, 2, 0.5, 3, 0.0, 1.0, 1e-10, ct.byref(o),
+                               alpha.ctypes.data, b.ctypes.data, None)
+        assert st == binding.E_INVALID_ARG, kw
+        assert pl.plssvm_last_error()
+
+
 def test_partition_invalid():
     with pytest.raises(pl.PlssvmError):
         pl.plssvm_partition(1, 1, 0)
