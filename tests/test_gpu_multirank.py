@@ -132,3 +132,22 @@ def test_fp32_int8_engine_multirank(tmp_path, world, kernel, mode):
     a1, b1, st1, _ = pl.plssvm_train_ex(X, y, kernel, 1.0 / d, 3, 0.5, 1.0, 1e-6, opts=pl.options(mode=mode))
     assert int(r["st"]) == 0 and st1 == 0 and int(r["ranks"]) == world
     assert np.linalg.norm(r["alpha"] - a1) <= 1e-3 * np.linalg.norm(a1)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_p_invariance_of_the_trained_model(tmp_path, world):
+    """SURVEY §8(c) multi-GPU pin: the row sharding changes only the summation order (DESIGN.md
+    R-16), so the model trained on P ranks equals the one-GPU model far inside the parity bar
+    (RBF, well conditioned: <= 1e-10 relative), with the same iteration count up to 1."""
+    import paper_2202_12674_b200 as pl
+    import synth
+
+    m, d = 1000, 33
+    path = str(tmp_path / "r.npz")
+    mp.spawn(_worker, args=(world, _free_port(), path, 2, 1, m, d, True), nprocs=world, join=True)
+    r = np.load(path)
+    X, y, _, _ = synth.planes(m, d, 64, seed=21 + 2)
+    a1, b1, st1, s1 = pl.plssvm_train_ex(X, y, 2, 1.0 / d, 3, 0.5, 1.0, 1e-10, opts=pl.options(mode=1))
+    assert int(r["st"]) == 0 and st1 == 0 and abs(int(r["it"]) - s1.iterations) <= 1
+    assert np.linalg.norm(r["alpha"] - a1) <= 1e-10 * np.linalg.norm(a1)
+    assert abs(float(r["b"]) - b1) <= 1e-10 * max(abs(b1), np.abs(a1).max())
