@@ -70,8 +70,8 @@ struct Oz {
     static constexpr int TMEM_COLS = 512;
     static_assert(LV * TN <= TMEM_COLS && LV0 * TN <= TMEM_COLS, "a pass's level accumulators must fit TMEM");
     // misc: barriers (256 B) + column data 4 x 128 doubles + row partials 2 x 128 + col partials 4 x 128
-    // + the 64-entry exp table
-    static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN + 64) * 8;
+    // + the 64-entry exp table + the tile's p / q.p sums (4 warps x 4)
+    static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN + 64 + 16) * 8;
     static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + MISC;
     // instruction descriptor: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 128, M = 256 (2 SMs)
     static constexpr uint32_t IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TN >> 3) << 17) | ((256u >> 4) << 24);
@@ -382,6 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     T *redr = reinterpret_cast<T *>(colsc + 4 * TN);         // [2][128]
     T *redc = reinterpret_cast<T *>(colsc + 4 * TN + 2 * kTile);  // [4][128]
     double *etab = colsc + 8 * TN + 2 * kTile;               // [64] 2^(j/64) (fp64 RBF, exp_tab)
+    T *psum = reinterpret_cast<T *>(etab + 64);              // [4][4] MATVEC: per warp sum p_j, q_j p_j, p_i, q_i p_i
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -534,6 +535,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             const T pi = (MODE == OZ_MATVEC && used) ? p[gi] : T(0);
             const T ni = (KT == RBF && used) ? na[gi] : T(0);
             const T cqi = Qmm - qi;  // Eq. 16 row constant
+            if constexpr (MODE == OZ_MATVEC) {
+                // Eq. 16 by rows: sum_j Q~_ij p_j = sum_j k_ij p_j + (Q_mm - q_i) sum_j p_j - sum_j q_j p_j
+                // (+ p_i / C on the diagonal), likewise for the mirrored column sums -- the entries
+                // need only the kernel value; the per-tile sums come from warps 4-7 (et = lr there)
+                if (et < TN) {
+                    const T pj = p[col0 + et];
+                    T v[4] = {pj, qv[col0 + et] * pj, pi, qi * pi};
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) v[u] += __shfl_xor_sync(0xffffffffu, v[u], o);
+                    if (lane == 0)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) psum[(et >> 5) * 4 + u] = v[u];
+                }
+            }
             asm volatile("bar.sync 1, 256;" ::: "memory");  // B1
 
             // Pass 0 (levels 4-6) -> the low-order part W = 2^16 sum_{l<3} 2^{-8l} acc_{4+l} (exact
@@ -644,6 +661,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         }
                         if constexpr (MODE == OZ_PREDICT) {
                             rs = fma(colp[lc], kv, rs);
+                        } else if constexpr (MODE == OZ_MATVEC) {
+                            w[j] = kv;  // Eq. 16's other terms per row / column at the end (p = 0 on padding)
                         } else {  // qtilde_value (Eq. 16) with the row constant Q_mm - q_i hoisted
                             const T v = (kv + (diag ? invC : T(0))) - colq[lc] + cqi;
                             w[j] = (gi < m1 && gj < m1) ? v : T(0);
@@ -698,13 +717,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 asm volatile("bar.sync 1, 256;" ::: "memory");  // B2
                 if (used) {
                     const int64_t lrow0 = row0 - int64_t(band0) * kTile;
-                    if (et < kTile) {
-                        Ypart[int64_t(J) * band_rows + lrow0 + et] = redr[et] + redr[kTile + et];
+                    auto tsum = [&](int u) { return (psum[u] + psum[4 + u]) + (psum[8 + u] + psum[12 + u]); };
+                    if (et < kTile) {  // row et (= this thread's lr): + (Q_mm - q_i) sum p_J - sum (q p)_J
+                        const T corr = fma(cqi, tsum(0), -tsum(1)) + ((I == J) ? invC * pi : T(0));
+                        Ypart[int64_t(J) * band_rows + lrow0 + et] = (redr[et] + redr[kTile + et]) + corr;
                     } else if (mirrored) {
                         const int cidx = et - kTile;
                         const int64_t lcol0 = col0 - int64_t(band0) * kTile;
+                        const T corr = fma(Qmm - colq[cidx], tsum(2), -tsum(3));
                         Ypart[int64_t(I) * band_rows + lcol0 + cidx] =
-                            (redc[cidx] + redc[TN + cidx]) + (redc[2 * TN + cidx] + redc[3 * TN + cidx]);
+                            ((redc[cidx] + redc[TN + cidx]) + (redc[2 * TN + cidx] + redc[3 * TN + cidx])) + corr;
                     }
                 }
             } else if constexpr (MODE == OZ_PREDICT) {
