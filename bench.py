@@ -364,6 +364,7 @@ def main():
             "train": {"iterations_per_step": iters / args.steps, "t_train_s": stats0.t_total,
                       "t_cg_s": stats0.t_cg, "t_precompute_s": stats0.t_precompute,
                       "t_transform_s": stats0.t_transform, "t_q_s": stats0.t_q, "rel_residual": stats0.rel_residual,
+                      "t_comm_s": stats0.t_comm,
                       "bytes_per_gpu": stats0.bytes_per_gpu, "launches_in_cg": stats0.launches_in_cg,
                       "matvec_ms_avg": 1e3 * avg_mv, "matvec_ms_min": 1e3 * stats0.t_matvec_min,
                       # the paper's variability measure: coefficient of variation over the K steps

@@ -176,6 +176,10 @@ typedef struct {
     int32_t cg_loop_used;            /* PLSSVM_CG_BATCHED or PLSSVM_CG_GRAPH */
     int32_t fp32_engine_used;        /* fp32 calls: PLSSVM_FP32_OZAKI, _TCGEN05 or _FFMA; 0 for fp64 */
     int32_t reserved1;
+    double t_comm;                   /* summed duration of the CG loop's collectives (all-gather of p,
+                                        scalar all-reduces, reduce-scatter of the partial products;
+                                        CUDA events, batched loop; 0 on one GPU) -- inside t_matvec for
+                                        the reduce-scatter, which is part of the product */
 } plssvm_stats_t;
 
 PLSSVM_API void plssvm_default_options(plssvm_options_t *opts);

@@ -353,7 +353,20 @@ struct Ctx {
     T *yred = nullptr;               // fsplit: the all-reduced product
     bool graph_used = false;         // the CG loop ran as one CUDA graph (WHILE node)
     int pap_slot = S_PAP;            // scalar slot of finalize's p.Q~p (Chronopoulos-Gear: S_CG_DELTA)
+    // collective timing (stats.t_comm, SURVEY §8(d) "NCCL time separated with events"): event
+    // pairs around every collective of the current CG iteration, when set
+    cudaEvent_t *cev = nullptr;
+    int ncev = 0, cev_cap = 0;
 };
+
+// Runs `f` (one collective on c.s) between two of the iteration's timing events, if any.
+template <typename T, typename F>
+void timed_comm(Ctx<T> &c, F f) {
+    const bool t = c.cev && c.ncev + 2 <= c.cev_cap;
+    if (t) PLS_CUDA(cudaEventRecord(c.cev[c.ncev++], c.s));
+    f();
+    if (t) PLS_CUDA(cudaEventRecord(c.cev[c.ncev++], c.s));
+}
 
 template <typename T>
 void set_smem_attrs() {
@@ -775,7 +788,7 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
         k_slot_sum<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, g.T, g.mpad, g.m1, c.yfull, c.cur_ctrl);
         PLS_CHECK_LAUNCH();
         ++c.launches;
-        comm_reduce_scatter(c.comm, c.yfull, c.ysc, g.nb, dtype_of(T()), c.s);
+        timed_comm(c, [&] { comm_reduce_scatter(c.comm, c.yfull, c.ysc, g.nb, dtype_of(T()), c.s); });
         c.Yfin = c.ysc;
         return 1;
     }
@@ -846,7 +859,7 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
     k_slot_sum<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, nslots, g.mpad, g.m1, c.yfull, c.cur_ctrl);
     PLS_CHECK_LAUNCH();
     ++c.launches;
-    comm_reduce_scatter(c.comm, c.yfull, c.ysc, g.nb, dtype_of(T()), c.s);
+    timed_comm(c, [&] { comm_reduce_scatter(c.comm, c.yfull, c.ysc, g.nb, dtype_of(T()), c.s); });
     c.Yfin = c.ysc;
     return 1;
 }
@@ -888,7 +901,7 @@ void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par,
                                                                c.partials, c.counter, 0, c.cur_ctrl, S_PAP);
             PLS_CHECK_LAUNCH();
             ++c.launches;
-            comm_allreduce_sum_f64(c.comm, c.yred, c.yred, g.nb, c.s);
+            timed_comm(c, [&] { comm_allreduce_sum_f64(c.comm, c.yred, c.yred, g.nb, c.s); });
             Y = c.yred;
             nslots = 1;
             nsub = 1;
@@ -904,11 +917,12 @@ void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par,
 // Row-sharded exchanges; with the feature split the CG vectors and scalars are replicated.
 template <typename T>
 void allreduce(Ctx<T> &c, int slot, int count) {
-    if (c.comm && !c.fsplit) comm_allreduce_sum_f64(c.comm, c.scal + slot + S_L, c.scal + slot, count, c.s);
+    if (c.comm && !c.fsplit)
+        timed_comm(c, [&] { comm_allreduce_sum_f64(c.comm, c.scal + slot + S_L, c.scal + slot, count, c.s); });
 }
 template <typename T>
 void allgather(Ctx<T> &c, T *full) {
-    if (c.comm && !c.fsplit) comm_allgather(c.comm, full, c.g.nb, dtype_of(T()), c.s);
+    if (c.comm && !c.fsplit) timed_comm(c, [&] { comm_allgather(c.comm, full, c.g.nb, dtype_of(T()), c.s); });
 }
 
 // Common setup: geometry, buffers, H2D, transform, q.  Returns the context.
@@ -1189,11 +1203,17 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     int *hctrl = reinterpret_cast<int *>(hs + S_COUNT);
     const int64_t launches_before_cg = c.launches;
     constexpr int kBatch = 8;
+    constexpr int kCommEv = 12;  // event slots per iteration for collectives (<= 5 collectives)
     cudaEvent_t mv0[kBatch], mv1[kBatch];
+    cudaEvent_t cev[kBatch][kCommEv];
+    int ncev[kBatch] = {};
     for (int b = 0; b < kBatch; ++b) {
         mv0[b] = E.make();
         mv1[b] = E.make();
+        if (c.comm)
+            for (int k = 0; k < kCommEv; ++k) cev[b][k] = E.make();
     }
+    double t_comm = 0.0;
     double t_mv = 0.0, t_mv_min = 1e30;
     int64_t it = 0;
     c.cur_ctrl = c.ctrl;
@@ -1317,7 +1337,16 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         c.graph_used = true;
     } else {
         while (true) {
-            for (int b = 0; b < kBatch; ++b) enqueue_iteration(it + b, mv0[b], mv1[b], 0ull, 0);
+            for (int b = 0; b < kBatch; ++b) {
+                if (c.comm) {
+                    c.cev = cev[b];
+                    c.ncev = 0;
+                    c.cev_cap = kCommEv;
+                }
+                enqueue_iteration(it + b, mv0[b], mv1[b], 0ull, 0);
+                ncev[b] = c.ncev;
+                c.cev = nullptr;
+            }
             PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
             PLS_CUDA(cudaMemcpyAsync(hctrl, c.ctrl, C_COUNT * sizeof(int), cudaMemcpyDeviceToHost, c.s));
             PLS_CUDA(cudaStreamSynchronize(c.s));
@@ -1326,6 +1355,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
                 const double tm = elapsed(mv0[b], mv1[b]);
                 t_mv += tm;
                 t_mv_min = std::min(t_mv_min, tm);
+                for (int k = 0; k + 1 < ncev[b]; k += 2) t_comm += elapsed(cev[b][k], cev[b][k + 1]);
             }
             it = hctrl[C_IT];
             if (std::getenv("PLSSVM_DEBUG"))
@@ -1395,6 +1425,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         st->t_bias_d2h = elapsed(e_cg, e_end);
         st->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
         st->t_matvec = t_mv;
+        st->t_comm = t_comm;
         st->t_matvec_min = it > 0 ? t_mv_min : 0.0;
         st->bytes_per_gpu = A.bytes;
         st->gpu_launches = c.launches;

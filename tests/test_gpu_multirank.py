@@ -44,7 +44,7 @@ def _worker(rank, world, port, path, kernel, mode, m, d, circ, mg=0, x0=0, f32=0
                                              opts=pl.options(mode=mode, comm=comm, multi_gpu=mg, x0=x0))
     if rank == 0:
         np.savez(path, out=out, alpha=alpha, b=b, st=st, it=stats.iterations, ranks=stats.num_ranks,
-                 mode_used=stats.mode_used)
+                 mode_used=stats.mode_used, tcomm=stats.t_comm, tcg=stats.t_cg)
     pl.plssvm_comm_destroy(comm)
     dist.barrier()
     dist.destroy_process_group()
@@ -81,6 +81,8 @@ def test_row_sharded_train_matches_oracle(tmp_path, world, kernel, mode, m, d, c
     assert int(r["st"]) == 0 and int(r["ranks"]) == world and int(r["mode_used"]) == mode
     assert np.linalg.norm(r["alpha"] - a_ref) <= 1e-7 * np.linalg.norm(a_ref)
     assert abs(float(r["b"]) - b_ref) <= 1e-7 * max(abs(b_ref), np.abs(a_ref).max())
+    # the collectives are timed separately: positive, inside the CG time
+    assert 0.0 < float(r["tcomm"]) < float(r["tcg"])
 
 
 @pytest.mark.parametrize("world,m,d,x0", [
