@@ -82,3 +82,29 @@ def test_fp32_ozaki_scale_and_peaked_rows():
     out, _ = pl.plssvm_qtilde_matvec(X, p, pl.LINEAR, 1.0, 3, 0.0, 1.0,
                                      opts=pl.options(mode=pl.MODE_IMPLICIT, fp32_engine=pl.FP32_OZAKI))
     assert rel(out, ref) <= 1e-5, rel(out, ref)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_fp32_ozaki_zero_duplicate_and_extreme_rows(kernel):
+    """Zero rows (E = 0, all digits 0), duplicated points (exact-zero RBF distance), rows scaled by
+    1e+15 / 1e-15 (the per-row scale 2^(E-14) is kept in fp64): the product stays within the fp32
+    bars against the oracle on the same fp32 inputs."""
+    rng = np.random.default_rng(77 + kernel)
+    m, d = 600, 40
+    X = rng.standard_normal((m, d)).astype(np.float32)
+    X[10] = 0.0
+    X[11] = X[12]
+    if kernel == pl.LINEAR:  # magnitudes far from 1 (the kernels with gamma would overflow / vanish)
+        X[20] *= np.float32(1e15)
+        X[21] *= np.float32(1e-15)
+    p = rng.standard_normal(m - 1).astype(np.float32)
+    gamma = float(np.float32(1.0 / d))
+    coef0 = 0.5 if kernel == pl.POLYNOMIAL else 0.0
+    Qt = oracle.qtilde(X.astype(np.float64), kernel, gamma, 3, coef0, 1.0)
+    ref = Qt @ p.astype(np.float64)
+    scale = np.abs(Qt) @ np.abs(p.astype(np.float64))
+    for mode in (pl.MODE_IMPLICIT, pl.MODE_CACHED):
+        out, _ = pl.plssvm_qtilde_matvec(X, p, kernel, gamma, 3, coef0, 1.0,
+                                         opts=pl.options(mode=mode, fp32_engine=pl.FP32_OZAKI))
+        out = out.astype(np.float64)
+        assert np.all(np.abs(out - ref) <= 1e-5 * scale + 1e-30), (mode, np.max(np.abs(out - ref) / scale))
