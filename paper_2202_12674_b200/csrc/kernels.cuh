@@ -566,12 +566,26 @@ __global__ void __launch_bounds__(256) k_rowdot(const T *__restrict__ X, int64_t
 template <typename T>
 __global__ void __launch_bounds__(kVecThreads)
     k_slot_sum(const T *__restrict__ Ypart, int nslots, int64_t rows, int64_t m1, T *__restrict__ y, const int *ctrl) {
+    // k_finalize's layout: 32-row chunks x 8 slot groups, fixed-order combine (deterministic)
+    constexpr int G = kVecThreads / 32;
+    __shared__ T grp[G][33];
     if (cg_done(ctrl)) return;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        T s = T(0);
-        for (int k = 0; k < nslots; ++k) s += Ypart[static_cast<int64_t>(k) * rows + i];
-        y[i] = i < m1 ? s : T(0);
+    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const int64_t nchunks = (rows + 31) / 32;
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const int64_t i = ch * 32 + lane;
+        T sg = T(0);
+        if (i < rows)
+            for (int k = q; k < nslots; k += G) sg += Ypart[static_cast<int64_t>(k) * rows + i];
+        grp[q][lane] = sg;
+        __syncthreads();
+        if (q == 0 && i < rows) {
+            T s = T(0);
+#pragma unroll
+            for (int g = 0; g < G; ++g) s += grp[g][lane];
+            y[i] = i < m1 ? s : T(0);
+        }
+        __syncthreads();
     }
 }
 
