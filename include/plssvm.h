@@ -153,8 +153,9 @@ typedef enum { PLSSVM_FP32_TCGEN05 = 0, PLSSVM_FP32_FFMA = 1, PLSSVM_FP32_OZAKI 
  *  DMMA:  fp64 tensor cores (mma.sync f64, error <~ d u sum_k |x_ik||x_jk|).
  *         Needs d <= 16384 (the int32 level sums; larger d with OZAKI -> PLSSVM_E_INVALID_ARG).
  *  AUTO:  OZAKI unless some point has max_k |x_ik| > 64 * rms_k(x_ik) (a peaked row whose small
- *         features would lose relative precision under the row-max scaling) or d > 16384,
- *         then DMMA. */
+ *         features would lose relative precision under the row-max scaling), d > 16384, or the
+ *         problem is tiny (at most 384 padded points, where the persistent kernel's fixed cost
+ *         dominates), then DMMA. */
 typedef enum { PLSSVM_FP64_AUTO = 0, PLSSVM_FP64_OZAKI = 1, PLSSVM_FP64_DMMA = 2 } plssvm_fp64_engine_t;
 
 /* Statistics of one training call (all times are device-event seconds). */

@@ -541,6 +541,7 @@ float *oz_point_major(Arena &A, const float *Xs, int64_t m, int64_t d, int64_t r
 // of any operand array peaks above kOzPeakMax x its RMS.
 constexpr double kOzPeakMax = 64.0;
 constexpr int64_t kOzMaxD = 16384;
+constexpr int64_t kOzMinRows = 384;  // AUTO: padded point counts up to this use DMMA
 // The largest row peak max_k |x_ik| / rms_k(x_ik) over the given point-major arrays (one sync).
 template <typename TIN>
 float oz_row_peak(std::initializer_list<const TIN *> arrays, std::initializer_list<int64_t> rows, int64_t dpad,
@@ -574,6 +575,12 @@ bool oz_choose(int engine, std::initializer_list<const double *> arrays, std::in
         return true;
     }
     if (!fits) return false;
+    // tiny problems: the persistent 2-SM kernel's fixed cost (~20 us: TMEM allocation, barriers,
+    // two TMEM passes) exceeds the whole DMMA product (profiles/r01_small_engines.txt: 256 x 16
+    // 24.6 vs 16.7 us per product)
+    int64_t most = 0;
+    for (int64_t r : rows) most = std::max(most, r);
+    if (most <= kOzMinRows) return false;
     return oz_row_peak<double>(arrays, rows, dpad, d, A, s, launches) <= kOzPeakMax;
 }
 

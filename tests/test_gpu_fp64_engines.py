@@ -161,7 +161,7 @@ def test_engines_agree_on_planes_c1_slice():
 def test_wide_d_limit():
     """int32 level sums bound d (<= 16384): AUTO switches to DMMA beyond it, forced OZAKI refuses."""
     rng = np.random.default_rng(8)
-    m, d = 40, 16400
+    m, d = 400, 16400  # > 384 points: AUTO's tiny-problem rule would pick DMMA regardless of d
     X = rng.standard_normal((m, d)) * 0.05
     y = np.where(np.arange(m) % 2 == 0, 1.0, -1.0)
     alpha, b, st, stats = pl.plssvm_train_ex(X, y, pl.RBF, 1.0 / d, eps=1e-10)
@@ -196,3 +196,17 @@ def test_ozaki_rbf_table_exp_across_the_exponent_range(gamma):
     f_ref, _ = oracle.predict(X, alpha, 0.25, Z, pl.RBF, gamma)
     K = np.exp(-gamma * ((Z[:, None, :] - X[None, :, :]) ** 2).sum(-1))
     assert np.all(np.abs(f - f_ref) <= 1e-12 * (np.abs(K) @ np.abs(alpha) + 0.25))
+
+
+def test_auto_picks_dmma_for_tiny_problems():
+    """AUTO: at most 384 padded points -> DMMA (the persistent int8 kernel's fixed cost dominates);
+    both engines stay within the parity bar there."""
+    rng = np.random.default_rng(12)
+    for m, want in ((256, pl.FP64_DMMA), (300, pl.FP64_DMMA), (385, pl.FP64_OZAKI)):
+        X = rng.standard_normal((m, 20))
+        y = np.where(rng.random(m) < 0.5, 1.0, -1.0)
+        y[0], y[1] = 1.0, -1.0
+        a, b, st, stats = pl.plssvm_train_ex(X, y, pl.RBF, 0.05, eps=1e-10)
+        assert st == 0 and stats.fp64_engine_used == want, (m, stats.fp64_engine_used)
+        a_ref, _, _, _ = oracle.train(X, y, pl.RBF, 0.05, eps=1e-10)
+        assert rel(a, a_ref) <= 1e-7
