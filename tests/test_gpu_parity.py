@@ -244,6 +244,42 @@ def test_c1_full_size_sampled_rows_and_residual():
     assert np.array_equal(lab[zi], lab_ref)
 
 
+def test_c4_full_size_sampled_rows_residual_and_predict():
+    """BASELINE config C4 (2^17 x 2^12 RBF fp64) on one GPU, at full size: the cached product (68.8 GB
+    of symmetric-packed Q~ in HBM) and the implicit product on sampled rows against the oracle's
+    rows, the trained model's residual on the same rows, and predict on the 2^15 test points
+    (decision values and labels on a subset vs the oracle)."""
+    import torch
+
+    if torch.cuda.mem_get_info()[1] < 150e9:
+        pytest.skip("needs a 180 GB B200 (68.8 GB packed Q~ + data)")
+    cfg = synth.configs()["C4"]
+    X, y, Z, yz = synth.config_data(cfg)
+    m = cfg.m
+    rng = np.random.default_rng(44)
+    p = rng.standard_normal(m - 1)
+    rows = _sampled_rows(m, rng, 19)
+    R = oracle.qtilde_rows(X, rows, cfg.kernel, cfg.gamma, C=cfg.C)
+    ref = R @ p
+    scale = np.abs(R) @ np.abs(p)
+    for mode in (pl.MODE_CACHED, pl.MODE_IMPLICIT):
+        out, _ = pl.plssvm_qtilde_matvec(X, p, cfg.kernel, cfg.gamma, C=cfg.C, opts=pl.options(mode=mode))
+        assert np.all(np.abs(out[rows] - ref) <= 1e-12 * scale), mode
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, cfg.kernel, cfg.gamma, C=cfg.C, eps=cfg.eps,
+                                             opts=pl.options(mode=pl.MODE_AUTO))
+    assert st == 0 and stats.mode_used == pl.MODE_CACHED
+    rhs = y[:-1] - y[-1]
+    res = np.abs(R @ alpha[:-1] - rhs[rows])
+    assert np.max(res) <= 1e-8 * np.linalg.norm(rhs)
+    assert abs(alpha.sum()) <= 1e-10 * np.abs(alpha).max()
+    zi = np.arange(0, Z.shape[0], 512)
+    f_ref, lab_ref = oracle.predict(X, alpha, b, Z[zi], cfg.kernel, cfg.gamma)
+    f, lab = pl.plssvm_predict(X, alpha, b, Z, cfg.kernel, cfg.gamma)
+    K = np.abs(f_ref) + 1.0
+    assert np.all(np.abs(f[zi] - f_ref) <= 1e-9 * K)
+    assert np.array_equal(lab[zi], lab_ref)
+
+
 def _sampled_rows(m, rng, k=48):
     return np.unique(np.concatenate([[0, 1, 127, 128, m - 2], rng.integers(0, m - 1, k)]))
 
