@@ -228,6 +228,9 @@ def main():
     ap.add_argument("--mode", default="implicit", choices=["implicit", "cached", "auto"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # testing the multi-rank bench logic on a one-GPU box: every rank on cuda:0, exchanges through
+    # the host-staged gloo transport (NCCL refuses two ranks on one device).  Not for measurement.
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     cfg = synth.configs()[args.config]
     if args.impl == "reference":
@@ -240,12 +243,20 @@ def main():
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
-    local = env_int("LOCAL_RANK", 0)
+    local = env_int("LOCAL_RANK", 0) if args.transport == "nccl" else 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    comm = pl.comm_from_torch_distributed(local) if world > 1 else None
+        if args.transport == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    if world > 1:
+        comm = pl.comm_from_torch_distributed(local) if args.transport == "nccl" else \
+            pl.comm_host_staged(local, circulant=True)
+    else:
+        comm = None
+    rdev = dev if args.transport == "nccl" else torch.device("cpu")  # device of the timing all-reduces
 
     mode = {"implicit": pl.MODE_IMPLICIT, "cached": pl.MODE_CACHED, "auto": pl.MODE_AUTO}[args.mode]
     dt = np.float32 if cfg.dtype == "f32" else np.float64
@@ -286,7 +297,7 @@ def main():
         dist.barrier()
     t = ev0.elapsed_time(ev1) / 1e3
     if world > 1:
-        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        tt = torch.tensor([t], device=rdev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
     clocks = sampler.summary()
@@ -388,7 +399,7 @@ def main():
             its_e += stt.iterations
         te = time.perf_counter() - t0
         if world > 1:
-            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            tt = torch.tensor([te], device=rdev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
         es = X.itemsize
