@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <initializer_list>
+#include <atomic>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -368,8 +369,19 @@ void timed_comm(Ctx<T> &c, F f) {
     if (t) PLS_CUDA(cudaEventRecord(c.cev[c.ncev++], c.s));
 }
 
+// cudaFuncSetAttribute is per function and device: each attribute group is applied once per device
+// (the ~30 calls cost a few us each and ran on every training / predict call).
+bool first_on_device(int group) {
+    static std::atomic<uint64_t> done[8] = {};  // group -> mask of devices already configured
+    int dev = 0;
+    PLS_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    return (done[group].fetch_or(bit) & bit) == 0;
+}
+
 template <typename T>
 void set_smem_attrs() {
+    if (!first_on_device(std::is_same<T, double>::value ? 0 : 1)) return;
     const int bytes = static_cast<int>(Engine<T>::SMEM_BYTES);
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<LINEAR, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<POLYNOMIAL, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -437,6 +449,7 @@ void tc_dispatch(int kernel, Args &&...args) {
 }
 
 void tc_set_attrs() {
+    if (!first_on_device(2)) return;
     const int bytes = static_cast<int>(Tc::SMEM_BYTES);
 #define PLS_TC_ATTR(K, M) PLS_CUDA(cudaFuncSetAttribute(k_tile_tc<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
     PLS_TC_ATTR(LINEAR, TC_MATVEC); PLS_TC_ATTR(POLYNOMIAL, TC_MATVEC); PLS_TC_ATTR(RBF, TC_MATVEC);
@@ -602,6 +615,7 @@ bool oz_choose_f32(int engine, std::initializer_list<const float *> arrays, std:
 
 template <typename T>
 void oz_set_attrs() {
+    if (!first_on_device(std::is_same<T, double>::value ? 3 : 4)) return;
     constexpr int S = oz_digits<T>();
     const int bytes = static_cast<int>(Oz<S>::SMEM_BYTES);
 #define PLS_OZ_ATTR(K, M) \
