@@ -18,18 +18,42 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
+
+
+def _host_tag() -> str:
+    """-march=native code is specific to the host CPU: one build per CPU model / flag set (the repo
+    snapshot travels to the GPU box, whose host may not run this machine's instructions)."""
+    import hashlib
+
+    key = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith(("model name", "flags")):
+                    key += ln
+                if ln.startswith("flags"):
+                    break
+    except OSError:
+        pass
+    return hashlib.sha1(key.encode()).hexdigest()[:10]
+
+
+_LIB = os.path.join(_HERE, f"liboracle_{_host_tag()}.so")
 
 LINEAR, POLYNOMIAL, RBF = 0, 1, 2
 OK, E_INVALID, E_NUMERICAL, W_NOT_CONVERGED = 0, 1, 6, 7
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c (plain -O2, no fast-math, OpenMP over rows)."""
+    """Compile oracle.c: -O3 -march=native (SURVEY §8(d) oracle-timing protocol), ISO C11 with
+    -ffp-contract=off and no fast-math (every rounding is the one the source spells out), OpenMP
+    over independent rows only."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
-                               "-o", _LIB, _SRC, "-lm"])
+        tmp = f"{_LIB}.{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", "-O3", "-march=native", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+                               "-fPIC", "-shared", "-std=c11", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 

@@ -133,6 +133,13 @@ static double dot(const double *a, const double *b, int64_t n) {
  *       if replace_every>0 and i>0 and i%replace_every==0: r=b-Ax  else: r=r-alpha q
  *       delta_old=delta_new; delta_new=r.r; beta=delta_new/delta_old; d=r+beta d; i++
  * x holds x0 on entry (ZERO by default).  d.q <= 0 or non-finite -> OR_E_NUMERICAL.
+ * Stagnation guard (SURVEY.md §5 "failure detection" and App. A.7; reading R-20),
+ * active only when replace_every = R > 0: delta_best starts at delta_0; after iteration i, a
+ * delta_new < delta_best / 4 makes delta_best = delta_new and i_best = i; otherwise, once
+ * i - i_best >= W = 2 max(R, 50), the loop stops with OR_W_NOT_CONVERGED (replacement makes the
+ * recurrence oscillate instead of converging at high condition numbers, App. A.2/A.7).  SURVEY
+ * states the window as 2R for Shewchuk's R = 50; the floor of 100 keeps small R from firing on
+ * CG's ordinary plateaus (several iterations without a 4x drop are normal).
  * trace (nullable, length imax+1) receives sqrt(delta) per iteration. */
 int oracle_cg(const double *A, int64_t n, const double *b, double *x, double eps, int64_t imax,
               int64_t replace_every, int64_t *iters_out, double *trace) {
@@ -144,7 +151,9 @@ int oracle_cg(const double *A, int64_t n, const double *b, double *x, double eps
     for (int64_t k = 0; k < n; ++k) r[k] = b[k] - qv[k];
     memcpy(dd, r, sizeof(double) * (size_t)n);
     double delta_new = dot(r, r, n), delta0 = delta_new;
-    int64_t i = 0;
+    double delta_best = delta0;
+    int64_t i = 0, i_best = 0;
+    int stagnated = 0;
     if (trace) trace[0] = sqrt(delta_new);
     while (i < imax && delta_new > eps * eps * delta0) {
         oracle_matvec(A, n, dd, qv);
@@ -165,8 +174,18 @@ int oracle_cg(const double *A, int64_t n, const double *b, double *x, double eps
         for (int64_t k = 0; k < n; ++k) dd[k] = r[k] + beta * dd[k];
         ++i;
         if (trace) trace[i] = sqrt(delta_new);
+        if (replace_every > 0) {
+            if (delta_new < 0.25 * delta_best) {
+                delta_best = delta_new;
+                i_best = i;
+            } else if (i - i_best >= 2 * (replace_every > 50 ? replace_every : 50) &&
+                       delta_new > eps * eps * delta0) {
+                stagnated = 1;
+                break;
+            }
+        }
     }
-    if (status == OR_OK && delta_new > eps * eps * delta0) status = OR_W_NOT_CONVERGED;
+    if (status == OR_OK && (stagnated || delta_new > eps * eps * delta0)) status = OR_W_NOT_CONVERGED;
     *iters_out = i;
     free(r); free(dd); free(qv);
     return status;

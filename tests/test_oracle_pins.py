@@ -349,3 +349,105 @@ def test_c0_reference_values():
     assert st == oracle.OK and 17 <= it <= 25
     assert rel(alpha, a_ref) <= 1e-9 and abs(b - b_ref) <= 1e-9
     assert abs(b - (-0.218075516159)) <= 1e-9
+
+
+# ---------------------------------------------------------------- CG options: x0 = ONES, residual replacement
+# (these branches of oracle_cg / oracle_train were only compared with the GPU.)  The
+# KKT solution of Eq. 11 is unique, so every start vector and replacement period must reach it; the
+# traces pin WHAT the branches compute (r0 = rhs - Q~ x0, the replaced residual is the true one).
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("x0", [0, 1])
+@pytest.mark.parametrize("R", [0, 1, 3, 5])
+def test_train_options_match_dense_kkt_lu(kernel, x0, R):
+    rng = np.random.default_rng(300 + 10 * kernel + 2 * R + x0)
+    for trial in range(3):
+        m, d = int(rng.integers(8, 80)), int(rng.integers(2, 9))
+        X, y = synth.random_small(rng, m, d)
+        gam, deg, r = 1.0 / d, int(rng.integers(1, 4)), float(rng.uniform(0, 1))
+        a_ref, b_ref = kkt_solve(X, y, kernel, gam, deg, r, 1.0)
+        # imax = 10 m: in floating point CG may need more than m - 1 iterations to reach 1e-12
+        alpha, b, it, st = oracle.train(X, y, kernel, gam, deg, r, 1.0, eps=1e-12, x0=x0, replace_every=R,
+                                        imax=10 * m)
+        assert st == oracle.OK
+        assert rel(alpha, a_ref) <= 1e-9, (m, d, trial)
+        assert abs(b - b_ref) <= 1e-8 * max(abs(b_ref), np.abs(a_ref).max())
+
+
+def test_cg_start_vector_residual():
+    """r0 = rhs - A x0 (Shewchuk B2 line 2): A = diag(2, 3, 4), rhs = (2, 6, 12), x0 = 1 gives
+    r0 = (0, 3, 8), |r0| = sqrt(73); x0 = the exact solution (1, 2, 3) gives r0 = 0 and no iteration."""
+    A = np.diag([2.0, 3.0, 4.0])
+    rhs = np.array([2.0, 6.0, 12.0])
+    x, it, st, tr = oracle.cg(A, rhs, eps=1e-14, x0=np.ones(3), trace=True)
+    assert tr[0] == math.sqrt(73.0)
+    assert np.allclose(x, [1.0, 2.0, 3.0], rtol=0, atol=1e-14) and st == oracle.OK
+    x, it, st = oracle.cg(A, rhs, eps=1e-14, x0=np.array([1.0, 2.0, 3.0]))
+    assert it == 0 and np.array_equal(x, [1.0, 2.0, 3.0])
+
+
+def test_train_x0_ones_first_residual():
+    """oracle.train(x0=1): delta_0 = |rhs - Q~ 1|^2 with rhs = y_bar - y_m 1 (Eq. 14) -- checked through
+    the trace of the same system, Q~ built independently as B^T Q B (Eq. 13)."""
+    rng = np.random.default_rng(41)
+    X, y = synth.random_small(rng, 30, 4)
+    m = X.shape[0]
+    Q = gram_lib(X, X, oracle.RBF, 0.25, 1, 0.0) + np.eye(m)
+    B = np.vstack([np.eye(m - 1), -np.ones((1, m - 1))])
+    Qt = B.T @ Q @ B
+    rhs = y[:-1] - y[-1]
+    _, _, _, tr = oracle.cg(oracle.qtilde(X, oracle.RBF, 0.25), rhs, eps=1e-12, x0=np.ones(m - 1), trace=True)
+    assert abs(tr[0] - np.linalg.norm(rhs - Qt @ np.ones(m - 1))) <= 1e-12 * tr[0]
+    a_ref, b_ref = kkt_solve(X, y, oracle.RBF, 0.25, 1, 0.0, 1.0)
+    alpha, b, it, st = oracle.train(X, y, oracle.RBF, 0.25, eps=1e-12, x0=1)
+    assert st == oracle.OK and rel(alpha, a_ref) <= 1e-9
+
+
+def _ill_conditioned(n=120, cond=1e10, seed=17):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    A = (U * np.geomspace(1.0, cond, n)) @ U.T
+    return 0.5 * (A + A.T), rng.standard_normal(n)
+
+
+@pytest.mark.parametrize("R", [3, 5, 7])
+def test_residual_replacement_period_and_value(R):
+    """Residual replacement (Shewchuk B2, option R): the trace equals the pure recurrence's bit for bit
+    up to iteration R (no replacement before i = R), departs from it at the first replacement, and at
+    every replacement iteration (i - 1) % R == 0, i > 1, the recorded |r_i| is the TRUE residual
+    |rhs - A x_i| (x_i from a run capped at imax = i) to rounding."""
+    A, rhs = _ill_conditioned()
+    imax = 40
+    _, _, _, tr0 = oracle.cg(A, rhs, eps=1e-30, imax=imax, replace_every=0, trace=True)
+    x, it, st, tr = oracle.cg(A, rhs, eps=1e-30, imax=imax, replace_every=R, trace=True)
+    assert it == imax
+    assert np.array_equal(tr[:R + 1], tr0[:R + 1]) and tr[R + 1] != tr0[R + 1]
+    for i in range(R + 1, it + 1, R):
+        xi, iti, _ = oracle.cg(A, rhs, eps=1e-30, imax=i, replace_every=R)
+        assert iti == i
+        assert abs(tr[i] - np.linalg.norm(rhs - A @ xi)) <= 1e-12 * np.linalg.norm(rhs)
+
+
+def test_stagnation_guard():
+    """Stagnation guard (R-20): with replacement on and an unreachable
+    eps, the oracle stops with W_NOT_CONVERGED W = 2 max(R, 50) iterations after the last 4x drop of
+    delta, long before imax, and its x still solves the system to ~kappa u; without replacement (R = 0) the guard is
+    off and the loop runs to imax."""
+    A, rhs = _ill_conditioned(cond=1e4)
+    ref = scipy.linalg.cho_solve(scipy.linalg.cho_factor(A), rhs)
+    R, imax = 5, 3000
+    x, it, st, tr = oracle.cg(A, rhs, eps=1e-17, imax=imax, replace_every=R, trace=True)
+    assert st == oracle.W_NOT_CONVERGED and it < imax
+    # the exit is the rule's first firing: the best delta (last 4x drop) is exactly 2R iterations old
+    d = tr ** 2
+    best, ib = d[0], 0
+    fired = None
+    for i in range(1, it + 1):
+        if d[i] < 0.25 * best:
+            best, ib = d[i], i
+        elif i - ib >= 2 * max(R, 50):
+            fired = i
+            break
+    assert fired == it
+    assert rel(x, ref) <= 1e4 * 1e-15 * 10  # at the attainable accuracy ~ kappa u
+    x2, it2, st2 = oracle.cg(A, rhs, eps=1e-17, imax=150, replace_every=0)
+    assert it2 == 150 and st2 == oracle.W_NOT_CONVERGED
