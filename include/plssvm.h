@@ -38,6 +38,8 @@
  * There is no CPU fallback: without a usable CUDA device every compute call returns
  * PLSSVM_E_CUDA.
  * Thread safety: concurrent calls must use different devices or different streams.
+ * Multi-GPU: either one process per GPU with a communicator (options.comm, plssvm_comm_init) or one
+ * call driving options.num_gpus devices itself (a host thread per device, NCCL or peer transport).
  */
 #ifndef PLSSVM_B200_H
 #define PLSSVM_B200_H
@@ -66,7 +68,8 @@ typedef enum {
     PLSSVM_E_CUDA = 4,         /* CUDA runtime error / no device */
     PLSSVM_E_NCCL = 5,         /* NCCL error in row-sharded mode */
     PLSSVM_E_NUMERICAL = 6,    /* CG breakdown: p.Q~p <= 0 or non-finite */
-    PLSSVM_W_NOT_CONVERGED = 7, /* max_iter reached before ||r|| <= eps ||r0||; alpha, b filled */
+    PLSSVM_W_NOT_CONVERGED = 7, /* max_iter reached (or the stagnation guard fired, stats.stop_reason)
+                                   before ||r|| <= eps ||r0||; alpha, b filled */
     PLSSVM_E_IO = 8            /* file open / read / write failure or malformed file (message names the line) */
 } plssvm_status_t;
 
@@ -101,7 +104,30 @@ typedef struct {
     int32_t cg_loop;         /* plssvm_cg_loop_t: how the CG iterations are issued [AUTO] */
     int32_t multi_gpu;       /* plssvm_multi_gpu_t: how `comm`'s ranks share the work [ROWS] */
     int32_t cg_variant;      /* plssvm_cg_variant_t [SHEWCHUK] */
+    int32_t num_gpus;        /* single-process multi-GPU: this call drives num_gpus devices
+                                [device, device+1, ...) (modulo the visible device count: ranks beyond it
+                                share devices round-robin -- correct, not faster) with one host thread and
+                                one row shard per device; <= 0 means the PLSSVM_NUM_GPUS environment
+                                variable, else 1 [0].  Not with `comm` (that is the one-process-per-GPU
+                                mode).  train: rank 0 (on `device`) writes alpha, b; predict: the test
+                                points are split over the devices */
+    int32_t transport;       /* plssvm_transport_t: collectives of the num_gpus mode [AUTO] */
+    int32_t true_residual;   /* 1: after CG, one more product gives ||rhs - Q~x|| / ||r0|| in
+                                stats.rel_residual_true (SURVEY §5 metrics) [0: not computed, stats -1] */
+    int32_t reserved0;
 } plssvm_options_t;
+
+/* Collectives of the single-process multi-GPU mode (options.num_gpus > 1).
+ *  NCCL: ncclCommInitAll over the devices (needs distinct devices); all-gather of p, all-reduces
+ *        of the CG scalars, reduce-scatter of the circulant partial products over NVLink.
+ *  PEER: the library's own transport over peer memory (NVLink P2P): the p update kernel stores its
+ *        band straight into every rank's p buffer (the all-gather fused into the CG update,
+ *        SURVEY §8(f) NEXT-1), scalars and partial products are pulled with peer copies and summed
+ *        in rank order by every rank (deterministic, identical on all ranks); cross-device order
+ *        comes from CUDA events, no host round trip per collective beyond an enqueue barrier.
+ *        Works with ranks sharing a device.
+ *  AUTO: NCCL when every rank has its own device, else PEER. */
+typedef enum { PLSSVM_TRANSPORT_AUTO = 0, PLSSVM_TRANSPORT_NCCL = 1, PLSSVM_TRANSPORT_PEER = 2 } plssvm_transport_t;
 
 /* CG formulation.  SHEWCHUK: the paper's loop (two inner products per iteration, each
  * its own reduction / all-reduce).  SINGLE_REDUCTION: Chronopoulos-Gear CG:
@@ -181,7 +207,21 @@ typedef struct {
                                         scalar all-reduces, reduce-scatter of the partial products;
                                         CUDA events, batched loop; 0 on one GPU) -- inside t_matvec for
                                         the reduce-scatter, which is part of the product */
+    double rel_residual_true;        /* ||rhs - Q~x|| / ||r0|| from one extra product after CG
+                                        (options.true_residual = 1), else -1 */
+    int32_t stop_reason;             /* plssvm_stop_t: why the CG loop ended */
+    int32_t transport_used;          /* num_gpus mode: PLSSVM_TRANSPORT_NCCL or _PEER; 0 otherwise */
 } plssvm_stats_t;
+
+/* Why the CG loop stopped (stats.stop_reason). */
+typedef enum {
+    PLSSVM_STOP_CONVERGED = 0,   /* ||r|| <= eps ||r0|| (recurrence residual) */
+    PLSSVM_STOP_MAX_ITER = 1,    /* options.max_iter (or m-1) iterations -> PLSSVM_W_NOT_CONVERGED */
+    PLSSVM_STOP_FIXED = 2,       /* options.fixed_iter iterations done */
+    PLSSVM_STOP_STAGNATED = 3,   /* stagnation guard (replace_every > 0, R-20): no 4x drop of
+                                    r.r within 2 max(R, 50) iterations -> PLSSVM_W_NOT_CONVERGED */
+    PLSSVM_STOP_BREAKDOWN = 4    /* p.Q~p <= 0 or non-finite -> PLSSVM_E_NUMERICAL */
+} plssvm_stop_t;
 
 PLSSVM_API void plssvm_default_options(plssvm_options_t *opts);
 

@@ -13,10 +13,14 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libplssvm_b200.so")
+# experiment build (-DPLSSVM_OZ_EXPERIMENTS: the PLSSVM_OZ_DEBUG / PLSSVM_OZ_GROUP switches of the Ozaki
+# kernel, which make results WRONG); only tools/ load it, through PLSSVM_EXPERIMENT_LIB=1
+LIB_EXP = os.path.join(LIBDIR, "libplssvm_b200_exp.so")
 BINDIR = os.path.join(PKG, "bin")
 CLI = os.path.join(BINDIR, "plssvm")
-SOURCES = ["capi.cu", "driver.cu", "comm.cu", "io.cpp"]
-HEADERS = ["common.cuh", "tile_engine.cuh", "kernels.cuh", "tc_engine.cuh", "ozaki_engine.cuh", "driver.h", "io.h"]
+SOURCES = ["capi.cu", "driver.cu", "comm.cu", "multi.cu", "io.cpp"]
+HEADERS = ["common.cuh", "tile_engine.cuh", "kernels.cuh", "tc_engine.cuh", "ozaki_engine.cuh", "driver.h", "io.h",
+           "comm.h"]
 
 
 def nccl_dirs():
@@ -26,10 +30,10 @@ def nccl_dirs():
     return os.path.join(base, "include"), os.path.join(base, "lib")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "plssvm.h"), __file__]
     return any(os.path.getmtime(p) > t for p in deps)
 
@@ -51,27 +55,33 @@ def build_cli(force: bool = False) -> str:
     return CLI
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        build_cli()
-        return LIB
+def build(force: bool = False, verbose: bool = False, variant: str = "product") -> str:
+    lib = LIB if variant == "product" else LIB_EXP
+    if not force and not _stale(lib):
+        if variant == "product":
+            build_cli()
+        return lib
     os.makedirs(LIBDIR, exist_ok=True)
     inc, libd = nccl_dirs()
+    tmp = f"{lib}.{os.getpid()}.tmp"
     cmd = [
         "nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-        "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
+        "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared", "--threads", "4",
         "-I", os.path.join(ROOT, "include"), "-I", inc,
-        "-o", LIB, *[os.path.join(CSRC, f) for f in SOURCES],
+        *(["-DPLSSVM_OZ_EXPERIMENTS"] if variant != "product" else []),
+        "-o", tmp, *[os.path.join(CSRC, f) for f in SOURCES],
         "-L", libd, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libd}", "-lcudart",
     ]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    build_cli(force=True)
-    return LIB
+    os.replace(tmp, lib)
+    if variant == "product":
+        build_cli(force=True)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                variant="exp" if "--exp" in sys.argv else "product"))

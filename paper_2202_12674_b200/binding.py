@@ -22,6 +22,8 @@ CG_AUTO, CG_BATCHED, CG_GRAPH = 0, 1, 2
 MULTI_GPU_ROWS, MULTI_GPU_FEATURES = 0, 1
 CG_SHEWCHUK, CG_SINGLE_REDUCTION = 0, 1
 FP32_TCGEN05, FP32_FFMA, FP32_OZAKI, FP32_AUTO = 0, 1, 2, 3
+TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_PEER = 0, 1, 2
+STOP_CONVERGED, STOP_MAX_ITER, STOP_FIXED, STOP_STAGNATED, STOP_BREAKDOWN = 0, 1, 2, 3, 4
 OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED, E_IO = range(9)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
                 6: "E_NUMERICAL", 7: "W_NOT_CONVERGED", 8: "E_IO"}
@@ -39,7 +41,9 @@ class plssvm_options_t(ct.Structure):
                 ("fixed_iter", ct.c_int64), ("device", ct.c_int32), ("device_pointers", ct.c_int32),
                 ("stream", ct.c_void_p), ("comm", ct.c_void_p), ("cache_budget_bytes", ct.c_int64),
                 ("fp32_engine", ct.c_int32), ("linear_w", ct.c_int32), ("fp64_engine", ct.c_int32),
-                ("cg_loop", ct.c_int32), ("multi_gpu", ct.c_int32), ("cg_variant", ct.c_int32)]
+                ("cg_loop", ct.c_int32), ("multi_gpu", ct.c_int32), ("cg_variant", ct.c_int32),
+                ("num_gpus", ct.c_int32), ("transport", ct.c_int32), ("true_residual", ct.c_int32),
+                ("reserved0", ct.c_int32)]
 
 
 class plssvm_stats_t(ct.Structure):
@@ -51,7 +55,8 @@ class plssvm_stats_t(ct.Structure):
                 ("t_matvec", ct.c_double), ("t_matvec_min", ct.c_double), ("bytes_per_gpu", ct.c_int64),
                 ("gpu_launches", ct.c_int64), ("launches_in_cg", ct.c_int64), ("fp64_engine_used", ct.c_int32),
                 ("cg_loop_used", ct.c_int32), ("fp32_engine_used", ct.c_int32), ("reserved1", ct.c_int32),
-                ("t_comm", ct.c_double)]
+                ("t_comm", ct.c_double), ("rel_residual_true", ct.c_double), ("stop_reason", ct.c_int32),
+                ("transport_used", ct.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -77,7 +82,9 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    """The product library; PLSSVM_EXPERIMENT_LIB=1 selects the experiment build (tools/ only: its
+    PLSSVM_OZ_DEBUG switches make results wrong; bench.py refuses to run with it)."""
+    return _build.LIB_EXP if os.environ.get("PLSSVM_EXPERIMENT_LIB") == "1" else _build.LIB
 
 
 def load(build_if_missing: bool = True):
@@ -85,11 +92,12 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_build.LIB):
+    path = lib_path()
+    if not os.path.exists(path):
         if not build_if_missing:
-            raise FileNotFoundError(f"{_build.LIB} missing: run __graft_entry__.build()")
-        _build.build()
-    L = ct.CDLL(_build.LIB)
+            raise FileNotFoundError(f"{path} missing: run __graft_entry__.build()")
+        _build.build(variant="exp" if path == _build.LIB_EXP else "product")
+    L = ct.CDLL(path)
     vp, i64, i32, d, i = ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_double, ct.c_int
     L.plssvm_default_options.argtypes = [ct.POINTER(plssvm_options_t)]
     L.plssvm_default_options.restype = None
@@ -159,6 +167,22 @@ def options(**kw) -> plssvm_options_t:
     return o
 
 
+def _same_device_tensor(name, t, X, n):
+    """A torch CUDA tensor that can be passed as a device pointer beside X: same dtype, same device,
+    contiguous, n elements.  Anything else raises (a wrong dtype would be read with X's element size,
+    a host tensor's pointer would be dereferenced on the device)."""
+    if not _is_torch_cuda(t):
+        raise TypeError(f"{name} must be a CUDA tensor on {X.device} like X (got {type(t).__name__}"
+                        f"{' on ' + str(t.device) if hasattr(t, 'device') else ''})")
+    if t.device != X.device:
+        raise ValueError(f"{name} is on {t.device}, X on {X.device}")
+    if t.dtype != X.dtype:
+        raise TypeError(f"{name} has dtype {t.dtype}, X has {X.dtype}")
+    if t.numel() != n:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {n}")
+    return t.contiguous()
+
+
 def _device_opts(o, tensors):
     import torch
 
@@ -224,9 +248,13 @@ def plssvm_train_ex(X, y, kernel, gamma=1.0, degree=3, coef0=0.0, C=1.0, eps=1e-
         import torch
 
         _device_opts(o, [X])
-        X, y = X.contiguous(), y.contiguous()
+        X = X.contiguous()
+        y = _same_device_tensor("y", y, X, m)
         alpha = torch.empty(m, dtype=X.dtype, device=X.device) if alpha is None else alpha
         b = torch.empty(1, dtype=X.dtype, device=X.device) if b is None else b
+        if not (alpha.is_contiguous() and b.is_contiguous()):
+            raise ValueError("alpha and b outputs must be contiguous")
+        alpha, b = _same_device_tensor("alpha", alpha, X, m), _same_device_tensor("b", b, X, 1)
         st = L.plssvm_train_ex(X.data_ptr(), y.data_ptr(), m, d, dt, kernel, gamma, degree, coef0, C, eps,
                                ct.byref(o), alpha.data_ptr(), b.data_ptr(), ct.byref(stats))
         _check(st, (OK, W_NOT_CONVERGED))
@@ -267,10 +295,13 @@ def plssvm_predict_ex(X, alpha, b, Z, kernel, gamma=1.0, degree=3, coef0=0.0, op
         import torch
 
         _device_opts(o, [X])
+        X = X.contiguous()
+        alpha = _same_device_tensor("alpha", alpha, X, m)
+        Z = _same_device_tensor("Z", Z, X, n * d)
         f = torch.empty(n, dtype=X.dtype, device=X.device)
         lab = torch.empty(n, dtype=torch.int32, device=X.device)
-        _check(L.plssvm_predict_ex(X.contiguous().data_ptr(), alpha.contiguous().data_ptr(), float(b), m, d, dt,
-                                   kernel, gamma, degree, coef0, Z.contiguous().data_ptr(), n, ct.byref(o),
+        _check(L.plssvm_predict_ex(X.data_ptr(), alpha.data_ptr(), float(b), m, d, dt,
+                                   kernel, gamma, degree, coef0, Z.data_ptr(), n, ct.byref(o),
                                    f.data_ptr(), lab.data_ptr(), tk))
         return f, lab, tuple(tk)
     X, alpha, Z = _host(X, dt), _host(alpha, dt), _host(Z, dt)
@@ -292,8 +323,10 @@ def plssvm_qtilde_matvec(X, p, kernel, gamma=1.0, degree=3, coef0=0.0, C=1.0, re
         import torch
 
         _device_opts(o, [X])
+        X = X.contiguous()
+        p = _same_device_tensor("p", p, X, m - 1)
         out = torch.empty(m - 1, dtype=X.dtype, device=X.device)
-        _check(L.plssvm_qtilde_matvec(X.contiguous().data_ptr(), p.contiguous().data_ptr(), m, d, dt, kernel, gamma,
+        _check(L.plssvm_qtilde_matvec(X.data_ptr(), p.data_ptr(), m, d, dt, kernel, gamma,
                                       degree, coef0, C, repeats, ct.byref(o), out.data_ptr(), tk))
         return out, tuple(tk)
     X, p = _host(X, dt), _host(p, dt)

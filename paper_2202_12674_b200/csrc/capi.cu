@@ -82,6 +82,13 @@ int check_engines(const plssvm_options_t &o) {
 // PLSSVM_MULTI_GPU_FEATURES (paper §III-C5): linear kernel, fp64, implicit, d >= P.
 int check_multi_gpu(const plssvm_options_t &o, int kernel, int dtype, int64_t d) {
     if (int s = check_engines(o)) return s;
+    if (o.transport < PLSSVM_TRANSPORT_AUTO || o.transport > PLSSVM_TRANSPORT_PEER)
+        return fail(PLSSVM_E_INVALID_ARG, "options.transport must be 0 (AUTO), 1 (NCCL) or 2 (PEER)");
+    if (o.comm && plssvm::resolve_num_gpus(o) > 1)
+        return fail(PLSSVM_E_INVALID_ARG, "options.num_gpus > 1 (one call drives several GPUs) cannot be combined "
+                                          "with options.comm (one process per GPU)");
+    if (o.comm && o.device != plssvm::comm_device(static_cast<plssvm::CommHandle *>(o.comm)))
+        return fail(PLSSVM_E_INVALID_ARG, "options.device must be the device the communicator was created on");
     if (o.multi_gpu != PLSSVM_MULTI_GPU_ROWS && o.multi_gpu != PLSSVM_MULTI_GPU_FEATURES)
         return fail(PLSSVM_E_INVALID_ARG, "options.multi_gpu must be 0 (ROWS) or 1 (FEATURES)");
     if (o.multi_gpu != PLSSVM_MULTI_GPU_FEATURES) return PLSSVM_OK;
@@ -118,6 +125,9 @@ void plssvm_default_options(plssvm_options_t *o) {
     o->cg_loop = PLSSVM_CG_AUTO;
     o->multi_gpu = PLSSVM_MULTI_GPU_ROWS;
     o->cg_variant = PLSSVM_CG_SHEWCHUK;
+    o->num_gpus = 0;  // PLSSVM_NUM_GPUS, else 1
+    o->transport = PLSSVM_TRANSPORT_AUTO;
+    o->true_residual = 0;
 }
 
 int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtype, int kernel, double gamma, int degree,
@@ -143,6 +153,8 @@ int plssvm_train_ex(const void *X, const void *y, int64_t m, int64_t d, int dtyp
     if ((s = device_ok(o.device))) return s;
     if (stats) std::memset(stats, 0, sizeof(*stats));
     plssvm::Problem pb{X, y, m, d, dtype, kernel, gamma, degree, coef0, C, eps};
+    const int P = plssvm::resolve_num_gpus(o);
+    if (P > 1) return guarded([&] { return plssvm::train_multi(pb, o, P, alpha, b, stats); });
     return guarded([&] { return plssvm::train(pb, o, alpha, b, stats); });
 }
 
@@ -170,8 +182,12 @@ int plssvm_predict_ex(const void *X, const void *alpha, double b, int64_t m, int
     if (n == 0) return PLSSVM_OK;
     if (!std::isfinite(b)) return fail(PLSSVM_E_INVALID_ARG, "b is not finite");
     if ((s = check_engines(o))) return s;
+    if (o.transport < PLSSVM_TRANSPORT_AUTO || o.transport > PLSSVM_TRANSPORT_PEER)
+        return fail(PLSSVM_E_INVALID_ARG, "options.transport must be 0 (AUTO), 1 (NCCL) or 2 (PEER)");
     if ((s = device_ok(o.device))) return s;
     plssvm::Problem pb{X, nullptr, m, d, dtype, kernel, gamma, degree, coef0, 1.0, 1.0};
+    const int P = plssvm::resolve_num_gpus(o);
+    if (P > 1) return guarded([&] { return plssvm::predict_multi(pb, alpha, b, Z, n, o, P, decision, labels, t_kernel); });
     return guarded([&] { return plssvm::predict(pb, alpha, b, Z, n, o, decision, labels, t_kernel); });
 }
 

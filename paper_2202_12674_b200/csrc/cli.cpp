@@ -70,6 +70,7 @@ int read_data(const char *path, Data &D, int64_t min_d) {
 int cmd_train(int argc, char **argv) {
     int kernel = PLSSVM_RBF, degree = 3, mode = PLSSVM_MODE_AUTO;
     double gamma = -1.0, coef0 = 0.0, C = 1.0, eps = 1e-6;
+    bool gamma_given = false;
     int64_t max_iter = 0;
     bool fp32 = false, quiet = false;
     std::vector<const char *> pos;
@@ -95,7 +96,7 @@ int cmd_train(int argc, char **argv) {
                     kernel = static_cast<int>(v);
                     break;
                 case 'd': degree = static_cast<int>(v); break;
-                case 'g': gamma = v; break;
+                case 'g': gamma = v; gamma_given = true; break;
                 case 'r': coef0 = v; break;
                 case 'c': C = v; break;
                 case 'e': eps = v; break;
@@ -121,7 +122,9 @@ int cmd_train(int argc, char **argv) {
     // first-seen label -> +1, the other -> -1
     std::vector<double> ypm(D.y.size());
     for (size_t i = 0; i < D.y.size(); ++i) ypm[i] = D.y[i] == D.labels[0] ? 1.0 : -1.0;
-    if (gamma <= 0.0) gamma = 1.0 / static_cast<double>(D.d);  // LIBSVM default 1/num_features
+    // LIBSVM default 1/num_features only when -g is absent; an explicit -g <= 0 reaches the
+    // library's validation ("gamma must be > 0")
+    if (!gamma_given) gamma = 1.0 / static_cast<double>(D.d);
     const auto t1 = clk::now();
     plssvm_options_t o;
     plssvm_default_options(&o);

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <initializer_list>
 #include <atomic>
+#include <mutex>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -358,6 +359,10 @@ struct Ctx {
     // pairs around every collective of the current CG iteration, when set
     cudaEvent_t *cev = nullptr;
     int ncev = 0, cev_cap = 0;
+    // PEER transport with direct peer access: every rank's full p (device array), for the p update
+    // that stores its band into all of them (the all-gather fused into k_update_p)
+    T **peer_p = nullptr;
+    int npeer = 0;
 };
 
 // Runs `f` (one collective on c.s) between two of the iteration's timing events, if any.
@@ -370,18 +375,26 @@ void timed_comm(Ctx<T> &c, F f) {
 }
 
 // cudaFuncSetAttribute is per function and device: each attribute group is applied once per device
-// (the ~30 calls cost a few us each and ran on every training / predict call).
-bool first_on_device(int group) {
-    static std::atomic<uint64_t> done[8] = {};  // group -> mask of devices already configured
+// (the ~30 calls cost a few us each and ran on every training / predict call).  The group's bit is
+// set only after every attribute call succeeded, under a mutex, so a concurrent caller on the same
+// device waits for the setup instead of launching before the smem limit is raised, and a failed
+// setup is retried by the next call.
+template <typename F>
+void once_per_device(int group, F apply) {
+    static std::mutex mu;
+    static uint64_t done[8] = {};  // group -> mask of devices already configured
     int dev = 0;
     PLS_CUDA(cudaGetDevice(&dev));
     const uint64_t bit = uint64_t(1) << (dev & 63);
-    return (done[group].fetch_or(bit) & bit) == 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done[group] & bit) return;
+    apply();
+    done[group] |= bit;
 }
 
 template <typename T>
 void set_smem_attrs() {
-    if (!first_on_device(std::is_same<T, double>::value ? 0 : 1)) return;
+    once_per_device(std::is_same<T, double>::value ? 0 : 1, [] {
     const int bytes = static_cast<int>(Engine<T>::SMEM_BYTES);
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<LINEAR, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     PLS_CUDA(cudaFuncSetAttribute(k_matvec_implicit<POLYNOMIAL, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -401,6 +414,7 @@ void set_smem_attrs() {
     PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<LINEAR, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<POLYNOMIAL, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     PLS_CUDA(cudaFuncSetAttribute(k_predict_tiles<RBF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    });
 }
 
 void tc_set_attrs();
@@ -449,7 +463,7 @@ void tc_dispatch(int kernel, Args &&...args) {
 }
 
 void tc_set_attrs() {
-    if (!first_on_device(2)) return;
+    once_per_device(2, [] {
     const int bytes = static_cast<int>(Tc::SMEM_BYTES);
 #define PLS_TC_ATTR(K, M) PLS_CUDA(cudaFuncSetAttribute(k_tile_tc<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
     PLS_TC_ATTR(LINEAR, TC_MATVEC); PLS_TC_ATTR(POLYNOMIAL, TC_MATVEC); PLS_TC_ATTR(RBF, TC_MATVEC);
@@ -463,6 +477,7 @@ void tc_set_attrs() {
     PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<LINEAR, TC_PREDICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
     PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<POLYNOMIAL, TC_PREDICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
     PLS_CUDA(cudaFuncSetAttribute(k_tile_tc_wide<RBF, TC_PREDICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, wb));
+    });
 }
 
 template <int KT, int MODE>
@@ -615,7 +630,7 @@ bool oz_choose_f32(int engine, std::initializer_list<const float *> arrays, std:
 
 template <typename T>
 void oz_set_attrs() {
-    if (!first_on_device(std::is_same<T, double>::value ? 3 : 4)) return;
+    once_per_device(std::is_same<T, double>::value ? 3 : 4, [] {
     constexpr int S = oz_digits<T>();
     const int bytes = static_cast<int>(Oz<S>::SMEM_BYTES);
 #define PLS_OZ_ATTR(K, M) \
@@ -624,16 +639,22 @@ void oz_set_attrs() {
     PLS_OZ_ATTR(LINEAR, OZ_PRECOMPUTE); PLS_OZ_ATTR(POLYNOMIAL, OZ_PRECOMPUTE); PLS_OZ_ATTR(RBF, OZ_PRECOMPUTE);
     PLS_OZ_ATTR(LINEAR, OZ_PREDICT); PLS_OZ_ATTR(POLYNOMIAL, OZ_PREDICT); PLS_OZ_ATTR(RBF, OZ_PREDICT);
 #undef PLS_OZ_ATTR
+    });
 }
 
-// Experiments only (PLSSVM_OZ_DEBUG, results are wrong when set): 1 = no epilogue, 2 = no TMA,
-// 4 = no MMAs.  0 in production.
+// Decomposition experiments (results are WRONG when set): 1 = no epilogue, 2 = no TMA, 4 = no MMAs.
+// Only in the experiment build (_build.build(variant="exp"), -DPLSSVM_OZ_EXPERIMENTS, a separate .so
+// the tools load explicitly); the product library has no switch that changes what is computed.
 int oz_debug_flags() {
+#ifdef PLSSVM_OZ_EXPERIMENTS
     static int f = [] {
         const char *e = std::getenv("PLSSVM_OZ_DEBUG");
         return e ? std::atoi(e) : 0;
     }();
     return f;
+#else
+    return 0;
+#endif
 }
 
 // One persistent CTA per SM (the 512-column TMEM allocation admits one per SM anyway), in
@@ -648,8 +669,8 @@ void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb
     if (npt <= 0) return;
     // Only co-resident clusters (a pair must fit in one GPC): a statically scheduled grid with one
     // cluster too many would run that cluster's tiles as a second wave.
-    static int max_clusters[3][3] = {};
-    int &mc = max_clusters[KT][MODE];
+    static std::atomic<int> max_clusters[3][3] = {};
+    int mc = max_clusters[KT][MODE].load();
     if (mc == 0) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(num_sms()), 1, 1);
@@ -657,6 +678,7 @@ void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb
         cfg.dynamicSmemBytes = O::SMEM_BYTES;
         PLS_CUDA(cudaOccupancyMaxActiveClusters(&mc, k_tile_ozaki<KT, S, MODE, T>, &cfg));
         if (mc <= 0) mc = num_sms() / 2;
+        max_clusters[KT][MODE].store(mc);
         if (std::getenv("PLSSVM_DEBUG")) std::fprintf(stderr, "[plssvm] k_tile_ozaki co-resident pairs: %d\n", mc);
     }
     const int grid = 2 * std::min(npt, mc);
@@ -673,14 +695,16 @@ void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb
 // Row blocks per raster group: the group's row-operand digits (7 planes x 128 rows x d8 bytes per
 // block) should stay L2-resident while the co-resident pairs sweep the column blocks -- 32 blocks
 // up to ~40 MB (C1: DRAM reads per product 902 -> 405 MB, ncu), fewer for wide points (C2 at 32:
-// 117 MB, L2 thrash, +4 % time).  PLSSVM_OZ_GROUP overrides (experiments).
+// 117 MB, L2 thrash, +4 % time).  PLSSVM_OZ_GROUP overrides it in the experiment build only.
 int oz_group_rows(int64_t d8, int S) {
+#ifdef PLSSVM_OZ_EXPERIMENTS
     static int forced = [] {
         const char *e = std::getenv("PLSSVM_OZ_GROUP");
         const int v = e ? std::atoi(e) : 0;
         return v >= 2 ? (v & ~1) : 0;
     }();
     if (forced) return forced;
+#endif
     const int64_t per_block = int64_t(S) * 128 * d8;
     const int64_t budget = int64_t(40) << 20;
     return per_block * 32 <= budget ? 32 : per_block * 16 <= budget ? 16 : 8;
@@ -1158,6 +1182,9 @@ void select_mode(Ctx<T> &c, const plssvm_options_t &o) {
     c.packed = c.cached && can_pack;
 }
 
+// delta of the current iterate from a control snapshot (Shewchuk: double-buffered by parity).
+double delta_now(const double *hs, int64_t it, bool cgcg) { return cgcg ? hs[S_CG_GAMMA] : hs[S_DELTA + (it & 1)]; }
+
 template <typename T>
 int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, void *b_out, plssvm_stats_t *st) {
     PLS_CUDA(cudaSetDevice(o.device));
@@ -1217,7 +1244,8 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     c.ctrl = A.alloc<int>(C_COUNT);
     const int imax_i = static_cast<int>(std::min<int64_t>(imax, INT32_MAX));
     const int fixed_i = static_cast<int>(std::min<int64_t>(std::max<int64_t>(o.fixed_iter, 0), INT32_MAX));
-    k_cg_start<<<1, 1, 0, c.s>>>(c.scal, c.ctrl, pb.eps * pb.eps, imax_i, fixed_i);
+    const int repl_i = static_cast<int>(std::min<int64_t>(std::max<int64_t>(o.replace_every, 0), INT32_MAX));
+    k_cg_start<<<1, 1, 0, c.s>>>(c.scal, c.ctrl, pb.eps * pb.eps, imax_i, fixed_i, repl_i);
     PLS_CHECK_LAUNCH();
     ++c.launches;
     double *hs = reinterpret_cast<double *>(pinned_scratch(S_COUNT * sizeof(double) + C_COUNT * sizeof(int)));
@@ -1244,6 +1272,13 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     // Chronopoulos-Gear variant: c.p (full) carries r (the product's operand), c.r (band) the
     // search direction p, scg the recurrence s = Q~ p; one all-reduce of (gamma, delta).
     const bool cgcg = o.cg_variant == PLSSVM_CG_SINGLE_REDUCTION;
+    if (c.comm && comm_is_peer(c.comm) && comm_peer_direct(c.comm) && !c.fsplit && !cgcg) {
+        // fused all-gather of p (PEER transport): learn every rank's p buffer once
+        std::vector<void *> all = comm_peer_exchange_ptr(c.comm, c.p);
+        c.npeer = static_cast<int>(all.size());
+        c.peer_p = A.alloc<T *>(c.npeer);
+        PLS_CUDA(cudaMemcpyAsync(c.peer_p, all.data(), all.size() * sizeof(void *), cudaMemcpyHostToDevice, c.s));
+    }
     T *scg = nullptr;
     if (cgcg) {
         scg = A.alloc<T>(g.nb);
@@ -1285,10 +1320,13 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
             allreduce(c, S_DELTA + (par ^ 1), 1);
         }
         k_update_p<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter, loop,
-                                                           use_loop);
+                                                           use_loop, c.peer_p, c.npeer, g.g0);
         PLS_CHECK_LAUNCH();
         ++c.launches;
-        allgather(c, c.p);
+        if (c.npeer > 0)  // p already stored into every rank's buffer: only the cross-device order remains
+            timed_comm(c, [&] { comm_peer_fence(c.comm, c.s); });
+        else
+            allgather(c, c.p);
     };
     const bool graph_ok = c.comm == nullptr && o.replace_every <= 0;
     const bool use_graph = graph_ok && (o.cg_loop == PLSSVM_CG_GRAPH ||
@@ -1390,10 +1428,15 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     int64_t matvecs = it + ((o.x0 == 0) ? 0 : 1) + (cgcg ? 1 : 0);  // CG-CG: the product of the final r
     if (o.replace_every > 0 && it > 1) matvecs += (it - 1) / o.replace_every;
     const double delta0 = hs[S_DELTA0];
-    const double delta = cgcg ? hs[S_CG_GAMMA] : hs[S_DELTA + (it & 1)];
+    const double delta = delta_now(hs, it, cgcg);
     const double eps2 = pb.eps * pb.eps;
     int status = PLSSVM_OK;
-    if (hctrl[C_DONE] == 2) status = PLSSVM_E_NUMERICAL;
+    if (hctrl[C_DONE] == 2)  // name the iteration and the offending scalars
+        throw Error(PLSSVM_E_NUMERICAL, "CG breakdown at iteration " + std::to_string(it) + ": p.Q~p = " +
+                                            std::to_string(cgcg ? hs[S_CG_DELTA] : hs[S_PAP]) + ", delta = " +
+                                            std::to_string(delta_now(hs, it, cgcg)) +
+                                            " (p.Q~p must be > 0 and finite; Q~ is not positive definite for "
+                                            "these kernel parameters, or the input overflowed)");
     c.launches_cg = c.launches - launches_before_cg;
     PLS_CUDA(cudaEventRecord(e_cg, c.s));
     if (status == PLSSVM_OK && o.fixed_iter <= 0 && delta > eps2 * delta0) status = PLSSVM_W_NOT_CONVERGED;
@@ -1425,11 +1468,26 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
             PLS_CUDA(cudaMemcpyAsync(b_out, b_d, sizeof(T), cudaMemcpyDeviceToHost, c.s));
         }
     }
+    // true residual (options.true_residual, SURVEY §5 metrics): one more product of the final x
+    double rel_true = -1.0;
+    if (o.true_residual && status != PLSSVM_E_NUMERICAL) {
+        const int ns = launch_qtilde_product<T>(c, c.xfull);
+        finalize<T>(c, ns, nullptr, 1, nullptr, S_TRUE - S_DELTA, 0);  // mode 1 into slot S_TRUE
+        allreduce(c, S_TRUE, 1);
+        PLS_CUDA(cudaMemcpyAsync(hs + S_TRUE, c.scal + S_TRUE, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    }
     PLS_CUDA(cudaEventRecord(e_end, c.s));
     PLS_CUDA(cudaStreamSynchronize(c.s));
+    if (o.true_residual && status != PLSSVM_E_NUMERICAL) rel_true = delta0 > 0 ? std::sqrt(hs[S_TRUE] / delta0) : 0.0;
     if (st) {
+        st->rel_residual_true = rel_true;
+        st->stop_reason = hctrl[C_DONE] == 3 ? PLSSVM_STOP_STAGNATED
+                          : o.fixed_iter > 0  ? PLSSVM_STOP_FIXED
+                          : delta <= eps2 * delta0 ? PLSSVM_STOP_CONVERGED
+                                                   : PLSSVM_STOP_MAX_ITER;
+        st->transport_used = 0;
         st->iterations = it;
-        st->matvecs = matvecs;
+        st->matvecs = matvecs + (rel_true >= 0.0 ? 1 : 0);
         st->rel_residual = delta0 > 0 ? std::sqrt(delta / delta0) : 0.0;
         st->mode_used = c.lowrank ? PLSSVM_MODE_LOWRANK : (c.cached ? PLSSVM_MODE_CACHED : PLSSVM_MODE_IMPLICIT);
         st->num_ranks = c.nranks;

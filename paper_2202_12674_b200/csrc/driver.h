@@ -1,6 +1,7 @@
 // driver.h -- internal (C++) interface between the C ABI (capi.cu) and the device driver.
 #pragma once
 #include <cstdint>
+#include <vector>
 #include "../../include/plssvm.h"
 
 namespace plssvm {
@@ -30,10 +31,20 @@ int predict(const Problem &pb, const void *alpha, double b, const void *Z, int64
 int qtilde_matvec(const Problem &pb, const void *p, int32_t repeats, const plssvm_options_t &o, void *out,
                   double *t_kernel);
 
+// multi.cu: the num_gpus mode (one host thread per device, NCCL or PEER transport)
+int resolve_num_gpus(const plssvm_options_t &o);
+int train_multi(const Problem &pb, const plssvm_options_t &o, int P, void *alpha, void *b, plssvm_stats_t *st);
+int predict_multi(const Problem &pb, const void *alpha, double b, const void *Z, int64_t n, const plssvm_options_t &o,
+                  int P, void *decision, int32_t *labels, double *t_kernel);
+
 // comm.cu
 int comm_rank(const CommHandle *c);
 int comm_size(const CommHandle *c);
 int comm_device(const CommHandle *c);
+bool comm_is_peer(const CommHandle *c);
+bool comm_peer_direct(const CommHandle *c);
+void comm_peer_fence(CommHandle *c, void *stream);
+std::vector<void *> comm_peer_exchange_ptr(CommHandle *c, void *ptr);
 void comm_allreduce_sum_f64(CommHandle *c, const double *send, double *recv, int64_t count, void *stream);
 void comm_allgather(CommHandle *c, void *buf, int64_t count_per_rank, int dtype, void *stream);
 bool comm_has_reduce_scatter(const CommHandle *c);

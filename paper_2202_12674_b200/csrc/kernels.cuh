@@ -35,13 +35,18 @@ enum Scal : int {
     S_L = 16,       // slot s + S_L holds this rank's local partial of slot s; the multi-GPU
                     // all-reduce is out of place (local -> global), hence idempotent: iterations
                     // enqueued after convergence cannot corrupt the global scalars
-    S_COUNT = 32
+    S_BEST = 32,    // stagnation guard: delta at the last 4x drop (replicated, never all-reduced)
+    S_TRUE = 33,    // |rhs - Q~x|^2 after CG (options.true_residual; partial at S_TRUE + S_L)
+    S_COUNT = 56
 };
 
 // Device-side CG control block (int32[4]): the loop runs without a host round trip per
 // iteration; every loop kernel returns immediately once `done` is set, so the host can enqueue
 // iterations in batches and read the state once per batch.
-enum Ctl : int { C_IT = 0, C_DONE = 1, C_IMAX = 2, C_FIXED = 3, C_COUNT = 4 };
+// Device CG control block.  C_DONE: 0 running, 1 finished (converged / imax / fixed count), 2 breakdown
+// (S:259), 3 stagnated (R-20: residual replacement on, no 4x drop of delta within the window).
+// C_REPL = replace_every (0: guard off), C_IBEST = iteration of the last 4x drop (S_BEST holds its delta).
+enum Ctl : int { C_IT = 0, C_DONE = 1, C_IMAX = 2, C_FIXED = 3, C_REPL = 4, C_IBEST = 5, C_COUNT = 6 };
 __device__ __forceinline__ bool cg_done(const int *ctrl) { return ctrl != nullptr && *(volatile const int *)(ctrl + C_DONE) != 0; }
 
 // ---------------------------------------------------------------------------------------
@@ -692,17 +697,27 @@ __global__ void __launch_bounds__(kVecThreads)
 // `fixed` iterations.
 template <typename T>
 __global__ void __launch_bounds__(kVecThreads)
-    k_update_p(T *__restrict__ p, const T *__restrict__ r, int64_t nb, const double *scal, int *ctrl,
-               unsigned *counter, cudaGraphConditionalHandle loop, int use_loop) {
+    k_update_p(T *__restrict__ p, const T *__restrict__ r, int64_t nb, double *scal, int *ctrl,
+               unsigned *counter, cudaGraphConditionalHandle loop, int use_loop, T *const *__restrict__ peer_p,
+               int npeer, int64_t g0) {
     if (cg_done(ctrl)) {
         if (use_loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0u);
         return;
     }
     const int par = ctrl[C_IT] & 1;
     const T b = static_cast<T>(scal[S_DELTA + (par ^ 1)] / scal[S_DELTA + par]);
+    // npeer > 0 (single-process multi-GPU, PEER transport): the all-gather of p fused into the update --
+    // the new band goes straight into every rank's full p (peer_p[q] + g0, NVLink P2P stores; this
+    // rank's own buffer is one of them), so no separate exchange of p follows (comm.cu)
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        p[i] = fma(b, p[i], r[i]);
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const T v = fma(b, p[i], r[i]);
+        if (npeer > 0) {
+            for (int q = 0; q < npeer; ++q) peer_p[q][g0 + i] = v;
+        } else {
+            p[i] = v;
+        }
+    }
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -718,6 +733,19 @@ __global__ void __launch_bounds__(kVecThreads)
         if (!(pap > 0.0) || !isfinite(pap) || !isfinite(dnew)) done = 2;
         else if (ctrl[C_FIXED] > 0 ? (it >= ctrl[C_FIXED] || dnew == 0.0) : (dnew <= scal[S_THR])) done = 1;
         else if (it >= ctrl[C_IMAX]) done = 1;
+        if (done == 0 && ctrl[C_REPL] > 0 && ctrl[C_FIXED] <= 0) {
+            // stagnation guard (R-20, the oracle's rule): a 4x drop of delta below the best
+            // resets the window; no such drop within W = 2 max(R, 50) iterations stops the loop
+            const int R = ctrl[C_REPL];
+            const int W = 2 * (R > 50 ? R : 50);
+            double *best = scal + S_BEST;
+            if (dnew < 0.25 * *best) {
+                *best = dnew;
+                ctrl[C_IBEST] = it;
+            } else if (it - ctrl[C_IBEST] >= W) {
+                done = 3;
+            }
+        }
         ctrl[C_IT] = it;
         ctrl[C_DONE] = done;
         *counter = 0u;
@@ -792,8 +820,11 @@ __global__ void __launch_bounds__(kVecThreads)
 }
 
 // Loop entry (after delta_0 is final on every rank): threshold and control block.
-__global__ void k_cg_start(double *scal, int *ctrl, double eps2, int imax, int fixed) {
+__global__ void k_cg_start(double *scal, int *ctrl, double eps2, int imax, int fixed, int repl) {
     const double d0 = scal[S_DELTA0];
+    scal[S_BEST] = d0;
+    ctrl[C_REPL] = repl;
+    ctrl[C_IBEST] = 0;
     scal[S_CG_GAMMA] = d0;  // Chronopoulos-Gear: gamma_0 = r_0.r_0 (global and this rank's partial)
     scal[S_CG_GAMMA + S_L] = scal[S_DELTA0 + S_L];
     scal[S_THR] = eps2 * d0;

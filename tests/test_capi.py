@@ -47,6 +47,31 @@ def test_default_options():
     assert (o.mode, o.x0, o.max_iter, o.replace_every, o.fixed_iter, o.device, o.device_pointers) == (0, 0, 0, 0, 0, 0, 0)
     assert o.stream is None and o.comm is None
     assert (o.cg_loop, o.multi_gpu) == (pl.CG_AUTO, pl.MULTI_GPU_ROWS)
+    assert (o.num_gpus, o.transport, o.true_residual) == (0, pl.TRANSPORT_AUTO, 0)
+
+
+def test_struct_layout_matches_header(tmp_path):
+    """The binding's ctypes mirrors of plssvm_options_t / plssvm_stats_t have the header's size and
+    field offsets (a C program compiled against include/plssvm.h prints them)."""
+    import subprocess
+
+    opts = [f for f, _ in binding.plssvm_options_t._fields_]
+    stats = [f for f, _ in binding.plssvm_stats_t._fields_]
+    src = tmp_path / "layout.c"
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "plssvm.h"', 'int main(void) {',
+             'printf("%zu %zu\\n", sizeof(plssvm_options_t), sizeof(plssvm_stats_t));']
+    lines += [f'printf("%zu\\n", offsetof(plssvm_options_t, {f}));' for f in opts]
+    lines += [f'printf("%zu\\n", offsetof(plssvm_stats_t, {f}));' for f in stats]
+    lines += ['return 0; }']
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    out = subprocess.check_output([str(exe)]).decode().split()
+    so, ss = int(out[0]), int(out[1])
+    assert so == ct.sizeof(binding.plssvm_options_t) and ss == ct.sizeof(binding.plssvm_stats_t)
+    offs = [int(v) for v in out[2:]]
+    assert offs[:len(opts)] == [getattr(binding.plssvm_options_t, f).offset for f in opts]
+    assert offs[len(opts):] == [getattr(binding.plssvm_stats_t, f).offset for f in stats]
 
 
 @pytest.mark.parametrize("m,P", [(2, 1), (256, 1), (16384, 1), (16384, 8), (1000, 3), (65536, 8), (131072, 8)])
@@ -86,7 +111,8 @@ def test_engine_options_validated():
     X = np.random.default_rng(0).standard_normal((10, 3))
     y = np.array([1, -1] * 5, dtype=float)
     alpha, b = np.zeros(10), np.zeros(1)
-    for kw in (dict(fp64_engine=3), dict(fp32_engine=4), dict(cg_loop=3), dict(cg_variant=2), dict(multi_gpu=2)):
+    for kw in (dict(fp64_engine=3), dict(fp32_engine=4), dict(cg_loop=3), dict(cg_variant=2), dict(multi_gpu=2),
+               dict(transport=3), dict(num_gpus=2, comm=1)):
         o = pl.options(**kw)
         st = L.plssvm_train_ex(X.ctypes.data, y.ctypes.data, 10, 3, 0, 2, 0.5, 3, 0.0, 1.0, 1e-10, ct.byref(o),
                                alpha.ctypes.data, b.ctypes.data, None)

@@ -362,3 +362,54 @@ def test_linear_predict_w_shortcut(dtype):
         assert rel(f, f_ref) <= tol, (lw, rel(f, f_ref))
         safe = np.abs(f_ref) > 1e3 * tol * np.abs(f_ref).max()
         assert np.array_equal(lab[safe], lab_ref[safe])
+
+
+# ------------------------------------------------------------------------------ full-size model parity
+def test_c1_full_training_parity_all_labels():
+    """The north_star targets at the bench's workload (C1, 2^14 x 2^10 RBF fp64, eps 1e-10) in the launch
+    configuration bench.py times (implicit, batched CG loop, default fp64 engine): the GPU-trained
+    (alpha, b) against the ORACLE-trained model (full oracle training, ~20 s on the host cores),
+    ||a - a*|| / ||a*|| <= 1e-7 and |b - b*| <= 1e-7 max(|b*|, ||a*||_inf); then every one of the 8192
+    test labels, GPU-trained + GPU-predicted vs oracle-trained + oracle-predicted, bit-identical
+    (SURVEY §8(c) parity metrics; min |f| printed so a mismatch could be attributed to a margin)."""
+    cfg = synth.configs()["C1"]
+    X, y, Z, yz = synth.config_data(cfg)
+    opts = pl.options(mode=pl.MODE_IMPLICIT, cg_loop=pl.CG_BATCHED)
+    alpha, b, st, stats = pl.plssvm_train_ex(X, y, cfg.kernel, cfg.gamma, C=cfg.C, eps=cfg.eps, opts=opts)
+    assert st == 0 and stats.fp64_engine_used == pl.FP64_OZAKI and stats.mode_used == pl.MODE_IMPLICIT
+    a_ref, b_ref, it_ref, st_ref = oracle.train(X, y, cfg.kernel, cfg.gamma, C=cfg.C, eps=cfg.eps)
+    assert st_ref == 0
+    ea = rel(alpha, a_ref)
+    eb = abs(b - b_ref) / max(abs(b_ref), np.abs(a_ref).max())
+    print(f"C1: iterations GPU {stats.iterations} oracle {it_ref}; |da|/|a| = {ea:.3e}, db = {eb:.3e}")
+    assert ea <= 1e-7 and eb <= 1e-7
+    assert abs(stats.iterations - it_ref) <= 2  # SURVEY §8(c) c-13
+    f, lab, _ = pl.plssvm_predict_ex(X, alpha, b, Z, cfg.kernel, cfg.gamma, opts=pl.options())
+    f_ref, lab_ref = oracle.predict(X, a_ref, b_ref, Z, cfg.kernel, cfg.gamma)
+    print(f"C1 predict: {Z.shape[0]} labels, mismatches {int(np.sum(lab != lab_ref))}, min |f*| = "
+          f"{np.abs(f_ref).min():.3e}, max |f - f*| = {np.abs(f - f_ref).max():.3e}")
+    assert Z.shape[0] == 8192 and np.array_equal(lab, lab_ref)
+
+
+def test_c2_full_training_vs_exact_ridge_solution():
+    """C2 (2^16 x 2^12 linear fp64, eps 1e-10) trained on the GPU against the EXACT solution of Eq. 11 in
+    closed form (the linear LS-SVM is ridge regression with an unpenalised intercept,
+    w = (Xc^T Xc + I/C)^-1 Xc^T yc, b = ybar - xbar.w, alpha = C (y - X w - b); a d x d solve, pinned
+    -m 'not gpu' by test_linear_ridge_closed_form).  Cached (what AUTO picks), implicit (the paper's
+    method) and the low-rank product; bar 1e-7 (north_star)."""
+    cfg = synth.configs()["C2"]
+    X, y, _, _ = synth.config_data(cfg, n_test=0)
+    C = cfg.C
+    xb, yb = X.mean(0), y.mean()
+    Xc, yc = X - xb, y - yb
+    w = np.linalg.solve(Xc.T @ Xc + np.eye(X.shape[1]) / C, Xc.T @ yc)
+    b_ex = yb - xb @ w
+    a_ex = C * (y - X @ w - b_ex)
+    for mode in (pl.MODE_AUTO, pl.MODE_IMPLICIT, pl.MODE_LOWRANK):
+        a, b, st, s = pl.plssvm_train_ex(X, y, cfg.kernel, cfg.gamma, C=C, eps=cfg.eps, opts=pl.options(mode=mode))
+        ea = rel(a, a_ex)
+        eb = abs(b - b_ex) / max(abs(b_ex), np.abs(a_ex).max())
+        print(f"C2 mode {s.mode_used}: {s.iterations} iterations, |da|/|a| = {ea:.2e}, db = {eb:.2e}")
+        assert st == 0 and ea <= 1e-7 and eb <= 1e-7, (mode, ea, eb)
+        if mode == pl.MODE_AUTO:
+            assert s.mode_used == pl.MODE_CACHED
