@@ -85,12 +85,15 @@ def env_int(name, default):
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
 
-    def __init__(self, device):
+    def __init__(self, device, enabled=True):
         self.device = device
+        self.enabled = enabled
         self.proc = None
         self.path = None
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -114,6 +117,8 @@ class ClockSampler:
 
     def summary(self):
         rows = []
+        if not self.enabled:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["sampled on rank 0"], "samples": 0}
         try:
             with open(self.path) as fh:
                 for ln in fh:
@@ -133,14 +138,59 @@ class ClockSampler:
         mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": reasons, "samples": len(rows)}
+        gpus = sorted({r[0] for r in rows})
+        if len(gpus) > 1:  # every GPU of the job: median SM clock and reasons per device
+            out["per_gpu"] = {g: {"sm_mhz": statistics.median([float(r[1]) for r in rows if r[0] == g and
+                                                               r[1].replace(".", "").isdigit()] or [0.0]),
+                                  "reasons": sorted({names[k] for r in rows if r[0] == g for k in range(4)
+                                                     if r[5 + k].lower() == "active"})} for g in gpus}
+        return out
 
 
 def matvec_flops(m, d):
     """Algorithmic flops of one Q~p product: 2d per distinct entry of the symmetric Q~."""
     m1 = m - 1
     return 2.0 * d * m1 * (m1 + 1) / 2.0
+
+
+def host_info():
+    """CPU model and core counts of the box (state the CPU beside every oracle number)."""
+    info = {"cpu_model": None, "nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "Model name":
+                info["cpu_model"] = v
+            elif k == "Socket(s)":
+                info["sockets"] = int(v)
+            elif k == "Core(s) per socket":
+                info["cores_per_socket"] = int(v)
+            elif k == "Thread(s) per core":
+                info["threads_per_core"] = int(v)
+    except (OSError, ValueError, subprocess.SubprocessError):
+        pass
+    return info
+
+
+def c0_single_thread():
+    """C0 also single-threaded -- the oracle's full C0 training in a child process with
+    OMP_NUM_THREADS=1 (the OpenMP runtime fixes its thread count at load)."""
+    code = ("import sys, time; sys.path.insert(0, %r); import oracle, synth; cfg = synth.configs()['C0']; "
+            "X, y, _, _ = synth.config_data(cfg, n_test=0); t = time.perf_counter(); "
+            "a, b, it, st = oracle.train(X, y, cfg.kernel, cfg.gamma, cfg.degree, cfg.coef0, cfg.C, cfg.eps); "
+            "print(it, time.perf_counter() - t, oracle.num_threads())") % ROOT
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
+                             env=dict(os.environ, OMP_NUM_THREADS="1")).stdout.split()
+        it, ts, th = int(out[0]), float(out[1]), int(out[2])
+        return {"value": it / ts, "unit": UNIT, "cores": th, "sample": f"C0 (256 x 16 linear): {it} CG iterations "
+                                                                      f"in {ts * 1e3:.2f} ms, one thread"}
+    except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+        return None
 
 
 def cpu_baseline(cfg, X, y, target_s=15.0, m_cap=None):
@@ -170,7 +220,11 @@ def cpu_baseline(cfg, X, y, target_s=15.0, m_cap=None):
     return {"value": it / (ts * scale), "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"oracle.train on the first {ms} of {m} points (d={cfg.d}, {KNAMES[cfg.kernel]}, eps "
                       f"{cfg.eps:g}): {it} CG iterations in {ts:.2f} s (Q~ formation {tm[0]:.2f} s, CG {tm[1]:.2f} s);"
-                      f" time scaled by (m/m_s)^2 = {scale:.2f} to the full workload",
+                      f" time scaled by (m/m_s)^2 = {scale:.2f} to the full workload"
+                      + (" (extrapolated)" if scale > 1.0 else " (full workload, not extrapolated)"),
+            "extrapolated": scale > 1.0,
+            "build": "gcc -O3 -march=native -ffp-contract=off, OpenMP over rows (oracle/__init__.py)",
+            "host": host_info(),
             "sample_seconds": ts, "sample_iterations": it, "sample_m": ms}
 
 
@@ -203,8 +257,10 @@ def run_reference(args, cfg):
             "config": config_dict(cfg, args, "oracle"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cal["cores"], "kind": "oracle",
                              "sample": f"each step: oracle.train on the first {ms} of {cfg.m} points; time scaled "
-                                       f"by (m/m_s)^2 = {scale:.2f}"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                                       f"by (m/m_s)^2 = {scale:.2f}" + (" (extrapolated)" if scale > 1.0 else ""),
+                             "extrapolated": scale > 1.0, "host": host_info()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "extrapolated": scale > 1.0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -233,6 +289,17 @@ def main():
     ap.add_argument("--transport", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     cfg = synth.configs()[args.config]
+    bad = sorted(k for k in os.environ if k.startswith("PLSSVM_"))
+    if bad:  # experiment switches / library overrides must not leak into a measurement
+        print(json.dumps({"error": f"refusing to benchmark with {bad} set"}), flush=True)
+        return 2
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` launches its own N ranks (one process per GPU, NCCL), the same way the
+        # driver's scaling run does; this process only waits for them
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 2000}",
+               os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -254,6 +321,9 @@ def main():
     if world > 1:
         comm = pl.comm_from_torch_distributed(local) if args.transport == "nccl" else \
             pl.comm_host_staged(local, circulant=True)
+        if rank == 0:  # the communicator the library uses, for the driver's rank check
+            print(f"[bench] communicator: {args.transport} nranks={world} devices={world if args.transport == 'nccl' else 1}"
+                  f" ({pl.plssvm_version()})", file=sys.stderr, flush=True)
     else:
         comm = None
     rdev = dev if args.transport == "nccl" else torch.device("cpu")  # device of the timing all-reduces
@@ -284,7 +354,9 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
+    # clocks of every GPU of the job (rank 0 samples them all; one process per GPU, devices 0..N-1)
+    sampler = ClockSampler(",".join(str(i) for i in range(world)) if args.transport == "nccl" else local,
+                           enabled=rank == 0)
     per = []
     with sampler:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -392,11 +464,12 @@ def main():
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        its_e = 0
+        its_e, t_h2d = 0, 0.0
         for _ in range(args.steps):
             a_h, b_h, st, stt = pl.plssvm_train_ex(hX, hy, cfg.kernel, C=cfg.C, eps=cfg.eps, opts=opts(), **kw)
             f_h, lab_h, _ = pl.plssvm_predict_ex(hX, a_h, b_h, hZ, cfg.kernel, opts=opts(), **kw)
             its_e += stt.iterations
+            t_h2d += stt.t_h2d
         te = time.perf_counter() - t0
         if world > 1:
             tt = torch.tensor([te], device=rdev, dtype=torch.float64)
@@ -407,10 +480,13 @@ def main():
         d2h = a_h.nbytes + es + f_h.nbytes + lab_h.nbytes
         line["e2e"] = {"value": its_e / te, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                        "ms_per_step": 1e3 * te / args.steps,
+                       # training's own staging copy (device events; predict's copies are inside its call)
+                       "train_h2d_ms_per_step": 1e3 * t_h2d / args.steps,
                        "api": "plssvm_train_ex + plssvm_predict_ex on pinned host numpy buffers"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, X, y)
+        line["cpu_baseline"]["c0_single_thread"] = c0_single_thread()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm is not None:

@@ -166,22 +166,27 @@ typedef enum { PLSSVM_MULTI_GPU_ROWS = 0, PLSSVM_MULTI_GPU_FEATURES = 1 } plssvm
  *  FFMA:    CUDA-core fp32 FMA tiles.
  *  OZAKI:   int8 tensor cores (tcgen05 kind::i8, 2-SM UMMA) on a 3-digit balanced base-256 split of
  *           every point, rounded to 22 bits below its row maximum (6 digit pairs, exact int32 sums,
- *           one TMEM pass): error of x_i.x_j <~ d 2^-22 ||x_i||_inf ||x_j||_inf.  d <= 16384.
- *  AUTO:    OZAKI unless some point has max_k |x_ik| > 8 * rms_k(x_ik) or d > 16384, then TCGEN05. */
+ *           one TMEM pass): |s~ - s| <= u32 |s| + 40.2 d u32 ||x_i||_inf ||x_j||_inf, u32 = 2^-24.
+ *           d <= 16384.
+ *  AUTO:    OZAKI when 40.2 rho^2 <= d (rho as for fp64: the bound is then no larger than an fp32
+ *           dot product's in Cauchy-Schwarz form) and d <= 16384, else TCGEN05. */
 typedef enum { PLSSVM_FP32_TCGEN05 = 0, PLSSVM_FP32_FFMA = 1, PLSSVM_FP32_OZAKI = 2, PLSSVM_FP32_AUTO = 3 } plssvm_fp32_engine_t;
 
 /* fp64 contraction engines.
- *  OZAKI: int8 tensor cores (tcgen05 kind::i8, 2-SM UMMA) on an EXACT split of every point into
- *         7 balanced base-256 int8 digits times a power of two (x_i = 2^(E_i-54) sum_a D_a 256^(6-a),
- *         D_a in [-128, 127]); the 28 digit-pair products of levels a+b <= 6 are summed exactly in
- *         int32 and combined in fp64.  Error of x_i.x_j <~ 7 d 2^-56 ||x_i||_inf ||x_j||_inf
- *         (an fp64-GEMM-type bound weighted by the row maxima instead of |x_ik||x_jk|).
+ *  OZAKI: int8 tensor cores (tcgen05 kind::i8, 2-SM UMMA).  Every point is rounded to the fixed-point
+ *         grid 2^(E_i-54) of its row maximum (2^(E_i-1) <= max_k |x_ik| < 2^E_i; features within a
+ *         factor 4 of the maximum are exact) and written as 7 balanced base-256 int8 digits; the 28
+ *         digit-pair products of levels a+b <= 6 are summed exactly in int32 and combined with one fp64
+ *         rounding.  Error of s = x_i.x_j:
+ *             |s~ - s| <= u |s| + 13.04 d u ||x_i||_inf ||x_j||_inf,   u = 2^-53
+ *         i.e. an fp64-GEMM-type bound weighted by the row maxima, not the componentwise
+ *         d u sum_k |x_ik x_jk| of an fp64 dot.  Needs d <= 16384 (int32 level sums).
  *  DMMA:  fp64 tensor cores (mma.sync f64, error <~ d u sum_k |x_ik||x_jk|).
- *         Needs d <= 16384 (the int32 level sums; larger d with OZAKI -> PLSSVM_E_INVALID_ARG).
- *  AUTO:  OZAKI unless some point has max_k |x_ik| > 64 * rms_k(x_ik) (a peaked row whose small
- *         features would lose relative precision under the row-max scaling), d > 16384, or the
- *         problem is tiny (at most 384 padded points, where the persistent kernel's fixed cost
- *         dominates), then DMMA. */
+ *  AUTO:  OZAKI when its bound is no larger than the fp64 dot product's in Cauchy-Schwarz form
+ *         (d u ||x_i||_2 ||x_j||_2): 13.04 rho^2 <= d with rho = max over points of
+ *         max_k |x_ik| / rms_k(x_ik) (N(0,1)-like data: rho ~ 5, so d >= ~330); else DMMA.  Also DMMA
+ *         for d > 16384 and for tiny problems (at most 384 padded points, where the persistent
+ *         kernel's fixed cost dominates). */
 typedef enum { PLSSVM_FP64_AUTO = 0, PLSSVM_FP64_OZAKI = 1, PLSSVM_FP64_DMMA = 2 } plssvm_fp64_engine_t;
 
 /* Statistics of one training call (all times are device-event seconds). */

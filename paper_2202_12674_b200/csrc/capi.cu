@@ -320,6 +320,13 @@ int plssvm_scale_apply(double *X, int64_t m, int64_t d, const double *fmin, cons
 
 const char *plssvm_last_error(void) { return g_last_error.c_str(); }
 
+#ifdef PLSSVM_OZ_EXPERIMENTS
+// Experiment build only (not part of the product ABI): copy / reset the k_tile_ozaki cycle counters.
+PLSSVM_API int plssvm_exp_oz_profile(unsigned long long *out /* 160 x 8 */, int reset) {
+    return plssvm::exp_oz_profile(out, reset);
+}
+#endif
+
 const char *plssvm_version(void) {
     static std::string v;
     if (v.empty()) {

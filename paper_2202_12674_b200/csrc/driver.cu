@@ -112,6 +112,60 @@ char *pinned_scratch(size_t bytes) {
     return b.p;
 }
 
+// Thread-local pinned staging for host-built index lists (tile lists, pair-tile lists, peer pointers):
+// their H2D copies are then truly asynchronous -- a cudaMemcpyAsync from pageable memory waits for the
+// stream to drain first, which put a host round trip per list into every call.  Bump allocation inside
+// one call; reset at the start of the next (after the last upload's event: no copy of this thread is
+// then in flight); growing synchronises once.
+struct Upload {
+    char *p = nullptr;
+    size_t cap = 0, off = 0;
+    cudaEvent_t last = nullptr;
+    int dev = -1;
+    ~Upload() {
+        if (last) cudaEventDestroy(last);
+        if (p) cudaFreeHost(p);
+    }
+};
+Upload &upload_buf() {
+    thread_local Upload u;
+    return u;
+}
+void upload_reset() {
+    Upload &u = upload_buf();
+    if (u.last) PLS_CUDA(cudaEventSynchronize(u.last));
+    u.off = 0;
+}
+template <typename V>
+void upload(V *dst, const V *src, size_t n, cudaStream_t s) {
+    Upload &u = upload_buf();
+    const size_t bytes = n * sizeof(V), padded = (bytes + 255) / 256 * 256;
+    if (bytes == 0) return;
+    if (u.off + padded > u.cap) {
+        if (u.last) PLS_CUDA(cudaEventSynchronize(u.last));  // every earlier copy from the buffer is done
+        if (u.p) PLS_CUDA(cudaFreeHost(u.p));
+        u.p = nullptr;
+        u.cap = std::max<size_t>({2 * u.cap, padded, size_t(1) << 20});
+        PLS_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&u.p), u.cap, cudaHostAllocPortable));
+        u.off = 0;
+    }
+    int dev = 0;
+    PLS_CUDA(cudaGetDevice(&dev));
+    if (u.last && u.dev != dev) {  // events belong to a device
+        PLS_CUDA(cudaEventSynchronize(u.last));
+        cudaEventDestroy(u.last);
+        u.last = nullptr;
+    }
+    if (!u.last) {
+        PLS_CUDA(cudaEventCreateWithFlags(&u.last, cudaEventDisableTiming));
+        u.dev = dev;
+    }
+    std::memcpy(u.p + u.off, src, bytes);
+    PLS_CUDA(cudaMemcpyAsync(dst, u.p + u.off, bytes, cudaMemcpyHostToDevice, s));
+    PLS_CUDA(cudaEventRecord(u.last, s));
+    u.off += padded;
+}
+
 void setup_mempool(int dev) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -129,37 +183,51 @@ const T *stage_input(Arena &A, const void *src, int64_t n, bool device_ptr, cuda
 }
 
 // Device-side input validation (replaces host scans of the caller's arrays): every listed array
-// is checked for non-finite values, labels for {-1, +1} with both classes.  One sync; throws the
-// plssvm.h status with a message.  Outputs are untouched (nothing is written before this).
+// is checked for non-finite values, labels for {-1, +1} with both classes.  Arrays with row_len > 0
+// (point-major rows: X, Z) also give the largest row peak max_k |x_ik| / rms_k(x_ik) that the engine
+// choice needs (oz_choose) -- in the SAME pass and the same single sync.  Throws the plssvm.h status
+// with a message.  Outputs are untouched (nothing is written before this).  Returns the peak (0 if no
+// array asked for it).
 template <typename T>
 struct VCheck {
     const T *a;
     int64_t n;
     unsigned bit;
+    int64_t row_len;  // > 0: rows of this length feed the row-peak reduction
 };
 template <typename T>
-void validate_inputs(Arena &A, std::initializer_list<VCheck<T>> arrays, const T *y, int64_t m, cudaStream_t s,
-                     int64_t &launches) {
-    unsigned *flags = A.alloc<unsigned>(1);
-    PLS_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned), s));
+float validate_inputs(Arena &A, std::initializer_list<VCheck<T>> arrays, const T *y, int64_t m, cudaStream_t s,
+                      int64_t &launches) {
+    unsigned *flags = A.alloc<unsigned>(2);  // [0] validation bits, [1] row peak (float bits)
+    PLS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned), s));
     bool first = true;
     for (const VCheck<T> &v : arrays) {
         k_validate<T><<<4 * 148, 256, 0, s>>>(v.a, v.n, v.bit, first ? y : nullptr, m, flags);
         PLS_CHECK_LAUNCH();
         ++launches;
         first = false;
+        if (v.row_len > 0) {
+            const int64_t rows = v.n / v.row_len;
+            k_row_peak<T><<<static_cast<unsigned>(std::max<int64_t>(1, ceil_div(rows * 32, 256))), 256, 0, s>>>(
+                v.a, rows, v.row_len, v.row_len, flags + 1);
+            PLS_CHECK_LAUNCH();
+            ++launches;
+        }
     }
-    unsigned h = 0;
-    PLS_CUDA(cudaMemcpyAsync(&h, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    unsigned *h = reinterpret_cast<unsigned *>(pinned_scratch(2 * sizeof(unsigned)));
+    PLS_CUDA(cudaMemcpyAsync(h, flags, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     PLS_CUDA(cudaStreamSynchronize(s));
-    if (h & V_NONFINITE_X) throw Error(PLSSVM_E_INVALID_ARG, "X is not finite");
-    if (h & V_NONFINITE_Z) throw Error(PLSSVM_E_INVALID_ARG, "Z is not finite");
-    if (h & V_NONFINITE_ALPHA) throw Error(PLSSVM_E_INVALID_ARG, "alpha is not finite");
-    if (h & V_NONFINITE_P) throw Error(PLSSVM_E_INVALID_ARG, "p is not finite");
+    if (h[0] & V_NONFINITE_X) throw Error(PLSSVM_E_INVALID_ARG, "X is not finite");
+    if (h[0] & V_NONFINITE_Z) throw Error(PLSSVM_E_INVALID_ARG, "Z is not finite");
+    if (h[0] & V_NONFINITE_ALPHA) throw Error(PLSSVM_E_INVALID_ARG, "alpha is not finite");
+    if (h[0] & V_NONFINITE_P) throw Error(PLSSVM_E_INVALID_ARG, "p is not finite");
     if (y) {
-        if (h & V_BADLABEL) throw Error(PLSSVM_E_LABELS, "labels must be +1 or -1");
-        if (!(h & V_POS) || !(h & V_NEG)) throw Error(PLSSVM_E_LABELS, "both classes (+1 and -1) must be present");
+        if (h[0] & V_BADLABEL) throw Error(PLSSVM_E_LABELS, "labels must be +1 or -1");
+        if (!(h[0] & V_POS) || !(h[0] & V_NEG)) throw Error(PLSSVM_E_LABELS, "both classes (+1 and -1) must be present");
     }
+    float peak;
+    std::memcpy(&peak, &h[1], sizeof(float));
+    return peak;
 }
 
 // rows = padded point count of the destination array (its column count is dpad).
@@ -565,34 +633,19 @@ float *oz_point_major(Arena &A, const float *Xs, int64_t m, int64_t d, int64_t r
     return Xp;
 }
 
-// fp64 engine choice (plssvm.h plssvm_fp64_engine_t): OZAKI, DMMA, or AUTO = OZAKI unless a row
-// of any operand array peaks above kOzPeakMax x its RMS.
-constexpr double kOzPeakMax = 64.0;
+// fp64 engine choice (plssvm.h plssvm_fp64_engine_t): OZAKI, DMMA, or AUTO.  AUTO takes OZAKI only
+// when its worst-case error is no larger than the textbook fp64 one: per inner product
+// |s~ - s| <= u|s| + kOzC64 d u ||x_i||inf ||x_j||inf (ozaki_engine.cuh), and an fp64 dot obeys
+// gamma_d sum|x_ik x_jk| <= ~d u ||x_i||_2 ||x_j||_2 (Cauchy-Schwarz form); with the row peak
+// rho = ||x||_inf / rms(x), ||x_i||inf ||x_j||inf = rho_i rho_j ||x_i||_2 ||x_j||_2 / d, so OZAKI's bound is
+// the smaller one iff kOzC64 rho_i rho_j <= d: AUTO checks kOzC64 rho_max^2 <= d.  (N(0,1)-like data:
+// rho_max ~ 5 -> d >= 330; C1's d = 1024 allows rho <= 8.9, C2 / C4's 4096 rho <= 17.7.)
+constexpr double kOzC64 = 13.04;  // 1 (input rounding to the row grid) + 12.04 (dropped levels 7..12)
 constexpr int64_t kOzMaxD = 16384;
 constexpr int64_t kOzMinRows = 384;  // AUTO: padded point counts up to this use DMMA
-// The largest row peak max_k |x_ik| / rms_k(x_ik) over the given point-major arrays (one sync).
-template <typename TIN>
-float oz_row_peak(std::initializer_list<const TIN *> arrays, std::initializer_list<int64_t> rows, int64_t dpad,
-                  int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
-    unsigned *bits = A.alloc<unsigned>(1);
-    PLS_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned), s));
-    auto r = rows.begin();
-    for (const TIN *X : arrays) {
-        const int64_t n = *r++;
-        k_row_peak<TIN><<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(X, n, dpad, d, bits);
-        PLS_CHECK_LAUNCH();
-        ++launches;
-    }
-    unsigned hb = 0;
-    PLS_CUDA(cudaMemcpyAsync(&hb, bits, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    PLS_CUDA(cudaStreamSynchronize(s));
-    float peak;
-    std::memcpy(&peak, &hb, sizeof(float));
-    return peak;
-}
-
-bool oz_choose(int engine, std::initializer_list<const double *> arrays, std::initializer_list<int64_t> rows,
-               int64_t dpad, int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
+// rho = the largest row peak of the operand arrays (validate_inputs), most_rows = the largest padded
+// point count among them.
+bool oz_choose(int engine, double rho, int64_t most_rows, int64_t d) {
     if (engine == PLSSVM_FP64_DMMA) return false;
     // int32 level sums: |acc_l| <= 7 d8 2^14 < 2^31 needs d8 <= 18724; limit 16384 (ozaki_engine.cuh)
     const bool fits = round_up(d, OzC::BK) <= kOzMaxD;
@@ -606,18 +659,17 @@ bool oz_choose(int engine, std::initializer_list<const double *> arrays, std::in
     // tiny problems: the persistent 2-SM kernel's fixed cost (~20 us: TMEM allocation, barriers,
     // two TMEM passes) exceeds the whole DMMA product (profiles/r01_small_engines.txt: 256 x 16
     // 24.6 vs 16.7 us per product)
-    int64_t most = 0;
-    for (int64_t r : rows) most = std::max(most, r);
-    if (most <= kOzMinRows) return false;
-    return oz_row_peak<double>(arrays, rows, dpad, d, A, s, launches) <= kOzPeakMax;
+    if (most_rows <= kOzMinRows) return false;
+    return kOzC64 * rho * rho <= static_cast<double>(d);
 }
 
-// fp32 engine choice (plssvm.h plssvm_fp32_engine_t): AUTO = OZAKI (3 digits, error <~ d 2^-22
-// ||x_i||_inf ||x_j||_inf) unless a row peaks above kOzPeakMax32 x its RMS (its small features
-// would lose relative accuracy against the fp32 bar) or d > 16384; then TCGEN05 (3xTF32).
-constexpr double kOzPeakMax32 = 8.0;
-bool oz_choose_f32(int engine, std::initializer_list<const float *> arrays, std::initializer_list<int64_t> rows,
-                   int64_t dpad, int64_t d, Arena &A, cudaStream_t s, int64_t &launches) {
+// fp32 engine choice (plssvm.h plssvm_fp32_engine_t): AUTO = OZAKI under the same criterion as fp64
+// with the fp32 unit u32 = 2^-24: the 3-digit split (22 bits below the row maximum, levels <= 2) has
+// |s~ - s| <= u32|s| + kOzC32 d u32 ||x_i||inf ||x_j||inf (input rounding 2^-23 of the row scale: 8 d u32;
+// dropped levels 3..4: 32.2 d u32), so AUTO needs kOzC32 rho_max^2 <= d (C3's d = 2048: rho <= 7.1),
+// else TCGEN05 (3xTF32); d > 16384 also TCGEN05.
+constexpr double kOzC32 = 40.2;
+bool oz_choose_f32(int engine, double rho, int64_t d) {
     if (engine == PLSSVM_FP32_TCGEN05 || engine == PLSSVM_FP32_FFMA) return false;
     const bool fits = round_up(d, Oz<3>::BK) <= kOzMaxD;
     if (engine == PLSSVM_FP32_OZAKI) {
@@ -625,7 +677,7 @@ bool oz_choose_f32(int engine, std::initializer_list<const float *> arrays, std:
         return true;
     }
     if (!fits) return false;
-    return oz_row_peak<float>(arrays, rows, dpad, d, A, s, launches) <= kOzPeakMax32;
+    return kOzC32 * rho * rho <= static_cast<double>(d);
 }
 
 template <typename T>
@@ -767,9 +819,8 @@ void oz_build_pairs(Ctx<T> &c, Arena &A, const std::vector<int2> &tl, int b0, in
     c.oz_npt = static_cast<int>(pt.size());
     c.oz_pt = A.alloc<int2>(c.oz_npt);
     c.oz_pk = A.alloc<int>(2 * c.oz_npt);
-    PLS_CUDA(cudaMemcpyAsync(c.oz_pt, pt.data(), pt.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
-    PLS_CUDA(cudaMemcpyAsync(c.oz_pk, pk.data(), pk.size() * sizeof(int), cudaMemcpyHostToDevice, c.s));
-    PLS_CUDA(cudaStreamSynchronize(c.s));
+    upload(c.oz_pt, pt.data(), pt.size(), c.s);
+    upload(c.oz_pk, pk.data(), pk.size(), c.s);
 }
 
 template <typename T>
@@ -1009,21 +1060,22 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.Xraw = Xs;
     c.m = pb.m;
     c.d = dl;
+    float rho = 0.f;  // largest row peak of X (this rank's slice), for the engine choice
     if (need_labels) {
         c.ylab = const_cast<T *>(stage_input<T>(A, pb.y, pb.m, dev, c.s));
-        validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * dl, V_NONFINITE_X}}, c.ylab, pb.m, c.s, c.launches);
+        rho = validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * dl, V_NONFINITE_X, dl}}, c.ylab, pb.m, c.s, c.launches);
     } else {
         c.ylab = A.alloc<T>(pb.m);
         PLS_CUDA(cudaMemsetAsync(c.ylab, 0, pb.m * sizeof(T), c.s));
-        validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * dl, V_NONFINITE_X}}, static_cast<const T *>(nullptr), 0, c.s,
-                           c.launches);
+        rho = validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * dl, V_NONFINITE_X, dl}}, static_cast<const T *>(nullptr), 0,
+                                 c.s, c.launches);
     }
     PLS_CUDA(cudaEventRecord(e_h2d, c.s));
     c.Xt = A.alloc<T>(g.dpad * g.mpad);
     launch_transform<T>(Xs, pb.m, dl, c.Xt, g.mpad, g.dpad, c.s, c.launches);
     c.ops = make_ops(c.Xt, g.mpad, c.Xt, g.mpad, g.ld);
     if constexpr (std::is_same<T, double>::value) {
-        c.oz = oz_choose(o.fp64_engine, {c.Xt}, {g.mpad}, g.dpad, dl, A, c.s, c.launches);
+        c.oz = oz_choose(o.fp64_engine, rho, g.mpad, dl);
         if (c.oz) {
             c.ozx = oz_prepare<7, double>(A, c.Xt, g.mpad, g.dpad, dl, true, true, c.s, c.launches);
             oz_set_attrs<double>();
@@ -1032,9 +1084,9 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
         if (o.fp32_engine == PLSSVM_FP32_OZAKI || o.fp32_engine == PLSSVM_FP32_AUTO) {
             // fp32 on the int8 tensor cores (3 digits): a point-major padded copy to split
             const int64_t d8 = round_up(dl, Oz<3>::BK);
-            float *Xp = oz_point_major(A, Xs, pb.m, dl, g.mpad, d8, c.s, c.launches);
-            c.oz = oz_choose_f32(o.fp32_engine, {Xp}, {g.mpad}, d8, dl, A, c.s, c.launches);
+            c.oz = oz_choose_f32(o.fp32_engine, rho, dl);
             if (c.oz) {
+                float *Xp = oz_point_major(A, Xs, pb.m, dl, g.mpad, d8, c.s, c.launches);
                 c.ozx = oz_prepare<3, float>(A, Xp, g.mpad, d8, dl, true, true, c.s, c.launches);
                 oz_set_attrs<float>();
             }
@@ -1059,8 +1111,7 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     std::vector<int2> tl = band_tiles(g, c.oz ? OzC::NSUB : Engine<T>::NSUB);
     c.ntiles = static_cast<int>(tl.size());
     c.tiles = A.alloc<int2>(c.ntiles);
-    PLS_CUDA(cudaMemcpyAsync(c.tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
-    PLS_CUDA(cudaStreamSynchronize(c.s));  // tl goes out of scope
+    upload(c.tiles, tl.data(), tl.size(), c.s);
     oz_build_pairs<T>(c, A, tl, g.band0, g.band1);
     set_smem_attrs<T>();
 }
@@ -1090,8 +1141,7 @@ void configure_product(Ctx<T> &c, Arena &A) {
         std::vector<int2> tl = circulant_tiles(g, c.nsub_eff);
         c.ntiles = static_cast<int>(tl.size());
         c.tiles = A.alloc<int2>(c.ntiles);
-        PLS_CUDA(cudaMemcpyAsync(c.tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
-        PLS_CUDA(cudaStreamSynchronize(c.s));
+        upload(c.tiles, tl.data(), tl.size(), c.s);
         oz_build_pairs<T>(c, A, tl, g.band0, g.band1);
         c.Ypart = A.alloc<T>(static_cast<int64_t>(g.T) * c.nsub_eff * g.mpad);
         c.yfull = A.alloc<T>(g.mpad);
@@ -1108,8 +1158,7 @@ void configure_product(Ctx<T> &c, Arena &A) {
         std::vector<int2> wl = wide_tiles(g.T);
         c.nwtiles = static_cast<int>(wl.size());
         c.wtiles = A.alloc<int2>(c.nwtiles);
-        PLS_CUDA(cudaMemcpyAsync(c.wtiles, wl.data(), wl.size() * sizeof(int2), cudaMemcpyHostToDevice, c.s));
-        PLS_CUDA(cudaStreamSynchronize(c.s));
+        upload(c.wtiles, wl.data(), wl.size(), c.s);
     }
 }
 
@@ -1188,6 +1237,7 @@ double delta_now(const double *hs, int64_t it, bool cgcg) { return cgcg ? hs[S_C
 template <typename T>
 int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, void *b_out, plssvm_stats_t *st) {
     PLS_CUDA(cudaSetDevice(o.device));
+    upload_reset();
     setup_mempool(o.device);
     StreamGuard sg(o.stream);
     Ctx<T> c{};
@@ -1277,7 +1327,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         std::vector<void *> all = comm_peer_exchange_ptr(c.comm, c.p);
         c.npeer = static_cast<int>(all.size());
         c.peer_p = A.alloc<T *>(c.npeer);
-        PLS_CUDA(cudaMemcpyAsync(c.peer_p, all.data(), all.size() * sizeof(void *), cudaMemcpyHostToDevice, c.s));
+        upload(reinterpret_cast<void **>(c.peer_p), all.data(), all.size(), c.s);
     }
     T *scg = nullptr;
     if (cgcg) {
@@ -1518,6 +1568,7 @@ template <typename T>
 int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, const plssvm_options_t &o, void *out,
                        double *t_kernel) {
     PLS_CUDA(cudaSetDevice(o.device));
+    upload_reset();
     setup_mempool(o.device);
     StreamGuard sg(o.stream);
     Ctx<T> c{};
@@ -1533,7 +1584,8 @@ int qtilde_matvec_impl(const Problem &pb, const void *pin, int32_t repeats, cons
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     const bool dev = o.device_pointers != 0;
     PLS_CUDA(cudaMemcpyAsync(c.p, pin, g.m1 * sizeof(T), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
-    validate_inputs<T>(A, {VCheck<T>{c.p, g.m1, V_NONFINITE_P}}, static_cast<const T *>(nullptr), 0, c.s, c.launches);
+    validate_inputs<T>(A, {VCheck<T>{c.p, g.m1, V_NONFINITE_P, 0}}, static_cast<const T *>(nullptr), 0, c.s,
+                       c.launches);
     select_mode<T>(c, o);  // throws E_OOM if CACHED does not fit
     configure_product<T>(c, A);
     double t_pre = 0.0;
@@ -1575,6 +1627,7 @@ template <typename T>
 int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *Zin, int64_t n, const plssvm_options_t &o,
                  void *decision, int32_t *labels, double *t_kernel) {
     PLS_CUDA(cudaSetDevice(o.device));
+    upload_reset();
     setup_mempool(o.device);
     StreamGuard sg(o.stream);
     cudaStream_t s = sg.s;
@@ -1593,9 +1646,9 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     const T *Xs = stage_input<T>(A, pb.X, m * d, dev, s);
     const T *Zs = stage_input<T>(A, Zin, n * d, dev, s);
     const T *al = stage_input<T>(A, alpha_in, m, dev, s);
-    validate_inputs<T>(A, {VCheck<T>{Xs, m * d, V_NONFINITE_X}, VCheck<T>{Zs, n * d, V_NONFINITE_Z},
-                           VCheck<T>{al, m, V_NONFINITE_ALPHA}},
-                       static_cast<const T *>(nullptr), 0, s, launches);
+    const float rho = validate_inputs<T>(A, {VCheck<T>{Xs, m * d, V_NONFINITE_X, d}, VCheck<T>{Zs, n * d, V_NONFINITE_Z, d},
+                                             VCheck<T>{al, m, V_NONFINITE_ALPHA, 0}},
+                                         static_cast<const T *>(nullptr), 0, s, launches);
     if (pb.kernel == LINEAR && o.linear_w) {
         // f(z) = <w, z> + b with w = sum_i alpha_i x_i (Eq. 15): O((m + n) d)
         const int64_t rpb = std::max<int64_t>(1, ceil_div(m, 4 * 148));
@@ -1640,12 +1693,12 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     bool oz64 = false;  // (the name: the Ozaki engine of either precision)
     const T *Xoz = nullptr, *Zoz = nullptr;  // fp32: point-major padded copies for the split
     if constexpr (std::is_same<T, double>::value) {
-        oz64 = oz_choose(o.fp64_engine, {Zl, Xl}, {zrows, xrows}, dpad, d, A, s, launches);
+        oz64 = oz_choose(o.fp64_engine, rho, std::max(zrows, xrows), d);
     } else if (o.fp32_engine == PLSSVM_FP32_OZAKI || o.fp32_engine == PLSSVM_FP32_AUTO) {
         const int64_t d8 = round_up(d, Oz<3>::BK);
         Zoz = oz_point_major(A, Zs, n, d, npad, d8, s, launches);
         Xoz = oz_point_major(A, Xs, m, d, mpad, d8, s, launches);
-        oz64 = oz_choose_f32(o.fp32_engine, {Zoz, Xoz}, {npad, mpad}, d8, d, A, s, launches);
+        oz64 = oz_choose_f32(o.fp32_engine, rho, d);
     }
     const bool tc = std::is_same<T, float>::value && !oz64 && o.fp32_engine != PLSSVM_FP32_FFMA;
     const int tilesI = static_cast<int>(npad / kTile),
@@ -1741,6 +1794,17 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
 }
 
 }  // namespace
+
+#ifdef PLSSVM_OZ_EXPERIMENTS
+int exp_oz_profile(unsigned long long *out, int reset) {
+    if (out) PLS_CUDA(cudaMemcpyFromSymbol(out, g_oz_prof, sizeof(g_oz_prof)));
+    if (reset) {
+        static unsigned long long zero[160][8] = {};
+        PLS_CUDA(cudaMemcpyToSymbol(g_oz_prof, zero, sizeof(zero)));
+    }
+    return PLSSVM_OK;
+}
+#endif
 
 int train(const Problem &pb, const plssvm_options_t &o, void *alpha, void *b, plssvm_stats_t *st) {
     return pb.dtype == PLSSVM_F32 ? train_impl<float>(pb, o, alpha, b, st) : train_impl<double>(pb, o, alpha, b, st);

@@ -31,6 +31,10 @@ int predict(const Problem &pb, const void *alpha, double b, const void *Z, int64
 int qtilde_matvec(const Problem &pb, const void *p, int32_t repeats, const plssvm_options_t &o, void *out,
                   double *t_kernel);
 
+#ifdef PLSSVM_OZ_EXPERIMENTS
+int exp_oz_profile(unsigned long long *out, int reset);
+#endif
+
 // multi.cu: the num_gpus mode (one host thread per device, NCCL or PEER transport)
 int resolve_num_gpus(const plssvm_options_t &o);
 int train_multi(const Problem &pb, const plssvm_options_t &o, int P, void *alpha, void *b, plssvm_stats_t *st);

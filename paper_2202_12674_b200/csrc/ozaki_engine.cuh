@@ -1,25 +1,31 @@
 // ozaki_engine.cuh -- fp64 pairwise contraction on the int8 tensor cores (tcgen05 kind::i8) by
-// exact digit splitting (Ozaki scheme): the fp64-accurate S = X_I X_J^T of the implicit Q~p
+// int8 digit splitting (Ozaki scheme): the fp64-accurate S = X_I X_J^T of the implicit Q~p
 // (Eq. 16), the cached-mode precompute and the predict (Eq. 10).
 //
 // Why: a B200 runs fp64 at 37 TFLOP/s (DMMA, profiles/r01_fp64_peak.txt) but int8 MMAs at
-// ~4.5 POPS.  Each point x_i is written EXACTLY as a 54-bit integer N_i = x_i 2^{54-E_i}
-// (E_i = the row's exponent, max_k |x_ik| < 2^{E_i}; exact because x's ulp is >= 2^{E_i-53})
-// in 7 BALANCED base-256 digits:
+// ~4.5 POPS.  Each point x_i is mapped to the integer vector N_i = rn(x_i 2^{54-E_i}) (E_i the
+// row's exponent: 2^{E_i-1} <= ||x_i||_inf < 2^{E_i}), a FIXED-POINT representation relative to the
+// row maximum: features with |x_ik| >= 2^{E_i-2} are exact, smaller ones are rounded to the grid
+// 2^{E_i-54} (|error| <= 2^{E_i-55}).  N_i is written in 7 BALANCED base-256 digits,
 //     N_i = sum_{a=0..6} D_a 256^{6-a},   D_a in [-128, 127]  (int8; |N| < 2^54 < the 7-digit range)
-// so  x_i . x_j = 2^{E_i+E_j-12} * sum_{l=0..12} 2^{-8l} acc_l,   acc_l = sum_{a+b=l} D_a(x_i) . D_b(x_j).
-// Levels l <= 6 are kept (28 digit pairs); the dropped ones are < 7 * 2^{-56} relative to
-// 2^{E_i+E_j} each (8 bits per digit: an 8 x 7-bit split needed 36 pairs for the same bound).
-// Every acc_l is an EXACT int32 sum (|acc_l| <= 7 d 2^14 < 2^31 for d <= 16384), accumulated in
-// TMEM by tcgen05.mma.kind::i8; the combination runs in fp64 (Horner over l, one rounding per
-// level), so the result is an fp64 dot product with a different (shorter) rounding history,
-// not a lower-precision one.
+// so  x^_i . x^_j = 2^{E_i+E_j-12} * sum_{l=0..12} 2^{-8l} acc_l,   acc_l = sum_{a+b=l} D_a(x_i) . D_b(x_j).
+// Levels l <= 6 are kept (28 digit pairs).  Every acc_l is an EXACT int32 sum (|acc_l| <= 7 d 2^14 <
+// 2^31 for d <= 16384) accumulated in TMEM by tcgen05.mma.kind::i8; the kept levels are combined in
+// exact int64 (V: levels 0-3, W: levels 4-6) and converted with ONE fp64 rounding.  Error of one
+// inner product s = x_i.x_j (DESIGN.md §5 derives it):
+//     |s~ - s| <= u |s| + 13.04 d u ||x_i||_inf ||x_j||_inf          (u = 2^-53)
+// = input rounding (<= d u ||.||inf ||.||inf) + dropped levels 7..12 (<= 12.04 d u ||.||inf ||.||inf)
+// + the final rounding.  Against the textbook fp64 dot-product bound in its Cauchy-Schwarz form,
+// gamma_d ||x_i||_2 ||x_j||_2 ~ d u ||x_i||_2 ||x_j||_2, this is no larger whenever
+// 13.04 rho_i rho_j <= d with rho = ||x||_inf / rms(x) -- AUTO's rule (driver.cu oz_choose).  It is
+// NOT the componentwise bound d u sum_k |x_ik x_jk| an fp64 dot satisfies: inner products that are
+// small against ||x_i||_inf ||x_j||_inf (orthogonal spikes) lose relative accuracy.
 //
 // Tile = 128 x 128 per CTA, computed by CTA pairs as 256 x 128 UMMAs (cta_group::2, below).
 // The 7 level accumulators of a tile need 7 x 128 int32
 // TMEM columns, more than the 512 available, so a tile runs in TWO PASSES over the features:
-// pass 0 accumulates levels 4-6 (18 digit pairs, digit planes 0-6), pass 1 levels 0-3 (10
-// pairs, planes 0-3), each in <= 4 x 128 TMEM columns.  N = 128 halves the shared-memory operand
+// pass 0 accumulates levels 0-3 (10 digit pairs, digit planes 0-3), pass 1 levels 4-6 (18
+// pairs, planes 0-6), each in <= 4 x 128 TMEM columns.  N = 128 halves the shared-memory operand
 // bytes per MMA cycle of an N = 64 tile (the SS-mode UMMA reads A and B from smem each time:
 // 128 B/clk at N = 128 = the smem bandwidth, 192 B/clk at N = 64 -- measured: tc pipe 84 %
 // busy, imma 46 % with 128 x 64 tiles), at the same L2 traffic per output element.
@@ -31,9 +37,10 @@
 //                       the pass
 //   warps 2-3         : idle (warpgroup 0 gives its registers to the epilogue: setmaxnreg 40 / 232)
 //   warps 4-11        : epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows), columns
-//                       64((w-4)/4).. of every level (tcgen05.ld 32x32b.x8), Horner-combines them
-//                       in fp64 (pass 0 -> w in fp32; pass 1 -> the 64 contractions v + 2^-32 w in
-//                       registers), releases the accumulators after each pass, and only then runs
+//                       64((w-4)/4).. of every level (tcgen05.ld 32x32b.x8), combines the levels
+//                       in exact int64 (pass 0 -> V, held exactly as fp64; pass 1 -> W and the 64
+//                       contractions (V + 2^-24 W) sc_i sc_j with one rounding, in registers),
+//                       releases the accumulators after each pass, and only then runs
 //                       the kernel function / Eq. 16 corrections and the row / column contributions
 //                       -- overlapped with the next pair-tile's MMAs.
 // Slot conventions: those of k_matvec_implicit with 128-wide column blocks (NSUB = 1).
@@ -46,7 +53,23 @@ namespace plssvm {
 
 enum OzMode : int { OZ_MATVEC = 0, OZ_PRECOMPUTE = 1, OZ_PREDICT = 2 };
 
-// S = 7 (fp64 engine): pass 0 = levels 4..6 (all 7 planes), pass 1 = levels 0..3 (planes 0..3).
+// Cycle accounting of k_tile_ozaki (experiment build only, -DPLSSVM_OZ_EXPERIMENTS; read back by
+// tools/oz_profile.py through plssvm_exp_oz_profile): per CTA, clock64 cycles spent by
+//   [0] the MMA thread waiting for the epilogue to drain the accumulators (tempty)
+//   [1] the MMA thread waiting for TMA stages (full)        [2] the MMA thread's whole loop
+//   [3] the TMA thread waiting for free stages (empty)
+//   [4] epilogue warp 4 waiting for accumulators (tfull)    [5] its pass-0 drain   [6] its pass-1 drain
+//   [7] its fp64 work after the release (kernel value, Eq. 16, row / column sums)
+#ifdef PLSSVM_OZ_EXPERIMENTS
+__device__ unsigned long long g_oz_prof[160][8];
+#define OZ_PROF_T0(v) const long long v = clock64()
+#define OZ_PROF_ADD(slot, v) atomicAdd(&g_oz_prof[blockIdx.x][slot], static_cast<unsigned long long>(clock64() - (v)))
+#else
+#define OZ_PROF_T0(v)
+#define OZ_PROF_ADD(slot, v)
+#endif
+
+// S = 7 (fp64 engine): pass 0 = levels 0..3 (planes 0..3), pass 1 = levels 4..6 (all 7 planes).
 // S = 3 (fp32 engine, plssvm.h PLSSVM_FP32_OZAKI): one pass, levels 0..2 (6 digit pairs, planes
 // 0..2) -- x rounded to 22 bits below its row maximum, i.e. the fp32 products of the inputs to
 // ~2^-22 relative to ||x_i||_inf ||x_j||_inf (the 3xTF32 split carries 21 + 21 bits).
@@ -79,7 +102,7 @@ struct Oz {
 
 // Digit planes a pass loads (S = 7: 7 then 4; S = 3: 3).
 template <int S>
-__host__ __device__ constexpr int oz_planes(int pass) { return (S == 7 && pass == 1) ? Oz<S>::LV : S; }
+__host__ __device__ constexpr int oz_planes(int pass) { return (S == 7 && pass == 0) ? Oz<S>::LV : S; }
 
 // K-major operand in 32-byte swizzle atoms (8 rows x 32 B): LBO 1 (unused), SBO = 256 B, type 6.
 __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
@@ -228,8 +251,9 @@ __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpa
     }
 }
 
-// Exact digit split of the point-major padded fp64 array Xp[rows][dpad] (rows a multiple of
-// 128) into S balanced base-256 int8 digit planes (plane 0 = most significant), stored
+// Digit split of the point-major padded array Xp[rows][dpad] (rows a multiple of 128): each row is
+// rounded to the fixed-point grid 2^{E_i - BITS} of its maximum (exact for |x| >= 2^{E_i-2} with S = 7)
+// and written in S balanced base-256 int8 digit planes (plane 0 = most significant), stored
 // PRE-SWIZZLED as the shared-memory images the UMMA reads:
 //   DA[rows/128][nk][S][128 x 32 B]  (row-operand role: 128-point blocks)
 //   DB[rows/64 ][nk][S][ 64 x 32 B]  (column-operand role: one CTA's half of a 2-SM B tile)
@@ -238,9 +262,10 @@ __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpa
 // operand, moved by TMA in 128-byte rows with no swizzle (4x fewer, 4x larger requests than
 // a 32-byte-row box: the tile kernel was feed-bound with them).  Either pointer may be null.
 // Row scales sc_i = 2^{E_i - SC_SHIFT} (S = 7: x_i . x_j = sc_i sc_j sum_l 2^{-8l} acc_l;
-// S = 3: sc_i sc_j (acc_0 2^16 + acc_1 2^8 + acc_2)).  S = 7 splits the fp64 value exactly
-// (N = x 2^{54-E}, |N| < 2^54); S = 3 rounds the (fp32) value to N = rint(x 2^{22-E}), |N| <= 2^22,
-// which three balanced digits hold.  One warp per row; 4 features per lane per step.
+// S = 3: sc_i sc_j (acc_0 2^16 + acc_1 2^8 + acc_2)).  S = 7: N = rn(x 2^{54-E}), |N| < 2^54 (exact
+// for the features within a factor 4 of the row maximum, rounded to 2^{E-54} below); S = 3 rounds the
+// (fp32) value to N = rint(x 2^{22-E}), |N| <= 2^22, which three balanced digits hold.  One warp per
+// row; 4 features per lane per step.
 template <int S, typename TIN>
 __global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t dpad8,
                               int8_t *__restrict__ DA, int8_t *__restrict__ DB, double *__restrict__ sc) {
@@ -262,7 +287,7 @@ __global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t 
     for (int64_t k0 = 4 * lane; k0 < dpad8; k0 += 128) {
         long long N[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v)  // S = 7: |N| < 2^54, exact (x's ulp >= 2^{E-53}); S = 3: rounded
+        for (int v = 0; v < 4; ++v)  // |N| < 2^{BITS}; exact when x's ulp >= 2^{E-BITS}, else rounded to nearest
             N[v] = (k0 + v < dpad) ? __double2ll_rn(ldexp(static_cast<double>(x[k0 + v]), Oz<S>::BITS - E)) : 0ll;
         const int64_t kb = k0 >> 5;
         const int c = static_cast<int>(k0 & 31);
@@ -443,7 +468,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     const int np = oz_planes<S>(pass);
                     for (int kb = 0; kb < nk; ++kb, ++g) {
                         const uint32_t s = g % O::STAGES;
-                        if (g >= O::STAGES) mbar_wait(&empty[s], ((g / O::STAGES) - 1) & 1);
+                        if (g >= O::STAGES) {
+                            OZ_PROF_T0(t0);
+                            mbar_wait(&empty[s], ((g / O::STAGES) - 1) & 1);
+                            OZ_PROF_ADD(3, t0);
+                        }
                         unsigned char *st = ring + size_t(s) * O::STAGE_BYTES;
                         if (dbg & 2) {  // experiment: no data movement
                             if (leader) mbar_arrive(&full[s]);
@@ -464,22 +493,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(O::CTRL_REGS));
         if (leader && lane == 0) {  // ---- MMA issuer (leader only): level l = a + b
             uint32_t g = 0, e = 0;  // e: accumulator events (two per pair-tile)
+            OZ_PROF_T0(tloop);
             for (int t = pair; t < ntiles; t += npairs) {
 #pragma unroll 1
                 for (int pass = 0; pass < O::NPASS; ++pass, ++e) {
                     if (e > 0) {  // both CTAs' epilogues have drained the previous pass
+                        OZ_PROF_T0(t0);
                         mbar_wait(tempty, (e - 1) & 1);
+                        OZ_PROF_ADD(0, t0);
                         asm volatile("tcgen05.fence::after_thread_sync;");
                     }
                     const int np = oz_planes<S>(pass);
                     for (int kb = 0; kb < nk; ++kb, ++g) {
                         const uint32_t s = g % O::STAGES;
-                        mbar_wait(&full[s], (g / O::STAGES) & 1);
+                        {
+                            OZ_PROF_T0(t0);
+                            mbar_wait(&full[s], (g / O::STAGES) & 1);
+                            OZ_PROF_ADD(1, t0);
+                        }
                         asm volatile("tcgen05.fence::after_thread_sync;");
                         const uint32_t sa = smem_addr(ring + size_t(s) * O::STAGE_BYTES);
                         const uint32_t sb = sa + np * O::PLANE;
                         if (dbg & 4) {  // experiment: data movement only
-                        } else if (S == 7 && pass == 0) {  // levels 4..6 (18 pairs), TMEM column block l - 4
+                        } else if (S == 7 && pass == 1) {  // levels 4..6 (18 pairs), TMEM column block l - 4
 #pragma unroll
                             for (int a = 0; a < S; ++a)
 #pragma unroll
@@ -503,6 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     umma_commit_2sm_mc(tfull);  // this pass's accumulators ready in both CTAs
                 }
             }
+            OZ_PROF_ADD(2, tloop);
         }
     } else if (warp < 4) {  // idle warps 2-3
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(O::CTRL_REGS));
@@ -553,15 +590,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");  // B1
 
-            // Pass 0 (levels 4-6) -> the low-order part W = 2^16 sum_{l<3} 2^{-8l} acc_{4+l} (exact
-            // int64), kept in fp32: it enters 2^{-48} below V, so its rounding is ~2^{-56}
-            // relative to the leading digit products, and 64 columns cost 64 registers.  Pass 1
-            // (levels 0-3): V = 2^24 sum_{l<4} 2^{-8l} acc_l (exact int64) + 2^{-24} W in fp64 for
-            // all 64 columns (registers), accumulators released, then the Q~ entry / kernel value
-            // and its row and column contributions (under the next pair-tile's MMAs).
+            // S = 7, pass 0 (levels 0-3): V = 2^24 sum_{l<4} 2^{-8l} acc_l, an exact int64 (|V| < d 2^38 <
+            // 2^53) held EXACTLY as fp64 in sv (64 columns in registers), accumulators released.  Pass 1
+            // (levels 4-6): W = 2^16 sum_{l<3} 2^{-8l} acc_{4+l}, exact int64 -> exact fp64, and the
+            // contraction is ONE fp64 rounding of the kept digit products: sv = (V + 2^-24 W) sc_i sc_j
+            // (DESIGN.md §5 error bound).  Then the accumulators are released and the Q~ entry / kernel
+            // value and its row and column contributions run under the next pair-tile's MMAs.
+            // S = 3: the single pass, V = acc_0 2^16 + acc_1 2^8 + acc_2.
             const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(grp * 64);
             const bool mirrored = used && (MODE != OZ_PREDICT) && (I != J) && (J >= band0) && (J < band1);
-            float wl[64];
             T rs = T(0);
             T *qdst = nullptr, *qmir = nullptr;
             if constexpr (MODE == OZ_PRECOMPUTE) {
@@ -572,9 +609,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     if (T_tiles >= 0 && mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
                 }
             }
-            // Pass 0 of S = 7: drain levels 4-6 into wl (fp32), release the accumulators.
+            T sv[64];
+            const bool prof = warp == 4 && lane == 0;
+            (void)prof;
             if constexpr (S == 7) {
-            mbar_wait(tfull, e & 1);
+                {
+                    OZ_PROF_T0(t0);
+                    mbar_wait(tfull, e & 1);
+                    if (prof) OZ_PROF_ADD(4, t0);
+                }
+                OZ_PROF_T0(tdr0);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                ++e;
+                if (!(dbg & 1)) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        uint32_t r0[8], r1[8], r2[8], r3[8];
+                        tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
+                        tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
+                        tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
+                        tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const long long V = (lv(r0[j]) << 24) + (lv(r1[j]) << 16) + (lv(r2[j]) << 8) + lv(r3[j]);
+                            sv[c * 8 + j] = i64_to_f64_exact(V);
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty0);  // the MMA may start pass 1
+                if (prof) OZ_PROF_ADD(5, tdr0);
+            }
+            {
+                OZ_PROF_T0(t0);
+                mbar_wait(tfull, e & 1);
+                if (prof) OZ_PROF_ADD(4, t0);
+            }
+            OZ_PROF_T0(tdr1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             ++e;
             if (!(dbg & 1)) {
@@ -586,61 +659,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {  // W = acc_4 2^16 + acc_5 2^8 + acc_6 (exact), rounded to fp32
-                        const long long W = (lv(r0[j]) << 16) + (lv(r1[j]) << 8) + lv(r2[j]);
-                        wl[c * 8 + j] = static_cast<float>(i64_to_f64_exact(W));
-                    }
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty0);  // the MMA may start pass 1
-            }
-            // Pass 1: drain levels 0-3 and finish the contraction sv (fp64, 64 columns in registers),
-            // then release the accumulators BEFORE the kernel function / Eq. 16 / row and column
-            // sums, so the MMAs of the next pair-tile's pass 0 overlap this fp64 work (the epilogue
-            // is fp64-pipe bound: ~40 DP ops per entry, ~20 % of a C1 tile when serialised).
-            mbar_wait(tfull, e & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            ++e;
-            T sv[64];
-            if (S == 3 && !(dbg & 1)) {  // the single pass of S = 3: V = acc_0 2^16 + acc_1 2^8 + acc_2
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t r0[8], r1[8], r2[8];
-                    tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
-                    tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
-                    tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
-                    tmem_ld_wait();
-#pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const long long V = (lv(r0[j]) << 16) + (lv(r1[j]) << 8) + lv(r2[j]);
-                        sv[c * 8 + j] = static_cast<T>(i64_to_f64_exact(V) * (sci * colsc[grp * 64 + c * 8 + j]));
-                    }
-                }
-            } else if (S == 7 && !(dbg & 1)) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t r0[8], r1[8], r2[8], r3[8];
-                    tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
-                    tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
-                    tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
-                    tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        // x_i.x_j = sc_i sc_j (V + 2^-24 W) 2^-24: level 4 is 2^-32 below level 0, W
-                        // carries 2^16 of it (the 2^-24 of V sits in sci)
-                        const long long V = (lv(r0[j]) << 24) + (lv(r1[j]) << 16) + (lv(r2[j]) << 8) + lv(r3[j]);
                         const int lc = grp * 64 + c * 8 + j;
-                        sv[c * 8 + j] = static_cast<T>(fma(static_cast<double>(wl[c * 8 + j]), 0x1p-24,
-                                                           i64_to_f64_exact(V)) * (sci * colsc[lc]));
+                        if constexpr (S == 7) {
+                            // x_i.x_j = sc_i sc_j (V + 2^-24 W) 2^-24 (level 4 is 2^-32 below level 0, W
+                            // carries 2^16 of it; the other 2^-24 sits in sci): one rounding
+                            const long long W = (lv(r0[j]) << 16) + (lv(r1[j]) << 8) + lv(r2[j]);
+                            sv[c * 8 + j] = fma(i64_to_f64_exact(W), 0x1p-24, sv[c * 8 + j]) * (sci * colsc[lc]);
+                        } else {
+                            const long long V = (lv(r0[j]) << 16) + (lv(r1[j]) << 8) + lv(r2[j]);
+                            sv[c * 8 + j] = static_cast<T>(i64_to_f64_exact(V) * (sci * colsc[lc]));
+                        }
                     }
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty0);  // the next pair-tile's MMAs may start
+            if (prof) OZ_PROF_ADD(6, tdr1);
+            OZ_PROF_T0(twork);
             if (!(dbg & 1)) {
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {  // 8-column chunks of this thread's 64 columns
@@ -735,6 +772,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 if (used && et < kTile) Ypart[int64_t(J) * band_rows + row0 + et] = redr[et] + redr[kTile + et];
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");  // B3: smem partials / column data reusable
+            if (prof) OZ_PROF_ADD(7, twork);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");

@@ -3,11 +3,12 @@ OZAKI (int8 tensor cores on an exact 7-digit split of every point, 2-SM UMMA) an
 tensor cores), plus the AUTO rule, against the CPU oracle.  Bars as in test_gpu_parity.py:
 product <= 1e-12 norm-wise and |y_i - y*_i| <= 1e-12 (|Q~||p|)_i element-wise; alpha, b <= 1e-7.
 
-The Ozaki error bound is d 2^-56 ||x_i||_inf ||x_j||_inf per inner product, so the cases below
-stress what the row-max scaling could get wrong: ragged shapes around the 32-feature slab and
+The Ozaki error bound is u|s| + 13.04 d u ||x_i||_inf ||x_j||_inf per inner product s (u = 2^-53,
+DESIGN.md §5), so the cases below stress what the row-max scaling could get wrong: ragged shapes around the 32-feature slab and
 the 128/256-point (pair-)tile edges, magnitudes far from 1, exact-integer data, zero rows,
-duplicated points, odd band / pair ends on several ranks (test_gpu_multirank.py), and the AUTO
-switch to DMMA for peaked rows."""
+duplicated points, odd band / pair ends on several ranks (test_gpu_multirank.py), peaked rows across
+the band peak / RMS = 12 .. 63 forced onto the int8 engine, the bound entry by entry, and the AUTO
+rule (OZAKI iff 13.04 rho^2 <= d)."""
 import numpy as np
 import pytest
 
@@ -88,39 +89,97 @@ def test_zero_rows_and_duplicates(engine):
         check(X, p, kernel, 1.0 / d, engine=engine)
 
 
-def test_auto_picks_dmma_for_peaked_rows_and_stays_exact():
-    rng = np.random.default_rng(4)
-    m, d = 400, 64
+def peaked(rng, m, d, rho, sigma_scale=1.0, spike_col=None):
+    """m rows of spike + noise with max_k |x_k| / rms_k(x_k) = rho exactly: the spike s = sigma_scale sits
+    in column spike_col(i) (default: random, so different rows' spikes are mostly orthogonal)."""
+    X = np.empty((m, d))
+    for i in range(m):
+        s = sigma_scale * (1.0 + rng.random())
+        sig = s * np.sqrt(max(d / rho**2 - 1.0, 0.0) / (d - 1))
+        x = rng.standard_normal(d)
+        x *= sig / max(np.sqrt(np.mean(x**2)), 1e-300)
+        k = rng.integers(0, d) if spike_col is None else spike_col(i)
+        x = np.clip(x, -0.99 * s, 0.99 * s)
+        x[k] = s if rng.random() < 0.5 else -s
+        ss = np.sum(x**2) - s * s  # rescale the noise so that rho is exact
+        want = s * s * (d / rho**2) - s * s
+        if ss > 0 and want > 0:
+            mask = np.arange(d) != k
+            x[mask] *= np.sqrt(want / ss)
+        X[i] = x
+    return X
+
+
+def row_peak(X):
+    return np.max(np.abs(X).max(1) / np.sqrt((X**2).mean(1)))
+
+
+@pytest.mark.parametrize("rho", [12, 24, 32, 48, 63])
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_ozaki_forced_across_the_peak_band(rho, kernel):
+    """rows with peak / RMS = rho (spike + small noise, spikes of different rows mostly
+    orthogonal), FORCED onto the int8 engine: the product meets the parity bars against the oracle
+    (1e-12 norm- and element-wise vs |Q~||p|), in implicit and cached mode; and the model trained on
+    them meets the 1e-7 bar.  d = 4096 so that rho up to 63 is possible (rho <= sqrt(d))."""
+    rng = np.random.default_rng(1000 * rho + kernel)
+    m, d = 400, 4096
+    X = peaked(rng, m, d, rho)
+    assert abs(row_peak(X) - rho) <= 1e-6 * rho
+    p = rng.standard_normal(m - 1)
+    gamma = 1.0 / d if kernel != pl.LINEAR else 1.0
+    for mode in (pl.MODE_IMPLICIT, pl.MODE_CACHED):
+        check(X, p, kernel, gamma, engine=pl.FP64_OZAKI, mode=mode)
     y = np.where(rng.random(m) < 0.5, 1.0, -1.0)
     y[0], y[1] = 1.0, -1.0
-    X = rng.standard_normal((m, d))
-    _, _, st, stats = pl.plssvm_train_ex(X, y, pl.RBF, 1.0 / d, eps=1e-10)
-    assert st == 0 and stats.fp64_engine_used == pl.FP64_OZAKI
-    Xp = X.copy()
-    Xp[17, 3] = 1e4  # one feature 1e4 x the row's scale: row peak ~ 1e4 / sqrt(1e8 / 64) = 8
-    Xp[18, :] = 1e-3
-    Xp[18, 9] = 10.0  # peak 10 / sqrt(100 / 64) = 8: still OZAKI
-    _, _, st, stats = pl.plssvm_train_ex(Xp, y, pl.RBF, 1.0 / d, eps=1e-10)
-    assert stats.fp64_engine_used == pl.FP64_OZAKI
-    Xq = X.copy()
-    Xq[21, :] = 1e-6
-    Xq[21, 0] = 1.0  # one spike among tiny features: peak = sqrt(64) = 8 -> OZAKI
-    Xq[22, :] = 1e-9
-    Xq[22, 1:3] = 1.0  # two spikes: peak sqrt(64 / 2) = 5.7
-    Xr = np.zeros((m, d))
-    Xr[:] = rng.standard_normal((m, d)) * 1e-6
-    Xr[:, 0] = rng.standard_normal(m) * 1e3  # every row peaks ~ 8 (one dominant feature of 64)
-    for Xc in (Xq, Xr):
-        _, _, st, stats = pl.plssvm_train_ex(Xc, y, pl.LINEAR, 1.0, eps=1e-10)
-        assert stats.fp64_engine_used == pl.FP64_OZAKI
-    # a row whose peak exceeds 64 x its RMS needs more than ~ d = 4096 features of mass 1e-4
-    Xw = rng.standard_normal((m, 8192)) * 1e-4
-    Xw[:, 0] += np.where(np.arange(m) == 5, 1.0, 0.0)  # row 5: peak 1 / sqrt((1 + 8191e-8) / 8192) ~ 90
-    yw = y
-    a_auto, b_auto, st, stats = pl.plssvm_train_ex(Xw, yw, pl.LINEAR, 1.0, eps=1e-10)
-    assert st == 0 and stats.fp64_engine_used == pl.FP64_DMMA
-    a_ref, b_ref, _, _ = oracle.train(Xw, yw, pl.LINEAR, 1.0, eps=1e-10)
-    assert rel(a_auto, a_ref) <= 1e-7
+    a_ref, b_ref, _, st_ref = oracle.train(X, y, kernel, gamma, 3, 0.5, 1.0, 1e-10)
+    a, b, st, s = pl.plssvm_train_ex(X, y, kernel, gamma, 3, 0.5, 1.0, 1e-10,
+                                     opts=pl.options(fp64_engine=pl.FP64_OZAKI, mode=pl.MODE_IMPLICIT))
+    assert st == st_ref == 0 and s.fp64_engine_used == pl.FP64_OZAKI
+    assert rel(a, a_ref) <= 1e-7 and abs(b - b_ref) <= 1e-7 * max(abs(b_ref), np.abs(a_ref).max())
+
+
+@pytest.mark.parametrize("rho", [8, 32, 63])
+def test_ozaki_entries_within_the_derived_bound(rho):
+    """Per-entry check of the documented bound (ozaki_engine.cuh): with p = e_j the product
+    is column j of Q~, so Q~_ij = k_ij - q_i - q_j + Q_mm comes out entry by entry; for the linear kernel
+    |Q~gpu_ij - Q~_ij| <= 13.04 d u ||x_i||inf ||x_j||inf (the contraction) + the fp64 rounding of Eq. 16's
+    four terms and of the oracle's own dot products (4 u (|k_ij| + |q_i| + |q_j| + Q_mm) + d u sum|x x|)."""
+    rng = np.random.default_rng(77 + rho)
+    m, d = 300, 4096
+    X = peaked(rng, m, d, rho)
+    u = 2.0**-53
+    Qt = oracle.qtilde(X, pl.LINEAR, 1.0, 3, 0.0, 1e300)  # C = 1e300: the 1/C terms vanish
+    q, Qmm = oracle.q_cache(X, pl.LINEAR, C=1e300)
+    inf = np.abs(X).max(1)
+    absdot = np.abs(X) @ np.abs(X).T
+    for j in (0, 7, 150, m - 2):
+        e = np.zeros(m - 1)
+        e[j] = 1.0
+        col, _ = pl.plssvm_qtilde_matvec(X, e, pl.LINEAR, 1.0, 3, 0.0, 1e300,
+                                         opts=pl.options(mode=pl.MODE_IMPLICIT, fp64_engine=pl.FP64_OZAKI))
+        k = Qt[:, j] + q + q[j] - Qmm
+        bound = (13.04 * d * u * inf[:-1] * inf[j] + 4 * u * (np.abs(k) + np.abs(q) + abs(q[j]) + Qmm)
+                 + d * u * absdot[:-1, j])
+        err = np.abs(col - Qt[:, j])
+        assert np.all(err <= bound), (j, np.max(err / bound))
+
+
+def test_auto_rule_follows_the_bound_and_stays_exact():
+    """AUTO takes OZAKI iff 13.04 rho^2 <= d (driver.cu oz_choose): on each side of the threshold the engine
+    choice is as the rule says and the trained model meets the 1e-7 bar."""
+    rng = np.random.default_rng(4)
+    m, d = 400, 1024  # threshold rho* = sqrt(1024 / 13.04) = 8.86
+    y = np.where(rng.random(m) < 0.5, 1.0, -1.0)
+    y[0], y[1] = 1.0, -1.0
+    for rho, want in ((6.0, pl.FP64_OZAKI), (8.5, pl.FP64_OZAKI), (9.5, pl.FP64_DMMA), (30.0, pl.FP64_DMMA)):
+        X = rng.standard_normal((m, d))
+        X[17] = peaked(rng, 1, d, rho)[0]  # the N(0,1) rows peak at ~4.5: this row decides
+        rho_max = row_peak(X)
+        a, b, st, s = pl.plssvm_train_ex(X, y, pl.RBF, 1.0 / d, eps=1e-10)
+        assert st == 0 and s.fp64_engine_used == want, (rho, rho_max, s.fp64_engine_used)
+        assert (13.04 * rho_max**2 <= d) == (want == pl.FP64_OZAKI)
+        a_ref, b_ref, _, _ = oracle.train(X, y, pl.RBF, 1.0 / d, eps=1e-10)
+        assert rel(a, a_ref) <= 1e-7 and abs(b - b_ref) <= 1e-7 * max(abs(b_ref), np.abs(a_ref).max())
 
 
 @pytest.mark.parametrize("engine", ENGINES)
@@ -202,11 +261,12 @@ def test_auto_picks_dmma_for_tiny_problems():
     """AUTO: at most 384 padded points -> DMMA (the persistent int8 kernel's fixed cost dominates);
     both engines stay within the parity bar there."""
     rng = np.random.default_rng(12)
+    d = 512  # N(0,1) rows peak at rho ~ 4.3: 13.04 rho^2 < d, so only the size rule decides
     for m, want in ((256, pl.FP64_DMMA), (300, pl.FP64_DMMA), (385, pl.FP64_OZAKI)):
-        X = rng.standard_normal((m, 20))
+        X = rng.standard_normal((m, d))
         y = np.where(rng.random(m) < 0.5, 1.0, -1.0)
         y[0], y[1] = 1.0, -1.0
-        a, b, st, stats = pl.plssvm_train_ex(X, y, pl.RBF, 0.05, eps=1e-10)
+        a, b, st, stats = pl.plssvm_train_ex(X, y, pl.RBF, 1.0 / d, eps=1e-10)
         assert st == 0 and stats.fp64_engine_used == want, (m, stats.fp64_engine_used)
-        a_ref, _, _, _ = oracle.train(X, y, pl.RBF, 0.05, eps=1e-10)
+        a_ref, _, _, _ = oracle.train(X, y, pl.RBF, 1.0 / d, eps=1e-10)
         assert rel(a, a_ref) <= 1e-7
