@@ -285,8 +285,9 @@ def _sampled_rows(m, rng, k=48):
 
 
 def test_c3_full_size_fp32_tensor_core_sampled_rows():
-    """C3 (2^15 x 2^11 poly-3 fp32) at full size on the default tcgen05 3xTF32 engine, implicit and
-    cached: sampled rows of Q~p against the oracle's rows (fp32-rounded inputs in fp64)."""
+    """C3 (2^15 x 2^11 poly-3 fp32) at full size on the default engine (AUTO -> the int8 fp32 engine on
+    these data), implicit and cached: sampled rows of Q~p against the oracle's rows (fp32-rounded
+    inputs in fp64)."""
     cfg = synth.configs()["C3"]
     X, y, Z, yz = synth.config_data(cfg, n_test=0)
     rng = np.random.default_rng(33)
