@@ -55,8 +55,11 @@ def build_cli(force: bool = False) -> str:
     return CLI
 
 
-def build(force: bool = False, verbose: bool = False, variant: str = "product") -> str:
-    lib = LIB if variant == "product" else LIB_EXP
+def build(force: bool = False, verbose: bool = False, variant: str = "product", out: str | None = None,
+          defines: tuple = ()) -> str:
+    """variant "product" (LIB), "exp" (LIB_EXP), or an A/B build of the current sources with extra
+    -D defines written to `out` (tools/ only, loaded through PLSSVM_LIB_PATH)."""
+    lib = out if out else (LIB if variant == "product" else LIB_EXP)
     if not force and not _stale(lib):
         if variant == "product":
             build_cli()
@@ -68,7 +71,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "product") 
         "nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
         "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared", "--threads", "4",
         "-I", os.path.join(ROOT, "include"), "-I", inc,
-        *(["-DPLSSVM_OZ_EXPERIMENTS"] if variant != "product" else []),
+        *(["-DPLSSVM_OZ_EXPERIMENTS"] if variant == "exp" else []), *[f"-D{x}" for x in defines],
         "-o", tmp, *[os.path.join(CSRC, f) for f in SOURCES],
         "-L", libd, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libd}", "-lcudart",
     ]
@@ -77,7 +80,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "product") 
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
     os.replace(tmp, lib)
-    if variant == "product":
+    if variant == "product" and not out:
         build_cli(force=True)
     return lib
 

@@ -84,6 +84,8 @@ _lib = None
 def lib_path() -> str:
     """The product library; PLSSVM_EXPERIMENT_LIB=1 selects the experiment build (tools/ only: its
     PLSSVM_OZ_DEBUG switches make results wrong; bench.py refuses to run with it)."""
+    if os.environ.get("PLSSVM_LIB_PATH"):  # tools/ A/B runs of two builds (bench.py refuses PLSSVM_*)
+        return os.environ["PLSSVM_LIB_PATH"]
     return _build.LIB_EXP if os.environ.get("PLSSVM_EXPERIMENT_LIB") == "1" else _build.LIB
 
 

@@ -187,7 +187,11 @@ const T *stage_input(Arena &A, const void *src, int64_t n, bool device_ptr, cuda
 // (point-major rows: X, Z) also give the largest row peak max_k |x_ik| / rms_k(x_ik) that the engine
 // choice needs (oz_choose) -- in the SAME pass and the same single sync.  Throws the plssvm.h status
 // with a message.  Outputs are untouched (nothing is written before this).  Returns the peak (0 if no
-// array asked for it).
+// array asked for it) and the largest |exponent| of the row maxima (k_row_peak).
+struct RowStats {
+    float rho = 0.f;
+    int emax = 0;
+};
 template <typename T>
 struct VCheck {
     const T *a;
@@ -196,10 +200,10 @@ struct VCheck {
     int64_t row_len;  // > 0: rows of this length feed the row-peak reduction
 };
 template <typename T>
-float validate_inputs(Arena &A, std::initializer_list<VCheck<T>> arrays, const T *y, int64_t m, cudaStream_t s,
-                      int64_t &launches) {
-    unsigned *flags = A.alloc<unsigned>(2);  // [0] validation bits, [1] row peak (float bits)
-    PLS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned), s));
+RowStats validate_inputs(Arena &A, std::initializer_list<VCheck<T>> arrays, const T *y, int64_t m, cudaStream_t s,
+                         int64_t &launches) {
+    unsigned *flags = A.alloc<unsigned>(3);  // [0] validation bits, [1] row peak (float bits), [2] max |E|
+    PLS_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(unsigned), s));
     bool first = true;
     for (const VCheck<T> &v : arrays) {
         k_validate<T><<<4 * 148, 256, 0, s>>>(v.a, v.n, v.bit, first ? y : nullptr, m, flags);
@@ -214,8 +218,8 @@ float validate_inputs(Arena &A, std::initializer_list<VCheck<T>> arrays, const T
             ++launches;
         }
     }
-    unsigned *h = reinterpret_cast<unsigned *>(pinned_scratch(2 * sizeof(unsigned)));
-    PLS_CUDA(cudaMemcpyAsync(h, flags, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    unsigned *h = reinterpret_cast<unsigned *>(pinned_scratch(3 * sizeof(unsigned)));
+    PLS_CUDA(cudaMemcpyAsync(h, flags, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     PLS_CUDA(cudaStreamSynchronize(s));
     if (h[0] & V_NONFINITE_X) throw Error(PLSSVM_E_INVALID_ARG, "X is not finite");
     if (h[0] & V_NONFINITE_Z) throw Error(PLSSVM_E_INVALID_ARG, "Z is not finite");
@@ -225,9 +229,10 @@ float validate_inputs(Arena &A, std::initializer_list<VCheck<T>> arrays, const T
         if (h[0] & V_BADLABEL) throw Error(PLSSVM_E_LABELS, "labels must be +1 or -1");
         if (!(h[0] & V_POS) || !(h[0] & V_NEG)) throw Error(PLSSVM_E_LABELS, "both classes (+1 and -1) must be present");
     }
-    float peak;
-    std::memcpy(&peak, &h[1], sizeof(float));
-    return peak;
+    RowStats r;
+    std::memcpy(&r.rho, &h[1], sizeof(float));
+    r.emax = static_cast<int>(h[2]);
+    return r;
 }
 
 // rows = padded point count of the destination array (its column count is dpad).
@@ -643,16 +648,25 @@ float *oz_point_major(Arena &A, const float *Xs, int64_t m, int64_t d, int64_t r
 constexpr double kOzC64 = 13.04;  // 1 (input rounding to the row grid) + 12.04 (dropped levels 7..12)
 constexpr int64_t kOzMaxD = 16384;
 constexpr int64_t kOzMinRows = 384;  // AUTO: padded point counts up to this use DMMA
-// rho = the largest row peak of the operand arrays (validate_inputs), most_rows = the largest padded
-// point count among them.
-bool oz_choose(int engine, double rho, int64_t most_rows, int64_t d) {
+// The epilogue converts 2^k V with k = E_i + E_j - 36 (and 2^{k-24} W) by building the exponent
+// directly (ozaki_engine.cuh scaled_exact): 1 <= 1074 + k - 24 and 1074 + k <= 2045 need
+// -1014 <= E_i + E_j <= 1007, i.e. row maxima within 2^-480 .. 2^480 (~1e-144 .. 1e144).
+constexpr int kOzMaxExp = 480;
+// rs = the largest row peak and row-maximum exponent of the operand arrays (validate_inputs),
+// most_rows = the largest padded point count among them.
+bool oz_choose(int engine, const RowStats &rs, int64_t most_rows, int64_t d) {
     if (engine == PLSSVM_FP64_DMMA) return false;
+    const double rho = rs.rho;
     // int32 level sums: |acc_l| <= 7 d8 2^14 < 2^31 needs d8 <= 18724; limit 16384 (ozaki_engine.cuh)
-    const bool fits = round_up(d, OzC::BK) <= kOzMaxD;
+    const bool fits = round_up(d, OzC::BK) <= kOzMaxD && rs.emax <= kOzMaxExp;
     if (engine == PLSSVM_FP64_OZAKI) {
-        if (!fits)
+        if (round_up(d, OzC::BK) > kOzMaxD)
             throw Error(PLSSVM_E_INVALID_ARG, "fp64_engine OZAKI supports d <= " + std::to_string(kOzMaxD) +
                                                   " (int32 digit-product sums); use AUTO or DMMA");
+        if (rs.emax > kOzMaxExp)
+            throw Error(PLSSVM_E_INVALID_ARG, "fp64_engine OZAKI supports row maxima within 2^-" +
+                                                  std::to_string(kOzMaxExp) + " .. 2^" + std::to_string(kOzMaxExp) +
+                                                  " (digit-scale exponents); use AUTO or DMMA");
         return true;
     }
     if (!fits) return false;
@@ -669,8 +683,9 @@ bool oz_choose(int engine, double rho, int64_t most_rows, int64_t d) {
 // dropped levels 3..4: 32.2 d u32), so AUTO needs kOzC32 rho_max^2 <= d (C3's d = 2048: rho <= 7.1),
 // else TCGEN05 (3xTF32); d > 16384 also TCGEN05.
 constexpr double kOzC32 = 40.2;
-bool oz_choose_f32(int engine, double rho, int64_t d) {
+bool oz_choose_f32(int engine, const RowStats &rs, int64_t d) {
     if (engine == PLSSVM_FP32_TCGEN05 || engine == PLSSVM_FP32_FFMA) return false;
+    const double rho = rs.rho;  // (fp32 exponents are always in the conversion's range)
     const bool fits = round_up(d, Oz<3>::BK) <= kOzMaxD;
     if (engine == PLSSVM_FP32_OZAKI) {
         if (!fits) throw Error(PLSSVM_E_INVALID_ARG, "fp32_engine OZAKI supports d <= " + std::to_string(kOzMaxD));
@@ -1060,7 +1075,7 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     c.Xraw = Xs;
     c.m = pb.m;
     c.d = dl;
-    float rho = 0.f;  // largest row peak of X (this rank's slice), for the engine choice
+    RowStats rho;  // largest row peak / exponent of X (this rank's slice), for the engine choice
     if (need_labels) {
         c.ylab = const_cast<T *>(stage_input<T>(A, pb.y, pb.m, dev, c.s));
         rho = validate_inputs<T>(A, {VCheck<T>{Xs, pb.m * dl, V_NONFINITE_X, dl}}, c.ylab, pb.m, c.s, c.launches);
@@ -1646,7 +1661,7 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     const T *Xs = stage_input<T>(A, pb.X, m * d, dev, s);
     const T *Zs = stage_input<T>(A, Zin, n * d, dev, s);
     const T *al = stage_input<T>(A, alpha_in, m, dev, s);
-    const float rho = validate_inputs<T>(A, {VCheck<T>{Xs, m * d, V_NONFINITE_X, d}, VCheck<T>{Zs, n * d, V_NONFINITE_Z, d},
+    const RowStats rho = validate_inputs<T>(A, {VCheck<T>{Xs, m * d, V_NONFINITE_X, d}, VCheck<T>{Zs, n * d, V_NONFINITE_Z, d},
                                              VCheck<T>{al, m, V_NONFINITE_ALPHA, 0}},
                                          static_cast<const T *>(nullptr), 0, s, launches);
     if (pb.kernel == LINEAR && o.linear_w) {

@@ -38,8 +38,9 @@
 //   warps 2-3         : idle (warpgroup 0 gives its registers to the epilogue: setmaxnreg 40 / 232)
 //   warps 4-11        : epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows), columns
 //                       64((w-4)/4).. of every level (tcgen05.ld 32x32b.x8), combines the levels
-//                       in exact int64 (pass 0 -> V, held exactly as fp64; pass 1 -> W and the 64
-//                       contractions (V + 2^-24 W) sc_i sc_j with one rounding, in registers),
+//                       in exact int64 (pass 0 -> V, held in registers; pass 1 -> W and the 64
+//                       contractions 2^k V + 2^{k-24} W, each term converted exactly in one fp64
+//                       operation (scaled_exact), one rounding in their sum),
 //                       releases the accumulators after each pass, and only then runs
 //                       the kernel function / Eq. 16 corrections and the row / column contributions
 //                       -- overlapped with the next pair-tile's MMAs.
@@ -93,8 +94,8 @@ struct Oz {
     static constexpr int TMEM_COLS = 512;
     static_assert(LV * TN <= TMEM_COLS && LV0 * TN <= TMEM_COLS, "a pass's level accumulators must fit TMEM");
     // misc: barriers (256 B) + column data 4 x 128 doubles + row partials 2 x 128 + col partials 4 x 128
-    // + the 64-entry exp table + the tile's p / q.p sums (4 warps x 4)
-    static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN + 64 + 16) * 8;
+    // + the 256-entry exp table + the tile's p / q.p sums (4 warps x 4)
+    static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN + 256 + 16) * 8;
     static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + MISC;
     // instruction descriptor: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 128, M = 256 (2 SMs)
     static constexpr uint32_t IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TN >> 3) << 17) | ((256u >> 4) << 24);
@@ -143,51 +144,99 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
 }
 
-// 2^(j/64), j = 0..63, correctly rounded (Decimal, 60 digits) -- the table of exp_tab.
-__constant__ double kExp2Tab64[64] = {
-    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
-    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
-    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
-    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
-    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
-    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
-    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
-    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
-    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
-    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
-    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
-    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
-    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
-    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
-    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
-    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+// 2^(j/256), j = 0..255, correctly rounded (tools/gen_exp_table.py: 60-digit Decimal, each value
+// checked against its neighbours) -- the table of exp_tab256.
+__constant__ double kExp2Tab256[256] = {
+    1.0, 1.0027112750502025, 1.0054299011128027, 1.0081558981184175,
+    1.0108892860517005, 1.0136300849514894, 1.016378314910953, 1.019133996077738,
+    1.0218971486541166, 1.0246677928971357, 1.0274459491187637, 1.030231637686041,
+    1.0330248790212284, 1.0358256936019572, 1.0386341019613787, 1.041450124688316,
+    1.0442737824274138, 1.0471050958792898, 1.0499440858006872, 1.0527907730046264,
+    1.0556451783605572, 1.0585073227945128, 1.061377227289262, 1.0642549128844645,
+    1.0671404006768237, 1.0700337118202419, 1.0729348675259756, 1.075843889062791,
+    1.0787607977571199, 1.0816856149932152, 1.0846183622133092, 1.0875590609177697,
+    1.0905077326652577, 1.0934643990728858, 1.0964290818163769, 1.099401802630222,
+    1.102382583307841, 1.1053714457017412, 1.1083684117236787, 1.1113735033448175,
+    1.1143867425958924, 1.1174081515673693, 1.1204377524096067, 1.12347556733302,
+    1.1265216186082418, 1.129575928566288, 1.1326385195987192, 1.1357094141578055,
+    1.1387886347566916, 1.1418762039695616, 1.1449721444318042, 1.148076478840179,
+    1.1511892299529827, 1.154310420590216, 1.1574400736337511, 1.1605782120274988,
+    1.1637248587775775, 1.1668800369524817, 1.1700437696832502, 1.1732160801636373,
+    1.1763969916502812, 1.1795865274628758, 1.182784710984341, 1.1859915656609938,
+    1.189207115002721, 1.1924313825831512, 1.1956643920398273, 1.1989061670743806,
+    1.202156731452703, 1.2054161090051239, 1.2086843236265816, 1.2119613992768012,
+    1.215247359980469, 1.2185422298274085, 1.2218460329727576, 1.2251587936371455,
+    1.22848053610687, 1.2318112847340759, 1.2351510639369334, 1.2384998981998165,
+    1.241857812073484, 1.245224830175258, 1.2486009771892048, 1.2519862778663162,
+    1.255380757024691, 1.2587844395497165, 1.2621973503942507, 1.2656195145788063,
+    1.2690509571917332, 1.2724917033894028, 1.275941778396392, 1.2794012075056693,
+    1.2828700160787783, 1.2863482295460256, 1.2898358734066657, 1.2933329732290895,
+    1.2968395546510096, 1.3003556433796506, 1.3038812651919358, 1.3074164459346773,
+    1.3109612115247644, 1.3145155879493546, 1.318079601266064, 1.3216532776031575,
+    1.3252366431597413, 1.3288297242059544, 1.3324325470831615, 1.3360451382041458,
+    1.339667524053303, 1.3432997311868353, 1.3469417862329458, 1.3505937158920345,
+    1.3542555469368927, 1.3579273062129011, 1.3616090206382248, 1.365300717204012,
+    1.3690024229745905, 1.3727141650876684, 1.3764359707545302, 1.380167867260238,
+    1.383909881963832, 1.387662042298529, 1.3914243757719262, 1.3951969099662003,
+    1.3989796725383112, 1.4027726912202048, 1.4065759938190154, 1.4103896082172707,
+    1.4142135623730951, 1.4180478843204152, 1.4218926021691656, 1.4257477441054942,
+    1.42961333839197, 1.433489413367789, 1.4373759974489824, 1.4412731191286257,
+    1.4451808069770467, 1.449099089642035, 1.4530279958490526, 1.4569675544014438,
+    1.460917794180647, 1.4648787441464057, 1.4688504333369818, 1.4728328908693675,
+    1.4768261459394993, 1.4808302278224719, 1.4848451658727524, 1.488870989524397,
+    1.4929077282912648, 1.4969554117672355, 1.5010140696264256, 1.5050837316234065,
+    1.5091644275934228, 1.5132561874526098, 1.5173590411982147, 1.5214730189088146,
+    1.5255981507445384, 1.529734466947287, 1.533881997840956, 1.5380407738316568,
+    1.5422108254079407, 1.5463921831410214, 1.550584877685, 1.5547889397770887,
+    1.559004400237837, 1.5632312899713576, 1.567469639965553, 1.5717194812923414,
+    1.5759808451078865, 1.5802537626528246, 1.5845382652524937, 1.588834384317164,
+    1.593142151342267, 1.597461597908627, 1.6017927556826934, 1.606135656416771,
+    1.6104903319492543, 1.6148568142048607, 1.6192351351948637, 1.6236253270173289,
+    1.6280274218573478, 1.632441451987275, 1.6368674497669644, 1.6413054476440063,
+    1.645755478153965, 1.6502175739206177, 1.6546917676561943, 1.6591780921616162,
+    1.6636765803267364, 1.6681872651305825, 1.6727101796415966, 1.6772453570178785,
+    1.681792830507429, 1.6863526334483934, 1.6909247992693053, 1.6955093614893326,
+    1.7001063537185235, 1.7047158096580513, 1.709337763100463, 1.713972247929926,
+    1.718619298122478, 1.723278947746274, 1.7279512309618377, 1.732636182022311,
+    1.7373338352737062, 1.7420442251551564, 1.746767386199169, 1.7515033530318782,
+    1.7562521603732995, 1.761013843037584, 1.7657884359332727, 1.7705759740635547,
+    1.7753764925265212, 1.7801900265154245, 1.785016611318935, 1.789856282321401,
+    1.7947090750031072, 1.7995750249405351, 1.804454167806624, 1.809346539371032,
+    1.8142521755003989, 1.8191711121586085, 1.8241033854070534, 1.8290490314048973,
+    1.8340080864093424, 1.8389805867758937, 1.843966568958626, 1.8489660695104508,
+    1.8539791250833855, 1.8590057724288205, 1.864046048397789, 1.8690999899412386,
+    1.8741676341103, 1.8792490180565602, 1.8843441790323345, 1.8894531543909392,
+    1.8945759815869656, 1.8997126981765553, 1.9048633418176741, 1.9100279502703899,
+    1.9152065613971474, 1.9203992131630474, 1.925605943636125, 1.930826790987627,
+    1.9360617934922943, 1.9413109895286405, 1.9465744175792332, 1.9518521162309783,
+    1.9571441241754002, 1.9624504802089273, 1.9677712232331759, 1.9731063922552343,
+    1.978456026387951, 1.9838201648502194, 1.9891988469672663, 1.9945921121709402,
+};
 
-// e^t for t <= 0 (the RBF kernel, t = -gamma ||x_i - x_j||^2) with ~1 ulp error and 10 DP
-// operations instead of exp()'s ~17 (the fp64 epilogue is the energy that separates C1 from
-// the MMA-only bound):  t = (64 k + j) ln2/64 + r, |r| <= ln2/128, so
-// e^t = 2^k * 2^(j/64) * e^r with e^r = 1 + q(r), q the degree-5 Taylor polynomial
-// (truncation |r|^6/720 < 4e-17).  n = 64 k + j by the 1.5 * 2^52 rounding trick; ln2/64 split
-// into a 36-bit head (n * head exact for |n| < 2^17) and a tail.  t < -708 (e^t < 1e-307,
-// below the normal range the exponent shift can reach) returns 0.  tab = kExp2Tab64 in smem.
-__device__ __forceinline__ double exp_tab(double t, const double *__restrict__ tab) {
-    constexpr double kInvL = 92.33248261689366;         // 64 / ln 2
-    constexpr double kLhi = 0.010830424696223417;       // ln2/64, 36-bit head
-    constexpr double kLlo = 2.572804622327669e-14;      // ln2/64 - kLhi
-    constexpr double kShift = 6755399441055744.0;       // 1.5 * 2^52
-    const double kd = fma(t, kInvL, kShift);
-    const int n = __double2loint(kd);                   // round(t * 64 / ln2), two's complement
-    const double kf = kd - kShift;
-    double r = fma(kf, -kLhi, t);
-    r = fma(kf, -kLlo, r);
-    double c = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-    c = fma(r, c, 1.0 / 6.0);
-    c = fma(r, c, 0.5);
-    c = fma(r, c, 1.0);
-    const double T = tab[n & 63];
-    const double e = fma(T, r * c, T);                  // 2^(j/64) e^r, in [0.99, 2)
-    const double v = __hiloint2double(__double2hiint(e) + ((n >> 6) << 20), __double2loint(e));
-    return t < -708.0 ? 0.0 : v;
+// e^t for t <= 0 (the RBF kernel, t = -gamma ||x_i - x_j||^2) given in the scaled form
+// tp = t 256/ln2 (the epilogue forms tp = 2 gamma (256/ln2) s + b_i + b_j directly from the inner
+// product s and the per-point terms b = -gamma (256/ln2) ||x||^2: no separate distance, multiply
+// or Cody-Waite reduction).  tp = n + r', n = 256 k + j, |r'| <= 1/2:
+//     e^t = 2^k 2^(j/256) e^{r' L},  L = ln2/256,  e^{r' L} - 1 = r'(C1 + r'(C2 + r'(C3 + r' C4)))
+// (C_k = L^k/k!; truncation |r'L|^5/120 < 4e-17).  n by the 1.5 * 2^52 rounding trick; r' = tp - n is
+// exact.  ~1 ulp, 9 DP operations (+ the clamp).  tp < -261000 (t < -706.8: e^t < 2e-307, where the
+// exponent shift could leave the normal range) returns 0.  tab = kExp2Tab256 in smem.
+__device__ __forceinline__ double exp_tab256(double tp, const double *__restrict__ tab) {
+    constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
+    constexpr double C1 = 0.0027076061740622863, C2 = 3.6655655969101062e-06, C3 = 3.3083026805413713e-09,
+                     C4 = 2.239395190875157e-12;
+    const double kd = tp + kShift;
+    const int n = __double2loint(kd);  // round(tp), two's complement
+    const double r = tp - (kd - kShift);
+    double c = fma(r, C4, C3);
+    c = fma(r, c, C2);
+    c = fma(r, c, C1);
+    const double T = tab[n & 255];
+    const double e = fma(T, r * c, T);  // 2^(j/256) e^{r' L}, in [0.997, 2)
+    const double v = __hiloint2double(__double2hiint(e) + ((n >> 8) << 20), __double2loint(e));
+    return tp < -261000.0 ? 0.0 : v;
 }
+constexpr double kExpScale256 = 369.3299304675746;  // 256 / ln 2
 
 // Exact int32 -> fp64 without the (slow, XU-pipe) I2F.F64: 2^52 + (r + 2^31) assembled from
 // bits, minus 2^52 + 2^31 -- one LOP3 + one DADD.
@@ -204,10 +253,27 @@ __device__ __forceinline__ double i64_to_f64_exact(long long v) {
 }
 
 // Level sums combined in INTEGER arithmetic (exact), one conversion per group instead of one per
-// level: pass 0 W = acc_4 2^16 + acc_5 2^8 + acc_6, pass 1 V = acc_0 2^24 + acc_1 2^16 + acc_2 2^8
-// + acc_3.  |acc_l| <= (l+1) d 2^14, so |V| <= d 2^38.01 < 2^53 for d <= 16384 (the engine's
-// limit) -- exactly representable, converted without rounding.
-__device__ __forceinline__ long long lv(uint32_t r) { return static_cast<long long>(static_cast<int>(r)); }
+// level: pass 0 V = acc_0 2^24 + acc_1 2^16 + acc_2 2^8 + acc_3, pass 1 W = acc_4 2^16 + acc_5 2^8 +
+// acc_6.  |acc_l| <= (l+1) d 2^14, so |V| <= d 2^38.02 < 2^53 for d <= 16384 (the engine's limit) and
+// |W| <= d 2^32.33 -- exactly representable, converted without rounding.
+// c + a b for a 32-bit signed level sum a: the level combinations (IMAD.WIDE).  (Written in C++: an
+// explicit mad.wide.s32 in PTX was lowered to IMAD.HI + IMAD pairs and made the C1 product 1.7 %
+// slower in an A/B run, tools/scripts/ab2.sh.)
+__device__ __forceinline__ long long mad_wide(uint32_t a, int b, long long c) {
+    return c + static_cast<long long>(static_cast<int>(a)) * b;
+}
+// The scaled exact conversion 2^k V of an integer |V| < 2^51 in ONE fp64 operation (the digit
+// scales are powers of two, so scaling is exact): u = V + 3 2^51 lies in [2^52, 2^53) and is the
+// significand of the double 2^k u, whose bits are u + ((1074 + k) << 52); subtracting 2^k 3 2^51
+// (exponent 1075 + k, mantissa 0.5) leaves 2^k V exactly.  ub = V + kOzBias (added in the integer
+// combination), kb = (1074 + k) << 20 (the exponent term of the high word; 1 <= 1074 + k <= 2045).
+// Replaces int64 -> fp64 (3 DP ops) + the scale multiply per group.
+constexpr long long kOzBias = 3ll << 51;
+__device__ __forceinline__ double scaled_exact(long long ub, int kb) {
+    const uint32_t hi = static_cast<uint32_t>(static_cast<unsigned long long>(ub) >> 32) + static_cast<uint32_t>(kb);
+    return __hiloint2double(static_cast<int>(hi), static_cast<int>(static_cast<uint32_t>(ub))) -
+           __hiloint2double(kb + 0x180000, 0);
+}
 
 // Sum of v[0..31] over the 32 lanes in 31 shuffles: afterwards lane l holds the total of
 // element l.  Fixed order (deterministic).
@@ -227,7 +293,9 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
 
 // AUTO engine check: the largest row "peak" max_k |x_ik| / rms_k(x_ik) over the rows of a
 // point-major padded fp64 array (zero rows skipped), as float bits in *peak_bits (atomicMax on
-// the bits of a non-negative float orders like the value).  One warp per row.
+// the bits of a non-negative float orders like the value), and the largest |E_i| of the row
+// maxima (2^{E_i-1} <= ||x_i||_inf < 2^{E_i}) in peak_bits[1]: the epilogue's one-operation
+// conversions need the digit scales' exponents in range (kOzMaxExp).  One warp per row.
 template <typename TIN>
 __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t d,
                            unsigned *__restrict__ peak_bits) {
@@ -245,9 +313,14 @@ __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpa
         mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         ss += __shfl_xor_sync(0xffffffffu, ss, o);
     }
-    if (lane == 0 && ss > 0.0) {
-        const float r = static_cast<float>(mx / sqrt(ss / static_cast<double>(d)));
-        atomicMax(peak_bits, __float_as_uint(r));
+    if (lane == 0 && mx > 0.0) {
+        int E;
+        frexp(mx, &E);
+        atomicMax(peak_bits + 1, static_cast<unsigned>(E < 0 ? -E : E));
+        if (ss > 0.0) {  // (underflowed squares: the exponent check above still applies)
+            const float r = static_cast<float>(mx / sqrt(ss / static_cast<double>(d)));
+            atomicMax(peak_bits, __float_as_uint(r));
+        }
     }
 }
 
@@ -400,14 +473,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     uint64_t *tfull = empty + O::STAGES;                  // a pass's accumulators ready (each CTA)
     uint64_t *tempty = tfull + 1;                         // a pass's accumulators drained (leader: 16 warps)
     uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(tempty + 1);
-    double *colsc = reinterpret_cast<double *>(misc + 256);  // [128]
+    double *colsc = reinterpret_cast<double *>(misc + 256);  // [128] 8-byte slots: colk, the column exponent terms
+    int *colk = reinterpret_cast<int *>(colsc);              // [128] e_j << 20 (scaled_exact)
     T *colq = reinterpret_cast<T *>(colsc + TN);             // [128] (8-byte slots for either T)
     T *colp = reinterpret_cast<T *>(colsc + 2 * TN);         // [128] (alpha for predict)
     T *coln = reinterpret_cast<T *>(colsc + 3 * TN);         // [128]
     T *redr = reinterpret_cast<T *>(colsc + 4 * TN);         // [2][128]
     T *redc = reinterpret_cast<T *>(colsc + 4 * TN + 2 * kTile);  // [4][128]
-    double *etab = colsc + 8 * TN + 2 * kTile;               // [64] 2^(j/64) (fp64 RBF, exp_tab)
-    T *psum = reinterpret_cast<T *>(etab + 64);              // [4][4] MATVEC: per warp sum p_j, q_j p_j, p_i, q_i p_i
+    double *etab = colsc + 8 * TN + 2 * kTile;               // [256] 2^(j/256) (fp64 RBF, exp_tab256)
+    T *psum = reinterpret_cast<T *>(etab + 256);             // [4][4] MATVEC: per warp sum p_j, q_j p_j, p_i, q_i p_i
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -546,7 +620,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     } else {  // ---- epilogue warps 4-11 (both CTAs): row 32(w%4) + lane, columns 64((w-4)/4) .. +63
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(O::EPI_REGS));
         constexpr bool kTabExp = KT == RBF && S == 7;
-        if (kTabExp && threadIdx.x - 128 < 64) etab[threadIdx.x - 128] = kExp2Tab64[threadIdx.x - 128];  // read after B1
+        if (kTabExp) etab[threadIdx.x - 128] = kExp2Tab256[threadIdx.x - 128];  // 256 epilogue threads; read after B1
+        // fp64 RBF: tp = a2 s + b_i + b_j = (256/ln2) (-gamma) (n_i + n_j - 2 s) (exp_tab256)
+        const double gK = kTabExp ? -static_cast<double>(kp.gamma) * kExpScale256 : 0.0, a2 = -2.0 * gK;
         const int quarter = warp & 3, grp = (warp - 4) >> 2;
         const int lr = quarter * 32 + lane;
         const int et = threadIdx.x - 128;  // 0..255
@@ -560,17 +636,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             const int64_t row0 = int64_t(I) * kTile, col0 = int64_t(J) * TN;
             if (et < TN) {  // column data of this tile (the previous tile's readers are done: B3)
                 const int64_t gj = col0 + et;
-                colsc[et] = scb[gj];
+                colk[et] = ((__double2hiint(scb[gj]) >> 20) - 1023) << 20;  // scb = 2^{e_j}
                 colq[et] = (MODE == OZ_PREDICT) ? T(0) : qv[gj];
                 colp[et] = (MODE == OZ_PRECOMPUTE) ? T(0) : p[gj];
-                coln[et] = (KT == RBF) ? nb_[gj] : T(0);
+                coln[et] = (KT == RBF) ? (kTabExp ? T(gK * nb_[gj]) : nb_[gj]) : T(0);  // fp64 RBF: b_j
             }
             const int64_t gi = row0 + lr;
-            // row scale (S = 7: with V's 2^-24 folded in)
-            const double sci = used ? sca[gi] * (S == 7 ? 0x1p-24 : 1.0) : 0.0;
+            // row exponent term of the scaled conversions (sca = 2^{e_i}): kb = rkb + colk[j] = (1074 + k) << 20
+            // with k = e_i + e_j - 24 (S = 7: the unit of V, level 3) or e_i + e_j (S = 3)
+            const int rkb = (1074 - (S == 7 ? 24 : 0) + (used ? (__double2hiint(sca[gi]) >> 20) - 1023 : 0)) << 20;
+            // |V| < 2^51 (the one-operation conversion) needs d8 <= 8096; wider points convert V in pass 0
+            const bool bigd = S == 7 && nk * Oz<S>::BK > 8096;
             const T qi = (MODE == OZ_PREDICT || !used) ? T(0) : qv[gi];
             const T pi = (MODE == OZ_MATVEC && used) ? p[gi] : T(0);
-            const T ni = (KT == RBF && used) ? na[gi] : T(0);
+            const T ni = (KT == RBF && used) ? (kTabExp ? T(gK * na[gi]) : na[gi]) : T(0);  // fp64 RBF: b_i
             const T cqi = Qmm - qi;  // Eq. 16 row constant
             if constexpr (MODE == OZ_MATVEC) {
                 // Eq. 16 by rows: sum_j Q~_ij p_j = sum_j k_ij p_j + (Q_mm - q_i) sum_j p_j - sum_j q_j p_j
@@ -632,8 +711,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         tmem_ld_wait();
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const long long V = (lv(r0[j]) << 24) + (lv(r1[j]) << 16) + (lv(r2[j]) << 8) + lv(r3[j]);
-                            sv[c * 8 + j] = i64_to_f64_exact(V);
+                            // V + 3 2^51, exact in int64; held as bits until pass 1 knows the scale
+                            const long long Vb = mad_wide(r0[j], 1 << 24, mad_wide(r1[j], 1 << 16,
+                                                           mad_wide(r2[j], 1 << 8, mad_wide(r3[j], 1, kOzBias))));
+                            sv[c * 8 + j] = bigd ? i64_to_f64_exact(Vb - kOzBias) : __longlong_as_double(Vb);
                         }
                     }
                 }
@@ -661,14 +742,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int lc = grp * 64 + c * 8 + j;
+                        const int kb = rkb + colk[lc];
                         if constexpr (S == 7) {
-                            // x_i.x_j = sc_i sc_j (V + 2^-24 W) 2^-24 (level 4 is 2^-32 below level 0, W
-                            // carries 2^16 of it; the other 2^-24 sits in sci): one rounding
-                            const long long W = (lv(r0[j]) << 16) + (lv(r1[j]) << 8) + lv(r2[j]);
-                            sv[c * 8 + j] = fma(i64_to_f64_exact(W), 0x1p-24, sv[c * 8 + j]) * (sci * colsc[lc]);
-                        } else {
-                            const long long V = (lv(r0[j]) << 16) + (lv(r1[j]) << 8) + lv(r2[j]);
-                            sv[c * 8 + j] = static_cast<T>(i64_to_f64_exact(V) * (sci * colsc[lc]));
+                            // x_i.x_j = 2^k V + 2^{k-24} W (level 4 is 2^-32 below level 0, W carries 2^16
+                            // of it), both terms exact: ONE rounding in their sum
+                            const long long Wb = mad_wide(r0[j], 1 << 16, mad_wide(r1[j], 1 << 8, mad_wide(r2[j], 1, kOzBias)));
+                            const double dw = scaled_exact(Wb, kb - (24 << 20));
+                            sv[c * 8 + j] = bigd ? fma(sv[c * 8 + j], __hiloint2double(kb - (51 << 20), 0), dw)  // x 2^k
+                                                 : scaled_exact(__double_as_longlong(sv[c * 8 + j]), kb) + dw;
+                        } else {  // S = 3: x_i.x_j = 2^k V, |V| < d 2^30.01 < 2^51, then one rounding to fp32
+                            const long long Vb = mad_wide(r0[j], 1 << 16, mad_wide(r1[j], 1 << 8, mad_wide(r2[j], 1, kOzBias)));
+                            sv[c * 8 + j] = static_cast<T>(scaled_exact(Vb, kb));
                         }
                     }
                 }
@@ -688,11 +772,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         const int64_t gj = col0 + lc;
                         const bool diag = (MODE != OZ_PREDICT) && gi == gj;
                         T kv;
-                        if constexpr (kTabExp) {  // kernel_value's RBF with the table exp
-                            double dist = ni + coln[lc] - 2.0 * sv[c * 8 + j];
-                            dist = dist > 0.0 ? dist : 0.0;
-                            if (diag) dist = 0.0;
-                            kv = exp_tab(-kp.gamma * dist, etab);
+                        if constexpr (kTabExp) {  // kernel_value's RBF (distance clamped at 0, exactly 0 on
+                            // the diagonal, R-9) in the scaled exponent form of exp_tab256
+                            double tp = fma(a2, sv[c * 8 + j], ni + coln[lc]);
+                            tp = fmin(tp, 0.0);
+                            if (diag) tp = 0.0;
+                            kv = exp_tab256(tp, etab);
                         } else {
                             kv = kernel_value<KT, T>(sv[c * 8 + j], ni, coln[lc], diag, kp);
                         }

@@ -270,3 +270,53 @@ def test_auto_picks_dmma_for_tiny_problems():
         assert st == 0 and stats.fp64_engine_used == want, (m, stats.fp64_engine_used)
         a_ref, _, _, _ = oracle.train(X, y, pl.RBF, 1.0 / d, eps=1e-10)
         assert rel(a, a_ref) <= 1e-7
+
+
+def test_exponent_range_limit():
+    """The epilogue builds the digit scales' exponents directly (ozaki_engine.cuh scaled_exact: 2^k V in
+    one fp64 operation), which needs row maxima within 2^-480 .. 2^480 (driver.cu kOzMaxExp): rows at
+    2^-470 and 2^470 still run on OZAKI within the parity bars; a row at 2^-500 makes AUTO take DMMA
+    and forced OZAKI refuse."""
+    rng = np.random.default_rng(21)
+    m, d = 600, 64
+    X = rng.standard_normal((m, d))
+    X[7] *= 2.0 ** -470
+    X[9] *= 2.0 ** 470
+    p = rng.standard_normal(m - 1)
+    Qt = oracle.qtilde(X, pl.LINEAR, 1.0, 3, 0.0, 1.0)
+    ref = oracle.matvec(Qt, p)
+    scale = np.abs(Qt) @ np.abs(p)
+    s0 = np.abs(ref).max()  # ~2^940: normalise before the norms (their squares would overflow)
+    for mode in (pl.MODE_IMPLICIT, pl.MODE_CACHED):
+        out, _ = pl.plssvm_qtilde_matvec(X, p, pl.LINEAR, 1.0, 3, 0.0, 1.0,
+                                         opts=pl.options(mode=mode, fp64_engine=pl.FP64_OZAKI))
+        assert rel(out / s0, ref / s0) <= 1e-12
+        assert np.all(np.abs(out - ref) <= 1e-12 * scale)
+    X2 = rng.standard_normal((m, d))
+    X2[7] *= 2.0 ** -470
+    check(X2, p, pl.RBF, 1.0 / d, engine=pl.FP64_OZAKI)
+    # AUTO's own rule: at d = 1024 N(0,1) rows pass the peak test (13.04 rho^2 <= d), so only the
+    # exponent range decides
+    X3 = rng.standard_normal((m, 1024))
+    y = np.where(np.arange(m) % 2 == 0, 1.0, -1.0)
+    _, _, st, stats = pl.plssvm_train_ex(X3, y, pl.RBF, 1.0 / 1024, eps=1e-10)
+    assert st == 0 and stats.fp64_engine_used == pl.FP64_OZAKI
+    X3[7] *= 2.0 ** -500
+    alpha, b, st, stats = pl.plssvm_train_ex(X3, y, pl.RBF, 1.0 / 1024, eps=1e-10)
+    assert st == 0 and stats.fp64_engine_used == pl.FP64_DMMA
+    a_ref, _, _, _ = oracle.train(X3, y, pl.RBF, 1.0 / 1024, eps=1e-10)
+    assert rel(alpha, a_ref) <= 1e-7
+    with pytest.raises(pl.PlssvmError, match="row maxima within"):
+        pl.plssvm_train_ex(X3, y, pl.RBF, 1.0 / 1024, eps=1e-10, opts=pl.options(fp64_engine=pl.FP64_OZAKI))
+
+
+@pytest.mark.parametrize("d", [8096, 8128])
+def test_conversion_width_boundary(d):
+    """|V| < 2^51 (the one-operation conversion of pass 0's levels) holds up to d8 = 8096; wider points
+    convert V exactly in pass 0 instead (ozaki_engine.cuh bigd).  Both sides of the switch vs the oracle."""
+    rng = np.random.default_rng(d)
+    m = 420
+    X = rng.standard_normal((m, d))
+    p = rng.standard_normal(m - 1)
+    check(X, p, pl.RBF, 1.0 / d, engine=pl.FP64_OZAKI)
+    check(X, p, pl.LINEAR, 1.0, engine=pl.FP64_OZAKI)
