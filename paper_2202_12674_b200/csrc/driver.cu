@@ -1120,7 +1120,7 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
     PLS_CHECK_LAUNCH();
     ++c.launches;
     PLS_CUDA(cudaEventRecord(e_q, c.s));
-    c.partials = A.alloc<T>(kVecBlocks);
+    c.partials = A.alloc<T>(2 * kVecBlocks);  // (k_cg_fused: one array per reduction)
     c.counter = A.alloc<unsigned>(1);
     PLS_CUDA(cudaMemsetAsync(c.counter, 0, sizeof(unsigned), c.s));
     std::vector<int2> tl = band_tiles(g, c.oz ? OzC::NSUB : Engine<T>::NSUB);
@@ -1337,6 +1337,10 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     // Chronopoulos-Gear variant: c.p (full) carries r (the product's operand), c.r (band) the
     // search direction p, scg the recurrence s = Q~ p; one all-reduce of (gamma, delta).
     const bool cgcg = o.cg_variant == PLSSVM_CG_SINGLE_REDUCTION;
+    // one cooperative launch for the vector work of an iteration: one GPU, no exchange, no residual
+    // replacement (the three-kernel sequence otherwise; PLSSVM_CG_UNFUSED=1 forces it for A/B runs)
+    const bool unfused_env = std::getenv("PLSSVM_CG_UNFUSED") != nullptr;  // (read per call: the A/B test)
+    const bool fused = !cgcg && c.comm == nullptr && !c.fsplit && o.replace_every <= 0 && c.npeer == 0 && !unfused_env;
     if (c.comm && comm_is_peer(c.comm) && comm_peer_direct(c.comm) && !c.fsplit && !cgcg) {
         // fused all-gather of p (PEER transport): learn every rank's p buffer once
         std::vector<void *> all = comm_peer_exchange_ptr(c.comm, c.p);
@@ -1369,6 +1373,23 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         if (ev0) PLS_CUDA(cudaEventRecord(ev0, c.s));
         const int ns = launch_qtilde_product<T>(c, c.p);
         if (ev1) PLS_CUDA(cudaEventRecord(ev1, c.s));
+        if (fused) {  // finalize + update_xr + update_p as one cooperative launch (bit-identical)
+            const T *Yf = c.Yfin;
+            const int nsub = (c.cached || c.circ) ? 1 : c.nsub_eff;
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(kVecBlocks);
+            lc.blockDim = dim3(kVecThreads);
+            lc.stream = c.s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            PLS_CUDA(cudaLaunchKernelEx(&lc, k_cg_fused<T>, Yf, ns, nsub, g.band0, g.nb, g.g0, g.m1, c.x, c.r, pband,
+                                        c.y, c.scal, c.ctrl, c.partials, loop, use_loop));
+            ++c.launches;
+            return;
+        }
         finalize<T>(c, ns, pband, 0, nullptr, 0, 0);
         allreduce(c, S_PAP, 1);
         k_update_xr<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.y, g.nb, c.scal, c.ctrl, c.partials,

@@ -8,9 +8,12 @@
 //   k_finalize         y = sum_slots Ypart ; p.y  (deterministic)
 //   k_update_xr        x += a p ; r -= a y ; r.r  (fused axpy + norm)
 //   k_update_p         p = r + b p ; loop condition (and the CUDA-graph WHILE condition)
+//   k_cg_fused         the three above in one cooperative launch (single GPU)
 //   k_init / k_bias    CG start, Eq. 15 bias + alpha assembly
 //   k_predict          f(z) = sum_i alpha_i k(x_i, z) + b                (Eq. 10)
 #pragma once
+#include <cooperative_groups.h>
+
 #include "tile_engine.cuh"
 
 namespace plssvm {
@@ -750,6 +753,124 @@ __global__ void __launch_bounds__(kVecThreads)
         ctrl[C_DONE] = done;
         *counter = 0u;
         // CUDA-graph CG loop (plssvm_cg_loop_t GRAPH): the WHILE node repeats while not done
+        if (use_loop) cudaGraphSetConditional(loop, done == 0 ? 1u : 0u);
+    }
+}
+
+// Block partial of a sum (grid_reduce's first half): warp shuffle tree, then the warps in order.
+template <typename T>
+__device__ __forceinline__ void block_partial(T v, T *partials) {
+    __shared__ T red[kVecThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T s = T(0);
+        for (int w = 0; w < kVecThreads / 32; ++w) s += red[w];
+        partials[blockIdx.x] = s;
+    }
+}
+// The total of the block partials in grid_reduce's fixed order (lane-strided, then a shuffle tree),
+// computed by every block after a grid barrier: all blocks hold the identical value.
+template <typename T>
+__device__ __forceinline__ T grid_total(const T *partials) {
+    __shared__ T tot;
+    if (threadIdx.x < 32) {
+        T s = T(0);
+        for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) s += ((volatile const T *)partials)[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) tot = s;
+    }
+    __syncthreads();
+    return tot;
+}
+
+// One Shewchuk CG iteration after the product, in ONE cooperative launch (single GPU, no residual
+// replacement): k_finalize (y = sum of the slots in fixed order, pAp = p.y) | grid barrier |
+// k_update_xr (a = delta_k / pAp; x += a p; r -= a y; delta_{k+1} = r.r) | grid barrier | k_update_p
+// (b = delta_{k+1} / delta_k; p = r + b p; loop condition and breakdown test).
+// The same arithmetic in the same order as the three kernels (same per-thread accumulations, block
+// trees and fixed-order grid totals), so the iterates are bit-identical; two launches and their
+// gaps per iteration fewer.  Partials: two arrays of gridDim.x (one per reduction).
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_cg_fused(const T *__restrict__ Ypart, int nslots, int nsub, int band0, int64_t nb, int64_t g0, int64_t m1,
+               T *__restrict__ x, T *__restrict__ r, T *__restrict__ p, T *__restrict__ y, double *scal, int *ctrl,
+               T *partials, cudaGraphConditionalHandle loop, int use_loop) {
+    namespace cg = cooperative_groups;
+    constexpr int G = kVecThreads / 32;
+    __shared__ T grp[G][33];
+    if (cg_done(ctrl)) {  // read by every block before the first barrier; written only after the last
+        if (use_loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0u);
+        return;
+    }
+    cg::grid_group grid = cg::this_grid();
+    const int par = ctrl[C_IT] & 1;
+    // ---- k_finalize (mode 0)
+    T part = T(0);
+    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const int64_t nchunks = (nb + 31) / 32;
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const int64_t i = ch * 32 + lane;
+        const int R = static_cast<int>((g0 + ch * 32) / kTile);
+        T sg = T(0);
+        if (i < nb) {
+            for (int k = q; k < nslots; k += G) {
+                if (nsub == 2 && (k & 1)) {
+                    const int J = k >> 1;
+                    if (J >= band0 && J < R) continue;
+                }
+                sg += Ypart[static_cast<int64_t>(k) * nb + i];
+            }
+        }
+        grp[q][lane] = sg;
+        __syncthreads();
+        if (q == 0 && i < nb) {
+            T s = T(0);
+#pragma unroll
+            for (int g = 0; g < G; ++g) s += grp[g][lane];
+            s = (g0 + i) < m1 ? s : T(0);
+            y[i] = s;
+            part = fma(p[i], s, part);
+        }
+        __syncthreads();
+    }
+    block_partial<T>(part, partials);
+    grid.sync();
+    const T pap = grid_total<T>(partials);
+    // ---- k_update_xr
+    const T a = static_cast<T>(scal[S_DELTA + par] / static_cast<double>(pap));
+    part = T(0);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        x[i] = fma(a, p[i], x[i]);
+        const T ri = fma(-a, y[i], r[i]);
+        r[i] = ri;
+        part = fma(ri, ri, part);
+    }
+    block_partial<T>(part, partials + gridDim.x);
+    grid.sync();
+    const T dnew_t = grid_total<T>(partials + gridDim.x);
+    // ---- k_update_p
+    const double dnew = static_cast<double>(dnew_t);
+    const T b = static_cast<T>(dnew / scal[S_DELTA + par]);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = fma(b, p[i], r[i]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const double papd = static_cast<double>(pap);
+        scal[S_PAP] = scal[S_PAP + S_L] = papd;
+        scal[S_DELTA + (par ^ 1)] = scal[S_DELTA + (par ^ 1) + S_L] = dnew;
+        scal[S_ALPHA] = static_cast<double>(a);
+        const int it = ctrl[C_IT] + 1;
+        int done = 0;
+        if (!(papd > 0.0) || !isfinite(papd) || !isfinite(dnew)) done = 2;
+        else if (ctrl[C_FIXED] > 0 ? (it >= ctrl[C_FIXED] || dnew == 0.0) : (dnew <= scal[S_THR])) done = 1;
+        else if (it >= ctrl[C_IMAX]) done = 1;
+        ctrl[C_IT] = it;
+        ctrl[C_DONE] = done;
         if (use_loop) cudaGraphSetConditional(loop, done == 0 ? 1u : 0u);
     }
 }

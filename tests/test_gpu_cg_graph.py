@@ -3,6 +3,7 @@ conditional node repeats the iteration body until k_update_p's last block clears
 (Shewchuk's loop condition).  The graph issues exactly the kernels of the batched
 host loop in the same order, so the trained model must be BIT-identical to BATCHED, and both
 must match the oracle (alpha, b <= 1e-7 relative at eps = 1e-10, the north_star bar)."""
+
 import numpy as np
 import pytest
 
@@ -36,7 +37,7 @@ def test_graph_loop_bit_identical_to_batched_and_matches_oracle(kernel, mode, m,
     assert st_g == st_b == 0 and s_g.iterations == s_b.iterations
     assert np.array_equal(a_g, a_b) and b_g == b_b
     # launches: the body's kernels once per iteration + the entry node
-    assert s_g.gpu_launches >= s_g.iterations * 3
+    assert s_g.gpu_launches >= s_g.iterations * 2  # product + the fused vector kernel (k_cg_fused)
     if dtype == np.float64:
         a_r, b_r, _, _ = oracle.train(X, y, kernel, g, 3, 0.0, 1.0, eps)
         assert np.linalg.norm(a_g - a_r) <= 1e-7 * np.linalg.norm(a_r)
@@ -75,3 +76,27 @@ def test_graph_loop_already_converged_start():
     a, b, st, s = _train(X, y, pl.RBF, 0.2, 0.9999, cg_loop=pl.CG_GRAPH)
     a2, b2, st2, s2 = _train(X, y, pl.RBF, 0.2, 0.9999, cg_loop=pl.CG_BATCHED)
     assert st == st2 and s.iterations == s2.iterations <= 2 and np.array_equal(a, a2)
+
+
+@pytest.mark.parametrize("kernel,mode,m,d,dtype,loop", [
+    (pl.RBF, pl.MODE_IMPLICIT, 1000, 33, np.float64, pl.CG_BATCHED),
+    (pl.RBF, pl.MODE_IMPLICIT, 1000, 33, np.float64, pl.CG_GRAPH),
+    (pl.POLYNOMIAL, pl.MODE_CACHED, 900, 24, np.float64, pl.CG_GRAPH),
+    (pl.LINEAR, pl.MODE_LOWRANK, 1200, 40, np.float64, pl.CG_BATCHED),
+    (pl.POLYNOMIAL, pl.MODE_IMPLICIT, 640, 31, np.float32, pl.CG_BATCHED),
+    (pl.RBF, pl.MODE_CACHED, 777, 20, np.float32, pl.CG_GRAPH),
+])
+def test_fused_vector_kernel_bit_identical_to_three_kernels(kernel, mode, m, d, dtype, loop, monkeypatch):
+    """k_cg_fused (finalize + update_xr + update_p in one cooperative launch, grid barriers in place of
+    the kernel boundaries) performs the same arithmetic in the same order as the three kernels: the
+    trained model is bit-identical; PLSSVM_CG_UNFUSED=1 selects the three-kernel sequence."""
+    X, y, _, _ = synth.planes(m, d, 16, seed=5 + kernel)
+    X, y = X.astype(dtype), y.astype(dtype)
+    eps = 1e-10 if dtype == np.float64 else 1e-6
+    a_f, b_f, st_f, s_f = _train(X, y, kernel, 1.0 / d, eps, mode=mode, cg_loop=loop)
+    monkeypatch.setenv("PLSSVM_CG_UNFUSED", "1")
+    a_u, b_u, st_u, s_u = _train(X, y, kernel, 1.0 / d, eps, mode=mode, cg_loop=loop)
+    monkeypatch.delenv("PLSSVM_CG_UNFUSED")
+    assert st_f == st_u == 0 and s_f.iterations == s_u.iterations
+    assert np.array_equal(a_f, a_u) and b_f == b_u
+    assert s_f.gpu_launches < s_u.gpu_launches
