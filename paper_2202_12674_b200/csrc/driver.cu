@@ -112,6 +112,29 @@ char *pinned_scratch(size_t bytes) {
     return b.p;
 }
 
+// Timing events of the CG loop (per-launch product events, collective events), created once per
+// host thread and device and reused by every call (creating ~100 events per call cost host time
+// while the GPU waited for the loop's first launches).  Calls on one thread are sequential.
+cudaEvent_t *event_pool(int n) {
+    int dev = 0;
+    PLS_CUDA(cudaGetDevice(&dev));
+    thread_local struct Pool {
+        std::vector<std::vector<cudaEvent_t>> per_dev;
+        ~Pool() {
+            for (auto &v : per_dev)
+                for (cudaEvent_t e : v) cudaEventDestroy(e);
+        }
+    } pool;
+    if (static_cast<int>(pool.per_dev.size()) <= dev) pool.per_dev.resize(dev + 1);
+    std::vector<cudaEvent_t> &v = pool.per_dev[dev];
+    while (static_cast<int>(v.size()) < n) {
+        cudaEvent_t e;
+        PLS_CUDA(cudaEventCreate(&e));
+        v.push_back(e);
+    }
+    return v.data();
+}
+
 // Thread-local pinned staging for host-built index lists (tile lists, pair-tile lists, peer pointers):
 // their H2D copies are then truly asynchronous -- a cudaMemcpyAsync from pageable memory waits for the
 // stream to drain first, which put a host round trip per list into every call.  Bump allocation inside
@@ -288,6 +311,23 @@ CUtensorMap make_tmap_digit_blocks(int8_t *base, int64_t bytes, uint32_t box_row
     if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled (digits) failed: " + std::to_string(int(r)));
     return m;
 }
+
+// The column-operand view of the same digit blocks: a 3-D map (128 B, 128-byte row within a 4 KiB
+// plane, plane) whose box {128, 16, planes} is one 64-point half of a 128-point block -- rows
+// 16 r .. 16 r + 15 of each of the first `planes` planes -- landing in shared memory as [planes][64 x 32 B],
+// the B-half image the 2-SM UMMA reads.
+CUtensorMap make_tmap_digit_halves(int8_t *base, int64_t bytes, uint32_t planes) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {128u, 32u, static_cast<cuuint64_t>(bytes / 4096)};
+    const cuuint64_t strides[2] = {128u, 4096u};
+    const cuuint32_t box[3] = {128u, 16u, planes};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(PLSSVM_E_CUDA, "cuTensorMapEncodeTiled (digit halves) failed: " + std::to_string(int(r)));
+    return m;
+}
 CUtensorMap make_tmap_2d_f32(float *base, int64_t inner, int64_t outer, uint32_t box_inner, uint32_t box_outer) {
     return make_tmap_2d(base, 4, inner, outer, box_inner, box_outer);
 }
@@ -367,14 +407,16 @@ std::vector<int2> circulant_tiles(const Geometry &g, int nsub) {
     return t;
 }
 
-// Digit blocks of a point-major padded fp64 array (ozaki_engine.cuh): TMA maps whose boxes carry
-// the first 4 (pass 1) or all 8 (pass 0) planes of a slab block, in the row-operand layout DA
-// (128 points) and / or the column-operand layout DB (64 points).
+// Digit blocks of a point-major padded array (ozaki_engine.cuh k_ozaki_split, ONE layout DA of
+// 128-point blocks): TMA maps whose boxes carry the first LV (pass 0) or all S planes of a slab
+// block -- t4 / t8 for the row operand (a whole 128-point block), h4 / h8 for the column operand
+// (one 64-point half of a block: 16 of each plane's 32 rows of 128 B, planes 4 KiB apart).  Both
+// roles read the same bytes, so a point's digits are stored and cached once.
 struct OzOperand {
-    int8_t *DA = nullptr, *DB = nullptr;
+    int8_t *DA = nullptr;
     double *sc = nullptr;
-    CUtensorMap t4, t8;  // DA boxes
-    CUtensorMap h4, h8;  // DB boxes
+    CUtensorMap t4, t8;  // row-operand boxes
+    CUtensorMap h4, h8;  // column-operand (half-block) boxes
     int nk = 0;
 };
 
@@ -607,11 +649,10 @@ OzOperand oz_prepare(Arena &A, const TIN *Xp, int64_t rows, int64_t dpad, int64_
     OzOperand o;
     const int64_t d8 = round_up(d, O::BK);
     const int64_t bytes = S * rows * d8;
-    if (row_role) o.DA = A.alloc<int8_t>(bytes);
-    if (col_role) o.DB = A.alloc<int8_t>(bytes);
+    o.DA = A.alloc<int8_t>(bytes);
     o.sc = A.alloc<double>(rows);
     k_ozaki_split<S, TIN><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, s>>>(Xp, rows, dpad, d8, o.DA,
-                                                                                         o.DB, o.sc);
+                                                                                         o.sc);
     PLS_CHECK_LAUNCH();
     ++launches;
     if (row_role) {
@@ -619,8 +660,8 @@ OzOperand oz_prepare(Arena &A, const TIN *Xp, int64_t rows, int64_t dpad, int64_
         o.t8 = make_tmap_digit_blocks(o.DA, bytes, S * 32);
     }
     if (col_role) {
-        o.h4 = make_tmap_digit_blocks(o.DB, bytes, O::LV * 16);
-        o.h8 = make_tmap_digit_blocks(o.DB, bytes, S * 16);
+        o.h4 = make_tmap_digit_halves(o.DA, bytes, O::LV);
+        o.h8 = make_tmap_digit_halves(o.DA, bytes, S);
     }
     o.nk = static_cast<int>(d8 / O::BK);
     return o;
@@ -1316,17 +1357,16 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     double *hs = reinterpret_cast<double *>(pinned_scratch(S_COUNT * sizeof(double) + C_COUNT * sizeof(int)));
     int *hctrl = reinterpret_cast<int *>(hs + S_COUNT);
     const int64_t launches_before_cg = c.launches;
-    constexpr int kBatch = 8;
+    // Batches: the first has kBatch iterations; each later one is sized from the convergence rate of
+    // the previous batch (the iterations still needed to reach delta <= eps^2 delta_0, + 1), so a
+    // C1 training takes 2-3 host round trips instead of one per 8 iterations, with few no-op
+    // iterations at the end (one GPU; several ranks keep batches of kBatch).
+    constexpr int kBatch = 8, kBatchMax = 32;
     constexpr int kCommEv = 12;  // event slots per iteration for collectives (<= 5 collectives)
-    cudaEvent_t mv0[kBatch], mv1[kBatch];
-    cudaEvent_t cev[kBatch][kCommEv];
-    int ncev[kBatch] = {};
-    for (int b = 0; b < kBatch; ++b) {
-        mv0[b] = E.make();
-        mv1[b] = E.make();
-        if (c.comm)
-            for (int k = 0; k < kCommEv; ++k) cev[b][k] = E.make();
-    }
+    cudaEvent_t *evp = event_pool(2 * kBatchMax + (c.comm ? kBatchMax * kCommEv : 0));
+    cudaEvent_t *mv0 = evp, *mv1 = evp + kBatchMax;
+    auto cev = [&](int b) { return evp + 2 * kBatchMax + b * kCommEv; };
+    int ncev[kBatchMax] = {};
     double t_comm = 0.0;
     double t_mv = 0.0, t_mv_min = 1e30;
     int64_t it = 0;
@@ -1481,10 +1521,13 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         c.launches += 1 + per_it * it;
         c.graph_used = true;
     } else {
+        int batch = kBatch;
+        double d_prev = -1.0;
+        int64_t it_prev = 0;
         while (true) {
-            for (int b = 0; b < kBatch; ++b) {
+            for (int b = 0; b < batch; ++b) {
                 if (c.comm) {
-                    c.cev = cev[b];
+                    c.cev = cev(b);
                     c.ncev = 0;
                     c.cev_cap = kCommEv;
                 }
@@ -1496,18 +1539,33 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
             PLS_CUDA(cudaMemcpyAsync(hctrl, c.ctrl, C_COUNT * sizeof(int), cudaMemcpyDeviceToHost, c.s));
             PLS_CUDA(cudaStreamSynchronize(c.s));
             const int64_t ran = hctrl[C_IT] - it;  // iterations of this batch that did work
-            for (int b = 0; b < ran && b < kBatch; ++b) {
+            for (int b = 0; b < ran && b < batch; ++b) {
                 const double tm = elapsed(mv0[b], mv1[b]);
                 t_mv += tm;
                 t_mv_min = std::min(t_mv_min, tm);
-                for (int k = 0; k + 1 < ncev[b]; k += 2) t_comm += elapsed(cev[b][k], cev[b][k + 1]);
+                for (int k = 0; k + 1 < ncev[b]; k += 2) t_comm += elapsed(cev(b)[k], cev(b)[k + 1]);
             }
             it = hctrl[C_IT];
             if (std::getenv("PLSSVM_DEBUG"))
                 std::fprintf(stderr, "[plssvm] batch: it=%d done=%d d0=%.6e d[0]=%.6e d[1]=%.6e thr=%.6e pap=%.6e\n",
                              hctrl[C_IT], hctrl[C_DONE], hs[S_DELTA0], hs[S_DELTA], hs[S_DELTA + 1], hs[S_THR],
                              hs[S_PAP]);
-            if (hctrl[C_DONE] != 0 || ran < kBatch) break;
+            if (hctrl[C_DONE] != 0 || ran < batch) break;
+            // next batch: iterations to the threshold at the last batch's rate (+ 1), or the fixed count
+            const double dn = delta_now(hs, it, cgcg), base = d_prev > 0.0 ? d_prev : hs[S_DELTA0];
+            int64_t next = kBatch;
+            if (c.comm) {
+                // several ranks: fixed batches (the CG-CG host snapshot holds this rank's partial of the
+                // next gamma, so a rate-based size could differ between ranks and mismatch collectives)
+            } else if (o.fixed_iter > 0) {
+                next = o.fixed_iter - it;
+            } else if (dn > 0.0 && base > dn && hs[S_THR] > 0.0 && it > it_prev) {
+                const double rate = std::log(dn / base) / static_cast<double>(it - it_prev);  // < 0
+                next = static_cast<int64_t>(std::ceil(std::log(hs[S_THR] / dn) / rate)) + 1;
+            }
+            batch = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({next, kBatchMax, imax - it})));
+            d_prev = dn;
+            it_prev = it;
         }
     }
     c.cur_ctrl = nullptr;

@@ -601,6 +601,31 @@ __global__ void __launch_bounds__(kVecThreads)
 // CG vector kernels on this rank's band (local length nb, rows with global index >= m1 are
 // padding and stay 0).  Scalars live in `scal` (double) so no host round trip is needed.
 
+// Slot group q of row i: sum_{k = q, q + 8, ...} Ypart[k][i] in increasing k (the fixed order), with the
+// loads issued 8 at a time ahead of the adds (the sum was a chain of dependent L2 round trips: 16 per
+// row at C1, ~11 us of the fused CG kernel's 16).  Slot validity (k_matvec_implicit): with NSUB = 2
+// column sub-blocks, the odd slot of an in-band column block J below row block R carries nothing.
+template <typename T>
+__device__ __forceinline__ T slot_group_sum(const T *__restrict__ Ypart, int nslots, int nsub, int band0, int R,
+                                            int64_t nb, int64_t i, int q) {
+    constexpr int G = kVecThreads / 32, U = 8;
+    T sg = T(0);
+    for (int k0 = q; k0 < nslots; k0 += G * U) {
+        T v[U];
+        bool use[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int k = k0 + u * G;
+            use[u] = k < nslots && !(nsub == 2 && (k & 1) && (k >> 1) >= band0 && (k >> 1) < R);
+            v[u] = use[u] ? Ypart[static_cast<int64_t>(k) * nb + i] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (use[u]) sg += v[u];
+    }
+    return sg;
+}
+
 // y_i = sum_s Ypart[s][i] (fixed slot order), then pAp = p . y  (mode 0), or for the initial
 // / replaced residual (mode 1): r_i = rhs_i - y_i, r.r -> S_DELTA+par (and S_DELTA0 if init);
 // par < 0: take the slot from the device iteration counter.
@@ -628,16 +653,7 @@ __global__ void __launch_bounds__(kVecThreads)
         // in-band column block J below this row block R carries nothing (mirrored column sums
         // go to the even slot).  R is uniform over a 32-row chunk.
         const int R = static_cast<int>((g0 + ch * 32) / kTile);
-        T sg = T(0);
-        if (i < nb) {
-            for (int k = q; k < nslots; k += G) {
-                if (nsub == 2 && (k & 1)) {
-                    const int J = k >> 1;
-                    if (J >= band0 && J < R) continue;
-                }
-                sg += Ypart[static_cast<int64_t>(k) * nb + i];
-            }
-        }
+        const T sg = (i < nb) ? slot_group_sum<T>(Ypart, nslots, nsub, band0, R, nb, i, q) : T(0);
         grp[q][lane] = sg;
         __syncthreads();
         if (q == 0 && i < nb) {
@@ -815,16 +831,7 @@ __global__ void __launch_bounds__(kVecThreads)
     for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
         const int64_t i = ch * 32 + lane;
         const int R = static_cast<int>((g0 + ch * 32) / kTile);
-        T sg = T(0);
-        if (i < nb) {
-            for (int k = q; k < nslots; k += G) {
-                if (nsub == 2 && (k & 1)) {
-                    const int J = k >> 1;
-                    if (J >= band0 && J < R) continue;
-                }
-                sg += Ypart[static_cast<int64_t>(k) * nb + i];
-            }
-        }
+        const T sg = (i < nb) ? slot_group_sum<T>(Ypart, nslots, nsub, band0, R, nb, i, q) : T(0);
         grp[q][lane] = sg;
         __syncthreads();
         if (q == 0 && i < nb) {

@@ -328,12 +328,14 @@ __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpa
 // rounded to the fixed-point grid 2^{E_i - BITS} of its maximum (exact for |x| >= 2^{E_i-2} with S = 7)
 // and written in S balanced base-256 int8 digit planes (plane 0 = most significant), stored
 // PRE-SWIZZLED as the shared-memory images the UMMA reads:
-//   DA[rows/128][nk][S][128 x 32 B]  (row-operand role: 128-point blocks)
-//   DB[rows/64 ][nk][S][ 64 x 32 B]  (column-operand role: one CTA's half of a 2-SM B tile)
+//   DA[rows/128][nk][S][128 x 32 B]  (128-point blocks)
 // (nk = dpad8 / 32 feature slabs), each 32-byte row in the SWIZZLE_32B pattern (16-byte chunk
-// index XOR bit 2 of the row).  A stage of the tile kernel is then ONE contiguous block per
-// operand, moved by TMA in 128-byte rows with no swizzle (4x fewer, 4x larger requests than
-// a 32-byte-row box: the tile kernel was feed-bound with them).  Either pointer may be null.
+// index XOR bit 2 of the row).  A stage of the tile kernel is then ONE contiguous block for the
+// row operand, moved by TMA in 128-byte rows with no swizzle (4x fewer, 4x larger requests than
+// a 32-byte-row box: the tile kernel was feed-bound with them), and for the column operand (one
+// CTA's 64-point half of a 2-SM B tile) the half of every plane's image, [planes][64 x 32 B]: the
+// swizzle depends on bit 2 of the row only, so a 64-row half of a 128-row image is itself a valid
+// 64-row image.  One layout serves both roles (the digits are written, stored and L2-cached once).
 // Row scales sc_i = 2^{E_i - SC_SHIFT} (S = 7: x_i . x_j = sc_i sc_j sum_l 2^{-8l} acc_l;
 // S = 3: sc_i sc_j (acc_0 2^16 + acc_1 2^8 + acc_2)).  S = 7: N = rn(x 2^{54-E}), |N| < 2^54 (exact
 // for the features within a factor 4 of the row maximum, rounded to 2^{E-54} below); S = 3 rounds the
@@ -341,7 +343,7 @@ __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpa
 // row; 4 features per lane per step.
 template <int S, typename TIN>
 __global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t dpad8,
-                              int8_t *__restrict__ DA, int8_t *__restrict__ DB, double *__restrict__ sc) {
+                              int8_t *__restrict__ DA, double *__restrict__ sc) {
     static_assert(8 * S >= Oz<S>::BITS + 1, "S balanced base-256 digits must hold the split integer");
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -355,8 +357,8 @@ __global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t 
     if (mx > 0.0) frexp(mx, &E);  // mx = f 2^E, f in [0.5, 1)  =>  |x_ik| < 2^E
     if (lane == 0) sc[i] = ldexp(1.0, E - Oz<S>::SC_SHIFT);
     const int64_t nk = dpad8 / 32;
-    const int r128 = static_cast<int>(i & 127), r64 = static_cast<int>(i & 63);
-    const int flip = (r128 >> 2) & 1;  // = (r64 >> 2) & 1
+    const int r128 = static_cast<int>(i & 127);
+    const int flip = (r128 >> 2) & 1;
     for (int64_t k0 = 4 * lane; k0 < dpad8; k0 += 128) {
         long long N[4];
 #pragma unroll
@@ -365,8 +367,7 @@ __global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t 
         const int64_t kb = k0 >> 5;
         const int c = static_cast<int>(k0 & 31);
         const int inrow = ((((c >> 4) ^ flip) << 4) | (c & 15));
-        int8_t *pa = DA ? DA + ((i >> 7) * nk + kb) * (S * 4096) + r128 * 32 + inrow : nullptr;
-        int8_t *pb = DB ? DB + ((i >> 6) * nk + kb) * (S * 2048) + r64 * 32 + inrow : nullptr;
+        int8_t *pa = DA + ((i >> 7) * nk + kb) * (S * 4096) + r128 * 32 + inrow;
 #pragma unroll
         for (int a = S - 1; a >= 0; --a) {  // least significant digit first
             char4 dg;
@@ -377,8 +378,7 @@ __global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t 
                 N[v] = (N[v] - dd) >> 8;                                       // exact
                 dv[v] = dd;
             }
-            if (pa) *reinterpret_cast<char4 *>(pa + a * 4096) = dg;
-            if (pb) *reinterpret_cast<char4 *>(pb + a * 2048) = dg;
+            *reinterpret_cast<char4 *>(pa + a * 4096) = dg;
         }
     }
 }
@@ -448,7 +448,8 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t *bar) {  // arrive o
 //                  rows, with the mirrored transposed copy) -- k_precompute's layout
 //  OZ_PREDICT    : alpha_j k(z_i, x_j) -> Fpart[J][npad]
 // ta4/ta8: maps over the pre-swizzled row-operand digits DA (boxes of 4 / 8 planes of a 128-point
-// slab block, 128-byte rows); tb4/tb8: the same over DB (64-point half blocks).
+// slab block, 128-byte rows); tb4/tb8: 3-D maps over the SAME digits selecting one 64-point half of a
+// block (driver.cu make_tmap_digit_halves).
 // T: the value type of the epilogue and of q, norms, p, the products and Q~ (double with S = 7,
 // float with S = 3); the digit scales are fp64 either way.
 template <int KT, int S, int MODE, typename T>
@@ -554,11 +555,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         }
                         if (leader) mbar_expect_tx(&full[s], 2u * np * (O::PLANE + O::PLANE / 2));  // both CTAs' bytes
                         const uint32_t fb = full0 + s * 8;
-                        // pre-swizzled blocks: A (row block I0 + r, slab kb) = S x 4 KiB at 128-B row
-                        // (I * nk + kb) * 256; B (64-row block 2 J + r, slab kb) = S x 2 KiB at (.) * 128
+                        // pre-swizzled blocks: A (row block I0 + r, slab kb) = np x 4 KiB at 128-B row
+                        // (I * nk + kb) * S * 32; B = half r of block J: rows 16 r .. 16 r + 15 of the
+                        // planes (J * nk + kb) * S + a, a < np
                         tma_load_2d_2sm(st, np == S ? &ta8 : &ta4, fb, 0, ((I0 + int(rank)) * nk + kb) * (S * 32));  // ta8: all S planes
-                        tma_load_2d_2sm(st + np * O::PLANE, np == S ? &tb8 : &tb4, fb, 0,
-                                        ((2 * J + int(rank)) * nk + kb) * (S * 16));
+                        tma_load_3d_2sm(st + np * O::PLANE, np == S ? &tb8 : &tb4, fb, 0, 16 * int(rank),
+                                        (J * nk + kb) * S);
                     }
                 }
             }
@@ -688,7 +690,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     if (T_tiles >= 0 && mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
                 }
             }
-            T sv[64];
+            // the thread's 64 entries, one 64-bit register pair each: S = 7 the pass-0 V + 3 2^51, then the
+            // fp64 contractions' bits; S = 3 V + 3 2^51, then the fp32 contractions' bits (one array for
+            // both stages keeps the epilogue within the kernel's register budget)
+            long long sv[64];
+            auto sval = [&](int k) -> T {
+                if constexpr (S == 7) return __longlong_as_double(sv[k]);
+                else return __int_as_float(static_cast<int>(sv[k]));
+            };
             const bool prof = warp == 4 && lane == 0;
             (void)prof;
             if constexpr (S == 7) {
@@ -714,7 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                             // V + 3 2^51, exact in int64; held as bits until pass 1 knows the scale
                             const long long Vb = mad_wide(r0[j], 1 << 24, mad_wide(r1[j], 1 << 16,
                                                            mad_wide(r2[j], 1 << 8, mad_wide(r3[j], 1, kOzBias))));
-                            sv[c * 8 + j] = bigd ? i64_to_f64_exact(Vb - kOzBias) : __longlong_as_double(Vb);
+                            sv[c * 8 + j] = bigd ? __double_as_longlong(i64_to_f64_exact(Vb - kOzBias)) : Vb;
                         }
                     }
                 }
@@ -731,35 +740,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             OZ_PROF_T0(tdr1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             ++e;
-            if (!(dbg & 1)) {
+            if constexpr (S == 3) {
+                // fp32 engine (one pass, no second TMEM buffer): the drain only combines the levels
+                // (V + 3 2^51, exact int64), the accumulators are released, and the conversions run
+                // under the next pair-tile's MMAs (the MMA waited ~8 % of its loop for drains, C3)
+                if (!(dbg & 1)) {
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t r0[8], r1[8], r2[8];
-                    tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
-                    tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
-                    tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
-                    tmem_ld_wait();
+                    for (int c = 0; c < 8; ++c) {
+                        uint32_t r0[8], r1[8], r2[8];
+                        tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
+                        tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
+                        tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int lc = grp * 64 + c * 8 + j;
-                        const int kb = rkb + colk[lc];
-                        if constexpr (S == 7) {
+                        for (int j = 0; j < 8; ++j)  // S = 3: x_i.x_j = 2^k V, |V| < d 2^30.01 < 2^51
+                            sv[c * 8 + j] = mad_wide(r0[j], 1 << 16, mad_wide(r1[j], 1 << 8, mad_wide(r2[j], 1, kOzBias)));
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty0);  // the next pair-tile's MMAs may start
+                if (!(dbg & 1)) {
+#pragma unroll
+                    for (int k = 0; k < 64; ++k)  // then one rounding to fp32
+                        sv[k] = static_cast<uint32_t>(__float_as_int(static_cast<float>(scaled_exact(sv[k], rkb + colk[grp * 64 + k]))));
+                }
+            } else {
+                if (!(dbg & 1)) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        uint32_t r0[8], r1[8], r2[8];
+                        tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
+                        tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
+                        tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int kb = rkb + colk[grp * 64 + c * 8 + j];
                             // x_i.x_j = 2^k V + 2^{k-24} W (level 4 is 2^-32 below level 0, W carries 2^16
                             // of it), both terms exact: ONE rounding in their sum
                             const long long Wb = mad_wide(r0[j], 1 << 16, mad_wide(r1[j], 1 << 8, mad_wide(r2[j], 1, kOzBias)));
                             const double dw = scaled_exact(Wb, kb - (24 << 20));
-                            sv[c * 8 + j] = bigd ? fma(sv[c * 8 + j], __hiloint2double(kb - (51 << 20), 0), dw)  // x 2^k
-                                                 : scaled_exact(__double_as_longlong(sv[c * 8 + j]), kb) + dw;
-                        } else {  // S = 3: x_i.x_j = 2^k V, |V| < d 2^30.01 < 2^51, then one rounding to fp32
-                            const long long Vb = mad_wide(r0[j], 1 << 16, mad_wide(r1[j], 1 << 8, mad_wide(r2[j], 1, kOzBias)));
-                            sv[c * 8 + j] = static_cast<T>(scaled_exact(Vb, kb));
+                            sv[c * 8 + j] = __double_as_longlong(
+                                bigd ? fma(__longlong_as_double(sv[c * 8 + j]), __hiloint2double(kb - (51 << 20), 0), dw)  // x 2^k
+                                     : scaled_exact(sv[c * 8 + j], kb) + dw);
                         }
                     }
                 }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty0);  // the next pair-tile's MMAs may start
             }
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty0);  // the next pair-tile's MMAs may start
             if (prof) OZ_PROF_ADD(6, tdr1);
             OZ_PROF_T0(twork);
             if (!(dbg & 1)) {
@@ -774,12 +805,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         T kv;
                         if constexpr (kTabExp) {  // kernel_value's RBF (distance clamped at 0, exactly 0 on
                             // the diagonal, R-9) in the scaled exponent form of exp_tab256
-                            double tp = fma(a2, sv[c * 8 + j], ni + coln[lc]);
+                            double tp = fma(a2, sval(c * 8 + j), ni + coln[lc]);
                             tp = fmin(tp, 0.0);
                             if (diag) tp = 0.0;
                             kv = exp_tab256(tp, etab);
                         } else {
-                            kv = kernel_value<KT, T>(sv[c * 8 + j], ni, coln[lc], diag, kp);
+                            kv = kernel_value<KT, T>(sval(c * 8 + j), ni, coln[lc], diag, kp);
                         }
                         if constexpr (MODE == OZ_PREDICT) {
                             rs = fma(colp[lc], kv, rs);
