@@ -414,3 +414,28 @@ def test_c2_full_training_vs_exact_ridge_solution():
         assert st == 0 and ea <= 1e-7 and eb <= 1e-7, (mode, ea, eb)
         if mode == pl.MODE_AUTO:
             assert s.mode_used == pl.MODE_CACHED
+
+
+def test_c2_residual_replacement_stagnation_guard():
+    """SURVEY §8(a5) / §5 and App. A.7 (DESIGN R-20): at C2 (kappa ~ 2.6e8) Shewchuk's every-50 residual
+    replacement oscillates between 1e-9 and 1e-6 and never reaches eps = 1e-10; the stagnation guard
+    (no 4x drop of delta below the best within 2 max(R, 50) iterations) must stop it near the survey's
+    143 iterations with W_NOT_CONVERGED, alpha and b filled, instead of running to m - 1 = 65535.  The
+    model is checked against the exact ridge solution (survey: within 3.3e-9 at the guard's exit)."""
+    cfg = synth.configs()["C2"]
+    X, y, _, _ = synth.config_data(cfg, n_test=0)
+    xb, yb = X.mean(0), y.mean()
+    Xc, yc = X - xb, y - yb
+    w = np.linalg.solve(Xc.T @ Xc + np.eye(X.shape[1]) / cfg.C, Xc.T @ yc)
+    b_ex = yb - xb @ w
+    a_ex = cfg.C * (y - X @ w - b_ex)
+    a, b, st, s = pl.plssvm_train_ex(X, y, cfg.kernel, cfg.gamma, C=cfg.C, eps=cfg.eps,
+                                     opts=pl.options(replace_every=50))
+    ea = rel(a, a_ex)
+    eb = abs(b - b_ex) / max(abs(b_ex), np.abs(a_ex).max())
+    print(f"C2 replace_every=50: status {st}, stop {s.stop_reason}, {s.iterations} iterations, "
+          f"rel residual {s.rel_residual:.2e}, |da|/|a| = {ea:.2e}, db = {eb:.2e}")
+    assert st == pl.binding.W_NOT_CONVERGED and s.stop_reason == pl.binding.STOP_STAGNATED
+    assert 100 <= s.iterations <= 400
+    assert abs(np.sum(a)) <= 1e-8 * np.abs(a).sum()
+    assert ea <= 1e-7 and eb <= 1e-7, (ea, eb)
