@@ -229,14 +229,17 @@ RowStats validate_inputs(Arena &A, std::initializer_list<VCheck<T>> arrays, cons
     PLS_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(unsigned), s));
     bool first = true;
     for (const VCheck<T> &v : arrays) {
-        k_validate<T><<<4 * 148, 256, 0, s>>>(v.a, v.n, v.bit, first ? y : nullptr, m, flags);
-        PLS_CHECK_LAUNCH();
-        ++launches;
+        // row arrays: k_row_peak checks finiteness in the same pass (k_validate then only checks labels)
+        if (v.row_len == 0 || (first && y)) {
+            k_validate<T><<<4 * 148, 256, 0, s>>>(v.a, v.row_len > 0 ? 0 : v.n, v.bit, first ? y : nullptr, m, flags);
+            PLS_CHECK_LAUNCH();
+            ++launches;
+        }
         first = false;
         if (v.row_len > 0) {
             const int64_t rows = v.n / v.row_len;
             k_row_peak<T><<<static_cast<unsigned>(std::max<int64_t>(1, ceil_div(rows * 32, 256))), 256, 0, s>>>(
-                v.a, rows, v.row_len, v.row_len, flags + 1);
+                v.a, rows, v.row_len, v.row_len, flags + 1, flags, v.bit);
             PLS_CHECK_LAUNCH();
             ++launches;
         }
@@ -643,16 +646,16 @@ int num_sms() {
 // S digit planes of the point-major padded array Xp (fp64 with S = 7, fp32 with S = 3).  Maps:
 // t8 / h8 carry all S planes of a slab block, t4 / h4 the first LV planes (S = 7's pass 1).
 template <int S, typename TIN>
-OzOperand oz_prepare(Arena &A, const TIN *Xp, int64_t rows, int64_t dpad, int64_t d, bool row_role, bool col_role,
-                     cudaStream_t s, int64_t &launches) {
+OzOperand oz_prepare(Arena &A, const TIN *Xp, int64_t rows, int64_t m_valid, int64_t dpad, int64_t d, bool row_role,
+                     bool col_role, cudaStream_t s, int64_t &launches) {
     using O = Oz<S>;
     OzOperand o;
     const int64_t d8 = round_up(d, O::BK);
     const int64_t bytes = S * rows * d8;
     o.DA = A.alloc<int8_t>(bytes);
     o.sc = A.alloc<double>(rows);
-    k_ozaki_split<S, TIN><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, s>>>(Xp, rows, dpad, d8, o.DA,
-                                                                                         o.sc);
+    k_ozaki_split<S, TIN><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, s>>>(Xp, rows, m_valid, dpad, d8,
+                                                                                         o.DA, o.sc);
     PLS_CHECK_LAUNCH();
     ++launches;
     if (row_role) {
@@ -665,18 +668,6 @@ OzOperand oz_prepare(Arena &A, const TIN *Xp, int64_t rows, int64_t dpad, int64_
     }
     o.nk = static_cast<int>(d8 / O::BK);
     return o;
-}
-
-// Point-major padded fp32 copy [rows][d8] of the caller's row-major X (zero padding) -- the
-// layout k_ozaki_split reads; the fp32 engines otherwise use the feature-major one.
-float *oz_point_major(Arena &A, const float *Xs, int64_t m, int64_t d, int64_t rows, int64_t d8, cudaStream_t s,
-                      int64_t &launches) {
-    float *Xp = A.alloc<float>(rows * d8);
-    dim3 grid(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(ceil_div(d8, 32)));
-    k_transform<float><<<grid, dim3(32, 8), 0, s>>>(Xs, m, d, Xp, rows, d8, 1);
-    PLS_CHECK_LAUNCH();
-    ++launches;
-    return Xp;
 }
 
 // fp64 engine choice (plssvm.h plssvm_fp64_engine_t): OZAKI, DMMA, or AUTO.  AUTO takes OZAKI only
@@ -1127,37 +1118,38 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
                                  c.s, c.launches);
     }
     PLS_CUDA(cudaEventRecord(e_h2d, c.s));
-    c.Xt = A.alloc<T>(g.dpad * g.mpad);
-    launch_transform<T>(Xs, pb.m, dl, c.Xt, g.mpad, g.dpad, c.s, c.launches);
-    c.ops = make_ops(c.Xt, g.mpad, c.Xt, g.mpad, g.ld);
+    // The int8 engines split the caller's row-major X directly (padding rows read as 0) and the q /
+    // norm pass reads it too: no transformed copy.  The other engines use the transformed layout.
     if constexpr (std::is_same<T, double>::value) {
         c.oz = oz_choose(o.fp64_engine, rho, g.mpad, dl);
         if (c.oz) {
-            c.ozx = oz_prepare<7, double>(A, c.Xt, g.mpad, g.dpad, dl, true, true, c.s, c.launches);
+            c.ozx = oz_prepare<7, double>(A, Xs, g.mpad, pb.m, dl, dl, true, true, c.s, c.launches);
             oz_set_attrs<double>();
         }
     } else {
         if (o.fp32_engine == PLSSVM_FP32_OZAKI || o.fp32_engine == PLSSVM_FP32_AUTO) {
-            // fp32 on the int8 tensor cores (3 digits): a point-major padded copy to split
-            const int64_t d8 = round_up(dl, Oz<3>::BK);
-            c.oz = oz_choose_f32(o.fp32_engine, rho, dl);
+            c.oz = oz_choose_f32(o.fp32_engine, rho, dl);  // fp32 on the int8 tensor cores (3 digits)
             if (c.oz) {
-                float *Xp = oz_point_major(A, Xs, pb.m, dl, g.mpad, d8, c.s, c.launches);
-                c.ozx = oz_prepare<3, float>(A, Xp, g.mpad, d8, dl, true, true, c.s, c.launches);
+                c.ozx = oz_prepare<3, float>(A, Xs, g.mpad, pb.m, dl, dl, true, true, c.s, c.launches);
                 oz_set_attrs<float>();
             }
         }
         c.tc = !c.oz && o.fp32_engine != PLSSVM_FP32_FFMA;
         if (c.tc) setup_tc<T>(c, A, Xs, pb.m, dl);
     }
+    if (!c.oz) {
+        c.Xt = A.alloc<T>(g.dpad * g.mpad);
+        launch_transform<T>(Xs, pb.m, dl, c.Xt, g.mpad, g.dpad, c.s, c.launches);
+        c.ops = make_ops(c.Xt, g.mpad, c.Xt, g.mpad, g.ld);
+    }
     PLS_CUDA(cudaEventRecord(e_tr, c.s));
     c.q = A.alloc<T>(g.mpad);
     c.nrm = A.alloc<T>(g.mpad);
     c.scal = A.alloc<double>(S_COUNT);
     PLS_CUDA(cudaMemsetAsync(c.scal, 0, S_COUNT * sizeof(double), c.s));
-    k_q_norms<T><<<static_cast<unsigned>(ceil_div(g.mpad * 32, 256)), 256, 0, c.s>>>(c.Xt, g.mpad, g.dpad, pb.m, dl,
-                                                                                      c.kp, c.invC, c.ylab, c.q, c.nrm,
-                                                                                      c.scal);
+    // (int8 engines: from the caller's row-major X, row stride dl)
+    k_q_norms<T><<<static_cast<unsigned>(ceil_div(g.mpad * 32, 256)), 256, 0, c.s>>>(
+        c.oz ? Xs : c.Xt, g.mpad, g.dpad, pb.m, dl, c.kp, c.invC, c.ylab, c.q, c.nrm, c.scal, c.oz ? dl : 0);
     PLS_CHECK_LAUNCH();
     ++c.launches;
     PLS_CUDA(cudaEventRecord(e_q, c.s));
@@ -1770,29 +1762,36 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
         }
         return PLSSVM_OK;
     }
-    T *Xl = A.alloc<T>(dpad * xrows), *Zl = A.alloc<T>(dpad * zrows);
-    launch_transform<T>(Xs, m, d, Xl, xrows, dpad, s, launches);
-    launch_transform<T>(Zs, n, d, Zl, zrows, dpad, s, launches);
+    bool oz64 = false;  // (the name: the Ozaki engine of either precision)
+    if constexpr (std::is_same<T, double>::value) {
+        oz64 = oz_choose(o.fp64_engine, rho, std::max(zrows, xrows), d);
+    } else if (o.fp32_engine == PLSSVM_FP32_OZAKI || o.fp32_engine == PLSSVM_FP32_AUTO) {
+        oz64 = oz_choose_f32(o.fp32_engine, rho, d);
+    }
+    // the int8 engines split (and take norms of) the caller's row-major X and Z directly; the other
+    // engines use the transformed layouts
+    T *Xl = nullptr, *Zl = nullptr;
+    if (!oz64) {
+        Xl = A.alloc<T>(dpad * xrows);
+        Zl = A.alloc<T>(dpad * zrows);
+        launch_transform<T>(Xs, m, d, Xl, xrows, dpad, s, launches);
+        launch_transform<T>(Zs, n, d, Zl, zrows, dpad, s, launches);
+    }
     T *alpha = A.alloc<T>(xrows);
     PLS_CUDA(cudaMemsetAsync(alpha, 0, xrows * sizeof(T), s));
     PLS_CUDA(cudaMemcpyAsync(alpha, al, m * sizeof(T), cudaMemcpyDeviceToDevice, s));
     T *nx = A.alloc<T>(xrows), *nz = A.alloc<T>(zrows);
     KParams<T> kp{pb.kernel, static_cast<T>(pb.gamma), pb.degree, static_cast<T>(pb.coef0)};
     if (pb.kernel == RBF) {
-        k_norms<T><<<static_cast<unsigned>(ceil_div(xrows * 32, 256)), 256, 0, s>>>(Xl, xrows, dpad, xrows, d, nx);
-        k_norms<T><<<static_cast<unsigned>(ceil_div(zrows * 32, 256)), 256, 0, s>>>(Zl, zrows, dpad, zrows, d, nz);
+        if (oz64) {  // rows m .. xrows - 1 (n .. zrows - 1) get 0
+            k_norms<T><<<static_cast<unsigned>(ceil_div(xrows * 32, 256)), 256, 0, s>>>(Xs, xrows, dpad, m, d, nx, d);
+            k_norms<T><<<static_cast<unsigned>(ceil_div(zrows * 32, 256)), 256, 0, s>>>(Zs, zrows, dpad, n, d, nz, d);
+        } else {
+            k_norms<T><<<static_cast<unsigned>(ceil_div(xrows * 32, 256)), 256, 0, s>>>(Xl, xrows, dpad, xrows, d, nx);
+            k_norms<T><<<static_cast<unsigned>(ceil_div(zrows * 32, 256)), 256, 0, s>>>(Zl, zrows, dpad, zrows, d, nz);
+        }
         PLS_CHECK_LAUNCH();
         launches += 2;
-    }
-    bool oz64 = false;  // (the name: the Ozaki engine of either precision)
-    const T *Xoz = nullptr, *Zoz = nullptr;  // fp32: point-major padded copies for the split
-    if constexpr (std::is_same<T, double>::value) {
-        oz64 = oz_choose(o.fp64_engine, rho, std::max(zrows, xrows), d);
-    } else if (o.fp32_engine == PLSSVM_FP32_OZAKI || o.fp32_engine == PLSSVM_FP32_AUTO) {
-        const int64_t d8 = round_up(d, Oz<3>::BK);
-        Zoz = oz_point_major(A, Zs, n, d, npad, d8, s, launches);
-        Xoz = oz_point_major(A, Xs, m, d, mpad, d8, s, launches);
-        oz64 = oz_choose_f32(o.fp32_engine, rho, d);
     }
     const bool tc = std::is_same<T, float>::value && !oz64 && o.fp32_engine != PLSSVM_FP32_FFMA;
     const int tilesI = static_cast<int>(npad / kTile),
@@ -1834,14 +1833,9 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
     const bool oz = oz64;
     if (oz) {  // int8 tensor cores: test points = row operand, training points = columns
         OzOperand oz_z, oz_x;
-        if constexpr (std::is_same<T, double>::value) {
-            oz_z = oz_prepare<7, double>(A, Zl, zrows, dpad, d, true, false, s, launches);
-            oz_x = oz_prepare<7, double>(A, Xl, xrows, dpad, d, false, true, s, launches);
-        } else {
-            const int64_t d8 = round_up(d, Oz<3>::BK);
-            oz_z = oz_prepare<3, float>(A, Zoz, npad, d8, d, true, false, s, launches);
-            oz_x = oz_prepare<3, float>(A, Xoz, mpad, d8, d, false, true, s, launches);
-        }
+        constexpr int S = oz_digits<T>();
+        oz_z = oz_prepare<S, T>(A, Zs, npad, n, d, d, true, false, s, launches);
+        oz_x = oz_prepare<S, T>(A, Xs, mpad, m, d, d, false, true, s, launches);
         oz_set_attrs<T>();
         PLS_CUDA(cudaEventRecord(e0, s));
         oz_dispatch<OZ_PREDICT, T>(pb.kernel, ((tilesI + 1) / 2) * tilesJ, s, oz_z, oz_x,
@@ -1851,7 +1845,7 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
                                    static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,
                                    static_cast<T *>(nullptr), 0, static_cast<const int *>(nullptr));
     }
-    const Ops<T> pops = make_ops(Zl, zrows, Xl, xrows, EN::kPointMajor ? dpad : L);
+    const Ops<T> pops = (tc || oz64) ? Ops<T>{} : make_ops(Zl, zrows, Xl, xrows, EN::kPointMajor ? dpad : L);
     if (!tc && !oz) PLS_CUDA(cudaEventRecord(e0, s));
     if (!tc && !oz) switch (pb.kernel) {
         case LINEAR:

@@ -149,14 +149,19 @@ __device__ __forceinline__ T elem(const T *X, int64_t i, int64_t k, int64_t mpad
 // One warp per point (lanes stride the features; fixed shuffle tree -> deterministic).
 template <typename T>
 __global__ void k_q_norms(const T *__restrict__ X, int64_t mpad, int64_t dpad, int64_t m, int64_t d, KParams<T> kp,
-                          T invC, const T *__restrict__ y, T *__restrict__ q, T *__restrict__ nrm, double *scal) {
+                          T invC, const T *__restrict__ y, T *__restrict__ q, T *__restrict__ nrm, double *scal,
+                          int64_t ld_raw) {
+    // ld_raw > 0: X is the caller's row-major m x d array (row stride ld_raw; rows >= m read as 0),
+    // else the engine's padded layout
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= mpad) return;
     const int64_t xm = m - 1;
+    const bool real = i < m;
     T s = T(0), n = T(0), dist = T(0);
     for (int64_t k = lane; k < d; k += 32) {
-        const T a = elem(X, i, k, mpad, dpad), b = elem(X, xm, k, mpad, dpad);
+        const T a = ld_raw > 0 ? (real ? X[i * ld_raw + k] : T(0)) : elem(X, i, k, mpad, dpad);
+        const T b = ld_raw > 0 ? X[xm * ld_raw + k] : elem(X, xm, k, mpad, dpad);
         s = fma(a, b, s);
         n = fma(a, a, n);
         const T t = a - b;
@@ -1057,13 +1062,15 @@ __global__ void __launch_bounds__(Engine<T>::THREADS, Engine<T>::MIN_BLOCKS)
 }
 
 template <typename T>
-__global__ void k_norms(const T *__restrict__ X, int64_t mpad, int64_t dpad, int64_t n, int64_t d, T *__restrict__ nrm) {
+__global__ void k_norms(const T *__restrict__ X, int64_t mpad, int64_t dpad, int64_t n, int64_t d, T *__restrict__ nrm,
+                        int64_t ld_raw = 0) {
+    // ld_raw > 0: X is the caller's row-major n x d array (row stride ld_raw), rows n .. mpad - 1 get 0
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (i >= n) return;
+    if (i >= (ld_raw > 0 ? mpad : n)) return;
     T s = T(0);
     for (int64_t k = lane; k < d; k += 32) {
-        const T a = elem(X, i, k, mpad, dpad);
+        const T a = ld_raw > 0 ? (i < n ? X[i * ld_raw + k] : T(0)) : elem(X, i, k, mpad, dpad);
         s = fma(a, a, s);
     }
 #pragma unroll

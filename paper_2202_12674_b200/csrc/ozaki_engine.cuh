@@ -295,18 +295,26 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
 // point-major padded fp64 array (zero rows skipped), as float bits in *peak_bits (atomicMax on
 // the bits of a non-negative float orders like the value), and the largest |E_i| of the row
 // maxima (2^{E_i-1} <= ||x_i||_inf < 2^{E_i}) in peak_bits[1]: the epilogue's one-operation
-// conversions need the digit scales' exponents in range (kOzMaxExp).  One warp per row.
+// conversions need the digit scales' exponents in range (kOzMaxExp).  The same pass is the input
+// validation of the array (driver.cu validate_inputs): a non-finite element sets `bad` in flags[0].
+// One warp per row.
 template <typename TIN>
 __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t d,
-                           unsigned *__restrict__ peak_bits) {
+                           unsigned *__restrict__ peak_bits, unsigned *__restrict__ flags, unsigned bad) {
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= rows) return;
     double mx = 0.0, ss = 0.0;
+    bool fin = true;
     for (int64_t k = lane; k < d; k += 32) {
         const double v = static_cast<double>(Xp[i * dpad + k]);
+        fin = fin && isfinite(v);
         mx = fmax(mx, fabs(v));
         ss = fma(v, v, ss);
+    }
+    if (!__all_sync(0xffffffffu, fin)) {
+        if (lane == 0) atomicOr(flags, bad);
+        return;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -324,7 +332,8 @@ __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpa
     }
 }
 
-// Digit split of the point-major padded array Xp[rows][dpad] (rows a multiple of 128): each row is
+// Digit split of the point-major array Xp[rows][dpad] (row stride dpad; rows a multiple of 128, rows
+// m_valid .. rows - 1 are padding and read as 0 -- the caller's unpadded X can be split directly): each row is
 // rounded to the fixed-point grid 2^{E_i - BITS} of its maximum (exact for |x| >= 2^{E_i-2} with S = 7)
 // and written in S balanced base-256 int8 digit planes (plane 0 = most significant), stored
 // PRE-SWIZZLED as the shared-memory images the UMMA reads:
@@ -342,15 +351,17 @@ __global__ void k_row_peak(const TIN *__restrict__ Xp, int64_t rows, int64_t dpa
 // (fp32) value to N = rint(x 2^{22-E}), |N| <= 2^22, which three balanced digits hold.  One warp per
 // row; 4 features per lane per step.
 template <int S, typename TIN>
-__global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t dpad, int64_t dpad8,
+__global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t m_valid, int64_t dpad, int64_t dpad8,
                               int8_t *__restrict__ DA, double *__restrict__ sc) {
     static_assert(8 * S >= Oz<S>::BITS + 1, "S balanced base-256 digits must hold the split integer");
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= rows) return;
     const TIN *x = Xp + i * dpad;
+    const bool real = i < m_valid;  // rows m_valid .. rows - 1: padding, all digits 0
     double mx = 0.0;
-    for (int64_t k = lane; k < dpad; k += 32) mx = fmax(mx, fabs(static_cast<double>(x[k])));
+    if (real)
+        for (int64_t k = lane; k < dpad; k += 32) mx = fmax(mx, fabs(static_cast<double>(x[k])));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     int E = 0;
@@ -363,7 +374,7 @@ __global__ void k_ozaki_split(const TIN *__restrict__ Xp, int64_t rows, int64_t 
         long long N[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v)  // |N| < 2^{BITS}; exact when x's ulp >= 2^{E-BITS}, else rounded to nearest
-            N[v] = (k0 + v < dpad) ? __double2ll_rn(ldexp(static_cast<double>(x[k0 + v]), Oz<S>::BITS - E)) : 0ll;
+            N[v] = (real && k0 + v < dpad) ? __double2ll_rn(ldexp(static_cast<double>(x[k0 + v]), Oz<S>::BITS - E)) : 0ll;
         const int64_t kb = k0 >> 5;
         const int c = static_cast<int>(k0 & 31);
         const int inrow = ((((c >> 4) ^ flip) << 4) | (c & 15));
