@@ -65,6 +65,15 @@ def measured_peaks():
         return {}
 
 
+def ncu_entry(key):
+    """The ncu capture record of the dominant kernel (profiles/roofline_traffic.json), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as fh:
+            return json.load(fh).get(key) or {}
+    except (OSError, ValueError):
+        return {}
+
+
 def traffic_for(key):
     """ncu-measured DRAM bytes per launch of the dominant kernel (profiles/roofline_traffic.json)."""
     try:
@@ -403,6 +412,10 @@ def main():
                 "peak_source": "int8 dense = 2 x MEASURED_PEAKS.json bf16_tflops_sustained (guide ratio 4.5/2.25; "
                                "the kernel runs back to back at the 1 kW power cap)",
                 "frac_of_burst_peak": achieved / int8_peak_tops(sustained=False),
+                # utilisation as ncu counts it (one cold, serialised capture; profiles/): the tensor pipe's
+                # active cycles, which the fractions above (against a measured GEMM rate) can overstate
+                "ncu_tensor_pipe_pct": ncu_entry(f"{cfg.name}/implicit/k_tile_ozaki").get("ncu_tensor_pipe_pct")
+                if world == 1 else None,
                 "avg_launch_s": avg_mv}
         if cfg.dtype == "f64":
             roof["fp64_equivalent"] = {"achieved_tflops": fl / avg_mv / 1e12, "dmma_peak_tflops": FP64_PEAK_TFLOPS,
