@@ -207,7 +207,9 @@ typedef struct {
     int32_t fp64_engine_used;        /* PLSSVM_FP64_OZAKI or _DMMA for fp64 calls, 0 for fp32 */
     int32_t cg_loop_used;            /* PLSSVM_CG_BATCHED or PLSSVM_CG_GRAPH */
     int32_t fp32_engine_used;        /* fp32 calls: PLSSVM_FP32_OZAKI, _TCGEN05 or _FFMA; 0 for fp64 */
-    int32_t reserved1;
+    int32_t allgather_fused;         /* 1: the all-gather of p was part of the p update kernel (NCCL device
+                                        API stores into the ranks' symmetric windows, or the PEER
+                                        transport's peer stores); 0: a separate collective or one GPU */
     double t_comm;                   /* summed duration of the CG loop's collectives (all-gather of p,
                                         scalar all-reduces, reduce-scatter of the partial products;
                                         CUDA events, batched loop; 0 on one GPU) -- inside t_matvec for

@@ -54,7 +54,7 @@ class plssvm_stats_t(ct.Structure):
                 ("t_cg", ct.c_double), ("t_bias_d2h", ct.c_double), ("t_total", ct.c_double),
                 ("t_matvec", ct.c_double), ("t_matvec_min", ct.c_double), ("bytes_per_gpu", ct.c_int64),
                 ("gpu_launches", ct.c_int64), ("launches_in_cg", ct.c_int64), ("fp64_engine_used", ct.c_int32),
-                ("cg_loop_used", ct.c_int32), ("fp32_engine_used", ct.c_int32), ("reserved1", ct.c_int32),
+                ("cg_loop_used", ct.c_int32), ("fp32_engine_used", ct.c_int32), ("allgather_fused", ct.c_int32),
                 ("t_comm", ct.c_double), ("rel_residual_true", ct.c_double), ("stop_reason", ct.c_int32),
                 ("transport_used", ct.c_int32)]
 

@@ -13,8 +13,10 @@
 //              CG update kernel (direct peer stores, driver.cu); ranks may share a device.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <string>
 #include <thread>
@@ -173,6 +175,64 @@ std::vector<void *> comm_peer_exchange_ptr(CommHandle *c, void *ptr) {
 }
 bool comm_peer_direct(const CommHandle *c) { return c->kind == COMM_PEER && c->group->direct; }
 
+// ---- NCCL device API: symmetric window of p (fused all-gather) --------------
+// Every rank's full p lives in one NCCL symmetric window (ncclMemAlloc + ncclCommWindowRegister,
+// NCCL_WIN_COLL_SYMMETRIC); the p update kernel stores the new band straight into every LSA peer's
+// window (ncclGetLsaPointer: NVLink loads/stores) and meets the peers in a per-block LSA barrier
+// (kernels.cuh k_update_p_lsa) -- the all-gather of p becomes part of the update kernel.
+struct LsaState {
+    void *base = nullptr;
+    size_t bytes = 0;
+    ncclWindow_t win = nullptr;
+    ncclDevComm dev{};
+    bool have_dev = false, failed = false;
+};
+
+void *comm_lsa_buffer(CommHandle *c, size_t bytes) {
+    if (c->kind != COMM_NCCL || !c->lsa_allowed || std::getenv("PLSSVM_NO_LSA")) return nullptr;
+    if (!c->lsa) c->lsa = new LsaState{};
+    LsaState *L = c->lsa;
+    if (L->failed) return nullptr;
+    bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    if (!L->have_dev) {
+        ncclDevCommRequirements reqs{};
+        reqs.lsaBarrierCount = kVecBlocks;  // one barrier per block of the vector kernels
+        if (ncclDevCommCreate(c->nccl, &reqs, &L->dev) != ncclSuccess) {
+            L->failed = true;  // every rank sees the same environment, so every rank falls back
+            return nullptr;
+        }
+        L->have_dev = true;
+        if (L->dev.lsaSize != c->nranks) {  // a rank without load/store access: NCCL's all-gather instead
+            L->failed = true;
+            return nullptr;
+        }
+    }
+    if (bytes > L->bytes) {  // (collective: every rank trains the same problem size)
+        if (L->win) PLS_NCCL(ncclCommWindowDeregister(c->nccl, L->win));
+        if (L->base) PLS_NCCL(ncclMemFree(L->base));
+        L->win = nullptr;
+        L->base = nullptr;
+        L->bytes = 0;
+        PLS_NCCL(ncclMemAlloc(&L->base, bytes));
+        PLS_NCCL(ncclCommWindowRegister(c->nccl, L->base, bytes, &L->win, NCCL_WIN_COLL_SYMMETRIC));
+        L->bytes = bytes;
+    }
+    return L->base;
+}
+ncclWindow_t comm_lsa_window(const CommHandle *c) { return c->lsa ? c->lsa->win : nullptr; }
+const ncclDevComm *comm_lsa_devcomm(const CommHandle *c) { return c->lsa ? &c->lsa->dev : nullptr; }
+void comm_lsa_destroy(CommHandle *c) {
+    LsaState *L = c->lsa;
+    if (!L) return;
+    if (c->nccl) {
+        if (L->win) ncclCommWindowDeregister(c->nccl, L->win);
+        if (L->base) ncclMemFree(L->base);
+        if (L->have_dev) ncclDevCommDestroy(c->nccl, &L->dev);
+    }
+    delete L;
+    c->lsa = nullptr;
+}
+
 // ---- dispatch -----------------------------------------------------------------------------------
 // Out-of-place sum all-reduce (send: this rank's partials, recv: the global values).
 void comm_allreduce_sum_f64(CommHandle *c, const double *send, double *recv, int64_t count, void *stream) {
@@ -265,6 +325,7 @@ extern "C" int plssvm_comm_init_impl(const void *id128, int32_t nranks, int32_t 
     h->rank = rank;
     h->nranks = nranks;
     h->device = device;
+    h->lsa_allowed = true;
     ncclResult_t r = ncclCommInitRank(&h->nccl, nranks, id, rank);
     if (r != ncclSuccess) {
         delete h;
@@ -289,6 +350,7 @@ extern "C" int plssvm_comm_init_callbacks_impl(const plssvm_comm_callbacks_t *cb
 extern "C" int plssvm_comm_destroy_impl(void *c) {
     auto *h = static_cast<CommHandle *>(c);
     if (!h) return PLSSVM_OK;
+    plssvm::comm_lsa_destroy(h);
     if (h->kind == plssvm::COMM_NCCL && h->nccl) ncclCommDestroy(h->nccl);
     delete h;
     return PLSSVM_OK;

@@ -30,12 +30,16 @@ struct PeerGroup {
     void abort();
 };
 
+struct LsaState;  // comm.cu: NCCL symmetric window of p + device communicator (fused all-gather)
+
 struct CommHandle {
     int kind = COMM_NCCL;
     ncclComm_t nccl = nullptr;
     int rank = 0, nranks = 1, device = 0;
     plssvm_comm_callbacks_t cb{};
     PeerGroup *group = nullptr;  // COMM_PEER
+    LsaState *lsa = nullptr;     // COMM_NCCL, created on first use
+    bool lsa_allowed = false;    // one process per GPU (plssvm_comm_init): collective window (de)registration
 };
 
 void comm_nccl_init_all(const std::vector<int> &devs, std::vector<ncclComm_t> &out);

@@ -480,6 +480,7 @@ struct Ctx {
     // PEER transport with direct peer access: every rank's full p (device array), for the p update
     // that stores its band into all of them (the all-gather fused into k_update_p)
     T **peer_p = nullptr;
+    bool lsa = false;  // p in the NCCL symmetric window (k_update_p_lsa)
     int npeer = 0;
 };
 
@@ -1303,7 +1304,13 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     c.x = A.alloc<T>(g.nb);
     c.r = A.alloc<T>(g.nb);
     c.y = A.alloc<T>(g.nb);
-    c.p = A.alloc<T>(g.mpad);
+    // one process per GPU over NCCL: p in the communicator's symmetric window, so the p update stores
+    // every rank's band straight into every rank's p (k_update_p_lsa: the all-gather fused in)
+    c.p = nullptr;
+    if (c.comm && !c.fsplit && o.cg_variant != PLSSVM_CG_SINGLE_REDUCTION && o.replace_every <= 0)
+        c.p = static_cast<T *>(comm_lsa_buffer(c.comm, static_cast<size_t>(g.mpad) * sizeof(T)));
+    c.lsa = c.p != nullptr;
+    if (!c.p) c.p = A.alloc<T>(g.mpad);
     c.xfull = A.alloc<T>(g.mpad);
     PLS_CUDA(cudaMemsetAsync(c.p, 0, g.mpad * sizeof(T), c.s));
     T *pband = c.p + g.g0;
@@ -1436,6 +1443,14 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
             const int ns2 = launch_qtilde_product<T>(c, c.xfull);
             finalize<T>(c, ns2, nullptr, 1, nullptr, -1, 0);
             allreduce(c, S_DELTA + (par ^ 1), 1);
+        }
+        if (c.lsa) {  // fused all-gather through the NCCL device API (stores + LSA barrier in the kernel)
+            k_update_p_lsa<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter,
+                                                                   *comm_lsa_devcomm(c.comm), comm_lsa_window(c.comm),
+                                                                   g.g0);
+            PLS_CHECK_LAUNCH();
+            ++c.launches;
+            return;
         }
         k_update_p<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter, loop,
                                                            use_loop, c.peer_p, c.npeer, g.g0);
@@ -1622,6 +1637,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
                           : delta <= eps2 * delta0 ? PLSSVM_STOP_CONVERGED
                                                    : PLSSVM_STOP_MAX_ITER;
         st->transport_used = 0;
+        st->allgather_fused = (c.lsa || c.npeer > 0) ? 1 : 0;
         st->iterations = it;
         st->matvecs = matvecs + (rel_true >= 0.0 ? 1 : 0);
         st->rel_residual = delta0 > 0 ? std::sqrt(delta / delta0) : 0.0;

@@ -1,8 +1,12 @@
 // driver.h -- internal (C++) interface between the C ABI (capi.cu) and the device driver.
 #pragma once
+#include <nccl.h>
+
 #include <cstdint>
 #include <vector>
 #include "../../include/plssvm.h"
+
+struct ncclDevComm;  // nccl_device.h
 
 namespace plssvm {
 
@@ -54,5 +58,13 @@ void comm_allgather(CommHandle *c, void *buf, int64_t count_per_rank, int dtype,
 bool comm_has_reduce_scatter(const CommHandle *c);
 void comm_reduce_scatter(CommHandle *c, const void *send, void *recv, int64_t count_per_rank, int dtype, void *stream);
 const char *nccl_version_string();
+// NCCL device API (LSA: load/store-accessible peers) for the fused all-gather of p: a symmetric window
+// of at least `bytes` registered on the communicator (collective; grown on demand) and the device
+// communicator with one LSA barrier per vector-kernel block.  nullptr when the transport is not NCCL,
+// not every rank is load/store accessible (no NVLink path) or PLSSVM_NO_LSA is set.
+void *comm_lsa_buffer(CommHandle *c, size_t bytes);
+ncclWindow_t comm_lsa_window(const CommHandle *c);
+const ncclDevComm *comm_lsa_devcomm(const CommHandle *c);
+void comm_lsa_destroy(CommHandle *c);
 
 }  // namespace plssvm

@@ -13,6 +13,7 @@
 //   k_predict          f(z) = sum_i alpha_i k(x_i, z) + b                (Eq. 10)
 #pragma once
 #include <cooperative_groups.h>
+#include <nccl_device.h>
 
 #include "tile_engine.cuh"
 
@@ -884,6 +885,53 @@ __global__ void __launch_bounds__(kVecThreads)
         ctrl[C_IT] = it;
         ctrl[C_DONE] = done;
         if (use_loop) cudaGraphSetConditional(loop, done == 0 ? 1u : 0u);
+    }
+}
+
+// k_update_p with the all-gather of p fused in through the NCCL device API (one process per GPU,
+// NCCL transport, every rank load/store accessible over NVLink, the P2P path
+// the paper lacks): p lives in an NCCL symmetric window; each thread stores its new element
+// p_i = r_i + b p_i into EVERY rank's window at the same offset (ncclGetLsaPointer, NVLink stores;
+// this rank's own copy is one of them), then block b meets block b of every rank in an LSA barrier
+// (release / acquire), so when this kernel completes on a rank every rank's band has landed in its
+// p.  (A rank writes a peer's p only after that peer's product of the iteration: the scalar all-
+// reduces in between order it.)  Then k_update_p's loop condition (last block).  The convergence
+// decision is taken from global scalars, so all ranks skip the barrier together once done.
+template <typename T>
+__global__ void __launch_bounds__(kVecThreads)
+    k_update_p_lsa(T *__restrict__ p, const T *__restrict__ r, int64_t nb, double *scal, int *ctrl, unsigned *counter,
+                   ncclDevComm dev, ncclWindow_t win, int64_t g0) {
+    if (cg_done(ctrl)) return;
+    const int par = ctrl[C_IT] & 1;
+    const T b = static_cast<T>(scal[S_DELTA + (par ^ 1)] / scal[S_DELTA + par]);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const T v = fma(b, p[i], r[i]);
+        const size_t off = static_cast<size_t>(g0 + i) * sizeof(T);
+        for (int q = 0; q < dev.lsaSize; ++q) *static_cast<T *>(ncclGetLsaPointer(win, off, q)) = v;
+    }
+    {
+        ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dev, ncclTeamTagLsa(), blockIdx.x);
+        bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    }
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        const int it = ctrl[C_IT] + 1;
+        const double pap = scal[S_PAP], dnew = scal[S_DELTA + (par ^ 1)];
+        int done = 0;
+        if (!(pap > 0.0) || !isfinite(pap) || !isfinite(dnew)) done = 2;
+        else if (ctrl[C_FIXED] > 0 ? (it >= ctrl[C_FIXED] || dnew == 0.0) : (dnew <= scal[S_THR])) done = 1;
+        else if (it >= ctrl[C_IMAX]) done = 1;
+        ctrl[C_IT] = it;
+        ctrl[C_DONE] = done;
+        *counter = 0u;
     }
 }
 

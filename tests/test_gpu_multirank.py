@@ -174,18 +174,23 @@ def _worker_nccl1(rank, world, port, path):
     out, _ = pl.plssvm_qtilde_matvec(X, p, pl.RBF, 0.05, opts=pl.options(mode=pl.MODE_IMPLICIT, comm=comm))
     res = {}
     for name, kw in (("implicit", dict(mode=pl.MODE_IMPLICIT)), ("cached", dict(mode=pl.MODE_CACHED)),
-                     ("cgcg", dict(mode=pl.MODE_IMPLICIT, cg_variant=pl.CG_SINGLE_REDUCTION))):
+                     ("cgcg", dict(mode=pl.MODE_IMPLICIT, cg_variant=pl.CG_SINGLE_REDUCTION)),
+                     ("nolsa", dict(mode=pl.MODE_IMPLICIT))):
+        if name == "nolsa":  # the separate ncclAllGather of p instead of the device-API stores
+            os.environ["PLSSVM_NO_LSA"] = "1"
         a, b, st, s = pl.plssvm_train_ex(X, y, pl.RBF, 0.05, eps=1e-10, opts=pl.options(comm=comm, **kw))
-        res[name] = (a, b, st, s.num_ranks)
+        os.environ.pop("PLSSVM_NO_LSA", None)
+        res[name] = (a, b, st, s.num_ranks, s.allgather_fused)
     np.savez(path, out=out, **{f"{k}_a": v[0] for k, v in res.items()}, **{f"{k}_b": v[1] for k, v in res.items()},
-             **{f"{k}_st": v[2] for k, v in res.items()}, **{f"{k}_r": v[3] for k, v in res.items()})
+             **{f"{k}_st": v[2] for k, v in res.items()}, **{f"{k}_r": v[3] for k, v in res.items()},
+             **{f"{k}_fused": v[4] for k, v in res.items()})
     pl.plssvm_comm_destroy(comm)
     dist.destroy_process_group()
 
 
 def test_nccl_communicator_one_rank(tmp_path):
     """The NCCL transport itself (plssvm_comm_init through torch.distributed's id broadcast,
-    ncclAllGather in place, ncclAllReduce out of place) on a 1-rank communicator -- the one NCCL
+    ncclAllGather in place, ncclAllReduce out of place, the device-API fused all-gather of p) on a 1-rank communicator -- the one NCCL
     configuration a single-GPU box can run (NCCL refuses two ranks on one device); the multi-rank
     driver logic is covered above through the host-staged transport."""
     import oracle
@@ -199,7 +204,13 @@ def test_nccl_communicator_one_rank(tmp_path):
     ref = oracle.qtilde(X, 2, 0.05) @ p
     assert np.linalg.norm(r["out"] - ref) <= 1e-12 * np.linalg.norm(ref)
     a_ref, b_ref, _, _ = oracle.train(X, y, 2, 0.05, eps=1e-10)
-    for k in ("implicit", "cached", "cgcg"):
+    for k in ("implicit", "cached", "cgcg", "nolsa"):
         assert int(r[f"{k}_st"]) == 0 and int(r[f"{k}_r"]) == 1
         assert np.linalg.norm(r[f"{k}_a"] - a_ref) <= 1e-7 * np.linalg.norm(a_ref), k
         assert abs(float(r[f"{k}_b"]) - b_ref) <= 1e-7 * max(abs(b_ref), np.abs(a_ref).max()), k
+    # NCCL device API: p in the communicator's symmetric window, the all-gather
+    # fused into the p update (LSA stores + barrier) for the Shewchuk loop; the same iterates as the
+    # separate ncclAllGather, bit for bit
+    assert int(r["implicit_fused"]) == 1 and int(r["cached_fused"]) == 1
+    assert int(r["cgcg_fused"]) == 0 and int(r["nolsa_fused"]) == 0
+    assert np.array_equal(r["implicit_a"], r["nolsa_a"]) and float(r["implicit_b"]) == float(r["nolsa_b"])
