@@ -85,7 +85,13 @@ struct Oz {
     static constexpr int NSUB = kTile / TN;                        // 1
     static constexpr int LV = S == 7 ? 4 : 3;                      // levels of the last pass (0..LV-1)
     static constexpr int LV0 = S == 7 ? S - LV : LV;               // levels of pass 0
-    static constexpr int STAGES = S == 7 ? 4 : 8;
+#ifndef PLSSVM_OZ_STAGES7
+#define PLSSVM_OZ_STAGES7 5  // 5 x 42 KiB: A/B 3.077 -> 3.065 ms at C1 (tools/scripts/ab4.sh); the fp32 engine's 8 -> 10 was 0.4 % slower
+#endif
+#ifndef PLSSVM_OZ_STAGES3
+#define PLSSVM_OZ_STAGES3 8
+#endif
+    static constexpr int STAGES = S == 7 ? PLSSVM_OZ_STAGES7 : PLSSVM_OZ_STAGES3;  // (A/B builds may override)
     static constexpr uint32_t PLANE = kTile * BK;                  // 4 KiB: one A digit plane (B half: 2 KiB)
     static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: all S planes of A and of the B half
     static constexpr int EPI_WARPS = 8;
