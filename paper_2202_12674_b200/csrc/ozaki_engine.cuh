@@ -94,14 +94,23 @@ struct Oz {
     static constexpr int STAGES = S == 7 ? PLSSVM_OZ_STAGES7 : PLSSVM_OZ_STAGES3;  // (A/B builds may override)
     static constexpr uint32_t PLANE = kTile * BK;                  // 4 KiB: one A digit plane (B half: 2 KiB)
     static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: all S planes of A and of the B half
-    static constexpr int EPI_WARPS = 8;
-    static constexpr int THREADS = (EPI_WARPS + 4) * 32;             // warpgroup 0: control, 1-2: epilogue
-    static constexpr int CTRL_REGS = 40, EPI_REGS = 232;            // setmaxnreg split (4x40 + 8x232 <= 512 per lane)
+#ifndef PLSSVM_OZ_EPI
+#define PLSSVM_OZ_EPI 8
+#endif
+    static constexpr int EPI_WARPS = PLSSVM_OZ_EPI;                  // 8 or 16 epilogue warps
+    static constexpr int EPI_THREADS = EPI_WARPS * 32;
+    static constexpr int NG = EPI_WARPS / 4;                        // column groups per TMEM lane quarter
+    static constexpr int CPT = TN / NG;                             // columns per epilogue thread (64 / 32)
+    static constexpr int THREADS = (EPI_WARPS + 4) * 32;             // warpgroup 0: control, then the epilogue
+    // setmaxnreg split: the epilogue's increase must come out of what warpgroup 0 releases from the launch
+    // allocation (8 warps: 384 x 168 -> 4 x 40 + 8 x 232; 16 warps: 640 x 96 -> 4 x 24 + 16 x 112)
+    static constexpr int CTRL_REGS = EPI_WARPS == 8 ? 40 : 24, EPI_REGS = EPI_WARPS == 8 ? 232 : 112;
+    static_assert(EPI_WARPS == 8 || EPI_WARPS == 16, "8 or 16 epilogue warps");
     static constexpr int TMEM_COLS = 512;
     static_assert(LV * TN <= TMEM_COLS && LV0 * TN <= TMEM_COLS, "a pass's level accumulators must fit TMEM");
-    // misc: barriers (256 B) + column data 4 x 128 doubles + row partials 2 x 128 + col partials 4 x 128
+    // misc: barriers (256 B) + column data 4 x 128 doubles + row partials NG x 128 + col partials 4 x 128
     // + the 256-entry exp table + the tile's p / q.p sums (4 warps x 4)
-    static constexpr size_t MISC = 256 + (4 * TN + 2 * kTile + 4 * TN + 256 + 16) * 8;
+    static constexpr size_t MISC = 256 + (4 * TN + NG * kTile + 4 * TN + 256 + 16) * 8;
     static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + MISC;
     // instruction descriptor: D s32 (2), A s8 (1), B s8 (1), K-major both, N = 128, M = 256 (2 SMs)
     static constexpr uint32_t IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TN >> 3) << 17) | ((256u >> 4) << 24);
@@ -496,9 +505,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     T *colq = reinterpret_cast<T *>(colsc + TN);             // [128] (8-byte slots for either T)
     T *colp = reinterpret_cast<T *>(colsc + 2 * TN);         // [128] (alpha for predict)
     T *coln = reinterpret_cast<T *>(colsc + 3 * TN);         // [128]
-    T *redr = reinterpret_cast<T *>(colsc + 4 * TN);         // [2][128]
-    T *redc = reinterpret_cast<T *>(colsc + 4 * TN + 2 * kTile);  // [4][128]
-    double *etab = colsc + 8 * TN + 2 * kTile;               // [256] 2^(j/256) (fp64 RBF, exp_tab256)
+    T *redr = reinterpret_cast<T *>(colsc + 4 * TN);         // [NG][128]
+    T *redc = reinterpret_cast<T *>(colsc + 4 * TN + O::NG * kTile);  // [4][128]
+    double *etab = colsc + 8 * TN + O::NG * kTile;           // [256] 2^(j/256) (fp64 RBF, exp_tab256)
     T *psum = reinterpret_cast<T *>(etab + 256);             // [4][4] MATVEC: per warp sum p_j, q_j p_j, p_i, q_i p_i
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -636,15 +645,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
         }
     } else if (warp < 4) {  // idle warps 2-3
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(O::CTRL_REGS));
-    } else {  // ---- epilogue warps 4-11 (both CTAs): row 32(w%4) + lane, columns 64((w-4)/4) .. +63
+    } else {  // ---- epilogue warps 4.. (both CTAs): row 32(w%4) + lane, columns CPT((w-4)/4) .. + CPT - 1
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(O::EPI_REGS));
         constexpr bool kTabExp = KT == RBF && S == 7;
-        if (kTabExp) etab[threadIdx.x - 128] = kExp2Tab256[threadIdx.x - 128];  // 256 epilogue threads; read after B1
+        constexpr int CPT = O::CPT, NG = O::NG;
+        if (kTabExp && threadIdx.x - 128 < 256) etab[threadIdx.x - 128] = kExp2Tab256[threadIdx.x - 128];  // read after B1
         // fp64 RBF: tp = a2 s + b_i + b_j = (256/ln2) (-gamma) (n_i + n_j - 2 s) (exp_tab256)
         const double gK = kTabExp ? -static_cast<double>(kp.gamma) * kExpScale256 : 0.0, a2 = -2.0 * gK;
         const int quarter = warp & 3, grp = (warp - 4) >> 2;
         const int lr = quarter * 32 + lane;
-        const int et = threadIdx.x - 128;  // 0..255
+        const int et = threadIdx.x - 128;  // 0 .. EPI_THREADS - 1
         const T Qmm = (MODE == OZ_PREDICT) ? T(0) : static_cast<T>(scal[S_QMM]);
         uint32_t e = 0;
         for (int t = pair; t < ntiles; t += npairs) {
@@ -686,7 +696,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         for (int u = 0; u < 4; ++u) psum[(et >> 5) * 4 + u] = v[u];
                 }
             }
-            asm volatile("bar.sync 1, 256;" ::: "memory");  // B1
+            asm volatile("bar.sync 1, %0;" ::"n"(O::EPI_THREADS) : "memory");  // B1
 
             // S = 7, pass 0 (levels 0-3): V = 2^24 sum_{l<4} 2^{-8l} acc_l, an exact int64 (|V| < d 2^38 <
             // 2^53) held EXACTLY as fp64 in sv (64 columns in registers), accumulators released.  Pass 1
@@ -695,7 +705,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             // (DESIGN.md §5 error bound).  Then the accumulators are released and the Q~ entry / kernel
             // value and its row and column contributions run under the next pair-tile's MMAs.
             // S = 3: the single pass, V = acc_0 2^16 + acc_1 2^8 + acc_2.
-            const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(grp * 64);
+            const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(grp * CPT);
             const bool mirrored = used && (MODE != OZ_PREDICT) && (I != J) && (J >= band0) && (J < band1);
             T rs = T(0);
             T *qdst = nullptr, *qmir = nullptr;
@@ -703,14 +713,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 if (used) {
                     qdst = ((T_tiles < 0) ? Qc + int64_t(pk[2 * t + int(rank)]) * (kTile * kTile)
                                           : Qc + (int64_t(I - band0) * T_tiles + J) * (kTile * kTile)) +
-                           int64_t(lr) * kTile + grp * 64;
+                           int64_t(lr) * kTile + grp * CPT;
                     if (T_tiles >= 0 && mirrored) qmir = Qc + (int64_t(J - band0) * T_tiles + I) * (kTile * kTile) + lr;
                 }
             }
             // the thread's 64 entries, one 64-bit register pair each: S = 7 the pass-0 V + 3 2^51, then the
             // fp64 contractions' bits; S = 3 V + 3 2^51, then the fp32 contractions' bits (one array for
             // both stages keeps the epilogue within the kernel's register budget)
-            long long sv[64];
+            long long sv[CPT];
             auto sval = [&](int k) -> T {
                 if constexpr (S == 7) return __longlong_as_double(sv[k]);
                 else return __int_as_float(static_cast<int>(sv[k]));
@@ -728,7 +738,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 ++e;
                 if (!(dbg & 1)) {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
+                    for (int c = 0; c < CPT / 8; ++c) {
                         uint32_t r0[8], r1[8], r2[8], r3[8];
                         tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
                         tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
@@ -763,7 +773,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 // under the next pair-tile's MMAs (the MMA waited ~8 % of its loop for drains, C3)
                 if (!(dbg & 1)) {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
+                    for (int c = 0; c < CPT / 8; ++c) {
                         uint32_t r0[8], r1[8], r2[8];
                         tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
                         tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
@@ -779,13 +789,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 if (lane == 0) mbar_arrive_cluster(tempty0);  // the next pair-tile's MMAs may start
                 if (!(dbg & 1)) {
 #pragma unroll
-                    for (int k = 0; k < 64; ++k)  // then one rounding to fp32
-                        sv[k] = static_cast<uint32_t>(__float_as_int(static_cast<float>(scaled_exact(sv[k], rkb + colk[grp * 64 + k]))));
+                    for (int k = 0; k < CPT; ++k)  // then one rounding to fp32
+                        sv[k] = static_cast<uint32_t>(__float_as_int(static_cast<float>(scaled_exact(sv[k], rkb + colk[grp * CPT + k]))));
                 }
             } else {
                 if (!(dbg & 1)) {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
+                    for (int c = 0; c < CPT / 8; ++c) {
                         uint32_t r0[8], r1[8], r2[8];
                         tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
                         tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
@@ -793,7 +803,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         tmem_ld_wait();
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const int kb = rkb + colk[grp * 64 + c * 8 + j];
+                            const int kb = rkb + colk[grp * CPT + c * 8 + j];
                             // x_i.x_j = 2^k V + 2^{k-24} W (level 4 is 2^-32 below level 0, W carries 2^16
                             // of it), both terms exact: ONE rounding in their sum
                             const long long Wb = mad_wide(r0[j], 1 << 16, mad_wide(r1[j], 1 << 8, mad_wide(r2[j], 1, kOzBias)));
@@ -812,11 +822,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             OZ_PROF_T0(twork);
             if (!(dbg & 1)) {
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {  // 8-column chunks of this thread's 64 columns
+                for (int c = 0; c < CPT / 8; ++c) {  // 8-column chunks of this thread's 64 columns
                     T w[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int lc = grp * 64 + c * 8 + j;
+                        const int lc = grp * CPT + c * 8 + j;
                         const int64_t gj = col0 + lc;
                         const bool diag = (MODE != OZ_PREDICT) && gi == gj;
                         T kv;
@@ -841,7 +851,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     if constexpr (MODE == OZ_MATVEC) {
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            rs = fma(w[j], colp[grp * 64 + c * 8 + j], rs);
+                            rs = fma(w[j], colp[grp * CPT + c * 8 + j], rs);
                             w[j] *= pi;
                         }
                         if (mirrored) {  // CTA-uniform: column sums over the warp's 32 rows
@@ -861,7 +871,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                             tot += __shfl_xor_sync(0xffffffffu, tot, 1);
                             if ((lane & 3) == 0) {
                                 const int cc = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                                redc[quarter * TN + grp * 64 + c * 8 + cc] = tot;
+                                redc[quarter * TN + grp * CPT + c * 8 + cc] = tot;
                             }
                         }
                     } else if constexpr (MODE == OZ_PRECOMPUTE) {
@@ -876,7 +886,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         }
                         if (qmir) {  // transposed copy: column lc of this tile = row lc of tile (J, I)
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) qmir[int64_t(grp * 64 + c * 8 + j) * kTile] = w[j];  // coalesced
+                            for (int j = 0; j < 8; ++j) qmir[int64_t(grp * CPT + c * 8 + j) * kTile] = w[j];  // coalesced
                         }
                     }
                 }
@@ -884,14 +894,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
 
             if constexpr (MODE == OZ_MATVEC) {
                 redr[grp * kTile + lr] = rs;
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // B2
+                asm volatile("bar.sync 1, %0;" ::"n"(O::EPI_THREADS) : "memory");  // B2
+                auto rowsum = [&](int row) {  // the column groups' partials in fixed order
+                    if constexpr (NG == 2) return redr[row] + redr[kTile + row];
+                    else return (redr[row] + redr[kTile + row]) + (redr[2 * kTile + row] + redr[3 * kTile + row]);
+                };
                 if (used) {
                     const int64_t lrow0 = row0 - int64_t(band0) * kTile;
                     auto tsum = [&](int u) { return (psum[u] + psum[4 + u]) + (psum[8 + u] + psum[12 + u]); };
                     if (et < kTile) {  // row et (= this thread's lr): + (Q_mm - q_i) sum p_J - sum (q p)_J
                         const T corr = fma(cqi, tsum(0), -tsum(1)) + ((I == J) ? invC * pi : T(0));
-                        Ypart[int64_t(J) * band_rows + lrow0 + et] = (redr[et] + redr[kTile + et]) + corr;
-                    } else if (mirrored) {
+                        Ypart[int64_t(J) * band_rows + lrow0 + et] = rowsum(et) + corr;
+                    } else if (mirrored && et < 2 * kTile) {
                         const int cidx = et - kTile;
                         const int64_t lcol0 = col0 - int64_t(band0) * kTile;
                         const T corr = fma(Qmm - colq[cidx], tsum(2), -tsum(3));
@@ -901,10 +915,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 }
             } else if constexpr (MODE == OZ_PREDICT) {
                 redr[grp * kTile + lr] = rs;
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // B2
-                if (used && et < kTile) Ypart[int64_t(J) * band_rows + row0 + et] = redr[et] + redr[kTile + et];
+                asm volatile("bar.sync 1, %0;" ::"n"(O::EPI_THREADS) : "memory");  // B2
+                if (used && et < kTile) {
+                    const T fs = NG == 2 ? redr[et] + redr[kTile + et]
+                                         : (redr[et] + redr[kTile + et]) + (redr[2 * kTile + et] + redr[3 * kTile + et]);
+                    Ypart[int64_t(J) * band_rows + row0 + et] = fs;
+                }
             }
-            asm volatile("bar.sync 1, 256;" ::: "memory");  // B3: smem partials / column data reusable
+            asm volatile("bar.sync 1, %0;" ::"n"(O::EPI_THREADS) : "memory");  // B3: smem partials / column data reusable
             if (prof) OZ_PROF_ADD(7, twork);
         }
     }
