@@ -188,34 +188,51 @@ struct LsaState {
     bool have_dev = false, failed = false;
 };
 
+// Every rank must take the same path (the LSA update replaces a collective): the outcome of this rank's
+// setup is agreed by an all-reduce (min) before use.
+static bool lsa_agree(CommHandle *c, bool ok) {
+    int *d = nullptr;
+    int h = ok ? 1 : 0;
+    cudaStream_t s = nullptr;
+    bool agreed = false;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess && cudaMalloc(&d, sizeof(int)) == cudaSuccess &&
+        cudaMemcpyAsync(d, &h, sizeof(int), cudaMemcpyHostToDevice, s) == cudaSuccess &&
+        ncclAllReduce(d, d, 1, ncclInt32, ncclMin, c->nccl, s) == ncclSuccess &&
+        cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s) == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess)
+        agreed = h == 1;
+    if (d) cudaFree(d);
+    if (s) cudaStreamDestroy(s);
+    return agreed;
+}
+
 void *comm_lsa_buffer(CommHandle *c, size_t bytes) {
     if (c->kind != COMM_NCCL || !c->lsa_allowed || std::getenv("PLSSVM_NO_LSA")) return nullptr;
     if (!c->lsa) c->lsa = new LsaState{};
     LsaState *L = c->lsa;
     if (L->failed) return nullptr;
     bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    if (L->have_dev && bytes <= L->bytes) return L->base;
+    bool ok = true;
     if (!L->have_dev) {
         ncclDevCommRequirements reqs{};
         reqs.lsaBarrierCount = kVecBlocks;  // one barrier per block of the vector kernels
-        if (ncclDevCommCreate(c->nccl, &reqs, &L->dev) != ncclSuccess) {
-            L->failed = true;  // every rank sees the same environment, so every rank falls back
-            return nullptr;
-        }
-        L->have_dev = true;
-        if (L->dev.lsaSize != c->nranks) {  // a rank without load/store access: NCCL's all-gather instead
-            L->failed = true;
-            return nullptr;
-        }
+        ok = ncclDevCommCreate(c->nccl, &reqs, &L->dev) == ncclSuccess;
+        L->have_dev = ok;
+        ok = ok && L->dev.lsaSize == c->nranks;  // a rank without load/store access: NCCL's all-gather
     }
-    if (bytes > L->bytes) {  // (collective: every rank trains the same problem size)
-        if (L->win) PLS_NCCL(ncclCommWindowDeregister(c->nccl, L->win));
-        if (L->base) PLS_NCCL(ncclMemFree(L->base));
+    if (ok) {  // (collective: every rank trains the same problem size)
+        if (L->win) ncclCommWindowDeregister(c->nccl, L->win);
+        if (L->base) ncclMemFree(L->base);
         L->win = nullptr;
         L->base = nullptr;
         L->bytes = 0;
-        PLS_NCCL(ncclMemAlloc(&L->base, bytes));
-        PLS_NCCL(ncclCommWindowRegister(c->nccl, L->base, bytes, &L->win, NCCL_WIN_COLL_SYMMETRIC));
-        L->bytes = bytes;
+        ok = ncclMemAlloc(&L->base, bytes) == ncclSuccess &&
+             ncclCommWindowRegister(c->nccl, L->base, bytes, &L->win, NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess;
+        if (ok) L->bytes = bytes;
+    }
+    if (!lsa_agree(c, ok)) {
+        L->failed = true;
+        return nullptr;
     }
     return L->base;
 }
