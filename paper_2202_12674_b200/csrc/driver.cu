@@ -22,6 +22,7 @@
 #include <vector>
 
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "driver.h"
 #include "kernels.cuh"
@@ -31,6 +32,15 @@
 namespace plssvm {
 
 namespace {
+
+// NVTX range over a phase of a call (SURVEY §5 tracing): visible to nsys / ncu --nvtx when a tool is
+// attached, a no-op otherwise (header-only NVTX v3, no link dependency).
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx &) = delete;
+    Nvtx &operator=(const Nvtx &) = delete;
+};
 
 // ---- stream-ordered device allocations, freed at scope exit -------------------------------
 struct Arena {
@@ -1298,7 +1308,10 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
                 e_cg = E.make(), e_end = E.make();
     const auto wall0 = std::chrono::steady_clock::now();
     PLS_CUDA(cudaEventRecord(e0, c.s));
-    setup<T>(c, A, pb, o, true, E, e_h2d, e_tr, e_q);
+    {
+        Nvtx r("plssvm setup: stage, validate, split, q");
+        setup<T>(c, A, pb, o, true, E, e_h2d, e_tr, e_q);
+    }
     const Geometry &g = c.g;
 
     c.x = A.alloc<T>(g.nb);
@@ -1319,7 +1332,10 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     configure_product<T>(c, A);
     if (c.cached) c.Qc = A.alloc<T>(c.packed ? c.nstored * kTile * kTile : g.nb * g.mpad);
     PLS_CUDA(cudaEventRecord(e_alloc, c.s));
-    if (c.cached) launch_precompute<T>(c);
+    if (c.cached) {
+        Nvtx r("plssvm precompute");
+        launch_precompute<T>(c);
+    }
     PLS_CUDA(cudaEventRecord(e_pre, c.s));
 
     // ---- CG init (a2) ----
@@ -1346,6 +1362,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     // ---- CG loop (a3-a5, a8): the convergence test runs on the device (k_update_p), the host
     // enqueues iterations in batches of kBatch and reads the control block once per batch --
     // no host round trip per iteration; iterations enqueued after convergence are no-ops.
+    Nvtx r_cg("plssvm CG loop, bias, alpha");  // (to the end of the call)
     c.ctrl = A.alloc<int>(C_COUNT);
     const int imax_i = static_cast<int>(std::min<int64_t>(imax, INT32_MAX));
     const int fixed_i = static_cast<int>(std::min<int64_t>(std::max<int64_t>(o.fixed_iter, 0), INT32_MAX));
@@ -1911,15 +1928,18 @@ int exp_oz_profile(unsigned long long *out, int reset) {
 #endif
 
 int train(const Problem &pb, const plssvm_options_t &o, void *alpha, void *b, plssvm_stats_t *st) {
+    Nvtx r("plssvm_train");
     return pb.dtype == PLSSVM_F32 ? train_impl<float>(pb, o, alpha, b, st) : train_impl<double>(pb, o, alpha, b, st);
 }
 int predict(const Problem &pb, const void *alpha, double b, const void *Z, int64_t n, const plssvm_options_t &o,
             void *decision, int32_t *labels, double *t_kernel) {
+    Nvtx r("plssvm_predict");
     return pb.dtype == PLSSVM_F32 ? predict_impl<float>(pb, alpha, b, Z, n, o, decision, labels, t_kernel)
                                   : predict_impl<double>(pb, alpha, b, Z, n, o, decision, labels, t_kernel);
 }
 int qtilde_matvec(const Problem &pb, const void *p, int32_t repeats, const plssvm_options_t &o, void *out,
                   double *t_kernel) {
+    Nvtx r("plssvm_qtilde_matvec");
     return pb.dtype == PLSSVM_F32 ? qtilde_matvec_impl<float>(pb, p, repeats, o, out, t_kernel)
                                   : qtilde_matvec_impl<double>(pb, p, repeats, o, out, t_kernel);
 }
