@@ -466,6 +466,7 @@ struct Ctx {
     int64_t m = 0, d = 0;
     T *tpart = nullptr, *tvec = nullptr;
     double *tloc = nullptr;          // [2d]: local partial, global sum (multi-GPU)
+    double *psum = nullptr;          // [lr_parts]: slices of sum(p)
     int lr_parts = 1;
     int64_t lr_rpb = 1;
     T *yfull = nullptr, *ysc = nullptr, *Yfin = nullptr;
@@ -956,13 +957,16 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
     }
     if (c.lowrank) {  // Q~p = B^T (X (X^T (B p))) + (p + 1 sum p)/C, O(md)
         const int64_t r0 = g.g0, r1 = std::max<int64_t>(std::min<int64_t>(g.g0 + g.nb, c.m), g.g0);
-        k_sum_p<T><<<1, 256, 0, c.s>>>(pfull, g.m1, c.scal, c.cur_ctrl);
-        k_colsum_partial<T><<<c.lr_parts, 256, 0, c.s>>>(c.Xraw, c.d, r0, r1, c.lr_rpb, nullptr, pfull, c.m, c.scal,
-                                                         c.tpart, c.cur_ctrl);
-        k_colsum_reduce<T><<<static_cast<unsigned>(ceil_div(c.d, 256)), 256, 0, c.s>>>(c.tpart, c.lr_parts, c.d, c.tvec,
-                                                                                       c.tloc, c.cur_ctrl);
+        // X^T B p = sum_{i < m-1} p_i x_i - (sum p) x_{m-1}: the column sums of this rank's rows (and the
+        // slices of sum p), then the fixed-order reduce, which adds the x_{m-1} term on the rank holding it
+        const bool owns_last = c.m - 1 >= r0 && c.m - 1 < r1;
+        k_colsum_partial<T><<<c.lr_parts, 256, 0, c.s>>>(c.Xraw, c.d, r0, r1, c.lr_rpb, nullptr, pfull, c.m, c.tpart,
+                                                         c.psum, c.cur_ctrl);
+        k_colsum_reduce<T><<<static_cast<unsigned>(ceil_div(c.d, 256)), 256, 0, c.s>>>(
+            c.tpart, c.lr_parts, c.d, c.tvec, c.tloc, c.cur_ctrl, c.psum, owns_last ? c.Xraw + (c.m - 1) * c.d : nullptr,
+            c.scal);
         PLS_CHECK_LAUNCH();
-        c.launches += 3;
+        c.launches += 2;
         if (c.comm) {  // t = sum over ranks (out of place: idempotent after convergence)
             comm_allreduce_sum_f64(c.comm, c.tloc, c.tloc + c.d, c.d, c.s);
             k_cast<T><<<static_cast<unsigned>(ceil_div(c.d, 256)), 256, 0, c.s>>>(c.tloc + c.d, c.d, c.tvec);
@@ -1192,6 +1196,7 @@ void configure_product(Ctx<T> &c, Arena &A) {
         c.tpart = A.alloc<T>(static_cast<int64_t>(c.lr_parts) * c.d);
         c.tvec = A.alloc<T>(c.d);
         c.tloc = A.alloc<double>(2 * c.d);
+        c.psum = A.alloc<double>(c.lr_parts);
         c.Ypart = A.alloc<T>(g.nb);
         c.Yfin = c.Ypart;
         return;
@@ -1776,7 +1781,7 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
         T *f_d = (dev && decision) ? static_cast<T *>(decision) : A.alloc<T>(n);
         int32_t *l_d = (dev && labels) ? labels : A.alloc<int32_t>(n);
         PLS_CUDA(cudaEventRecord(e0, s));
-        k_colsum_partial<T><<<parts, 256, 0, s>>>(Xs, d, 0, m, rpb, al, nullptr, m, nullptr, wpart, nullptr);
+        k_colsum_partial<T><<<parts, 256, 0, s>>>(Xs, d, 0, m, rpb, al, nullptr, m, wpart, nullptr, nullptr);
         k_colsum_reduce<T><<<static_cast<unsigned>(ceil_div(d, 256)), 256, 0, s>>>(wpart, parts, d, w, nullptr, nullptr);
         k_rowdot<T><<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(Zs, d, 0, n, w, 0, static_cast<T>(b),
                                                                                  nullptr, n, T(0), nullptr, f_d, l_d,

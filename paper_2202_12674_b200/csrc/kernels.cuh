@@ -480,37 +480,120 @@ __global__ void __launch_bounds__(256, 4) k_gemv_sym(const T *__restrict__ Qc, c
 // Linear-kernel shortcuts (they change the cost model and are reported
 // separately from the implicit FLOP/s).  X here is the caller's row-major m x d array.
 //
-// Weighted column sums: part[b][k] = sum_{i in rows of block b} c_i X[i][k], with
-//   c_i = coef[i]                                  (coef != nullptr; predict: w = X^T alpha, Eq. 15)
-//   c_i = p[i] (i < m-1), -sum(p) (i = m-1)         (coef == nullptr; low-rank Q~p: X^T B p)
-// restricted to rows [r0, r1).  Deterministic: fixed row order per block, then k_colsum_reduce.
+// Weighted column sums: part[b][k] = sum_{i in rows of block b} c_i X[i][k], in increasing i, with
+//   c_i = coef[i]     (coef != nullptr: all rows; predict: w = X^T alpha, Eq. 15)
+//   c_i = p[i]        (coef == nullptr, the low-rank X^T B p: rows i < m-1 only -- the -sum(p) x_{m-1}
+//                      term of B p = (p, -sum p) is added once in k_colsum_reduce)
+// restricted to rows [r0, r1).  psum (low-rank): psum[b] = sum of block b's slice of p[0, m-1) (the
+// slices cover all of p whatever the row band, so every rank forms the same sum(p)).  Column pairs
+// (vec2 loads) and 8 rows per step with the loads issued ahead of the FMAs: the column sums are a
+// streaming read of X and need many loads in flight (one dependent FMA chain per column kept the
+// round-1 kernel at ~64 % of HBM).  Deterministic: fixed row order, then k_colsum_reduce.
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_partial(const T *__restrict__ X, int64_t d, int64_t r0, int64_t r1,
                                                         int64_t rows_per_block, const T *__restrict__ coef,
-                                                        const T *__restrict__ p, int64_t m, const double *scal,
-                                                        T *__restrict__ part, const int *ctrl) {
+                                                        const T *__restrict__ p, int64_t m, T *__restrict__ part,
+                                                        double *__restrict__ psum, const int *ctrl) {
+    using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
     if (cg_done(ctrl)) return;
     const int64_t b0 = r0 + static_cast<int64_t>(blockIdx.x) * rows_per_block;
-    const int64_t b1 = b0 + rows_per_block < r1 ? b0 + rows_per_block : r1;
-    const T negs = coef ? T(0) : static_cast<T>(-scal[S_SP]);
-    for (int64_t k = threadIdx.x; k < d; k += blockDim.x) {
-        T s = T(0);
-        for (int64_t i = b0; i < b1; ++i) {
-            const T ci = coef ? coef[i] : (i < m - 1 ? p[i] : negs);
-            s = fma(ci, X[i * d + k], s);
+    int64_t e1 = b0 + rows_per_block < r1 ? b0 + rows_per_block : r1;
+    if (!coef && e1 > m - 1) e1 = m - 1;
+    auto cf = [&](int64_t i) -> T { return coef ? coef[i] : p[i]; };
+    if (psum) {  // this block's slice of sum_{i < m-1} p_i (fixed order)
+        __shared__ double red[8];
+        const int64_t chunk = (m - 1 + gridDim.x - 1) / gridDim.x;
+        const int64_t s0 = static_cast<int64_t>(blockIdx.x) * chunk, s1 = s0 + chunk < m - 1 ? s0 + chunk : m - 1;
+        double v = 0.0;
+        for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) v += static_cast<double>(p[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < 8; ++w) t += red[w];
+            psum[blockIdx.x] = t;
         }
+    }
+    constexpr int U = 8;
+    if ((d & 1) == 0) {
+        const V2 *X2 = reinterpret_cast<const V2 *>(X);
+        const int64_t d2 = d >> 1;
+        for (int64_t k2 = threadIdx.x; k2 < d2; k2 += blockDim.x) {
+            T s0 = T(0), s1 = T(0);
+            int64_t i = b0;
+            for (; i + U <= e1; i += U) {
+                V2 v[U];
+                T c[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    v[u] = X2[(i + u) * d2 + k2];
+                    c[u] = cf(i + u);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    s0 = fma(c[u], v[u].x, s0);
+                    s1 = fma(c[u], v[u].y, s1);
+                }
+            }
+            for (; i < e1; ++i) {
+                const V2 v = X2[i * d2 + k2];
+                const T c = cf(i);
+                s0 = fma(c, v.x, s0);
+                s1 = fma(c, v.y, s1);
+            }
+            part[static_cast<int64_t>(blockIdx.x) * d + 2 * k2] = s0;
+            part[static_cast<int64_t>(blockIdx.x) * d + 2 * k2 + 1] = s1;
+        }
+        return;
+    }
+    for (int64_t k = threadIdx.x; k < d; k += blockDim.x) {  // odd d: rows not 2-element aligned
+        T s = T(0);
+        int64_t i = b0;
+        for (; i + U <= e1; i += U) {
+            T v[U], c[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                v[u] = X[(i + u) * d + k];
+                c[u] = cf(i + u);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) s = fma(c[u], v[u], s);
+        }
+        for (; i < e1; ++i) s = fma(cf(i), X[i * d + k], s);
         part[static_cast<int64_t>(blockIdx.x) * d + k] = s;
     }
 }
 
+// out[k] = sum_b part[b][k] (fixed order).  Low-rank (psum != nullptr): sum(p) = sum_b psum[b] (every block,
+// warp 0, lane-strided + shuffle tree: fixed order) -> scal[S_SP], and the rank whose band holds row m-1
+// (xlast = X + (m-1) d, else nullptr) adds its -sum(p) x_{m-1} term.
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_reduce(const T *__restrict__ part, int nparts, int64_t d,
-                                                       T *__restrict__ out, double *out_local, const int *ctrl) {
+                                                       T *__restrict__ out, double *out_local, const int *ctrl,
+                                                       const double *__restrict__ psum = nullptr,
+                                                       const T *__restrict__ xlast = nullptr, double *scal = nullptr) {
     if (cg_done(ctrl)) return;
+    __shared__ double sp_sh;
+    if (psum) {
+        if (threadIdx.x < 32) {
+            double v = 0.0;
+            for (int b = threadIdx.x; b < nparts; b += 32) v += psum[b];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (threadIdx.x == 0) {
+                sp_sh = v;
+                if (blockIdx.x == 0 && scal) scal[S_SP] = v;
+            }
+        }
+        __syncthreads();
+    }
     const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= d) return;
     T s = T(0);
     for (int b = 0; b < nparts; ++b) s += part[static_cast<int64_t>(b) * d + k];
+    if (psum && xlast) s = fma(static_cast<T>(-sp_sh), xlast[k], s);
     out[k] = s;
     if (out_local) out_local[k] = static_cast<double>(s);
 }
@@ -519,22 +602,6 @@ template <typename T>
 __global__ void k_cast(const double *__restrict__ a, int64_t n, T *__restrict__ b) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) b[i] = static_cast<T>(a[i]);
-}
-
-// sum_{i < m-1} p_i -> scal[S_SP] (single block, fixed order)
-template <typename T>
-__global__ void __launch_bounds__(256) k_sum_p(const T *__restrict__ p, int64_t m1, double *scal, const int *ctrl) {
-    if (cg_done(ctrl)) return;
-    __shared__ double red[256];
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < m1; i += blockDim.x) s += static_cast<double>(p[i]);
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) scal[S_SP] = red[0];
 }
 
 // Row dot products with a d-vector: out[i] = <X[r0 + i], w> + add (one warp per row).
@@ -553,9 +620,38 @@ __global__ void __launch_bounds__(256) k_rowdot(const T *__restrict__ X, int64_t
     const int64_t i = r0 + row;
     T s = T(0), sl = T(0);
     const bool real = i < m;
-    for (int64_t k = lane; k < d; k += 32) {
-        if (real) s = fma(X[i * d + k], w[k], s);
-        if (mode == 1) sl = fma(X[(m - 1) * d + k], w[k], sl);
+    if ((d & 1) == 0) {  // feature pairs (vec2 loads), 4 per lane in flight per step
+        using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+        const int64_t d2 = d >> 1;
+        const V2 *xr = reinterpret_cast<const V2 *>(X + (real ? i : 0) * d);
+        const V2 *xl = reinterpret_cast<const V2 *>(X + (m - 1) * d);
+        const V2 *w2 = reinterpret_cast<const V2 *>(w);
+        constexpr int U = 4;
+        for (int64_t k0 = lane; k0 < d2; k0 += 32 * U) {
+            V2 xv[U], lv[U], wv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t k2 = k0 + 32 * u;
+                const bool in = k2 < d2;
+                wv[u] = in ? w2[k2] : V2{};
+                xv[u] = (in && real) ? xr[k2] : V2{};
+                if (mode == 1) lv[u] = in ? xl[k2] : V2{};
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                s = fma(xv[u].x, wv[u].x, s);
+                s = fma(xv[u].y, wv[u].y, s);
+                if (mode == 1) {
+                    sl = fma(lv[u].x, wv[u].x, sl);
+                    sl = fma(lv[u].y, wv[u].y, sl);
+                }
+            }
+        }
+    } else {
+        for (int64_t k = lane; k < d; k += 32) {
+            if (real) s = fma(X[i * d + k], w[k], s);
+            if (mode == 1) sl = fma(X[(m - 1) * d + k], w[k], sl);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
