@@ -492,6 +492,10 @@ struct Ctx {
     // that stores its band into all of them (the all-gather fused into k_update_p)
     T **peer_p = nullptr;
     bool lsa = false;  // p in the NCCL symmetric window (k_update_p_lsa)
+    // blocks of the CG vector kernels: one per 64 band rows, at most kVecBlocks (a fixed function of
+    // the band length, so every kernel, loop and rank reduces in the same order); small problems no
+    // longer pay for 296 blocks in every grid reduction / barrier (C0: 4 blocks)
+    int vb = kVecBlocks;
     int npeer = 0;
 };
 
@@ -940,7 +944,7 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
             c.Yfin = c.Ypart;
             return g.T;
         }
-        k_slot_sum<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, g.T, g.mpad, g.m1, c.yfull, c.cur_ctrl);
+        k_slot_sum<T><<<c.vb, kVecThreads, 0, c.s>>>(c.Ypart, g.T, g.mpad, g.m1, c.yfull, c.cur_ctrl);
         PLS_CHECK_LAUNCH();
         ++c.launches;
         timed_comm(c, [&] { comm_reduce_scatter(c.comm, c.yfull, c.ysc, g.nb, dtype_of(T()), c.s); });
@@ -1014,7 +1018,7 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
         c.Yfin = c.Ypart;
         return nslots;
     }
-    k_slot_sum<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.Ypart, nslots, g.mpad, g.m1, c.yfull, c.cur_ctrl);
+    k_slot_sum<T><<<c.vb, kVecThreads, 0, c.s>>>(c.Ypart, nslots, g.mpad, g.m1, c.yfull, c.cur_ctrl);
     PLS_CHECK_LAUNCH();
     ++c.launches;
     timed_comm(c, [&] { comm_reduce_scatter(c.comm, c.yfull, c.ysc, g.nb, dtype_of(T()), c.s); });
@@ -1054,7 +1058,7 @@ void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par,
         if (c.fsplit) {
             // this rank's partial product (its feature slice) -> sum over the ranks,
             // then the usual finalize on the summed vector (one slot)
-            k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(Y, nslots, nsub, g.band0, g.nb, g.g0, g.m1, c.p + g.g0,
+            k_finalize<T><<<c.vb, kVecThreads, 0, c.s>>>(Y, nslots, nsub, g.band0, g.nb, g.g0, g.m1, c.p + g.g0,
                                                                c.yred, 0, c.ylab, c.r, nullptr, c.scal, 0, 0,
                                                                c.partials, c.counter, 0, c.cur_ctrl, S_PAP);
             PLS_CHECK_LAUNCH();
@@ -1065,7 +1069,7 @@ void finalize(Ctx<T> &c, int nslots, const T *pband, int mode, T *pout, int par,
             nsub = 1;
         }
     }
-    k_finalize<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(Y, nslots, nsub, g.band0, g.nb, g.g0, g.m1, pband, c.y, mode,
+    k_finalize<T><<<c.vb, kVecThreads, 0, c.s>>>(Y, nslots, nsub, g.band0, g.nb, g.g0, g.m1, pband, c.y, mode,
                                                        c.ylab, c.r, pout, c.scal, par, set_delta0, c.partials,
                                                        c.counter, 1, c.cur_ctrl, c.pap_slot);
     PLS_CHECK_LAUNCH();
@@ -1106,6 +1110,7 @@ void setup(Ctx<T> &c, Arena &A, const Problem &pb, const plssvm_options_t &o, bo
         root = fr == 0;
     }
     c.g = geometry<T>(pb.m, dl, P, rank);
+    c.vb = static_cast<int>(std::min<int64_t>(kVecBlocks, std::max<int64_t>(1, ceil_div(c.g.nb, 64))));
     const Geometry &g = c.g;
     c.kp = KParams<T>{pb.kernel, static_cast<T>(pb.gamma), pb.degree, static_cast<T>(pb.coef0)};
     c.invC = root ? static_cast<T>(1.0 / pb.C) : T(0);
@@ -1346,13 +1351,13 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     // ---- CG init (a2) ----
     const int64_t imax = o.max_iter > 0 ? o.max_iter : g.m1;
     if (o.x0 == 0) {
-        k_init<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.ylab, g.nb, g.g0, g.m1, T(0), 1, c.scal,
+        k_init<T><<<c.vb, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.ylab, g.nb, g.g0, g.m1, T(0), 1, c.scal,
                                                        c.partials, c.counter, 1);
         PLS_CHECK_LAUNCH();
         ++c.launches;
         allreduce(c, S_DELTA0, 2);
     } else {
-        k_init<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.ylab, g.nb, g.g0, g.m1, T(1), 0, c.scal,
+        k_init<T><<<c.vb, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.ylab, g.nb, g.g0, g.m1, T(1), 0, c.scal,
                                                        c.partials, c.counter, 1);
         PLS_CHECK_LAUNCH();
         ++c.launches;
@@ -1423,7 +1428,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
             if (ev1) PLS_CUDA(cudaEventRecord(ev1, c.s));
             finalize<T>(c, ns, pband, 0, nullptr, 0, 0);  // w -> c.y, delta = w.r (partial)
             allreduce(c, S_CG_GAMMA, 2);                   // (gamma, delta): the one reduction
-            k_cgcg_update<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, pband, c.r, scg, c.y, g.nb, c.scal, c.ctrl,
+            k_cgcg_update<T><<<c.vb, kVecThreads, 0, c.s>>>(c.x, pband, c.r, scg, c.y, g.nb, c.scal, c.ctrl,
                                                                   c.partials, c.counter, loop, use_loop);
             PLS_CHECK_LAUNCH();
             ++c.launches;
@@ -1438,7 +1443,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
             const T *Yf = c.Yfin;
             const int nsub = (c.cached || c.circ) ? 1 : c.nsub_eff;
             cudaLaunchConfig_t lc = {};
-            lc.gridDim = dim3(kVecBlocks);
+            lc.gridDim = dim3(c.vb);
             lc.blockDim = dim3(kVecThreads);
             lc.stream = c.s;
             cudaLaunchAttribute at[1];
@@ -1453,7 +1458,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         }
         finalize<T>(c, ns, pband, 0, nullptr, 0, 0);
         allreduce(c, S_PAP, 1);
-        k_update_xr<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.y, g.nb, c.scal, c.ctrl, c.partials,
+        k_update_xr<T><<<c.vb, kVecThreads, 0, c.s>>>(c.x, c.r, pband, c.y, g.nb, c.scal, c.ctrl, c.partials,
                                                             c.counter);
         PLS_CHECK_LAUNCH();
         ++c.launches;
@@ -1467,14 +1472,14 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
             allreduce(c, S_DELTA + (par ^ 1), 1);
         }
         if (c.lsa) {  // fused all-gather through the NCCL device API (stores + LSA barrier in the kernel)
-            k_update_p_lsa<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter,
+            k_update_p_lsa<T><<<c.vb, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter,
                                                                    *comm_lsa_devcomm(c.comm), comm_lsa_window(c.comm),
                                                                    g.g0);
             PLS_CHECK_LAUNCH();
             ++c.launches;
             return;
         }
-        k_update_p<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter, loop,
+        k_update_p<T><<<c.vb, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter, loop,
                                                            use_loop, c.peer_p, c.npeer, g.g0);
         PLS_CHECK_LAUNCH();
         ++c.launches;
@@ -1622,9 +1627,9 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
                 comm_allreduce_sum_f64(c.comm, c.scal + S_QMM, c.scal + S_QMM, 1, c.s);
             }
         }
-        k_bias_sums<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.q, g.nb, g.g0, c.scal, 0, c.partials, c.counter);
+        k_bias_sums<T><<<c.vb, kVecThreads, 0, c.s>>>(c.x, c.q, g.nb, g.g0, c.scal, 0, c.partials, c.counter);
         PLS_CHECK_LAUNCH();
-        k_bias_sums<T><<<kVecBlocks, kVecThreads, 0, c.s>>>(c.x, c.q, g.nb, g.g0, c.scal, 1, c.partials, c.counter);
+        k_bias_sums<T><<<c.vb, kVecThreads, 0, c.s>>>(c.x, c.q, g.nb, g.g0, c.scal, 1, c.partials, c.counter);
         PLS_CHECK_LAUNCH();
         c.launches += 2;
         allreduce(c, S_SUMX, 2);
