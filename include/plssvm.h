@@ -115,6 +115,12 @@ typedef struct {
     int32_t true_residual;   /* 1: after CG, one more product gives ||rhs - Q~x|| / ||r0|| in
                                 stats.rel_residual_true (SURVEY §5 metrics) [0: not computed, stats -1] */
     int32_t reserved0;
+    double *residual_trace;  /* HOST buffer (nullable) for the CG trace (SPEC CGTrace): on return
+                                residual_trace[k] = ||r_k||, the recurrence residual norm after iteration k,
+                                k = 0 .. min(iterations, residual_trace_len - 1) (entry 0: the initial
+                                residual); entries beyond are untouched.  Shewchuk variant only; the CG
+                                loop is then issued in batches (no CUDA graph) [NULL] */
+    int64_t residual_trace_len;  /* entries available in residual_trace [0] */
 } plssvm_options_t;
 
 /* Collectives of the single-process multi-GPU mode (options.num_gpus > 1).

@@ -43,7 +43,7 @@ class plssvm_options_t(ct.Structure):
                 ("fp32_engine", ct.c_int32), ("linear_w", ct.c_int32), ("fp64_engine", ct.c_int32),
                 ("cg_loop", ct.c_int32), ("multi_gpu", ct.c_int32), ("cg_variant", ct.c_int32),
                 ("num_gpus", ct.c_int32), ("transport", ct.c_int32), ("true_residual", ct.c_int32),
-                ("reserved0", ct.c_int32)]
+                ("reserved0", ct.c_int32), ("residual_trace", ct.c_void_p), ("residual_trace_len", ct.c_int64)]
 
 
 class plssvm_stats_t(ct.Structure):

@@ -1380,6 +1380,15 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     k_cg_start<<<1, 1, 0, c.s>>>(c.scal, c.ctrl, pb.eps * pb.eps, imax_i, fixed_i, repl_i);
     PLS_CHECK_LAUNCH();
     ++c.launches;
+    // residual trace (options.residual_trace, SPEC CGTrace): delta_k copied on the stream after
+    // every iteration's update (the global scalar slots), square roots taken on the host at the end
+    const bool want_trace = o.residual_trace != nullptr && o.residual_trace_len > 0;
+    if (want_trace && o.cg_variant == PLSSVM_CG_SINGLE_REDUCTION)
+        throw Error(PLSSVM_E_INVALID_ARG, "options.residual_trace needs the Shewchuk CG variant");
+    const int64_t trace_n = want_trace ? std::min<int64_t>(o.residual_trace_len, imax + 1) : 0;
+    double *trace_d = want_trace ? A.alloc<double>(trace_n) : nullptr;
+    if (want_trace)
+        PLS_CUDA(cudaMemcpyAsync(trace_d, c.scal + S_DELTA0, sizeof(double), cudaMemcpyDeviceToDevice, c.s));
     double *hs = reinterpret_cast<double *>(pinned_scratch(S_COUNT * sizeof(double) + C_COUNT * sizeof(int)));
     int *hctrl = reinterpret_cast<int *>(hs + S_COUNT);
     const int64_t launches_before_cg = c.launches;
@@ -1420,6 +1429,11 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         PLS_CUDA(cudaMemsetAsync(scg, 0, g.nb * sizeof(T), c.s));
         c.pap_slot = S_CG_DELTA;
     }
+    auto trace_after = [&](int64_t k) {  // delta_{k+1} -> trace[k + 1]
+        if (trace_d && k + 1 < trace_n)
+            PLS_CUDA(cudaMemcpyAsync(trace_d + k + 1, c.scal + S_DELTA + ((k & 1) ^ 1), sizeof(double),
+                                     cudaMemcpyDeviceToDevice, c.s));
+    };
     auto enqueue_iteration = [&](int64_t k, cudaEvent_t ev0, cudaEvent_t ev1, cudaGraphConditionalHandle loop,
                                  int use_loop) {
         if (cgcg) {
@@ -1454,6 +1468,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
             PLS_CUDA(cudaLaunchKernelEx(&lc, k_cg_fused<T>, Yf, ns, nsub, g.band0, g.nb, g.g0, g.m1, c.x, c.r, pband,
                                         c.y, c.scal, c.ctrl, c.partials, loop, use_loop));
             ++c.launches;
+            trace_after(k);
             return;
         }
         finalize<T>(c, ns, pband, 0, nullptr, 0, 0);
@@ -1477,22 +1492,25 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
                                                                    g.g0);
             PLS_CHECK_LAUNCH();
             ++c.launches;
+            trace_after(k);
             return;
         }
         k_update_p<T><<<c.vb, kVecThreads, 0, c.s>>>(pband, c.r, g.nb, c.scal, c.ctrl, c.counter, loop,
                                                            use_loop, c.peer_p, c.npeer, g.g0);
         PLS_CHECK_LAUNCH();
         ++c.launches;
+        trace_after(k);
         if (c.npeer > 0)  // p already stored into every rank's buffer: only the cross-device order remains
             timed_comm(c, [&] { comm_peer_fence(c.comm, c.s); });
         else
             allgather(c, c.p);
     };
-    const bool graph_ok = c.comm == nullptr && o.replace_every <= 0;
+    const bool graph_ok = c.comm == nullptr && o.replace_every <= 0 && !want_trace;
     const bool use_graph = graph_ok && (o.cg_loop == PLSSVM_CG_GRAPH ||
                                         (o.cg_loop == PLSSVM_CG_AUTO && (c.cached || c.lowrank || g.m1 <= 8192)));
     if (o.cg_loop == PLSSVM_CG_GRAPH && !graph_ok)
-        throw Error(PLSSVM_E_INVALID_ARG, "cg_loop GRAPH needs a single GPU (no comm) and replace_every = 0");
+        throw Error(PLSSVM_E_INVALID_ARG,
+                    "cg_loop GRAPH needs a single GPU (no comm), replace_every = 0 and no residual_trace");
     if (use_graph) {
         // The whole loop as ONE graph launch: entry kernel sets the WHILE
         // condition from the control block, the body (captured once) is one iteration, and
@@ -1654,8 +1672,12 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         allreduce(c, S_TRUE, 1);
         PLS_CUDA(cudaMemcpyAsync(hs + S_TRUE, c.scal + S_TRUE, sizeof(double), cudaMemcpyDeviceToHost, c.s));
     }
+    const int64_t trace_w = want_trace ? std::min<int64_t>(trace_n, it + 1) : 0;
+    if (trace_w > 0)
+        PLS_CUDA(cudaMemcpyAsync(o.residual_trace, trace_d, trace_w * sizeof(double), cudaMemcpyDeviceToHost, c.s));
     PLS_CUDA(cudaEventRecord(e_end, c.s));
     PLS_CUDA(cudaStreamSynchronize(c.s));
+    for (int64_t k = 0; k < trace_w; ++k) o.residual_trace[k] = std::sqrt(std::max(o.residual_trace[k], 0.0));
     if (o.true_residual && status != PLSSVM_E_NUMERICAL) rel_true = delta0 > 0 ? std::sqrt(hs[S_TRUE] / delta0) : 0.0;
     if (st) {
         st->rel_residual_true = rel_true;

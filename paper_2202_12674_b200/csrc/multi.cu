@@ -206,6 +206,7 @@ int train_multi(const Problem &pb, const plssvm_options_t &o, int P, void *alpha
         orr.num_gpus = 1;
         orr.comm = &R.h[r];
         orr.stream = r == 0 ? o.stream : nullptr;
+        if (r != 0) orr.residual_trace = nullptr;  // (the scalars are global: rank 0 writes the trace)
         Problem pr = pb;
         DevBuf kx, ky, ka, kb;
         std::vector<char> ha, hb;

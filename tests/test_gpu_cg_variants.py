@@ -107,3 +107,43 @@ def test_single_reduction_cg_multirank(tmp_path, world, kernel, mode, m, d, mg):
     a_r, b_r, _, _ = oracle.train(X, y, kernel, 1.0 / d, 3, 0.5, 1.0, 1e-10)
     assert int(r["st"]) == 0 and int(r["ranks"]) == world
     _close(r["alpha"], float(r["b"]), a_r, b_r)
+
+
+@pytest.mark.parametrize("mode,loop", [(pl.MODE_IMPLICIT, pl.CG_BATCHED), (pl.MODE_CACHED, pl.CG_AUTO)])
+def test_residual_trace(mode, loop):
+    """options.residual_trace (SURVEY §5 metrics, SPEC CGTrace): ||r_k|| for k = 0 .. iterations.  Pins:
+    entry 0 is ||rhs|| (x0 = 0, Eq. 14); entry j equals the recurrence residual a run capped at j
+    iterations stops with (the device path is deterministic, so bit for bit); the last entry is below the
+    threshold eps ||r_0|| and the one before above it; and the same quantity recorded by the oracle's CG
+    (sqrt(delta_k)) agrees over the first iterations (later the residual norm of CG is erratic on this
+    system -- non-monotone peaks that two summation orders place an iteration apart -- while both runs
+    stop within 2 iterations of each other)."""
+    X, y, _, _ = synth.planes(700, 24, 16, seed=17)
+    gamma, eps = 1.0 / 24, 1e-10
+
+    def run(**kw):
+        buf = np.full(400, -1.0)
+        a, b, st, s = pl.plssvm_train_ex(X, y, pl.RBF, gamma, 3, 0.0, 1.0, eps,
+                                         opts=pl.options(mode=mode, cg_loop=loop, residual_trace=buf.ctypes.data,
+                                                         residual_trace_len=buf.size, **kw))
+        return buf, st, s
+
+    buf, st, s = run()
+    assert st == 0 and s.cg_loop_used == pl.CG_BATCHED  # (a trace forces the batched loop)
+    n = s.iterations + 1
+    assert np.all(buf[:n] >= 0.0) and np.all(buf[n:] == -1.0)
+    rhs = y[:-1] - y[-1]
+    assert abs(buf[0] - np.linalg.norm(rhs)) <= 1e-13 * np.linalg.norm(rhs)
+    assert buf[s.iterations] <= eps * buf[0] < buf[s.iterations - 1]
+    for j in (1, 5, s.iterations // 2):
+        bj, stj, sj = run(max_iter=j)
+        assert sj.iterations == j and np.array_equal(bj[:j + 1], buf[:j + 1])
+        assert sj.rel_residual * buf[0] == pytest.approx(buf[j], rel=1e-14)
+    Qt = oracle.qtilde(X, pl.RBF, gamma, 3, 0.0, 1.0)
+    _, it_ref, _, tr = oracle.cg(Qt, rhs, eps=eps, trace=True)
+    assert abs(it_ref - s.iterations) <= 2
+    np.testing.assert_allclose(buf[:5], tr[:5], rtol=1e-9)
+    with pytest.raises(pl.PlssvmError, match="Shewchuk"):
+        pl.plssvm_train_ex(X, y, pl.RBF, gamma, 3, 0.0, 1.0, eps,
+                           opts=pl.options(cg_variant=pl.CG_SINGLE_REDUCTION, residual_trace=buf.ctypes.data,
+                                           residual_trace_len=buf.size))
