@@ -474,9 +474,11 @@ struct Ctx {
     int *ctrl = nullptr;             // device CG control block (kernels.cuh Ctl)
     bool oz = false;                 // fp64: int8 tensor-core digit engine (ozaki_engine.cuh)
     OzOperand ozx;
-    int2 *oz_pt = nullptr;            // 2-SM pair-tiles (ozaki_engine.cuh)
+    int4 *oz_pt = nullptr;            // 2-SM pair-tiles (ozaki_engine.cuh)
     int *oz_pk = nullptr;
     int oz_npt = 0;
+    int4 *oz_pt_mv = nullptr;         // one GPU: the products' pair-tiles with no dropped half
+    int oz_npt_mv = 0;                // (oz_pair_tiles_matvec; 0 = use oz_pt)
     const int *cur_ctrl = nullptr;   // ctrl inside the CG loop (loop kernels early-exit when done)
     bool fsplit = false;             // PLSSVM_MULTI_GPU_FEATURES: this rank's feature slice only,
                                      // partial products summed by an all-reduce
@@ -775,7 +777,7 @@ int oz_debug_flags() {
 // One persistent CTA per SM (the 512-column TMEM allocation admits one per SM anyway), in
 // clusters of 2 (cta_group::2): the grid is an even number of CTAs, at most the SM count.
 template <int KT, int MODE, typename T>
-void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb, const int2 *ptiles, const int *pk,
+void oz_launch(int npt, cudaStream_t s, const OzOperand &ra, const OzOperand &cb, const int4 *ptiles, const int *pk,
                int rowsI, const T *qv, const T *na, const T *nb_, const T *p, KParams<T> kp, T invC,
                const double *scal, int64_t m1, int band0, int band1, T *Ypart, int64_t band_rows, T *Qc, int T_tiles,
                const int *ctrl) {
@@ -825,7 +827,7 @@ int oz_group_rows(int64_t d8, int S) {
     return per_block * 32 <= budget ? 32 : per_block * 16 <= budget ? 16 : 8;
 }
 
-void oz_pair_tiles(const std::vector<int2> &tl, int b0, int b1, int T, int64_t d8, int S, std::vector<int2> &pt,
+void oz_pair_tiles(const std::vector<int2> &tl, int b0, int b1, int T, int64_t d8, int S, std::vector<int4> &pt,
                    std::vector<int> &pk) {
     std::vector<int> ord(static_cast<size_t>(b1 - b0) * T, -1);
     for (size_t k = 0; k < tl.size(); ++k) ord[static_cast<size_t>(tl[k].x - b0) * T + tl[k].y] = static_cast<int>(k);
@@ -839,10 +841,51 @@ void oz_pair_tiles(const std::vector<int2> &tl, int b0, int b1, int T, int64_t d
                 const int o1 = (I0 + 1 < b1) ? ord[static_cast<size_t>(I0 + 1 - b0) * T + J] : -1;
                 if (o0 < 0 && o1 < 0) continue;
                 const int use = (o0 >= 0 ? 1 : 0) | (o1 >= 0 ? 2 : 0);
-                pt.push_back(make_int2(I0 | (use << 24), J));
+                pt.push_back(make_int4(I0, I0 + 1, J, use));
                 pk.push_back(o0);
                 pk.push_back(o1);
             }
+}
+
+// Pair-tiles of the one-GPU implicit PRODUCT (OZ_MATVEC) with no dropped half.  The upper-triangle
+// list puts column block J's tiles (I, J), I = 0..J, in one column: J + 1 tiles, odd for every even
+// J, so oz_pair_tiles computes and drops the lower block (J + 1, J) of every diagonal pair-tile --
+// T/2 wasted half pair-tiles (C1: 4160 pair-tiles for 4128 of work, 57 instead of 56 rounds of the
+// 74 co-resident CTA pairs).  The product's epilogue treats a tile and its mirror alike (row sums of
+// (I, J) -> slot J of block I, column sums -> slot I of block J, whichever of I, J is larger), so
+// the tile {J1, J2} of two consecutive odd columns J1 < J2 can be computed as (J2, J1) in column J1:
+// every column even, every tile in exactly one pair (one single only when T(T+1)/2 is odd).  The
+// same (slot, block) entries are written exactly once as before.  Rows of a column are paired in
+// order (adjacent blocks except around the moved tiles) and the raster is oz_pair_tiles' (groups of
+// G row blocks, column blocks slowest inside a group).  The cached precompute keeps oz_pair_tiles'
+// list (its packed tiles are stored in the (I <= J) orientation).
+void oz_pair_tiles_matvec(int T, int64_t d8, int S, std::vector<int4> &pt) {
+    std::vector<std::vector<int>> rows(static_cast<size_t>(T));
+    for (int J = 0; J < T; ++J)
+        for (int I = 0; I <= J; ++I) rows[J].push_back(I);
+    std::vector<int> odd;
+    for (int J = 0; J < T; ++J)
+        if (rows[J].size() % 2) odd.push_back(J);
+    for (size_t k = 0; k + 1 < odd.size(); k += 2) {  // tile (J1, J2): column J2 -> column J1 as (J2, J1)
+        const int J1 = odd[k], J2 = odd[k + 1];
+        rows[J2].erase(std::find(rows[J2].begin(), rows[J2].end(), J1));
+        rows[J1].push_back(J2);
+    }
+    const int G = oz_group_rows(d8, S);
+    std::vector<std::pair<std::pair<int, int>, int4>> items;  // ((group, J), pair)
+    for (int J = 0; J < T; ++J) {
+        std::vector<int> &r = rows[J];
+        std::sort(r.begin(), r.end());
+        for (size_t k = 0; k < r.size(); k += 2) {
+            const bool two = k + 1 < r.size();
+            const int I0 = r[k], I1 = two ? r[k + 1] : r[k];
+            items.push_back({{I0 / G, J}, make_int4(I0, I1, J, two ? 3 : 1)});
+        }
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const auto &a, const auto &b) { return a.first < b.first; });
+    pt.clear();
+    for (const auto &it : items) pt.push_back(it.second);
 }
 
 template <int MODE, typename T, typename... Args>
@@ -864,6 +907,10 @@ bool launch_oz(Ctx<T> &c, const T *pfull, int b0, int b1, int64_t brows, bool pr
                                       static_cast<const T *>(nullptr), c.kp, c.invC, static_cast<const double *>(c.scal),
                                       g.m1, g.band0, g.band1, static_cast<T *>(nullptr), g.nb, c.Qc,
                                       c.packed ? -1 : g.T, static_cast<const int *>(nullptr));
+    else if (c.oz_npt_mv > 0)
+        oz_dispatch<OZ_MATVEC, T>(c.kp.kernel, c.oz_npt_mv, c.s, c.ozx, c.ozx, c.oz_pt_mv, c.oz_pk, 0, cq, cn, cn, pfull,
+                                  c.kp, c.invC, static_cast<const double *>(c.scal), g.m1, b0, b1, c.Ypart, brows,
+                                  static_cast<T *>(nullptr), g.T, c.cur_ctrl);
     else
         oz_dispatch<OZ_MATVEC, T>(c.kp.kernel, c.oz_npt, c.s, c.ozx, c.ozx, c.oz_pt, c.oz_pk, 0, cq, cn, cn, pfull,
                                   c.kp, c.invC, static_cast<const double *>(c.scal), g.m1, b0, b1, c.Ypart, brows,
@@ -876,14 +923,22 @@ bool launch_oz(Ctx<T> &c, const T *pfull, int b0, int b1, int64_t brows, bool pr
 template <typename T>
 void oz_build_pairs(Ctx<T> &c, Arena &A, const std::vector<int2> &tl, int b0, int b1) {
     if (!c.oz) return;
-    std::vector<int2> pt;
+    std::vector<int4> pt;
     std::vector<int> pk;
     oz_pair_tiles(tl, b0, b1, c.g.T, int64_t(c.ozx.nk) * 32, oz_digits<T>(), pt, pk);
     c.oz_npt = static_cast<int>(pt.size());
-    c.oz_pt = A.alloc<int2>(c.oz_npt);
+    c.oz_pt = A.alloc<int4>(c.oz_npt);
     c.oz_pk = A.alloc<int>(2 * c.oz_npt);
     upload(c.oz_pt, pt.data(), pt.size(), c.s);
     upload(c.oz_pk, pk.data(), pk.size(), c.s);
+    c.oz_npt_mv = 0;
+    if (c.g.P == 1 && b0 == 0 && b1 == c.g.T) {  // one GPU, upper triangle: products with no dropped half
+        std::vector<int4> pm;
+        oz_pair_tiles_matvec(c.g.T, int64_t(c.ozx.nk) * 32, oz_digits<T>(), pm);
+        c.oz_npt_mv = static_cast<int>(pm.size());
+        c.oz_pt_mv = A.alloc<int4>(c.oz_npt_mv);
+        upload(c.oz_pt_mv, pm.data(), pm.size(), c.s);
+    }
 }
 
 template <typename T>
@@ -1904,7 +1959,7 @@ int predict_impl(const Problem &pb, const void *alpha_in, double b, const void *
         oz_set_attrs<T>();
         PLS_CUDA(cudaEventRecord(e0, s));
         oz_dispatch<OZ_PREDICT, T>(pb.kernel, ((tilesI + 1) / 2) * tilesJ, s, oz_z, oz_x,
-                                   static_cast<const int2 *>(nullptr), static_cast<const int *>(nullptr), tilesI,
+                                   static_cast<const int4 *>(nullptr), static_cast<const int *>(nullptr), tilesI,
                                    static_cast<const T *>(nullptr), static_cast<const T *>(nz),
                                    static_cast<const T *>(nx), static_cast<const T *>(alpha), kp, T(0),
                                    static_cast<const double *>(nullptr), int64_t(0), 0, 0, Fpart, npad,

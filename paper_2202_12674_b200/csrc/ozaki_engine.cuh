@@ -458,16 +458,19 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t *bar) {  // arrive o
 }
 
 // Persistent 2-SM tile kernel (cluster of 2 CTAs, tcgen05 cta_group::2).  A CTA pair owns the
-// 256 x 128 pair-tile (row blocks I0, I0 + 1) x (column block J): CTA rank r stages the digit
-// planes of its row block I0 + r (A, 128 rows) and of HALF the column block (B, rows
+// 256 x 128 pair-tile (row blocks I0, I1) x (column block J): CTA rank r stages the digit
+// planes of its row block I_r (A, 128 rows) and of HALF the column block (B, rows
 // J*128 + 64 r .. +63); the leader's single MMA thread issues M = 256, N = 128 UMMAs that read A
 // and B from both CTAs' shared memory and accumulate each CTA's 128 rows in its own TMEM.  Per SM
 // the MMA reads 6 KiB of operands per 64-cycle UMMA instead of 8 (A 4 KiB + half of B), and the
 // pair loads each B plane once -- the 1-SM kernel was bound by shared-memory bandwidth
 // (operand reads + TMA writes ~1.3x the 128 B/clk an SM has).
-// Pair-tiles: MATVEC / PRECOMPUTE take a list of int2 (I0 | use << 24, J), use bit r = tile
-// (I0 + r, J) is one of this rank's (others are computed and dropped: only the diagonal pair's
-// lower block and odd band ends); PREDICT enumerates t -> (2 (t % pairsI), t / pairsI).
+// Pair-tiles: MATVEC / PRECOMPUTE take a list of int4 (I0, I1, J, use): CTA rank r computes the
+// tile (I_r, J); use bit r = that tile is one of this rank's (others are computed and dropped).  The
+// two row blocks need not be adjacent: a tile (I, J) with I > J is the mirror of the stored (J, I)
+// and the MATVEC epilogue's row and column sums treat both orientations alike (driver.cu
+// oz_pair_tiles_matvec uses that to pair every tile of the triangle, no dropped half);
+// PREDICT enumerates t -> (2 (t % pairsI) + r, t / pairsI).
 //  OZ_MATVEC     : Q~ entries -> row sums Ypart[J] (rows of I), mirrored tiles also column sums
 //                  Ypart[I] (rows of J) -- k_matvec_implicit's slots with 128-wide blocks
 //  OZ_PRECOMPUTE : Q~ entries -> cached tiled array Qc (packed: ordinal pk[2 t + r]; else band
@@ -482,7 +485,7 @@ template <int KT, int S, int MODE, typename T>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     k_tile_ozaki(const __grid_constant__ CUtensorMap ta4, const __grid_constant__ CUtensorMap ta8,
                  const __grid_constant__ CUtensorMap tb4, const __grid_constant__ CUtensorMap tb8, int nk,
-                 const int2 *__restrict__ tiles, const int *__restrict__ pk, int ntiles, int rowsI,
+                 const int4 *__restrict__ tiles, const int *__restrict__ pk, int ntiles, int rowsI,
                  const double *__restrict__ sca, const double *__restrict__ scb, const T *__restrict__ qv,
                  const T *__restrict__ na, const T *__restrict__ nb_, const T *__restrict__ p, KParams<T> kp, T invC,
                  const double *__restrict__ scal, int64_t m1, int band0, int band1, T *__restrict__ Ypart,
@@ -539,18 +542,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     const uint32_t full0 = mapa_shared(smem_addr(full), 0);     // leader's full[0] (cluster window)
     const uint32_t tempty0 = mapa_shared(smem_addr(tempty), 0);  // leader's tempty
 
-    // pair-tile t -> first row block, column block, use bits
-    auto tile_of = [&](int t, int &I0, int &J, int &use) {
+    // pair-tile t -> this CTA's row block, the column block, use bits
+    auto tile_of = [&](int t, int &I, int &J, int &use) {
         if constexpr (MODE == OZ_PREDICT) {
             const int pairsI = (rowsI + 1) / 2;
-            I0 = 2 * (t % pairsI);
+            const int I0 = 2 * (t % pairsI);
+            I = I0 + int(rank);
             J = t / pairsI;
             use = (I0 + 1 < rowsI) ? 3 : 1;
         } else {
-            const int2 tl = tiles[t];
-            I0 = tl.x & 0xFFFFFF;
-            J = tl.y;
-            use = tl.x >> 24;
+            const int4 tl = tiles[t];
+            I = rank ? tl.y : tl.x;
+            J = tl.z;
+            use = tl.w;
         }
     };
 
@@ -562,8 +566,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
         if (lane == 0) {  // ---- TMA producer (both CTAs): this CTA's A block and B half
             uint32_t g = 0;
             for (int t = pair; t < ntiles; t += npairs) {
-                int I0, J, use;
-                tile_of(t, I0, J, use);
+                int I, J, use;
+                tile_of(t, I, J, use);
 #pragma unroll 1
                 for (int pass = 0; pass < O::NPASS; ++pass) {
                     const int np = oz_planes<S>(pass);
@@ -581,10 +585,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         }
                         if (leader) mbar_expect_tx(&full[s], 2u * np * (O::PLANE + O::PLANE / 2));  // both CTAs' bytes
                         const uint32_t fb = full0 + s * 8;
-                        // pre-swizzled blocks: A (row block I0 + r, slab kb) = np x 4 KiB at 128-B row
+                        // pre-swizzled blocks: A (row block I_r, slab kb) = np x 4 KiB at 128-B row
                         // (I * nk + kb) * S * 32; B = half r of block J: rows 16 r .. 16 r + 15 of the
                         // planes (J * nk + kb) * S + a, a < np
-                        tma_load_2d_2sm(st, np == S ? &ta8 : &ta4, fb, 0, ((I0 + int(rank)) * nk + kb) * (S * 32));  // ta8: all S planes
+                        tma_load_2d_2sm(st, np == S ? &ta8 : &ta4, fb, 0, (I * nk + kb) * (S * 32));  // ta8: all S planes
                         tma_load_3d_2sm(st + np * O::PLANE, np == S ? &tb8 : &tb4, fb, 0, 16 * int(rank),
                                         (J * nk + kb) * S);
                     }
@@ -658,9 +662,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
         const T Qmm = (MODE == OZ_PREDICT) ? T(0) : static_cast<T>(scal[S_QMM]);
         uint32_t e = 0;
         for (int t = pair; t < ntiles; t += npairs) {
-            int I0, J, use;
-            tile_of(t, I0, J, use);
-            const int I = I0 + int(rank);
+            int I, J, use;
+            tile_of(t, I, J, use);
             const bool used = (use >> rank) & 1;  // CTA-uniform
             const int64_t row0 = int64_t(I) * kTile, col0 = int64_t(J) * TN;
             if (et < TN) {  // column data of this tile (the previous tile's readers are done: B3)
