@@ -739,28 +739,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                 OZ_PROF_T0(tdr0);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 ++e;
+                // Levels 0-2 first: pass 1 accumulates levels 4-6 into TMEM columns 0 .. 3 TN - 1 only, so
+                // the MMA may start pass 1 as soon as those are read; level 3 (columns 3 TN ..) is read
+                // after the release, under pass 1's MMAs -- the critical drain reads 3 levels, not 4.
                 if (!(dbg & 1)) {
 #pragma unroll
                     for (int c = 0; c < CPT / 8; ++c) {
-                        uint32_t r0[8], r1[8], r2[8], r3[8];
-                        tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
+                        uint32_t r0[8], r1[8], r2[8];
                         tmem_ld8_issue(tbase + uint32_t(2 * TN + c * 8), r2);
                         tmem_ld8_issue(tbase + uint32_t(1 * TN + c * 8), r1);
                         tmem_ld8_issue(tbase + uint32_t(c * 8), r0);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            // V + 3 2^51, exact in int64; held as bits until pass 1 knows the scale
-                            const long long Vb = mad_wide(r0[j], 1 << 24, mad_wide(r1[j], 1 << 16,
-                                                           mad_wide(r2[j], 1 << 8, mad_wide(r3[j], 1, kOzBias))));
-                            sv[c * 8 + j] = bigd ? __double_as_longlong(i64_to_f64_exact(Vb - kOzBias)) : Vb;
-                        }
+                        for (int j = 0; j < 8; ++j)  // V + 3 2^51 without level 3, exact in int64
+                            sv[c * 8 + j] = mad_wide(r0[j], 1 << 24, mad_wide(r1[j], 1 << 16, mad_wide(r2[j], 1 << 8, kOzBias)));
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(tempty0);  // the MMA may start pass 1
                 if (prof) OZ_PROF_ADD(5, tdr0);
+                if (!(dbg & 1)) {
+#pragma unroll
+                    for (int c = 0; c < CPT / 8; ++c) {
+                        uint32_t r3[8];
+                        tmem_ld8_issue(tbase + uint32_t(3 * TN + c * 8), r3);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            // V + 3 2^51, exact in int64; held as bits until pass 1 knows the scale
+                            const long long Vb = mad_wide(r3[j], 1, sv[c * 8 + j]);
+                            sv[c * 8 + j] = bigd ? __double_as_longlong(i64_to_f64_exact(Vb - kOzBias)) : Vb;
+                        }
+                    }
+                }
             }
             {
                 OZ_PROF_T0(t0);
