@@ -158,6 +158,19 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
 }
+// Wait with a suspend-time hint (A/B build option PLSSVM_OZ_SLEEP): the waiting thread may stay
+// suspended up to the hint (ns) instead of the system-dependent limit before try_wait returns false.
+__device__ __forceinline__ void mbar_wait_idle(uint64_t *b, uint32_t parity) {
+#ifdef PLSSVM_OZ_SLEEP
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
+        "r"(parity), "n"(PLSSVM_OZ_SLEEP));
+#else
+    mbar_wait(b, parity);
+#endif
+}
 
 // 2^(j/256), j = 0..255, correctly rounded (tools/gen_exp_table.py: 60-digit Decimal, each value
 // checked against its neighbours) -- the table of exp_tab256.
@@ -575,7 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         const uint32_t s = g % O::STAGES;
                         if (g >= O::STAGES) {
                             OZ_PROF_T0(t0);
-                            mbar_wait(&empty[s], ((g / O::STAGES) - 1) & 1);
+                            mbar_wait_idle(&empty[s], ((g / O::STAGES) - 1) & 1);
                             OZ_PROF_ADD(3, t0);
                         }
                         unsigned char *st = ring + size_t(s) * O::STAGE_BYTES;
@@ -733,7 +746,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             if constexpr (S == 7) {
                 {
                     OZ_PROF_T0(t0);
-                    mbar_wait(tfull, e & 1);
+                    mbar_wait_idle(tfull, e & 1);
                     if (prof) OZ_PROF_ADD(4, t0);
                 }
                 OZ_PROF_T0(tdr0);
@@ -776,7 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             }
             {
                 OZ_PROF_T0(t0);
-                mbar_wait(tfull, e & 1);
+                mbar_wait_idle(tfull, e & 1);
                 if (prof) OZ_PROF_ADD(4, t0);
             }
             OZ_PROF_T0(tdr1);
