@@ -280,7 +280,19 @@ def config_dict(cfg, args, mode):
             "m": cfg.m, "d": cfg.d, "kernel": KNAMES[cfg.kernel], "gamma": cfg.gamma, "degree": cfg.degree,
             "coef0": cfg.coef0, "C": cfg.C, "eps": cfg.eps, "mode": mode, "n_test": cfg.n_test,
             "parallelism": f"row-sharded Q~ x{args.gpus}" if args.gpus > 1 else "1 GPU",
-            "l2": "inputs larger than L2 (X 128 MiB + X^T 128 MiB + Z 64 MiB per step > 126 MB L2); no flush"}
+            "l2": l2_note(cfg)}
+
+
+def l2_note(cfg):
+    """The per-step working set against the 126 MB L2 (inputs larger than L2: no flush between steps)."""
+    s = 4 if cfg.dtype == "f32" else 8
+    digits = 3 if cfg.dtype == "f32" else 7  # int8 digit planes of the tensor-core engines (DESIGN.md §4)
+    d8 = -(-cfg.d // 32) * 32
+    x, z = cfg.m * cfg.d * s, cfg.n_test * cfg.d * s
+    dx, dz = digits * cfg.m * d8, digits * cfg.n_test * d8
+    mib = lambda b: f"{b / 2**20:.0f} MiB"  # noqa: E731
+    return (f"inputs larger than L2: X {mib(x)} + its digits {mib(dx)} (train, again in predict) + Z {mib(z)} + "
+            f"its digits {mib(dz)} per step > 126 MB L2; no flush")
 
 
 def main():
