@@ -247,8 +247,10 @@ __constant__ double kExp2Tab256[256] = {
 // or Cody-Waite reduction).  tp = n + r', n = 256 k + j, |r'| <= 1/2:
 //     e^t = 2^k 2^(j/256) e^{r' L},  L = ln2/256,  e^{r' L} - 1 = r'(C1 + r'(C2 + r'(C3 + r' C4)))
 // (C_k = L^k/k!; truncation |r'L|^5/120 < 4e-17).  n by the 1.5 * 2^52 rounding trick; r' = tp - n is
-// exact.  ~1 ulp, 9 DP operations (+ the clamp).  tp < -261000 (t < -706.8: e^t < 2e-307, where the
-// exponent shift could leave the normal range) returns 0.  tab = kExp2Tab256 in smem.
+// exact.  ~1 ulp, 9 DP operations.  Precondition tp <= 0 (the caller's clamp); tp < -261000 (t < -706.8:
+// e^t < 2e-307, where the exponent shift could leave the normal range) returns 0, tested on the high
+// word (a non-positive double below -261000 has the larger unsigned high word; 0xC10FDC40 = -261000.0,
+// whose low word is 0) -- an integer compare instead of a DP one.  tab = kExp2Tab256 in smem.
 __device__ __forceinline__ double exp_tab256(double tp, const double *__restrict__ tab) {
     constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
     constexpr double C1 = 0.0027076061740622863, C2 = 3.6655655969101062e-06, C3 = 3.3083026805413713e-09,
@@ -262,7 +264,7 @@ __device__ __forceinline__ double exp_tab256(double tp, const double *__restrict
     const double T = tab[n & 255];
     const double e = fma(T, r * c, T);  // 2^(j/256) e^{r' L}, in [0.997, 2)
     const double v = __hiloint2double(__double2hiint(e) + ((n >> 8) << 20), __double2loint(e));
-    return tp < -261000.0 ? 0.0 : v;
+    return static_cast<unsigned>(__double2hiint(tp)) > 0xC10FDC40u ? 0.0 : v;
 }
 constexpr double kExpScale256 = 369.3299304675746;  // 256 / ln 2
 
@@ -508,6 +510,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
     constexpr int TN = O::TN, LV = O::LV;
     if (cg_done(ctrl)) return;  // uniform across the cluster
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // (The integer round trip makes the epilogue's smem pointers generic: its column data, table and
+    // partials are read with generic LD.  Deriving them from smem_raw by pointer arithmetic turns them into
+    // LDS, which made predict 5 % and the C2 product 2 % SLOWER in an A/B run (profiles/r02_ab_epilogue_lean.txt).)
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char *ring = base;
     unsigned char *misc = base + size_t(O::STAGES) * O::STAGE_BYTES;
@@ -696,6 +701,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
             const T pi = (MODE == OZ_MATVEC && used) ? p[gi] : T(0);
             const T ni = (KT == RBF && used) ? (kTabExp ? T(gK * na[gi]) : na[gi]) : T(0);  // fp64 RBF: b_i
             const T cqi = Qmm - qi;  // Eq. 16 row constant
+            // this thread's diagonal entry (gi == gj: a diagonal tile, column lr): local column index
+            // jd in 0 .. CPT - 1, else -1 -- one compare with a constant per entry
+            const int jd = (MODE != OZ_PREDICT && I == J && lr >= grp * CPT && lr < grp * CPT + CPT) ? lr - grp * CPT : -1;
             if constexpr (MODE == OZ_MATVEC) {
                 // Eq. 16 by rows: sum_j Q~_ij p_j = sum_j k_ij p_j + (Q_mm - q_i) sum_j p_j - sum_j q_j p_j
                 // (+ p_i / C on the diagonal), likewise for the mirrored column sums -- the entries
@@ -856,14 +864,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                     for (int j = 0; j < 8; ++j) {
                         const int lc = grp * CPT + c * 8 + j;
                         const int64_t gj = col0 + lc;
-                        const bool diag = (MODE != OZ_PREDICT) && gi == gj;
+                        const bool diag = (c * 8 + j) == jd;  // gi == gj
                         T kv;
                         if constexpr (kTabExp) {  // kernel_value's RBF (distance clamped at 0, exactly 0 on
-                            // the diagonal, R-9) in the scaled exponent form of exp_tab256
+                            // the diagonal, R-9) in the scaled exponent form of exp_tab256: tp > 0 (a rounded
+                            // distance below 0) and the diagonal give +0.0, by masking both words with
+                            // (sign of tp) & (not diagonal) -- integer ops instead of fmin and selects
                             double tp = fma(a2, sval(c * 8 + j), ni + coln[lc]);
-                            tp = fmin(tp, 0.0);
-                            if (diag) tp = 0.0;
+                            const int th = __double2hiint(tp);
+                            const int keep = (th >> 31) & (diag ? 0 : -1);
+                            tp = __hiloint2double(th & keep, __double2loint(tp) & keep);
                             kv = exp_tab256(tp, etab);
+#ifdef PLSSVM_OZ_EPI_TAX  // experiment (A/B only, results perturbed by <= 1e-300): a second exp per entry,
+                          // to measure what epilogue instructions cost at the power cap
+                            kv = fma(1e-300, exp_tab256(tp * 0.999, etab), kv);
+#endif
                         } else {
                             kv = kernel_value<KT, T>(sval(c * 8 + j), ni, coln[lc], diag, kp);
                         }
