@@ -24,8 +24,10 @@
  * pointer after return and never returns memory the caller must free.  With
  * device_pointers != 0, X, y, alpha, b, Z, decision, labels, p, out are DEVICE pointers on
  * options.device (e.g. torch tensors' data_ptr()), and all work is ordered on
- * options.stream (cudaStream_t, NULL = a library-owned stream); the call still returns only
- * after the results are written (it synchronises that stream).
+ * options.stream (cudaStream_t; cudaStreamLegacy = the legacy default stream; NULL = the
+ * library's own non-blocking stream, one per host thread and device, NOT ordered after other
+ * streams' work); the call still returns only after the results are written (it synchronises
+ * that stream).
  * Layout: X is point-major (row i = point i), m x d, C-contiguous (numpy/torch default);
  * Z is n x d, same layout.  The device transposes to the paper's feature-major layout
  * itself.

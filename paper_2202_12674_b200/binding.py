@@ -23,6 +23,7 @@ MULTI_GPU_ROWS, MULTI_GPU_FEATURES = 0, 1
 CG_SHEWCHUK, CG_SINGLE_REDUCTION = 0, 1
 FP32_TCGEN05, FP32_FFMA, FP32_OZAKI, FP32_AUTO = 0, 1, 2, 3
 TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_PEER = 0, 1, 2
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 STOP_CONVERGED, STOP_MAX_ITER, STOP_FIXED, STOP_STAGNATED, STOP_BREAKDOWN = 0, 1, 2, 3, 4
 OK, E_INVALID_ARG, E_LABELS, E_OOM, E_CUDA, E_NCCL, E_NUMERICAL, W_NOT_CONVERGED, E_IO = range(9)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID_ARG", 2: "E_LABELS", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL",
@@ -190,7 +191,10 @@ def _device_opts(o, tensors):
 
     o.device_pointers = 1
     o.device = tensors[0].device.index or 0
-    o.stream = torch.cuda.current_stream(tensors[0].device).cuda_stream
+    # torch's current stream; its default stream has the handle 0, which the C ABI reads as "no stream"
+    # (a library stream, NOT ordered after torch's work on the legacy default stream), so that one is
+    # passed as cudaStreamLegacy (0x1)
+    o.stream = torch.cuda.current_stream(tensors[0].device).cuda_stream or CUDA_STREAM_LEGACY
     return o
 
 

@@ -62,23 +62,29 @@ struct Arena {
     }
 };
 
+// The stream of a call without a user stream: one non-blocking library stream per host thread and
+// device, created once.  (Creating, synchronising and destroying a stream in every call cost ~170 us
+// of host time per call, while the GPU idled: profiles/r02_host_overhead.txt.)  Calls on one thread
+// are sequential and every call synchronises its stream before it returns, so the stream is idle
+// between calls.
+cudaStream_t library_stream() {
+    int dev = 0;
+    PLS_CUDA(cudaGetDevice(&dev));
+    thread_local struct Pool {
+        std::vector<cudaStream_t> s;
+        ~Pool() {
+            for (cudaStream_t x : s)
+                if (x) cudaStreamDestroy(x);
+        }
+    } pool;
+    if (static_cast<int>(pool.s.size()) <= dev) pool.s.resize(dev + 1, nullptr);
+    if (!pool.s[dev]) PLS_CUDA(cudaStreamCreateWithFlags(&pool.s[dev], cudaStreamNonBlocking));
+    return pool.s[dev];
+}
+
 struct StreamGuard {
     cudaStream_t s = nullptr;
-    bool owned = false;
-    explicit StreamGuard(void *user) {
-        if (user) {
-            s = static_cast<cudaStream_t>(user);
-        } else {
-            PLS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-            owned = true;
-        }
-    }
-    ~StreamGuard() {
-        if (owned) {
-            cudaStreamSynchronize(s);
-            cudaStreamDestroy(s);
-        }
-    }
+    explicit StreamGuard(void *user) : s(user ? static_cast<cudaStream_t>(user) : library_stream()) {}
 };
 
 struct Events {
