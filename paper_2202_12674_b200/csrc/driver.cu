@@ -1459,10 +1459,16 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     // iterations at the end (one GPU; several ranks keep batches of kBatch).
     constexpr int kBatch = 8, kBatchMax = 32;
     constexpr int kCommEv = 12;  // event slots per iteration for collectives (<= 5 collectives)
-    cudaEvent_t *evp = event_pool(2 * kBatchMax + (c.comm ? kBatchMax * kCommEv : 0));
-    cudaEvent_t *mv0 = evp, *mv1 = evp + kBatchMax;
-    auto cev = [&](int b) { return evp + 2 * kBatchMax + b * kCommEv; };
-    int ncev[kBatchMax] = {};
+    // Two event sets, alternating by batch: the host reads a batch's launch times (cudaEventElapsedTime,
+    // ~2.7 us per call, profiles/r02_host_api_cost.txt) while the GPU runs the next batch, and the last
+    // batch's while it runs the bias / alpha kernels -- not at a batch boundary with the GPU idle.
+    const int kSet = 2 * kBatchMax + (c.comm ? kBatchMax * kCommEv : 0);
+    cudaEvent_t *evp = event_pool(2 * kSet);
+    auto mv0 = [&](int set) { return evp + set * kSet; };
+    auto mv1 = [&](int set) { return evp + set * kSet + kBatchMax; };
+    auto cev = [&](int set, int b) { return evp + set * kSet + 2 * kBatchMax + b * kCommEv; };
+    int ncev[2][kBatchMax] = {};
+    int pend_set = -1, pend_n = 0;  // the batch whose events are complete but not read yet
     double t_comm = 0.0;
     double t_mv = 0.0, t_mv_min = 1e30;
     int64_t it = 0;
@@ -1473,6 +1479,17 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     // Chronopoulos-Gear variant: c.p (full) carries r (the product's operand), c.r (band) the
     // search direction p, scg the recurrence s = Q~ p; one all-reduce of (gamma, delta).
     const bool cgcg = o.cg_variant == PLSSVM_CG_SINGLE_REDUCTION;
+    auto read_times = [&]() {  // the pending batch's product (and collective) times
+        if (pend_set < 0) return;
+        for (int b = 0; b < pend_n; ++b) {
+            const double tm = elapsed(mv0(pend_set)[b], mv1(pend_set)[b]);
+            t_mv += tm;
+            t_mv_min = std::min(t_mv_min, tm);
+            for (int k = 0; k + 1 < ncev[pend_set][b]; k += 2)
+                t_comm += elapsed(cev(pend_set, b)[k], cev(pend_set, b)[k + 1]);
+        }
+        pend_set = -1;
+    };
     // one cooperative launch for the vector work of an iteration: one GPU, no exchange, no residual
     // replacement (the three-kernel sequence otherwise; PLSSVM_CG_UNFUSED=1 forces it for A/B runs)
     const bool unfused_env = std::getenv("PLSSVM_CG_UNFUSED") != nullptr;  // (read per call: the A/B test)
@@ -1637,27 +1654,26 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
         int batch = kBatch;
         double d_prev = -1.0;
         int64_t it_prev = 0;
+        int set = 0;
         while (true) {
             for (int b = 0; b < batch; ++b) {
                 if (c.comm) {
-                    c.cev = cev(b);
+                    c.cev = cev(set, b);
                     c.ncev = 0;
                     c.cev_cap = kCommEv;
                 }
-                enqueue_iteration(it + b, mv0[b], mv1[b], 0ull, 0);
-                ncev[b] = c.ncev;
+                enqueue_iteration(it + b, mv0(set)[b], mv1(set)[b], 0ull, 0);
+                ncev[set][b] = c.ncev;
                 c.cev = nullptr;
             }
             PLS_CUDA(cudaMemcpyAsync(hs, c.scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c.s));
             PLS_CUDA(cudaMemcpyAsync(hctrl, c.ctrl, C_COUNT * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+            read_times();  // the previous batch's, while this one runs
             PLS_CUDA(cudaStreamSynchronize(c.s));
             const int64_t ran = hctrl[C_IT] - it;  // iterations of this batch that did work
-            for (int b = 0; b < ran && b < batch; ++b) {
-                const double tm = elapsed(mv0[b], mv1[b]);
-                t_mv += tm;
-                t_mv_min = std::min(t_mv_min, tm);
-                for (int k = 0; k + 1 < ncev[b]; k += 2) t_comm += elapsed(cev(b)[k], cev(b)[k + 1]);
-            }
+            pend_set = set;
+            pend_n = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ran, 0), batch));
+            set ^= 1;
             it = hctrl[C_IT];
             if (std::getenv("PLSSVM_DEBUG"))
                 std::fprintf(stderr, "[plssvm] batch: it=%d done=%d d0=%.6e d[0]=%.6e d[1]=%.6e thr=%.6e pap=%.6e\n",
@@ -1737,6 +1753,7 @@ int train_impl(const Problem &pb, const plssvm_options_t &o, void *alpha_out, vo
     if (trace_w > 0)
         PLS_CUDA(cudaMemcpyAsync(o.residual_trace, trace_d, trace_w * sizeof(double), cudaMemcpyDeviceToHost, c.s));
     PLS_CUDA(cudaEventRecord(e_end, c.s));
+    read_times();  // the last batch's, while the bias / alpha work runs
     PLS_CUDA(cudaStreamSynchronize(c.s));
     for (int64_t k = 0; k < trace_w; ++k) o.residual_trace[k] = std::sqrt(std::max(o.residual_trace[k], 0.0));
     if (o.true_residual && status != PLSSVM_E_NUMERICAL) rel_true = delta0 > 0 ? std::sqrt(hs[S_TRUE] / delta0) : 0.0;
