@@ -263,7 +263,9 @@ def run_reference(args, cfg):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * ts * scale / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(cfg, args, "oracle"),
+            "config": dict(config_dict(cfg, args, "oracle"),
+                           workload=f"{cfg.name} oracle training (CG to eps={cfg.eps:g}) on the first {ms} of {cfg.m} "
+                                    f"points, time scaled by (m/m_s)^2; no predict (CG it/s counts training only)"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cal["cores"], "kind": "oracle",
                              "sample": f"each step: oracle.train on the first {ms} of {cfg.m} points; time scaled "
                                        f"by (m/m_s)^2 = {scale:.2f}" + (" (extrapolated)" if scale > 1.0 else ""),
