@@ -92,13 +92,19 @@ def env_int(name, default):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms; summary() keeps the samples taken
+    inside the timed region (window(t0, t1), host wall clock; nvidia-smi stamps every sample).  The
+    sampler starts before the warm-up steps, so its ~0.5 s start-up does not eat a short timed region."""
 
     def __init__(self, device, enabled=True):
         self.device = device
         self.enabled = enabled
         self.proc = None
         self.path = None
+        self.t0 = self.t1 = None
+
+    def window(self, t0, t1):
+        self.t0, self.t1 = t0, t1
 
     def __enter__(self):
         if not self.enabled:
@@ -107,7 +113,7 @@ class ClockSampler:
         os.close(fd)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,timestamp")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -134,6 +140,16 @@ class ClockSampler:
                     parts = [x.strip() for x in ln.split(",")]
                     if len(parts) >= 9:
                         rows.append(parts)
+            if self.t0 is not None and rows and len(rows[0]) >= 10:  # samples inside the timed region
+                import datetime
+
+                def stamp(r):
+                    try:
+                        return datetime.datetime.strptime(r[9], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    except ValueError:
+                        return None
+                inside = [r for r in rows if (stamp(r) or 0.0) >= self.t0 - 0.1 and (stamp(r) or 0.0) <= self.t1 + 0.1]
+                rows = inside or rows
         except OSError:
             pass
         finally:
@@ -371,23 +387,26 @@ def main():
         f, lab, (tk, nl) = pl.plssvm_predict_ex(tX, alpha, float(b.item()), tZ, cfg.kernel, opts=opts(), **kw)
         return stats, nl, alpha, b, lab
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    # clocks of every GPU of the job (rank 0 samples them all; one process per GPU, devices 0..N-1)
+    # clocks of every GPU of the job (rank 0 samples them all; one process per GPU, devices 0..N-1),
+    # started before the warm-up; only the samples inside the timed region are summarised
     sampler = ClockSampler(",".join(str(i) for i in range(world)) if args.transport == "nccl" else local,
                            enabled=rank == 0)
     per = []
     with sampler:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.time()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         for _ in range(args.steps):
             per.append(step())
         ev1.record()
         torch.cuda.synchronize()
+        sampler.window(w0, time.time())
     if world > 1:
         dist.barrier()
     t = ev0.elapsed_time(ev1) / 1e3
