@@ -88,12 +88,28 @@ struct Oz {
 #ifndef PLSSVM_OZ_STAGES7
 #define PLSSVM_OZ_STAGES7 5  // 5 x 42 KiB: A/B 3.077 -> 3.065 ms at C1 (tools/scripts/ab4.sh); the fp32 engine's 8 -> 10 was 0.4 % slower
 #endif
+#ifndef PLSSVM_OZ_SLABS3
+// fp32 engine: 32-feature slabs per pipeline stage.  2 (4 stages of 36 KiB, 12 UMMAs per stage) instead of
+// 1 (8 stages of 18 KiB, 6 UMMAs): C3 product 5.81 -> 5.26 ms (A/B, profiles/r02_ab_slabs.txt) -- half the
+// stage handshakes and TMA requests per UMMA
+#define PLSSVM_OZ_SLABS3 2
+#endif
 #ifndef PLSSVM_OZ_STAGES3
-#define PLSSVM_OZ_STAGES3 8
+#define PLSSVM_OZ_STAGES3 (8 / PLSSVM_OZ_SLABS3)
 #endif
     static constexpr int STAGES = S == 7 ? PLSSVM_OZ_STAGES7 : PLSSVM_OZ_STAGES3;  // (A/B builds may override)
     static constexpr uint32_t PLANE = kTile * BK;                  // 4 KiB: one A digit plane (B half: 2 KiB)
-    static constexpr uint32_t STAGE_BYTES = S * (PLANE + PLANE / 2);  // pass 0: all S planes of A and of the B half
+    // 32-feature slabs per pipeline stage: SLABS for the passes that load all S planes (one TMA box spans
+    // them: the S planes of consecutive slabs are contiguous), SLABS_P0 for the fp64 engine's 4-plane pass 0
+    // (one box per slab)
+    static constexpr int SLABS = S == 7 ? 1 : PLSSVM_OZ_SLABS3;
+#ifndef PLSSVM_OZ_SLABS7P0
+#define PLSSVM_OZ_SLABS7P0 1
+#endif
+    static constexpr int SLABS_P0 = S == 7 ? PLSSVM_OZ_SLABS7P0 : SLABS;
+    static constexpr int LVP = S == 7 ? 4 : 3;  // planes of the fp64 engine's pass 0 (its LV)
+    static constexpr uint32_t STAGE_BYTES =
+        (SLABS * S > SLABS_P0 * LVP ? SLABS * S : SLABS_P0 * LVP) * (PLANE + PLANE / 2);  // A planes + B halves
 #ifndef PLSSVM_OZ_EPI
 #define PLSSVM_OZ_EPI 8
 #endif
@@ -589,7 +605,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
 #pragma unroll 1
                 for (int pass = 0; pass < O::NPASS; ++pass) {
                     const int np = oz_planes<S>(pass);
-                    for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int sl = (np == S) ? O::SLABS : O::SLABS_P0;  // slabs per stage in this pass
+                    for (int kb = 0; kb < nk; kb += sl, ++g) {
                         const uint32_t s = g % O::STAGES;
                         if (g >= O::STAGES) {
                             OZ_PROF_T0(t0);
@@ -601,14 +618,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                             if (leader) mbar_arrive(&full[s]);
                             continue;
                         }
-                        if (leader) mbar_expect_tx(&full[s], 2u * np * (O::PLANE + O::PLANE / 2));  // both CTAs' bytes
+                        // both CTAs' bytes (SLABS > 1: the boxes hold SLABS consecutive slabs; past the last slab of
+                        // a block they read the next block's digits, which no MMA uses; SLABS_P0 > 1: one box per
+                        // slab, only the block's slabs)
+                        const int nsl = (np == S) ? sl : (sl < nk - kb ? sl : nk - kb);
+                        if (leader) mbar_expect_tx(&full[s], 2u * nsl * np * (O::PLANE + O::PLANE / 2));
                         const uint32_t fb = full0 + s * 8;
                         // pre-swizzled blocks: A (row block I_r, slab kb) = np x 4 KiB at 128-B row
                         // (I * nk + kb) * S * 32; B = half r of block J: rows 16 r .. 16 r + 15 of the
                         // planes (J * nk + kb) * S + a, a < np
-                        tma_load_2d_2sm(st, np == S ? &ta8 : &ta4, fb, 0, (I * nk + kb) * (S * 32));  // ta8: all S planes
-                        tma_load_3d_2sm(st + np * O::PLANE, np == S ? &tb8 : &tb4, fb, 0, 16 * int(rank),
-                                        (J * nk + kb) * S);
+                        if (np == S) {  // all planes: one box each, spanning the stage's SLABS slabs
+                            tma_load_2d_2sm(st, &ta8, fb, 0, (I * nk + kb) * (S * 32));
+                            tma_load_3d_2sm(st + sl * np * O::PLANE, &tb8, fb, 0, 16 * int(rank), (J * nk + kb) * S);
+                        } else {
+                            for (int h = 0; h < nsl; ++h) {  // the first np planes of each slab
+                                tma_load_2d_2sm(st + h * np * O::PLANE, &ta4, fb, 0, (I * nk + kb + h) * (S * 32));
+                                tma_load_3d_2sm(st + sl * np * O::PLANE + h * np * (O::PLANE / 2), &tb4, fb, 0,
+                                                16 * int(rank), (J * nk + kb + h) * S);
+                            }
+                        }
                     }
                 }
             }
@@ -628,7 +656,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                         asm volatile("tcgen05.fence::after_thread_sync;");
                     }
                     const int np = oz_planes<S>(pass);
-                    for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int sl = (np == S) ? O::SLABS : O::SLABS_P0;
+                    for (int kb0 = 0; kb0 < nk; kb0 += sl, ++g) {
                         const uint32_t s = g % O::STAGES;
                         {
                             OZ_PROF_T0(t0);
@@ -636,8 +665,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                             OZ_PROF_ADD(1, t0);
                         }
                         asm volatile("tcgen05.fence::after_thread_sync;");
-                        const uint32_t sa = smem_addr(ring + size_t(s) * O::STAGE_BYTES);
-                        const uint32_t sb = sa + np * O::PLANE;
+                        const uint32_t sa0 = smem_addr(ring + size_t(s) * O::STAGE_BYTES);
+                        const uint32_t sb0 = sa0 + sl * np * O::PLANE;
+                        constexpr int kMaxSl = O::SLABS > O::SLABS_P0 ? O::SLABS : O::SLABS_P0;
+#pragma unroll
+                        for (int h = 0; h < kMaxSl; ++h) {
+                        const int kb = kb0 + h;
+                        if (kMaxSl > 1 && (h >= sl || kb >= nk)) break;
+                        const uint32_t sa = sa0 + h * np * O::PLANE, sb = sb0 + h * np * (O::PLANE / 2);
                         if (dbg & 4) {  // experiment: data movement only
                         } else if (S == 7 && pass == 1) {  // levels 4..6 (18 pairs), TMEM column block l - 4
 #pragma unroll
@@ -658,6 +693,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                                     umma_i8_2sm<S>(tmem + uint32_t((a + b) * TN), umma_desc_sw32(sa + a * O::PLANE),
                                                    umma_desc_sw32(sb + b * (O::PLANE / 2)), (kb > 0 || a > 0) ? 1u : 0u);
                         }
+                        }  // slabs of the stage
                         umma_commit_2sm_mc(&empty[s]);  // frees stage s in both CTAs
                     }
                     umma_commit_2sm_mc(tfull);  // this pass's accumulators ready in both CTAs
