@@ -682,13 +682,13 @@ OzOperand oz_prepare(Arena &A, const TIN *Xp, int64_t rows, int64_t m_valid, int
                                                                                          o.DA, o.sc);
     PLS_CHECK_LAUNCH();
     ++launches;
-    if (row_role) {  // (the full-plane boxes span O::SLABS consecutive slabs: the pipeline stage)
+    if (row_role) {  // (the full-plane boxes span O::BOXSL consecutive slabs of a pipeline stage)
         o.t4 = make_tmap_digit_blocks(o.DA, bytes, O::LV * 32);
-        o.t8 = make_tmap_digit_blocks(o.DA, bytes, O::SLABS * S * 32);
+        o.t8 = make_tmap_digit_blocks(o.DA, bytes, O::BOXSL * S * 32);
     }
     if (col_role) {
         o.h4 = make_tmap_digit_halves(o.DA, bytes, O::LV);
-        o.h8 = make_tmap_digit_halves(o.DA, bytes, O::SLABS * S);
+        o.h8 = make_tmap_digit_halves(o.DA, bytes, O::BOXSL * S);
     }
     o.nk = static_cast<int>(d8 / O::BK);
     return o;

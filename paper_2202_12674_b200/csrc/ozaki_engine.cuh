@@ -85,28 +85,39 @@ struct Oz {
     static constexpr int NSUB = kTile / TN;                        // 1
     static constexpr int LV = S == 7 ? 4 : 3;                      // levels of the last pass (0..LV-1)
     static constexpr int LV0 = S == 7 ? S - LV : LV;               // levels of pass 0
+// Pipeline stages: few and LARGE.  The MMA issuer and the TMA producer hand over once per stage (full /
+// empty mbarriers, tcgen05.commit), so the number of 32-feature slabs per stage sets how many UMMAs run
+// per handshake; A/B (profiles/r02_ab_slabs.txt): fp32 engine 1 slab x 8 stages -> 5 slabs x 2 stages
+// (6 -> 30 UMMAs per stage): C3 product 5.81 -> 4.90 ms; fp64 engine 1 slab x 5 stages -> 2 slabs x 2
+// stages (pass 1: 18 -> 36 UMMAs, pass 0: 10 -> 20): C1 3.00 -> 2.91 ms.  Two stages of 84 KiB (fp64)
+// or 90 KiB (fp32) still cover the L2 -> shared latency: each stage is ~1.5-2.5k MMA cycles.
 #ifndef PLSSVM_OZ_STAGES7
-#define PLSSVM_OZ_STAGES7 5  // 5 x 42 KiB: A/B 3.077 -> 3.065 ms at C1 (tools/scripts/ab4.sh); the fp32 engine's 8 -> 10 was 0.4 % slower
+#define PLSSVM_OZ_STAGES7 2
+#endif
+#ifndef PLSSVM_OZ_SLABS7
+#define PLSSVM_OZ_SLABS7 2  // fp64 pass 1 (all 7 planes): slabs per stage
+#endif
+#ifndef PLSSVM_OZ_SLABS7P0
+#define PLSSVM_OZ_SLABS7P0 2  // fp64 pass 0 (4 planes): slabs per stage (3: no change)
 #endif
 #ifndef PLSSVM_OZ_SLABS3
-// fp32 engine: 32-feature slabs per pipeline stage.  2 (4 stages of 36 KiB, 12 UMMAs per stage) instead of
-// 1 (8 stages of 18 KiB, 6 UMMAs): C3 product 5.81 -> 5.26 ms (A/B, profiles/r02_ab_slabs.txt) -- half the
-// stage handshakes and TMA requests per UMMA
-#define PLSSVM_OZ_SLABS3 2
+#define PLSSVM_OZ_SLABS3 5  // fp32 engine (3 planes): slabs per stage (4: +1 %)
 #endif
 #ifndef PLSSVM_OZ_STAGES3
-#define PLSSVM_OZ_STAGES3 (8 / PLSSVM_OZ_SLABS3)
+#define PLSSVM_OZ_STAGES3 2
 #endif
     static constexpr int STAGES = S == 7 ? PLSSVM_OZ_STAGES7 : PLSSVM_OZ_STAGES3;  // (A/B builds may override)
     static constexpr uint32_t PLANE = kTile * BK;                  // 4 KiB: one A digit plane (B half: 2 KiB)
-    // 32-feature slabs per pipeline stage: SLABS for the passes that load all S planes (one TMA box spans
-    // them: the S planes of consecutive slabs are contiguous), SLABS_P0 for the fp64 engine's 4-plane pass 0
-    // (one box per slab)
-    static constexpr int SLABS = S == 7 ? 1 : PLSSVM_OZ_SLABS3;
-#ifndef PLSSVM_OZ_SLABS7P0
-#define PLSSVM_OZ_SLABS7P0 1
-#endif
+    // SLABS for the passes that load all S planes (one TMA box per BOXSL slabs: the S planes of consecutive
+    // slabs are contiguous), SLABS_P0 for the fp64 engine's 4-plane pass 0 (one box per slab)
+    static constexpr int SLABS = S == 7 ? PLSSVM_OZ_SLABS7 : PLSSVM_OZ_SLABS3;
     static constexpr int SLABS_P0 = S == 7 ? PLSSVM_OZ_SLABS7P0 : SLABS;
+    // slabs one all-plane TMA box spans (a box dimension is at most 256 rows of 32 B per plane and slab)
+    static constexpr int box_slabs(int n) {  // the largest divisor of SLABS whose box fits 256 rows
+        return (SLABS % n == 0 && n * S * 32 <= 256) ? n : box_slabs(n - 1);
+    }
+    static constexpr int BOXSL = box_slabs(SLABS);
+    static_assert(SLABS % BOXSL == 0, "the stage's slabs must split into whole boxes");
     static constexpr int LVP = S == 7 ? 4 : 3;  // planes of the fp64 engine's pass 0 (its LV)
     static constexpr uint32_t STAGE_BYTES =
         (SLABS * S > SLABS_P0 * LVP ? SLABS * S : SLABS_P0 * LVP) * (PLANE + PLANE / 2);  // A planes + B halves
@@ -618,18 +629,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Oz<S>::THREADS, 1)
                             if (leader) mbar_arrive(&full[s]);
                             continue;
                         }
-                        // both CTAs' bytes (SLABS > 1: the boxes hold SLABS consecutive slabs; past the last slab of
-                        // a block they read the next block's digits, which no MMA uses; SLABS_P0 > 1: one box per
-                        // slab, only the block's slabs)
-                        const int nsl = (np == S) ? sl : (sl < nk - kb ? sl : nk - kb);
+                        // both CTAs' bytes: the boxes of the stage's slabs that exist (all-plane boxes span BOXSL
+                        // slabs; a box reaching past the block's last slab reads the next block's digits, which no
+                        // MMA uses)
+                        const int rem = sl < nk - kb ? sl : nk - kb;
+                        const int nsl = (np == S) ? (rem + O::BOXSL - 1) / O::BOXSL * O::BOXSL : rem;
                         if (leader) mbar_expect_tx(&full[s], 2u * nsl * np * (O::PLANE + O::PLANE / 2));
                         const uint32_t fb = full0 + s * 8;
                         // pre-swizzled blocks: A (row block I_r, slab kb) = np x 4 KiB at 128-B row
                         // (I * nk + kb) * S * 32; B = half r of block J: rows 16 r .. 16 r + 15 of the
                         // planes (J * nk + kb) * S + a, a < np
-                        if (np == S) {  // all planes: one box each, spanning the stage's SLABS slabs
-                            tma_load_2d_2sm(st, &ta8, fb, 0, (I * nk + kb) * (S * 32));
-                            tma_load_3d_2sm(st + sl * np * O::PLANE, &tb8, fb, 0, 16 * int(rank), (J * nk + kb) * S);
+                        if (np == S) {  // all planes: boxes spanning BOXSL consecutive slabs each
+#pragma unroll
+                            for (int h = 0; h < nsl; h += O::BOXSL) {
+                                tma_load_2d_2sm(st + h * np * O::PLANE, &ta8, fb, 0, (I * nk + kb + h) * (S * 32));
+                                tma_load_3d_2sm(st + sl * np * O::PLANE + h * np * (O::PLANE / 2), &tb8, fb, 0,
+                                                16 * int(rank), (J * nk + kb + h) * S);
+                            }
                         } else {
                             for (int h = 0; h < nsl; ++h) {  // the first np planes of each slab
                                 tma_load_2d_2sm(st + h * np * O::PLANE, &ta4, fb, 0, (I * nk + kb + h) * (S * 32));
