@@ -30,11 +30,11 @@
 // 128 B/clk at N = 128 = the smem bandwidth, 192 B/clk at N = 64 -- measured: tc pipe 84 %
 // busy, imma 46 % with 128 x 64 tiles), at the same L2 traffic per output element.
 // Persistent CTA pairs (one CTA per SM), warp-specialised:
-//   warp 0 (one lane) : TMA producer -- per 32-feature slab ONE 3-D box per operand brings the
-//                       pass's digit planes (32 B x 128 rows x 4|8 planes, SWIZZLE_32B)
-//   warp 1 (one lane) : TMEM owner; in the leader CTA the MMA issuer -- per slab the pass's digit pairs (K = 32 UMMAs)
-//                       into the level accumulators; tcgen05.commit frees the stage / signals
-//                       the pass
+//   warp 0 (one lane) : TMA producer -- per pipeline stage (Oz::SLABS consecutive 32-feature slabs)
+//                       the pass's pre-swizzled digit planes of the row block and the column half-block
+//   warp 1 (one lane) : TMEM owner; in the leader CTA the MMA issuer -- per slab of the stage the pass's digit
+//                       pairs (K = 32 UMMAs) into the level accumulators; tcgen05.commit frees the stage /
+//                       signals the pass
 //   warps 2-3         : idle (warpgroup 0 gives its registers to the epilogue: setmaxnreg 40 / 232)
 //   warps 4-11        : epilogue -- warp w reads TMEM lanes 32(w%4).. (tile rows), columns
 //                       64((w-4)/4).. of every level (tcgen05.ld 32x32b.x8), combines the levels
