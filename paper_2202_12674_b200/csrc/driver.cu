@@ -1038,10 +1038,11 @@ int launch_qtilde_product(Ctx<T> &c, const T *pfull) {
             PLS_CHECK_LAUNCH();
             ++c.launches;
         }
+        k_lastdot<T><<<1, 256, 0, c.s>>>(c.Xraw + (c.m - 1) * c.d, c.tvec, c.d, c.scal, c.cur_ctrl);
         k_rowdot<T><<<static_cast<unsigned>(ceil_div(g.nb * 32, 256)), 256, 0, c.s>>>(
             c.Xraw, c.d, g.g0, g.nb, c.tvec, 1, T(0), pfull, c.m, c.invC, c.scal, c.Ypart, nullptr, c.cur_ctrl);
         PLS_CHECK_LAUNCH();
-        ++c.launches;
+        c.launches += 2;
         c.Yfin = c.Ypart;
         return 1;
     }

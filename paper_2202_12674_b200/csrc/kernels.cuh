@@ -41,6 +41,7 @@ enum Scal : int {
                     // enqueued after convergence cannot corrupt the global scalars
     S_BEST = 32,    // stagnation guard: delta at the last 4x drop (replicated, never all-reduced)
     S_TRUE = 33,    // |rhs - Q~x|^2 after CG (options.true_residual; partial at S_TRUE + S_L)
+    S_XLT = 34,     // low-rank product: <x_{m-1}, t> of the current product (k_lastdot; replicated)
     S_COUNT = 56
 };
 
@@ -604,10 +605,31 @@ __global__ void k_cast(const double *__restrict__ a, int64_t n, T *__restrict__ 
     if (i < n) b[i] = static_cast<T>(a[i]);
 }
 
+// <x_{m-1}, t> of the low-rank product, once (one block, fixed-order tree: every rank and every
+// row-dot warp uses the same value) -> scal[S_XLT].  (Round 2: each warp of k_rowdot recomputed it,
+// re-reading the 8 d bytes of x_{m-1} once per row: as many load instructions as the streamed rows.)
+template <typename T>
+__global__ void __launch_bounds__(256) k_lastdot(const T *__restrict__ xlast, const T *__restrict__ t, int64_t d,
+                                                 double *scal, const int *ctrl) {
+    if (cg_done(ctrl)) return;
+    __shared__ T red[8];
+    T s = T(0);
+    for (int64_t k = threadIdx.x; k < d; k += blockDim.x) s = fma(xlast[k], t[k], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T v = T(0);
+        for (int w = 0; w < 8; ++w) v += red[w];
+        scal[S_XLT] = static_cast<double>(v);
+    }
+}
+
 // Row dot products with a d-vector: out[i] = <X[r0 + i], w> + add (one warp per row).
 //  mode 0 (predict):  f_i = <z_i, w> + b, label
 //  mode 1 (low-rank): v_i = <x_i, t> + u_i / C,  y_i = v_i - v_{m-1} for i < m-1 (0 beyond);
-//                     v_{m-1} is recomputed by every warp (it needs only x_{m-1} and t)
+//                     v_{m-1} = <x_{m-1}, t> (scal[S_XLT], k_lastdot) - sum p / C
 template <typename T>
 __global__ void __launch_bounds__(256) k_rowdot(const T *__restrict__ X, int64_t d, int64_t r0, int64_t nrows,
                                                 const T *__restrict__ w, int mode, T add, const T *__restrict__ p,
@@ -624,40 +646,30 @@ __global__ void __launch_bounds__(256) k_rowdot(const T *__restrict__ X, int64_t
         using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
         const int64_t d2 = d >> 1;
         const V2 *xr = reinterpret_cast<const V2 *>(X + (real ? i : 0) * d);
-        const V2 *xl = reinterpret_cast<const V2 *>(X + (m - 1) * d);
         const V2 *w2 = reinterpret_cast<const V2 *>(w);
         constexpr int U = 4;
         for (int64_t k0 = lane; k0 < d2; k0 += 32 * U) {
-            V2 xv[U], lv[U], wv[U];
+            V2 xv[U], wv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t k2 = k0 + 32 * u;
                 const bool in = k2 < d2;
                 wv[u] = in ? w2[k2] : V2{};
                 xv[u] = (in && real) ? xr[k2] : V2{};
-                if (mode == 1) lv[u] = in ? xl[k2] : V2{};
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 s = fma(xv[u].x, wv[u].x, s);
                 s = fma(xv[u].y, wv[u].y, s);
-                if (mode == 1) {
-                    sl = fma(lv[u].x, wv[u].x, sl);
-                    sl = fma(lv[u].y, wv[u].y, sl);
-                }
             }
         }
     } else {
-        for (int64_t k = lane; k < d; k += 32) {
+        for (int64_t k = lane; k < d; k += 32)
             if (real) s = fma(X[i * d + k], w[k], s);
-            if (mode == 1) sl = fma(X[(m - 1) * d + k], w[k], sl);
-        }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, o);
-        sl += __shfl_xor_sync(0xffffffffu, sl, o);
-    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (mode == 1) sl = static_cast<T>(scal[S_XLT]);
     if (lane != 0) return;
     if (mode == 0) {
         const T f = s + add;
